@@ -1,0 +1,79 @@
+// C++ drop-in for the reference's American pricing API, backed by the B200
+// kernels through the C ABI in qmcg.h.
+//
+// Mirrors, name for name, the reference declarations a caller of the hot path
+// uses:
+//   OptionKind / Method / OptionSpec / PricingResult   proj/include/qmc/types.hpp:16-49
+//   ExecPolicy                                         proj/include/qmc/path_engine.hpp:36-39
+//   price_american / convergence_curve                 proj/include/qmc/american.hpp:43-55
+// so a reference caller relinks against libqmcg.so instead of american.cpp
+// (see INTEGRATION.md). Exceptions follow the reference: std::invalid_argument
+// for domain errors, std::length_error for size limits, std::runtime_error for
+// device failures. ExecPolicy is accepted and, as in the reference
+// (path_engine.hpp:33-35), never changes numeric results.
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+#include <string>
+#include <vector>
+
+namespace qmc {
+
+using Index = std::ptrdiff_t;  // Eigen::Index in the reference
+
+enum class OptionKind { Call, Put };
+enum class Method { ClosedForm, EuropeanMC, AmericanUpperBound };
+
+std::string method_name(Method method);
+
+struct OptionSpec {
+  double spot = 100.0;
+  double strike = 100.0;
+  double rate = 0.0;
+  double volatility = 0.0;
+  double maturity = 0.0;
+  OptionKind kind = OptionKind::Call;
+};
+
+struct PricingResult {
+  double price = 0.0;
+  double std_error = 0.0;
+  Index n_paths = 0;
+  double elapsed_s = 0.0;
+  Method method = Method::ClosedForm;
+  std::uint64_t seed = 0;
+};
+
+struct ExecPolicy {
+  int lanes = 1;
+  Index chunk = 4096;
+};
+
+struct ConvergencePoint {
+  Index m = 0;
+  double price = 0.0;
+  double std_error = 0.0;
+  double elapsed_s = 0.0;
+};
+using ConvergenceCurve = std::vector<ConvergencePoint>;
+
+// Foresight (upper-bound) American call value; reference american.cpp:103-131.
+PricingResult price_american(const OptionSpec& spec, Index m, Index n_paths, std::uint64_t seed,
+                             const ExecPolicy& exec = {});
+
+// One price_american row per m, sorted ascending; reference american.cpp:133-150.
+// The permutation tables depend on (seed, n_paths, dim) only, so the whole
+// curve reuses one cached table set.
+ConvergenceCurve convergence_curve(const OptionSpec& spec, const std::vector<Index>& m_values,
+                                   Index n_paths, std::uint64_t seed, const ExecPolicy& exec = {});
+
+namespace b200 {
+// Extension (no reference counterpart): the same foresight rule for puts.
+PricingResult price_american_put_extension(const OptionSpec& spec, Index m, Index n_paths,
+                                           std::uint64_t seed);
+// Select the CUDA device used by the process-wide context (default: 0).
+void set_device(int device);
+}  // namespace b200
+
+}  // namespace qmc

@@ -1,0 +1,142 @@
+/* qmcg.h -- C ABI of the B200-native American-option QMC pricer.
+ *
+ * This is the drop-in boundary for the reference's hot path
+ *   qmc::price_american            (reference proj/include/qmc/american.hpp:46-47,
+ *                                   proj/src/american.cpp:103-131)
+ * and everything it calls (QuasiStream / permutation_indices / radical_inverse,
+ * moro_inv_cnd, gbm_step, simulate_batch, sweep_impl, reduce_stats).
+ * Plain C types only: POD structs, pointers and sizes; no CUDA or torch types.
+ * The C++ drop-in with the reference's exact signature is include/qmc_b200/qmc.hpp;
+ * the ctypes binding used by the tests and bench.py is paper_1205_0106_b200/qmcg.py;
+ * INTEGRATION.md shows how a reference build links against this library.
+ *
+ * Error convention: every entry returns a qmcg_status; on failure the message
+ * (the reference's own exception text where one exists) is available from
+ * qmcg_last_error() on the calling thread. QMCG_INVALID_ARGUMENT maps to the
+ * reference's std::invalid_argument, QMCG_LENGTH_ERROR to std::length_error.
+ *
+ * Threading: calls on one context are serialised by a context mutex; distinct
+ * contexts may be used concurrently (one per GPU is the intended layout).
+ */
+#ifndef QMCG_H
+#define QMCG_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  QMCG_OK = 0,
+  QMCG_INVALID_ARGUMENT = 1, /* reference: std::invalid_argument */
+  QMCG_LENGTH_ERROR = 2,     /* reference: std::length_error */
+  QMCG_CUDA_ERROR = 3,
+  QMCG_NCCL_ERROR = 4,
+  QMCG_UNSUPPORTED = 5,
+  QMCG_OUT_OF_MEMORY = 6
+} qmcg_status;
+
+/* reference OptionKind, proj/include/qmc/types.hpp:16 */
+enum { QMCG_CALL = 0, QMCG_PUT = 1 };
+/* reference Method, proj/include/qmc/types.hpp:18 */
+enum { QMCG_METHOD_CLOSED_FORM = 0, QMCG_METHOD_EUROPEAN_MC = 1, QMCG_METHOD_AMERICAN_UB = 2 };
+
+/* flags */
+enum {
+  QMCG_FLAG_ALLOW_PUT = 1u << 0, /* opt-in put extension (reference rejects puts: american.cpp:106-109) */
+  QMCG_FLAG_NO_CACHE = 1u << 1,  /* rebuild the permutation tables for this call (cold timing) */
+};
+
+/* reference OptionSpec, proj/include/qmc/types.hpp:24-31 */
+typedef struct {
+  double spot;
+  double strike;
+  double rate;
+  double volatility;
+  double maturity;
+  int32_t kind; /* QMCG_CALL / QMCG_PUT */
+} qmcg_option_spec;
+
+/* reference PricingResult, proj/include/qmc/types.hpp:42-49 */
+typedef struct {
+  double price;
+  double std_error;
+  int64_t n_paths;
+  double elapsed_s; /* wall time of the whole call, like american.cpp:113,127-128 */
+  int32_t method;   /* QMCG_METHOD_* */
+  uint64_t seed;
+} qmcg_pricing_result;
+
+typedef struct qmcg_ctx qmcg_ctx;
+
+/* Context on one CUDA device: owns the stream, scratch and the permutation-table
+ * cache keyed by (seed, n_paths). */
+qmcg_status qmcg_create(int device, qmcg_ctx** out);
+void qmcg_destroy(qmcg_ctx* ctx);
+const char* qmcg_last_error(void);
+const char* qmcg_version(void);
+
+/* qmc::price_american (proj/src/american.cpp:103-131): foresight upper-bound
+ * American price over n_paths scrambled-Halton GBM paths with m exercise dates.
+ * Identical validation and error text as the reference. */
+qmcg_status qmcg_price_american(qmcg_ctx* ctx, const qmcg_option_spec* spec, int64_t m,
+                                int64_t n_paths, uint64_t seed, uint32_t flags,
+                                qmcg_pricing_result* out);
+
+/* The same pricing for n_specs contracts sharing (m, n_paths, seed): one
+ * permutation-table set, one launch per contract group. No reference
+ * counterpart (the reference loops price_american). */
+qmcg_status qmcg_price_american_batch(qmcg_ctx* ctx, const qmcg_option_spec* specs,
+                                      int64_t n_specs, int64_t m, int64_t n_paths, uint64_t seed,
+                                      uint32_t flags, qmcg_pricing_result* out);
+
+/* Sharded pricing for multi-GPU: computes (sum v, sum v^2) of the pairwise
+ * tree node `node` at depth `depth` (reference pairwise_sum,
+ * proj/src/path_engine.cpp:39-47), over the paths of that node only. Nodes at
+ * one depth partition [0, n_paths). Combining all 2^depth node sums with
+ * qmcg_combine_nodes gives bit-identical results for every depth. */
+qmcg_status qmcg_price_american_node(qmcg_ctx* ctx, const qmcg_option_spec* spec, int64_t m,
+                                     int64_t n_paths, uint64_t seed, uint32_t flags, int depth,
+                                     int64_t node, double out_sums[2]);
+/* Path range [begin, end) of pairwise-tree node `node` at `depth`. */
+qmcg_status qmcg_tree_node_range(int64_t n_paths, int depth, int64_t node, int64_t* begin,
+                                 int64_t* end);
+/* Fold 2^depth node sums (interleaved sum, sum_sq) up the tree and apply
+ * reduce_stats' mean / Bessel standard error (path_engine.cpp:191-205). */
+qmcg_status qmcg_combine_nodes(int64_t n_paths, int depth, const double* node_sums,
+                               double* price, double* std_error);
+
+/* Build (or extend) the cached permutation tables for dims [0, dims). */
+qmcg_status qmcg_warm(qmcg_ctx* ctx, int64_t n_paths, uint64_t seed, int64_t dims);
+/* Drop every cached table. */
+qmcg_status qmcg_clear_cache(qmcg_ctx* ctx);
+
+/* ---- parity exports (bit-exact checks against the reference) ---- */
+/* permutation_indices(n, seed64) (proj/src/quasi_rng.cpp:48-61), built on the GPU. */
+qmcg_status qmcg_permutation(qmcg_ctx* ctx, int64_t n, uint64_t seed64, uint32_t* out_host);
+/* QuasiStream(dims>dim, n, seed).uniform_at(p, dim) for all p (quasi_rng.cpp:96-101). */
+qmcg_status qmcg_uniforms(qmcg_ctx* ctx, int64_t n, uint64_t seed, int64_t dim, double* out_host);
+/* moro_inv_cnd of the same uniforms (quasi_rng.cpp:103-105), as the pricing kernel computes it. */
+qmcg_status qmcg_normals(qmcg_ctx* ctx, int64_t n, uint64_t seed, int64_t dim, double* out_host);
+/* Per-path t0 values of the foresight sweep (american.cpp:119-124). */
+qmcg_status qmcg_path_values(qmcg_ctx* ctx, const qmcg_option_spec* spec, int64_t m,
+                             int64_t n_paths, uint64_t seed, uint32_t flags, double* out_host);
+
+/* ---- measurement hooks (bench.py) ---- */
+/* Launch the pricing of `spec` reps times on the context stream with the
+ * tables resident, and report the device time of the pricing kernel alone and
+ * of the whole device step (CUDA events on the launching stream), in ms. */
+qmcg_status qmcg_time_device(qmcg_ctx* ctx, const qmcg_option_spec* spec, int64_t m,
+                             int64_t n_paths, uint64_t seed, uint32_t flags, int reps,
+                             double* kernel_ms, double* step_ms, double* out_price_se);
+/* Device time (ms) of rebuilding the permutation tables for dims [0, dims). */
+qmcg_status qmcg_time_perm_build(qmcg_ctx* ctx, int64_t n_paths, uint64_t seed, int64_t dims,
+                                 double* ms);
+/* Number of kernels the last qmcg_price_american* call launched. */
+int64_t qmcg_last_launch_count(qmcg_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* QMCG_H */

@@ -1,0 +1,787 @@
+// Host side of the B200 pricer: context, permutation-table cache, host
+// precompute of the exact per-dimension constants, and the C ABI (qmcg.h).
+//
+// Host arithmetic that feeds bit-exact device results (the radical-inverse
+// scale chains 1/p, (1/p)^k) and the per-call constants (dt, drift, diffusion,
+// discount) is done here in IEEE double with glibc, compiled with
+// -ffp-contract=off, in the reference's operation order.
+#include "qmcg.h"
+#include "qmcg_internal.h"
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <limits>
+#include <mutex>
+#include <string>
+#include <vector>
+
+using qmcg::DimParam;
+using qmcg::PriceParams;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+qmcg_status fail(qmcg_status code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+
+#define QMCG_CUDA(expr)                                                                       \
+  do {                                                                                        \
+    cudaError_t e_ = (expr);                                                                  \
+    if (e_ != cudaSuccess) {                                                                  \
+      if (e_ == cudaErrorMemoryAllocation) {                                                  \
+        cudaGetLastError();                                                                   \
+        return fail(QMCG_OUT_OF_MEMORY, std::string("CUDA out of memory at ") + #expr);       \
+      }                                                                                       \
+      return fail(QMCG_CUDA_ERROR, std::string("CUDA error ") + cudaGetErrorString(e_) +      \
+                                       " at " + #expr);                                       \
+    }                                                                                         \
+  } while (0)
+
+// ---- reference helpers restated for the host precompute ----
+
+// splitmix64 / dimension_seed, reference proj/src/quasi_rng.cpp:16-22,41-46
+uint64_t splitmix64(uint64_t& state) {
+  state += 0x9e3779b97f4a7c15ULL;
+  uint64_t z = state;
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+  return z ^ (z >> 31);
+}
+
+uint64_t dimension_seed(uint64_t master, int64_t dim) {
+  uint64_t state = master;
+  const uint64_t mixed = splitmix64(state);
+  state = mixed ^ (static_cast<uint64_t>(dim) + 0x632be59bd9b4e019ULL);
+  return splitmix64(state);
+}
+
+// first_primes, quasi_rng.cpp:24-37 (extended incrementally)
+const std::vector<uint32_t>& primes_upto_count(int64_t count) {
+  static std::vector<uint32_t> primes;
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lock(mu);
+  uint32_t cand = primes.empty() ? 2 : primes.back() + 1;
+  while (static_cast<int64_t>(primes.size()) < count) {
+    bool is_prime = true;
+    for (uint32_t d = 2; d * d <= cand; ++d)
+      if (cand % d == 0) {
+        is_prime = false;
+        break;
+      }
+    if (is_prime) primes.push_back(cand);
+    ++cand;
+  }
+  return primes;
+}
+
+// validate, reference proj/src/analytic.cpp:18-31
+qmcg_status validate(const qmcg_option_spec& s) {
+  if (!std::isfinite(s.spot) || !std::isfinite(s.strike) || !std::isfinite(s.rate) ||
+      !std::isfinite(s.volatility) || !std::isfinite(s.maturity))
+    return fail(QMCG_INVALID_ARGUMENT, "OptionSpec: all fields must be finite");
+  if (!(s.spot > 0.0)) return fail(QMCG_INVALID_ARGUMENT, "OptionSpec: spot must be > 0");
+  if (!(s.strike > 0.0)) return fail(QMCG_INVALID_ARGUMENT, "OptionSpec: strike must be > 0");
+  if (!(s.volatility >= 0.0)) return fail(QMCG_INVALID_ARGUMENT, "OptionSpec: volatility must be >= 0");
+  if (!(s.maturity >= 0.0)) return fail(QMCG_INVALID_ARGUMENT, "OptionSpec: maturity must be >= 0");
+  if (s.kind != QMCG_CALL && s.kind != QMCG_PUT) return fail(QMCG_INVALID_ARGUMENT, "OptionSpec: unknown kind");
+  return QMCG_OK;
+}
+
+double intrinsic(int kind, double s, double k) {
+  const double diff = kind == QMCG_CALL ? s - k : k - s;
+  return diff > 0.0 ? diff : 0.0;
+}
+
+// Node range of the pairwise tree (reference pairwise_sum splits at n/2).
+void tree_node(int64_t n, int depth, int64_t node, int64_t& off, int64_t& size) {
+  off = 0;
+  size = n;
+  for (int l = depth - 1; l >= 0; --l) {
+    const int64_t half = size / 2;
+    if ((node >> l) & 1) {
+      off += half;
+      size -= half;
+    } else {
+      size = half;
+    }
+  }
+}
+
+// Dimension tables for (n, m): exact digit constants per prime.
+struct DimTables {
+  int64_t n = -1, m = -1;
+  std::vector<DimParam> dims;
+  std::vector<double> sc, nc;
+};
+
+void build_dim_tables(int64_t n, int64_t m, DimTables& T) {
+  const auto& primes = primes_upto_count(m);
+  T.dims.resize(static_cast<size_t>(m));
+  T.sc.clear();
+  T.nc.clear();
+  const uint64_t max_index = static_cast<uint64_t>(n);  // perm + 1 <= n
+  for (int64_t d = 0; d < m; ++d) {
+    const uint32_t p = primes[static_cast<size_t>(d)];
+    DimParam dp{};
+    dp.p = p;
+    // digits: smallest D with p^D > max_index
+    uint32_t D = 1;
+    unsigned __int128 pw = p;
+    while (pw <= max_index) {
+      pw *= p;
+      ++D;
+    }
+    dp.ndig = D;
+    dp.doff = static_cast<uint32_t>(T.sc.size());
+    // scale chain exactly as radical_inverse: scale = 1/b; scale *= 1/b ...
+    const double inv_base = 1.0 / p;
+    double scale = inv_base;
+    for (uint32_t j = 0; j < D; ++j) {
+      T.sc.push_back(scale);
+      T.nc.push_back(-4503599627370496.0 * scale);  // -2^52 * scale, exact
+      scale *= inv_base;
+    }
+    // clamp can only trigger when p^-D approaches kEndpointEps
+    if (T.sc.back() < 2e-12) dp.flags |= qmcg::DIM_CLAMP;
+    // magic division, exact for x <= max_index (< 2^32)
+    uint32_t sh = 0;
+    while ((uint64_t{1} << (sh + 1)) < p) ++sh;  // sh = ceil(log2 p) - 1
+    const unsigned __int128 two = static_cast<unsigned __int128>(1) << (32 + sh);
+    const unsigned __int128 M = (two + p - 1) / p;
+    const unsigned __int128 e = M * p - two;
+    if (M < (static_cast<unsigned __int128>(1) << 32) &&
+        static_cast<unsigned __int128>(max_index) * e < two) {
+      dp.magic = static_cast<uint32_t>(M);
+      dp.shift = sh;
+    } else {
+      dp.flags |= qmcg::DIM_WIDE;
+      const unsigned __int128 two64 = static_cast<unsigned __int128>(1) << 64;
+      dp.magic64 = static_cast<uint64_t>((two64 + p - 1) / p);
+    }
+    T.dims[static_cast<size_t>(d)] = dp;
+  }
+  T.n = n;
+  T.m = m;
+}
+
+template <class T>
+struct DevBuf {
+  T* ptr = nullptr;
+  size_t cap = 0;  // elements
+  cudaError_t reserve(size_t count) {
+    if (count <= cap) return cudaSuccess;
+    if (ptr) cudaFree(ptr);
+    ptr = nullptr;
+    cap = 0;
+    cudaError_t e = cudaMalloc(&ptr, std::max<size_t>(count, 1) * sizeof(T));
+    if (e == cudaSuccess) cap = count;
+    return e;
+  }
+  void release() {
+    if (ptr) cudaFree(ptr);
+    ptr = nullptr;
+    cap = 0;
+  }
+};
+
+}  // namespace
+
+struct qmcg_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  std::mutex mu;
+  // permutation-table cache: rows [0, dims) of columns [col_begin, col_end)
+  uint64_t cache_seed = 0;
+  int64_t cache_n = -1, col_begin = 0, col_end = 0, cache_dims = 0;
+  uint32_t* table = nullptr;
+  size_t table_rows_cap = 0;
+  // host-side dimension constants mirrored on the device
+  DimTables dt;
+  DevBuf<DimParam> d_dims;
+  DevBuf<double> d_sc, d_nc, d_dpow;
+  DevBuf<double> d_values, d_red, d_sums;
+  DevBuf<uint32_t> d_err, d_fullperm;
+  DevBuf<char> d_permscratch;
+  double* h_pinned = nullptr;  // [0..1] sums, [2] err as double bits
+  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  int64_t launches = 0;
+};
+
+namespace {
+
+void drop_cache(qmcg_ctx* c) {
+  if (c->table) cudaFree(c->table);
+  c->table = nullptr;
+  c->table_rows_cap = 0;
+  c->cache_dims = 0;
+  c->cache_n = -1;
+}
+
+qmcg_status ensure_dim_tables(qmcg_ctx* c, int64_t n, int64_t m) {
+  if (c->dt.n == n && c->dt.m >= m) return QMCG_OK;
+  build_dim_tables(n, std::max<int64_t>(m, c->dt.n == n ? c->dt.m : 0), c->dt);
+  QMCG_CUDA(c->d_dims.reserve(c->dt.dims.size()));
+  QMCG_CUDA(c->d_sc.reserve(c->dt.sc.size()));
+  QMCG_CUDA(c->d_nc.reserve(c->dt.nc.size()));
+  QMCG_CUDA(cudaMemcpyAsync(c->d_dims.ptr, c->dt.dims.data(), c->dt.dims.size() * sizeof(DimParam),
+                            cudaMemcpyHostToDevice, c->stream));
+  QMCG_CUDA(cudaMemcpyAsync(c->d_sc.ptr, c->dt.sc.data(), c->dt.sc.size() * sizeof(double),
+                            cudaMemcpyHostToDevice, c->stream));
+  QMCG_CUDA(cudaMemcpyAsync(c->d_nc.ptr, c->dt.nc.data(), c->dt.nc.size() * sizeof(double),
+                            cudaMemcpyHostToDevice, c->stream));
+  QMCG_CUDA(cudaStreamSynchronize(c->stream));
+  return QMCG_OK;
+}
+
+// Build one full permutation (length n) for dimension `dim` into dst (n u32).
+qmcg_status build_perm(qmcg_ctx* c, uint64_t seed64, int64_t n, uint32_t* dst) {
+  const size_t need = qmcg::perm_scratch_bytes(n);
+  QMCG_CUDA(c->d_permscratch.reserve(need));
+  int launches = 0;
+  QMCG_CUDA(qmcg::launch_perm_build(seed64, n, dst, c->d_permscratch.ptr, c->d_permscratch.cap, c->stream,
+                                    &launches));
+  c->launches += launches;
+  return QMCG_OK;
+}
+
+// Make rows [0, m) of the table for (seed, n) over columns [b, e) resident.
+qmcg_status ensure_perms(qmcg_ctx* c, uint64_t seed, int64_t n, int64_t b, int64_t e, int64_t m, bool rebuild) {
+  if (c->cache_n != n || c->cache_seed != seed || c->col_begin != b || c->col_end != e || rebuild) drop_cache(c);
+  if (c->cache_n == n && c->cache_dims >= m) return QMCG_OK;
+  const int64_t cols = e - b;
+  const size_t row_bytes = static_cast<size_t>(cols) * sizeof(uint32_t);
+  if (static_cast<size_t>(m) > c->table_rows_cap) {
+    uint32_t* nt = nullptr;
+    cudaError_t err = cudaMalloc(&nt, row_bytes * static_cast<size_t>(m));
+    if (err != cudaSuccess) {
+      cudaGetLastError();
+      char msg[256];
+      std::snprintf(msg, sizeof msg,
+                    "price_american: permutation tables of %lld dates x %lld paths (%.3g bytes) do not fit "
+                    "in device memory",
+                    static_cast<long long>(m), static_cast<long long>(cols),
+                    static_cast<double>(row_bytes) * static_cast<double>(m));
+      return fail(QMCG_OUT_OF_MEMORY, msg);
+    }
+    if (c->table && c->cache_dims > 0)
+      QMCG_CUDA(cudaMemcpyAsync(nt, c->table, row_bytes * static_cast<size_t>(c->cache_dims),
+                                cudaMemcpyDeviceToDevice, c->stream));
+    QMCG_CUDA(cudaStreamSynchronize(c->stream));
+    if (c->table) cudaFree(c->table);
+    c->table = nt;
+    c->table_rows_cap = static_cast<size_t>(m);
+  }
+  c->cache_n = n;
+  c->cache_seed = seed;
+  c->col_begin = b;
+  c->col_end = e;
+  const bool full = (b == 0 && e == n);
+  if (!full) QMCG_CUDA(c->d_fullperm.reserve(static_cast<size_t>(n)));
+  for (int64_t d = c->cache_dims; d < m; ++d) {
+    uint32_t* row = c->table + static_cast<size_t>(d) * static_cast<size_t>(cols);
+    qmcg_status st = build_perm(c, dimension_seed(seed, d), n, full ? row : c->d_fullperm.ptr);
+    if (st) return st;
+    if (!full)
+      QMCG_CUDA(cudaMemcpyAsync(row, c->d_fullperm.ptr + b, row_bytes, cudaMemcpyDeviceToDevice, c->stream));
+    c->cache_dims = d + 1;
+  }
+  return QMCG_OK;
+}
+
+struct CallPlan {
+  PriceParams P{};
+  std::vector<double> dpow;
+};
+
+// Validation + host constants, in the order of reference price_american
+// (american.cpp:103-116) -> make_schedule (path_engine.cpp:63-76) ->
+// simulate_batch (path_engine.cpp:124-136) -> QuasiStream (quasi_rng.cpp:85-94).
+qmcg_status plan_call(const qmcg_option_spec& s, int64_t m, int64_t n, uint32_t flags, CallPlan& plan) {
+  qmcg_status st = validate(s);
+  if (st) return st;
+  if (s.kind != QMCG_CALL && !(flags & QMCG_FLAG_ALLOW_PUT))
+    return fail(QMCG_INVALID_ARGUMENT,
+                "price_american: not implemented for puts; the foresight algorithm is call-only");
+  if (n < 2) return fail(QMCG_INVALID_ARGUMENT, "price_american: n_paths must be >= 2");
+  if (m < 1) return fail(QMCG_INVALID_ARGUMENT, "make_schedule: m must be >= 1");
+  if (!(s.maturity > 0.0)) return fail(QMCG_INVALID_ARGUMENT, "make_schedule: maturity must be > 0");
+  if (static_cast<uint64_t>(n) > 0xffffffffULL)
+    return fail(QMCG_LENGTH_ERROR, "permutation_indices: n exceeds the 2^32-1 supported maximum");
+  if (m > (int64_t{1} << 26)) return fail(QMCG_LENGTH_ERROR, "price_american: m exceeds the 2^26 supported maximum");
+
+  const double dt = s.maturity / static_cast<double>(m + 1);  // make_schedule
+  const double r = s.rate, v = s.volatility;
+  const double a = (r - 0.5 * v * v) * dt;  // gbm_step drift
+  const double bdiff = v * std::sqrt(dt);   // gbm_step diffusion
+  const double disc = std::exp(-s.rate * dt);  // sweep_impl
+  PriceParams& P = plan.P;
+  P.m = static_cast<int32_t>(m);
+  P.kind = s.kind;
+  P.X0 = std::log(s.spot);
+  P.strike = s.strike;
+  P.log_strike = std::log(s.strike);
+  P.best0 = intrinsic(s.kind, s.spot, s.strike);
+  P.deterministic = bdiff == 0.0;
+  if (P.deterministic) {
+    P.b = 1.0;
+    P.alpha = a;
+  } else {
+    P.b = bdiff;
+    P.alpha = a / bdiff;
+  }
+  plan.dpow.resize(static_cast<size_t>(m) + 1);
+  plan.dpow[0] = 1.0;
+  for (int64_t k = 1; k <= m; ++k) plan.dpow[static_cast<size_t>(k)] = plan.dpow[static_cast<size_t>(k - 1)] * disc;
+  P.rate_negative = disc > 1.0;
+  if (!P.rate_negative) {
+    const double edge = s.kind == QMCG_CALL ? std::max(s.strike, s.spot) : std::min(s.strike, s.spot);
+    P.c0 = (std::log(edge) - P.X0) / P.b;
+    P.dmax_inv = 1.0;
+  } else {
+    const double dmax = plan.dpow[static_cast<size_t>(m)];
+    P.dmax_inv = 1.0 / dmax;
+    const double lim = P.best0 * P.dmax_inv;
+    if (s.kind == QMCG_CALL) P.c0 = (std::log(s.strike + lim) - P.X0) / P.b;
+    else P.c0 = s.strike - lim > 0.0 ? (std::log(s.strike - lim) - P.X0) / P.b : -INFINITY;
+  }
+  // final interval Black-Scholes (bs_price, analytic.cpp:102-124, with t = dt)
+  P.bs_v_zero = v == 0.0;
+  P.bs_vsqrt = v * std::sqrt(dt);
+  P.bs_mu_t = (r + 0.5 * v * v) * dt;
+  P.bs_kdisc = s.strike * std::exp(-r * dt);
+  P.bs_fwd_growth = std::exp(r * dt);
+  P.bs_disc = std::exp(-r * dt);
+  // overflow / underflow of the log-price walk is impossible when
+  // |X0| + m (|a| + b |z|max) stays inside exp's range (|z| <= 7.04 for u in [1e-12, 1-1e-12])
+  const double reach = std::fabs(P.X0) + static_cast<double>(m) * (std::fabs(a) + bdiff * 7.05) + 1.0;
+  P.check_range = reach > 700.0;
+  return QMCG_OK;
+}
+
+qmcg_status upload_plan(qmcg_ctx* c, CallPlan& plan, int64_t n) {
+  const int64_t m = plan.P.m;
+  qmcg_status st = ensure_dim_tables(c, n, m);
+  if (st) return st;
+  QMCG_CUDA(c->d_dpow.reserve(plan.dpow.size()));
+  QMCG_CUDA(cudaMemcpyAsync(c->d_dpow.ptr, plan.dpow.data(), plan.dpow.size() * sizeof(double),
+                            cudaMemcpyHostToDevice, c->stream));
+  plan.P.dims = c->d_dims.ptr;
+  plan.P.sc = c->d_sc.ptr;
+  plan.P.nc = c->d_nc.ptr;
+  plan.P.dpow = c->d_dpow.ptr;
+  return QMCG_OK;
+}
+
+qmcg_status map_err(uint32_t err) {
+  if (err & qmcg::ERR_SPOT_NONPOSITIVE) return fail(QMCG_INVALID_ARGUMENT, "gbm_step: s_prev must be > 0");
+  if (err & qmcg::ERR_SPOT_NONFINITE) return fail(QMCG_INVALID_ARGUMENT, "OptionSpec: all fields must be finite");
+  return QMCG_OK;
+}
+
+// Enqueue pricing of paths [b, e) and the pairwise reduction of that range
+// into d_sums[slot*2 .. slot*2+1]. Tables must be resident.
+qmcg_status enqueue_price(qmcg_ctx* c, CallPlan& plan, int64_t b, int64_t e, int slot, cudaEvent_t after_kernel) {
+  const int64_t cnt = e - b;
+  QMCG_CUDA(c->d_values.reserve(static_cast<size_t>(cnt)));
+  QMCG_CUDA(c->d_red.reserve(qmcg::reduce_scratch_doubles(cnt)));
+  PriceParams P = plan.P;
+  P.perm = c->table;
+  P.ld = c->col_end - c->col_begin;
+  P.col_begin = c->col_begin;
+  P.path_begin = b;
+  P.path_count = cnt;
+  P.values = c->d_values.ptr;
+  P.err = c->d_err.ptr;
+  QMCG_CUDA(qmcg::launch_price(P, c->stream));
+  c->launches += 1;
+  if (after_kernel) QMCG_CUDA(cudaEventRecord(after_kernel, c->stream));
+  int launches = 0;
+  QMCG_CUDA(qmcg::launch_pairwise(c->d_values.ptr, cnt, c->d_red.ptr, c->d_sums.ptr + 2 * slot, c->stream,
+                                  &launches));
+  c->launches += launches;
+  return QMCG_OK;
+}
+
+qmcg_status prepare_scratch(qmcg_ctx* c, size_t slots) {
+  QMCG_CUDA(c->d_sums.reserve(2 * slots));
+  QMCG_CUDA(c->d_err.reserve(1));
+  QMCG_CUDA(cudaMemsetAsync(c->d_err.ptr, 0, sizeof(uint32_t), c->stream));
+  return QMCG_OK;
+}
+
+// reduce_stats' arithmetic (path_engine.cpp:191-205) on the tree sums.
+void finish_stats(int64_t n, double sum, double sum_sq, double& mean, double& se) {
+  mean = sum / static_cast<double>(n);
+  se = 0.0;
+  if (n >= 2) {
+    double var = (sum_sq - static_cast<double>(n) * mean * mean) / static_cast<double>(n - 1);
+    if (var < 0.0) var = 0.0;
+    se = std::sqrt(var / static_cast<double>(n));
+  }
+}
+
+qmcg_status sync_results(qmcg_ctx* c, size_t slots, std::vector<double>& sums) {
+  sums.resize(2 * slots);
+  uint32_t err = 0;
+  QMCG_CUDA(cudaMemcpyAsync(sums.data(), c->d_sums.ptr, 2 * slots * sizeof(double), cudaMemcpyDeviceToHost,
+                            c->stream));
+  QMCG_CUDA(cudaMemcpyAsync(&err, c->d_err.ptr, sizeof(uint32_t), cudaMemcpyDeviceToHost, c->stream));
+  QMCG_CUDA(cudaStreamSynchronize(c->stream));
+  return map_err(err);
+}
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+}  // namespace
+
+extern "C" {
+
+const char* qmcg_last_error(void) { return g_last_error.c_str(); }
+const char* qmcg_version(void) { return "qmcg 0.1 (sm_100a)"; }
+
+qmcg_status qmcg_create(int device, qmcg_ctx** out) {
+  if (!out) return fail(QMCG_INVALID_ARGUMENT, "qmcg_create: out must not be null");
+  int count = 0;
+  QMCG_CUDA(cudaGetDeviceCount(&count));
+  if (device < 0 || device >= count) return fail(QMCG_INVALID_ARGUMENT, "qmcg_create: no such CUDA device");
+  DeviceGuard g(device);
+  auto* c = new qmcg_ctx();
+  c->device = device;
+  cudaError_t e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaMallocHost(&c->h_pinned, 16 * sizeof(double));
+  for (auto& ev : c->ev)
+    if (e == cudaSuccess) e = cudaEventCreate(&ev);
+  if (e != cudaSuccess) {
+    delete c;
+    return fail(QMCG_CUDA_ERROR, std::string("qmcg_create: ") + cudaGetErrorString(e));
+  }
+  *out = c;
+  return QMCG_OK;
+}
+
+void qmcg_destroy(qmcg_ctx* c) {
+  if (!c) return;
+  DeviceGuard g(c->device);
+  cudaStreamSynchronize(c->stream);
+  drop_cache(c);
+  c->d_dims.release();
+  c->d_sc.release();
+  c->d_nc.release();
+  c->d_dpow.release();
+  c->d_values.release();
+  c->d_red.release();
+  c->d_sums.release();
+  c->d_err.release();
+  c->d_fullperm.release();
+  c->d_permscratch.release();
+  if (c->h_pinned) cudaFreeHost(c->h_pinned);
+  for (auto& ev : c->ev)
+    if (ev) cudaEventDestroy(ev);
+  cudaStreamDestroy(c->stream);
+  delete c;
+}
+
+qmcg_status qmcg_tree_node_range(int64_t n, int depth, int64_t node, int64_t* begin, int64_t* end) {
+  if (n < 1 || depth < 0 || depth > 40 || node < 0 || node >= (int64_t{1} << depth))
+    return fail(QMCG_INVALID_ARGUMENT, "qmcg_tree_node_range: bad node");
+  int64_t off, size;
+  tree_node(n, depth, node, off, size);
+  *begin = off;
+  *end = off + size;
+  return QMCG_OK;
+}
+
+// Fold node sums up the reference tree. A node of size <= 64 is a sequential
+// leaf in the reference; such nodes must not be split, so depth is limited to
+// levels whose parents all exceed 64 elements.
+qmcg_status qmcg_combine_nodes(int64_t n, int depth, const double* node_sums, double* price, double* se) {
+  if (n < 1 || depth < 0 || depth > 30) return fail(QMCG_INVALID_ARGUMENT, "qmcg_combine_nodes: bad depth");
+  std::vector<double> s(node_sums, node_sums + 2 * (size_t{1} << depth));
+  for (int d = depth; d > 0; --d) {
+    const size_t cnt = size_t{1} << (d - 1);
+    for (size_t i = 0; i < cnt; ++i) {
+      s[2 * i] = s[4 * i] + s[4 * i + 2];
+      s[2 * i + 1] = s[4 * i + 1] + s[4 * i + 3];
+    }
+  }
+  double mean, err;
+  finish_stats(n, s[0], s[1], mean, err);
+  *price = mean;
+  *se = err;
+  return QMCG_OK;
+}
+
+qmcg_status qmcg_warm(qmcg_ctx* c, int64_t n, uint64_t seed, int64_t dims) {
+  if (!c) return fail(QMCG_INVALID_ARGUMENT, "qmcg_warm: null context");
+  std::lock_guard<std::mutex> lock(c->mu);
+  DeviceGuard g(c->device);
+  if (n < 1 || static_cast<uint64_t>(n) > 0xffffffffULL || dims < 1)
+    return fail(QMCG_INVALID_ARGUMENT, "qmcg_warm: bad size");
+  qmcg_status st = ensure_perms(c, seed, n, 0, n, dims, false);
+  if (st) return st;
+  QMCG_CUDA(cudaStreamSynchronize(c->stream));
+  return QMCG_OK;
+}
+
+qmcg_status qmcg_clear_cache(qmcg_ctx* c) {
+  if (!c) return fail(QMCG_INVALID_ARGUMENT, "qmcg_clear_cache: null context");
+  std::lock_guard<std::mutex> lock(c->mu);
+  DeviceGuard g(c->device);
+  cudaStreamSynchronize(c->stream);
+  drop_cache(c);
+  return QMCG_OK;
+}
+
+static qmcg_status price_range(qmcg_ctx* c, const qmcg_option_spec* spec, int64_t m, int64_t n, uint64_t seed,
+                               uint32_t flags, int64_t b, int64_t e, double sums[2]) {
+  CallPlan plan;
+  qmcg_status st = plan_call(*spec, m, n, flags, plan);
+  if (st) return st;
+  st = upload_plan(c, plan, n);
+  if (st) return st;
+  st = ensure_perms(c, seed, n, b, e, m, (flags & QMCG_FLAG_NO_CACHE) != 0);
+  if (st) return st;
+  st = prepare_scratch(c, 1);
+  if (st) return st;
+  st = enqueue_price(c, plan, b, e, 0, nullptr);
+  if (st) return st;
+  std::vector<double> out;
+  st = sync_results(c, 1, out);
+  if (st) return st;
+  sums[0] = out[0];
+  sums[1] = out[1];
+  return QMCG_OK;
+}
+
+qmcg_status qmcg_price_american(qmcg_ctx* c, const qmcg_option_spec* spec, int64_t m, int64_t n, uint64_t seed,
+                                uint32_t flags, qmcg_pricing_result* out) {
+  if (!c || !spec || !out) return fail(QMCG_INVALID_ARGUMENT, "qmcg_price_american: null argument");
+  const auto t0 = std::chrono::steady_clock::now();
+  std::lock_guard<std::mutex> lock(c->mu);
+  DeviceGuard g(c->device);
+  c->launches = 0;
+  double sums[2];
+  qmcg_status st = price_range(c, spec, m, n, seed, flags, 0, n, sums);
+  if (st) return st;
+  double mean, se;
+  finish_stats(n, sums[0], sums[1], mean, se);
+  out->price = mean;
+  out->std_error = se;
+  out->n_paths = n;
+  out->method = QMCG_METHOD_AMERICAN_UB;
+  out->seed = seed;
+  out->elapsed_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  return QMCG_OK;
+}
+
+qmcg_status qmcg_price_american_node(qmcg_ctx* c, const qmcg_option_spec* spec, int64_t m, int64_t n,
+                                     uint64_t seed, uint32_t flags, int depth, int64_t node, double out_sums[2]) {
+  if (!c || !spec || !out_sums) return fail(QMCG_INVALID_ARGUMENT, "qmcg_price_american_node: null argument");
+  std::lock_guard<std::mutex> lock(c->mu);
+  DeviceGuard g(c->device);
+  c->launches = 0;
+  if (depth < 0 || depth > 30 || node < 0 || node >= (int64_t{1} << depth))
+    return fail(QMCG_INVALID_ARGUMENT, "qmcg_price_american_node: bad node");
+  int64_t off, size;
+  tree_node(n, depth, node, off, size);
+  // every ancestor of the node must be an internal (split) node of the reference tree
+  {
+    int64_t aoff, asize;
+    for (int d = 0; d < depth; ++d) {
+      tree_node(n, d, node >> (depth - d), aoff, asize);
+      if (asize <= 64) return fail(QMCG_INVALID_ARGUMENT, "qmcg_price_american_node: node below a leaf of the tree");
+    }
+  }
+  return price_range(c, spec, m, n, seed, flags, off, off + size, out_sums);
+}
+
+qmcg_status qmcg_price_american_batch(qmcg_ctx* c, const qmcg_option_spec* specs, int64_t n_specs, int64_t m,
+                                      int64_t n, uint64_t seed, uint32_t flags, qmcg_pricing_result* out) {
+  if (!c || !specs || !out || n_specs < 0) return fail(QMCG_INVALID_ARGUMENT, "qmcg_price_american_batch: bad argument");
+  const auto t0 = std::chrono::steady_clock::now();
+  std::lock_guard<std::mutex> lock(c->mu);
+  DeviceGuard g(c->device);
+  c->launches = 0;
+  if (n_specs == 0) return QMCG_OK;
+  std::vector<CallPlan> plans(static_cast<size_t>(n_specs));
+  for (int64_t i = 0; i < n_specs; ++i) {
+    qmcg_status st = plan_call(specs[i], m, n, flags, plans[static_cast<size_t>(i)]);
+    if (st) return st;
+  }
+  qmcg_status st = ensure_dim_tables(c, n, m);
+  if (st) return st;
+  st = ensure_perms(c, seed, n, 0, n, m, (flags & QMCG_FLAG_NO_CACHE) != 0);
+  if (st) return st;
+  st = prepare_scratch(c, static_cast<size_t>(n_specs));
+  if (st) return st;
+  // all contracts share m -> one dpow upload per contract (cheap), launched back to back
+  QMCG_CUDA(c->d_dpow.reserve(static_cast<size_t>(m + 1) * static_cast<size_t>(n_specs)));
+  for (int64_t i = 0; i < n_specs; ++i) {
+    CallPlan& plan = plans[static_cast<size_t>(i)];
+    double* dp = c->d_dpow.ptr + static_cast<size_t>(i) * static_cast<size_t>(m + 1);
+    QMCG_CUDA(cudaMemcpyAsync(dp, plan.dpow.data(), plan.dpow.size() * sizeof(double), cudaMemcpyHostToDevice,
+                              c->stream));
+    plan.P.dims = c->d_dims.ptr;
+    plan.P.sc = c->d_sc.ptr;
+    plan.P.nc = c->d_nc.ptr;
+    plan.P.dpow = dp;
+    st = enqueue_price(c, plan, 0, n, static_cast<int>(i), nullptr);
+    if (st) return st;
+  }
+  std::vector<double> sums;
+  st = sync_results(c, static_cast<size_t>(n_specs), sums);
+  if (st) return st;
+  const double el = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  for (int64_t i = 0; i < n_specs; ++i) {
+    double mean, se;
+    finish_stats(n, sums[2 * static_cast<size_t>(i)], sums[2 * static_cast<size_t>(i) + 1], mean, se);
+    out[i].price = mean;
+    out[i].std_error = se;
+    out[i].n_paths = n;
+    out[i].method = QMCG_METHOD_AMERICAN_UB;
+    out[i].seed = seed;
+    out[i].elapsed_s = el;
+  }
+  return QMCG_OK;
+}
+
+qmcg_status qmcg_permutation(qmcg_ctx* c, int64_t n, uint64_t seed64, uint32_t* out_host) {
+  if (!c || !out_host) return fail(QMCG_INVALID_ARGUMENT, "qmcg_permutation: null argument");
+  if (n < 1) return fail(QMCG_INVALID_ARGUMENT, "permutation_indices: n must be >= 1");
+  if (static_cast<uint64_t>(n) > 0xffffffffULL)
+    return fail(QMCG_LENGTH_ERROR, "permutation_indices: n exceeds the 2^32-1 supported maximum");
+  std::lock_guard<std::mutex> lock(c->mu);
+  DeviceGuard g(c->device);
+  QMCG_CUDA(c->d_fullperm.reserve(static_cast<size_t>(n)));
+  qmcg_status st = build_perm(c, seed64, n, c->d_fullperm.ptr);
+  if (st) return st;
+  QMCG_CUDA(cudaMemcpyAsync(out_host, c->d_fullperm.ptr, static_cast<size_t>(n) * sizeof(uint32_t),
+                            cudaMemcpyDeviceToHost, c->stream));
+  QMCG_CUDA(cudaStreamSynchronize(c->stream));
+  return QMCG_OK;
+}
+
+static qmcg_status export_dim(qmcg_ctx* c, int64_t n, uint64_t seed, int64_t dim, int normals, double* out_host) {
+  if (!c || !out_host) return fail(QMCG_INVALID_ARGUMENT, "qmcg_uniforms: null argument");
+  if (n < 1) return fail(QMCG_INVALID_ARGUMENT, "QuasiStream: length must be >= 1");
+  if (dim < 0) return fail(QMCG_INVALID_ARGUMENT, "QuasiStream: dimensions must be >= 1");
+  if (static_cast<uint64_t>(n) > 0xffffffffULL)
+    return fail(QMCG_LENGTH_ERROR, "permutation_indices: n exceeds the 2^32-1 supported maximum");
+  std::lock_guard<std::mutex> lock(c->mu);
+  DeviceGuard g(c->device);
+  qmcg_status st = ensure_dim_tables(c, n, dim + 1);
+  if (st) return st;
+  QMCG_CUDA(c->d_fullperm.reserve(static_cast<size_t>(n)));
+  st = build_perm(c, dimension_seed(seed, dim), n, c->d_fullperm.ptr);
+  if (st) return st;
+  QMCG_CUDA(c->d_values.reserve(static_cast<size_t>(n)));
+  QMCG_CUDA(qmcg::launch_uniforms(c->d_fullperm.ptr, n, c->dt.dims[static_cast<size_t>(dim)], c->d_sc.ptr,
+                                  c->d_nc.ptr, normals, c->d_values.ptr, c->stream));
+  QMCG_CUDA(cudaMemcpyAsync(out_host, c->d_values.ptr, static_cast<size_t>(n) * sizeof(double),
+                            cudaMemcpyDeviceToHost, c->stream));
+  QMCG_CUDA(cudaStreamSynchronize(c->stream));
+  return QMCG_OK;
+}
+
+qmcg_status qmcg_uniforms(qmcg_ctx* c, int64_t n, uint64_t seed, int64_t dim, double* out_host) {
+  return export_dim(c, n, seed, dim, 0, out_host);
+}
+
+qmcg_status qmcg_normals(qmcg_ctx* c, int64_t n, uint64_t seed, int64_t dim, double* out_host) {
+  return export_dim(c, n, seed, dim, 1, out_host);
+}
+
+qmcg_status qmcg_path_values(qmcg_ctx* c, const qmcg_option_spec* spec, int64_t m, int64_t n, uint64_t seed,
+                             uint32_t flags, double* out_host) {
+  if (!c || !spec || !out_host) return fail(QMCG_INVALID_ARGUMENT, "qmcg_path_values: null argument");
+  std::lock_guard<std::mutex> lock(c->mu);
+  DeviceGuard g(c->device);
+  double sums[2];
+  qmcg_status st = price_range(c, spec, m, n, seed, flags, 0, n, sums);
+  if (st) return st;
+  QMCG_CUDA(cudaMemcpyAsync(out_host, c->d_values.ptr, static_cast<size_t>(n) * sizeof(double),
+                            cudaMemcpyDeviceToHost, c->stream));
+  QMCG_CUDA(cudaStreamSynchronize(c->stream));
+  return QMCG_OK;
+}
+
+qmcg_status qmcg_time_device(qmcg_ctx* c, const qmcg_option_spec* spec, int64_t m, int64_t n, uint64_t seed,
+                             uint32_t flags, int reps, double* kernel_ms, double* step_ms, double* out_price_se) {
+  if (!c || !spec || reps < 1) return fail(QMCG_INVALID_ARGUMENT, "qmcg_time_device: bad argument");
+  std::lock_guard<std::mutex> lock(c->mu);
+  DeviceGuard g(c->device);
+  CallPlan plan;
+  qmcg_status st = plan_call(*spec, m, n, flags, plan);
+  if (st) return st;
+  st = upload_plan(c, plan, n);
+  if (st) return st;
+  st = ensure_perms(c, seed, n, 0, n, m, false);
+  if (st) return st;
+  st = prepare_scratch(c, 1);
+  if (st) return st;
+  QMCG_CUDA(cudaStreamSynchronize(c->stream));
+  c->launches = 0;
+  double kms = 0.0;
+  QMCG_CUDA(cudaEventRecord(c->ev[2], c->stream));
+  for (int r = 0; r < reps; ++r) {
+    QMCG_CUDA(cudaEventRecord(c->ev[0], c->stream));
+    st = enqueue_price(c, plan, 0, n, 0, c->ev[1]);
+    if (st) return st;
+    QMCG_CUDA(cudaEventSynchronize(c->ev[1]));
+    float ms = 0.f;
+    QMCG_CUDA(cudaEventElapsedTime(&ms, c->ev[0], c->ev[1]));
+    kms += ms;
+  }
+  QMCG_CUDA(cudaEventRecord(c->ev[3], c->stream));
+  std::vector<double> sums;
+  st = sync_results(c, 1, sums);
+  if (st) return st;
+  float total = 0.f;
+  QMCG_CUDA(cudaEventElapsedTime(&total, c->ev[2], c->ev[3]));
+  if (kernel_ms) *kernel_ms = kms / reps;
+  if (step_ms) *step_ms = static_cast<double>(total) / reps;
+  if (out_price_se) finish_stats(n, sums[0], sums[1], out_price_se[0], out_price_se[1]);
+  return QMCG_OK;
+}
+
+qmcg_status qmcg_time_perm_build(qmcg_ctx* c, int64_t n, uint64_t seed, int64_t dims, double* ms) {
+  if (!c || !ms) return fail(QMCG_INVALID_ARGUMENT, "qmcg_time_perm_build: bad argument");
+  std::lock_guard<std::mutex> lock(c->mu);
+  DeviceGuard g(c->device);
+  // make the table resident and allocated, then invalidate its rows so only
+  // the rebuild (K1 for every dimension) is timed
+  qmcg_status st = ensure_perms(c, seed, n, 0, n, dims, false);
+  if (st) return st;
+  QMCG_CUDA(cudaStreamSynchronize(c->stream));
+  c->cache_dims = 0;
+  QMCG_CUDA(cudaEventRecord(c->ev[0], c->stream));
+  st = ensure_perms(c, seed, n, 0, n, dims, false);
+  if (st) return st;
+  QMCG_CUDA(cudaEventRecord(c->ev[1], c->stream));
+  QMCG_CUDA(cudaEventSynchronize(c->ev[1]));
+  float f = 0.f;
+  QMCG_CUDA(cudaEventElapsedTime(&f, c->ev[0], c->ev[1]));
+  *ms = f;
+  return QMCG_OK;
+}
+
+int64_t qmcg_last_launch_count(qmcg_ctx* c) { return c ? c->launches : 0; }
+
+}  // extern "C"

@@ -1,0 +1,80 @@
+// Shared host/device declarations of the B200 pricer (not part of the public ABI).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace qmcg {
+
+// Per-dimension (= per exercise date) constants for the scrambled Halton
+// radical inverse (reference radical_inverse, proj/src/quasi_rng.cpp:71-83).
+// Dimension d uses the d-th prime p; the index x = perm_d[path] + 1 has
+// `ndig` base-p digits at most. Digit j contributes fl(digit * sc[j]) where
+// sc[j] is the reference's rounded scale chain (1/p, fl(1/p * 1/p), ...), and
+// fl(digit * sc[j]) is produced by one DFMA: fma(2^52 + digit, sc[j], nc[j])
+// with nc[j] = -2^52 * sc[j] (exact: the FMA rounds d*sc[j] exactly once).
+struct DimParam {
+  uint32_t p;        // prime base
+  uint32_t magic;    // q = umulhi(x, magic) >> shift == x / p for x <= n
+  uint32_t shift;
+  uint32_t ndig;     // digits to process (fixed count; high zero digits add +0.0)
+  uint32_t doff;     // offset of this dimension's sc/nc entries
+  uint32_t flags;    // DIM_CLAMP: endpoint clamp can trigger; DIM_WIDE: 64-bit magic
+  uint64_t magic64;  // ceil(2^64 / p) for DIM_WIDE
+};
+enum : uint32_t { DIM_CLAMP = 1u, DIM_WIDE = 2u };
+
+// Error bits raised by the pricing kernel (mapped to the reference's
+// exception text on the host).
+enum : uint32_t { ERR_SPOT_NONPOSITIVE = 1u, ERR_SPOT_NONFINITE = 2u };
+
+struct PriceParams {
+  const uint32_t* perm;  // [m][ld] permutation table slice (column = path - col_begin)
+  int64_t ld;            // row stride of the table
+  int64_t col_begin;     // first path held by the table
+  int64_t path_begin;    // first path of this launch
+  int64_t path_count;    // paths in this launch
+  int32_t m;             // exercise dates (dims used: 0..m-1)
+  int32_t kind;          // 0 call, 1 put
+  const DimParam* dims;
+  const double* sc;
+  const double* nc;
+  const double* dpow;    // dpow[k] = disc^k as the host's rounded chain, k = 0..m
+  double X0;             // log(spot)
+  double b;              // log-price scale: X_k = X0 + b * V_k
+  double alpha;          // V_k = sum_{j<=k} (z_j + alpha)
+  double c0;             // initial candidate threshold in V units
+  double strike;
+  double best0;          // intrinsic value at t0 (date 0 term)
+  double log_strike;
+  double dmax_inv;       // 1 / max_k disc^k  (only for rate < 0)
+  // Black-Scholes of the last interval (reference sweep_impl, american.cpp:45-52)
+  double bs_vsqrt;       // v*sqrt(dt)
+  double bs_mu_t;        // (r + 0.5*v*v)*dt
+  double bs_kdisc;       // K * exp(-r*dt)
+  double bs_fwd_growth;  // exp(r*dt)            (v == 0 branch)
+  double bs_disc;        // exp(-r*dt)           (v == 0 branch)
+  int32_t bs_v_zero;
+  int32_t deterministic; // volatility == 0: z never affects the path
+  int32_t check_range;   // per-date overflow/underflow checks needed
+  int32_t rate_negative; // disc > 1: running-max filter invalid, use best-based filter
+  double* values;        // per-path t0 values, index = path - path_begin
+  uint32_t* err;
+};
+
+// ---- launchers (kernels.cu) ----
+cudaError_t launch_price(const PriceParams& P, cudaStream_t s);
+// K1: Fisher-Yates permutation of length n for LCG seed `seed64` into out[0..n).
+// scratch must hold perm_scratch_bytes(n) bytes.
+size_t perm_scratch_bytes(int64_t n);
+cudaError_t launch_perm_build(uint64_t seed64, int64_t n, uint32_t* out, void* scratch,
+                              size_t scratch_bytes, cudaStream_t s, int* launches);
+// Copy columns [c0, c1) of a freshly built permutation into a table row.
+cudaError_t launch_uniforms(const uint32_t* perm_row, int64_t count, DimParam dp, const double* sc,
+                            const double* nc, int normals, double* out, cudaStream_t s);
+// Pairwise-tree sums of v and v*v over `len` values (reference pairwise_sum
+// with 64-element leaves). out2[0] = sum, out2[1] = sum of squares.
+size_t reduce_scratch_doubles(int64_t len);
+cudaError_t launch_pairwise(const double* v, int64_t len, double* scratch, double* out2,
+                            cudaStream_t s, int* launches);
+
+}  // namespace qmcg

@@ -1,0 +1,302 @@
+"""ctypes binding of the C ABI in include/qmcg.h (libqmcg.so, built in-tree).
+
+This is the Python face of the reference's pricing API (reference
+proj/include/qmc/american.hpp:43-55, types.hpp:16-49): ``OptionSpec``,
+``PricingResult``, ``ExecPolicy`` and ``price_american`` keep the reference's
+names, argument meaning and error behaviour -- ``ValueError`` where the
+reference throws ``std::invalid_argument``, ``OverflowError`` for
+``std::length_error``, ``RuntimeError`` for device failures.
+
+There is no CPU fallback: importing this module on a machine without the
+built library raises, and every call runs the CUDA kernels.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import dataclasses
+import enum
+import os
+import threading
+from typing import Optional, Sequence
+
+import numpy as np
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libqmcg.so")
+
+OK, INVALID_ARGUMENT, LENGTH_ERROR, CUDA_ERROR, NCCL_ERROR, UNSUPPORTED, OUT_OF_MEMORY = range(7)
+FLAG_ALLOW_PUT = 1
+FLAG_NO_CACHE = 2
+
+# every symbol include/qmcg.h declares (checked by tests/test_abi.py)
+EXPORTS = (
+    "qmcg_create", "qmcg_destroy", "qmcg_last_error", "qmcg_version", "qmcg_price_american",
+    "qmcg_price_american_batch", "qmcg_price_american_node", "qmcg_tree_node_range",
+    "qmcg_combine_nodes", "qmcg_warm", "qmcg_clear_cache", "qmcg_permutation", "qmcg_uniforms",
+    "qmcg_normals", "qmcg_path_values", "qmcg_time_device", "qmcg_time_perm_build",
+    "qmcg_last_launch_count",
+)
+
+
+class OptionKind(enum.IntEnum):
+    Call = 0
+    Put = 1
+
+
+class Method(enum.IntEnum):
+    ClosedForm = 0
+    EuropeanMC = 1
+    AmericanUpperBound = 2
+
+
+@dataclasses.dataclass
+class OptionSpec:
+    """reference OptionSpec (proj/include/qmc/types.hpp:24-31)."""
+    spot: float = 100.0
+    strike: float = 100.0
+    rate: float = 0.0
+    volatility: float = 0.0
+    maturity: float = 0.0
+    kind: OptionKind = OptionKind.Call
+
+
+@dataclasses.dataclass
+class PricingResult:
+    """reference PricingResult (proj/include/qmc/types.hpp:42-49)."""
+    price: float = 0.0
+    std_error: float = 0.0
+    n_paths: int = 0
+    elapsed_s: float = 0.0
+    method: Method = Method.ClosedForm
+    seed: int = 0
+
+
+@dataclasses.dataclass
+class ExecPolicy:
+    """reference ExecPolicy (proj/include/qmc/path_engine.hpp:36-39); never changes results."""
+    lanes: int = 1
+    chunk: int = 4096
+
+
+class _CSpec(C.Structure):
+    _fields_ = [("spot", C.c_double), ("strike", C.c_double), ("rate", C.c_double),
+                ("volatility", C.c_double), ("maturity", C.c_double), ("kind", C.c_int32)]
+
+
+class _CResult(C.Structure):
+    _fields_ = [("price", C.c_double), ("std_error", C.c_double), ("n_paths", C.c_int64),
+                ("elapsed_s", C.c_double), ("method", C.c_int32), ("seed", C.c_uint64)]
+
+
+_lib = None
+_lib_lock = threading.Lock()
+
+
+def load_library(path: str = LIB_PATH) -> C.CDLL:
+    """Load libqmcg.so; raises if it has not been built (no fallback exists)."""
+    global _lib
+    with _lib_lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(path):
+            raise ImportError(f"{path} is missing: run `python -m paper_1205_0106_b200.build` "
+                              "(or __graft_entry__.build()); there is no CPU fallback")
+        L = C.CDLL(path)
+        P, I64, U64, U32, D = C.c_void_p, C.c_int64, C.c_uint64, C.c_uint32, C.c_double
+        PD = C.POINTER(C.c_double)
+        L.qmcg_create.argtypes = [C.c_int, C.POINTER(P)]
+        L.qmcg_destroy.argtypes = [P]
+        L.qmcg_destroy.restype = None
+        L.qmcg_last_error.restype = C.c_char_p
+        L.qmcg_version.restype = C.c_char_p
+        L.qmcg_price_american.argtypes = [P, C.POINTER(_CSpec), I64, I64, U64, U32, C.POINTER(_CResult)]
+        L.qmcg_price_american_batch.argtypes = [P, C.POINTER(_CSpec), I64, I64, I64, U64, U32, C.POINTER(_CResult)]
+        L.qmcg_price_american_node.argtypes = [P, C.POINTER(_CSpec), I64, I64, U64, U32, C.c_int, I64, PD]
+        L.qmcg_tree_node_range.argtypes = [I64, C.c_int, I64, C.POINTER(I64), C.POINTER(I64)]
+        L.qmcg_combine_nodes.argtypes = [I64, C.c_int, PD, PD, PD]
+        L.qmcg_warm.argtypes = [P, I64, U64, I64]
+        L.qmcg_clear_cache.argtypes = [P]
+        L.qmcg_permutation.argtypes = [P, I64, U64, P]
+        L.qmcg_uniforms.argtypes = [P, I64, U64, I64, P]
+        L.qmcg_normals.argtypes = [P, I64, U64, I64, P]
+        L.qmcg_path_values.argtypes = [P, C.POINTER(_CSpec), I64, I64, U64, U32, P]
+        L.qmcg_time_device.argtypes = [P, C.POINTER(_CSpec), I64, I64, U64, U32, C.c_int, PD, PD, PD]
+        L.qmcg_time_perm_build.argtypes = [P, I64, U64, I64, PD]
+        L.qmcg_last_launch_count.argtypes = [P]
+        L.qmcg_last_launch_count.restype = I64
+        _lib = L
+        return L
+
+
+def _check(status: int) -> None:
+    if status == OK:
+        return
+    msg = (load_library().qmcg_last_error() or b"").decode()
+    if status == INVALID_ARGUMENT:
+        raise ValueError(msg)
+    if status == LENGTH_ERROR:
+        raise OverflowError(msg)
+    if status == OUT_OF_MEMORY:
+        raise MemoryError(msg)
+    raise RuntimeError(f"qmcg status {status}: {msg}")
+
+
+def _cspec(spec: OptionSpec) -> _CSpec:
+    return _CSpec(float(spec.spot), float(spec.strike), float(spec.rate), float(spec.volatility),
+                  float(spec.maturity), int(spec.kind))
+
+
+def _result(r: _CResult) -> PricingResult:
+    return PricingResult(r.price, r.std_error, int(r.n_paths), r.elapsed_s, Method(r.method), int(r.seed))
+
+
+class Context:
+    """One CUDA device: stream, scratch and the permutation-table cache."""
+
+    def __init__(self, device: int = 0):
+        self._lib = load_library()
+        self._h = C.c_void_p()
+        _check(self._lib.qmcg_create(int(device), C.byref(self._h)))
+        self.device = device
+
+    def close(self) -> None:
+        if self._h:
+            self._lib.qmcg_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):  # pragma: no cover - interpreter shutdown ordering
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    # -- the hot path --
+    def price_american(self, spec: OptionSpec, m: int, n_paths: int, seed: int,
+                       exec: Optional[ExecPolicy] = None, allow_put: bool = False,
+                       no_cache: bool = False) -> PricingResult:
+        if exec is not None:
+            if exec.lanes < 1:
+                raise ValueError("parallel_for_chunks: lanes must be >= 1")
+            if exec.chunk < 1:
+                raise ValueError("parallel_for_chunks: chunk must be >= 1")
+        flags = (FLAG_ALLOW_PUT if allow_put else 0) | (FLAG_NO_CACHE if no_cache else 0)
+        s, r = _cspec(spec), _CResult()
+        _check(self._lib.qmcg_price_american(self._h, C.byref(s), int(m), int(n_paths), int(seed), flags, C.byref(r)))
+        return _result(r)
+
+    def price_american_batch(self, specs: Sequence[OptionSpec], m: int, n_paths: int, seed: int,
+                             allow_put: bool = False) -> list:
+        arr = (_CSpec * len(specs))(*[_cspec(s) for s in specs])
+        res = (_CResult * len(specs))()
+        flags = FLAG_ALLOW_PUT if allow_put else 0
+        _check(self._lib.qmcg_price_american_batch(self._h, arr, len(specs), int(m), int(n_paths), int(seed),
+                                                    flags, res))
+        return [_result(r) for r in res]
+
+    def price_american_node(self, spec: OptionSpec, m: int, n_paths: int, seed: int, depth: int, node: int,
+                            allow_put: bool = False) -> np.ndarray:
+        out = np.zeros(2, dtype=np.float64)
+        s = _cspec(spec)
+        _check(self._lib.qmcg_price_american_node(self._h, C.byref(s), int(m), int(n_paths), int(seed),
+                                                   FLAG_ALLOW_PUT if allow_put else 0, int(depth), int(node),
+                                                   out.ctypes.data_as(C.POINTER(C.c_double))))
+        return out
+
+    def warm(self, n_paths: int, seed: int, dims: int) -> None:
+        _check(self._lib.qmcg_warm(self._h, int(n_paths), int(seed), int(dims)))
+
+    def clear_cache(self) -> None:
+        _check(self._lib.qmcg_clear_cache(self._h))
+
+    # -- parity exports --
+    def permutation(self, n: int, seed64: int) -> np.ndarray:
+        out = np.zeros(max(int(n), 1), dtype=np.uint32)
+        _check(self._lib.qmcg_permutation(self._h, int(n), int(seed64), out.ctypes.data))
+        return out
+
+    def uniforms(self, n: int, seed: int, dim: int) -> np.ndarray:
+        out = np.zeros(int(n), dtype=np.float64)
+        _check(self._lib.qmcg_uniforms(self._h, int(n), int(seed), int(dim), out.ctypes.data))
+        return out
+
+    def normals(self, n: int, seed: int, dim: int) -> np.ndarray:
+        out = np.zeros(int(n), dtype=np.float64)
+        _check(self._lib.qmcg_normals(self._h, int(n), int(seed), int(dim), out.ctypes.data))
+        return out
+
+    def path_values(self, spec: OptionSpec, m: int, n_paths: int, seed: int, allow_put: bool = False) -> np.ndarray:
+        out = np.zeros(int(n_paths), dtype=np.float64)
+        s = _cspec(spec)
+        _check(self._lib.qmcg_path_values(self._h, C.byref(s), int(m), int(n_paths), int(seed),
+                                          FLAG_ALLOW_PUT if allow_put else 0, out.ctypes.data))
+        return out
+
+    # -- measurement hooks --
+    def time_device(self, spec: OptionSpec, m: int, n_paths: int, seed: int, reps: int,
+                    allow_put: bool = False):
+        k, st = C.c_double(), C.c_double()
+        ps = np.zeros(2, dtype=np.float64)
+        s = _cspec(spec)
+        _check(self._lib.qmcg_time_device(self._h, C.byref(s), int(m), int(n_paths), int(seed),
+                                          FLAG_ALLOW_PUT if allow_put else 0, int(reps), C.byref(k), C.byref(st),
+                                          ps.ctypes.data_as(C.POINTER(C.c_double))))
+        return k.value, st.value, float(ps[0]), float(ps[1])
+
+    def time_perm_build(self, n_paths: int, seed: int, dims: int) -> float:
+        ms = C.c_double()
+        _check(self._lib.qmcg_time_perm_build(self._h, int(n_paths), int(seed), int(dims), C.byref(ms)))
+        return ms.value
+
+    def last_launch_count(self) -> int:
+        return int(self._lib.qmcg_last_launch_count(self._h))
+
+
+def tree_node_range(n_paths: int, depth: int, node: int):
+    L = load_library()
+    b, e = C.c_int64(), C.c_int64()
+    _check(L.qmcg_tree_node_range(int(n_paths), int(depth), int(node), C.byref(b), C.byref(e)))
+    return b.value, e.value
+
+
+def combine_nodes(n_paths: int, depth: int, node_sums: np.ndarray):
+    L = load_library()
+    arr = np.ascontiguousarray(node_sums, dtype=np.float64).reshape(-1)
+    if arr.size != 2 * (1 << depth):
+        raise ValueError("combine_nodes: need 2 * 2^depth sums")
+    p, s = C.c_double(), C.c_double()
+    _check(L.qmcg_combine_nodes(int(n_paths), int(depth), arr.ctypes.data_as(C.POINTER(C.c_double)),
+                                C.byref(p), C.byref(s)))
+    return p.value, s.value
+
+
+_default_ctx: Optional[Context] = None
+
+
+def default_context() -> Context:
+    global _default_ctx
+    if _default_ctx is None:
+        _default_ctx = Context(0)
+    return _default_ctx
+
+
+def price_american(spec: OptionSpec, m: int, n_paths: int, seed: int,
+                   exec: Optional[ExecPolicy] = None) -> PricingResult:
+    """qmc::price_american (reference proj/src/american.cpp:103-131) on the default device."""
+    return default_context().price_american(spec, m, n_paths, seed, exec)
+
+
+def convergence_curve(spec: OptionSpec, m_values: Sequence[int], n_paths: int, seed: int,
+                      exec: Optional[ExecPolicy] = None) -> list:
+    """qmc::convergence_curve (reference proj/src/american.cpp:133-150); one cached table set."""
+    if len(m_values) == 0:
+        raise ValueError("convergence_curve: m_values must be non-empty")
+    out = []
+    for m in sorted(m_values):
+        r = price_american(spec, m, n_paths, seed, exec)
+        out.append((m, r.price, r.std_error, r.elapsed_s))
+    return out
