@@ -36,24 +36,25 @@ def _stale(target: str, deps: list[str]) -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    os.makedirs(BUILD, exist_ok=True)
+def build(force: bool = False, verbose: bool = False, defines: tuple = (), lib: str = LIB,
+          build_dir: str = BUILD) -> str:
+    os.makedirs(build_dir, exist_ok=True)
     headers = [os.path.join(CSRC, h) for h in HEADERS] + [
         os.path.join(INCLUDE, "qmcg.h"), os.path.join(INCLUDE, "qmc_b200", "qmc.hpp")]
     objs = []
     for src in CU_SOURCES:
         s = os.path.join(CSRC, src)
-        o = os.path.join(BUILD, src + ".o")
+        o = os.path.join(build_dir, src + ".o")
         objs.append(o)
         if force or _stale(o, [s] + headers):
             cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
-                   "-Xptxas", "-v", "-I", INCLUDE, "-I", CSRC, "-c", s, "-o", o]
+                   "-Xptxas", "-v", "-I", INCLUDE, "-I", CSRC, *[f"-D{d}" for d in defines], "-c", s, "-o", o]
             if verbose:
                 print(" ".join(cmd))
             _run(cmd)
     for src in CXX_SOURCES:
         s = os.path.join(CSRC, src)
-        o = os.path.join(BUILD, src + ".o")
+        o = os.path.join(build_dir, src + ".o")
         objs.append(o)
         if force or _stale(o, [s] + headers):
             cmd = ["g++", "-std=c++17", "-O2", "-fPIC", "-ffp-contract=off", "-Wall",
@@ -61,12 +62,12 @@ def build(force: bool = False, verbose: bool = False) -> str:
             if verbose:
                 print(" ".join(cmd))
             _run(cmd)
-    if force or _stale(LIB, objs):
-        cmd = [NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-lcudart_static", "-lrt", "-ldl", "-lpthread"]
+    if force or _stale(lib, objs):
+        cmd = [NVCC, *ARCH, "-shared", "-o", lib, *objs, "-lcudart_static", "-lrt", "-ldl", "-lpthread"]
         if verbose:
             print(" ".join(cmd))
         _run(cmd)
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":

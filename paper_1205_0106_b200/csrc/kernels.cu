@@ -18,13 +18,22 @@
 
 #include <cub/device/device_radix_sort.cuh>
 
+#include "log_table.h"
+
 namespace qmcg {
 namespace {
 
 constexpr unsigned kFull = 0xffffffffu;
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
-constexpr int kTile = 8;      // dates per tile (tail compaction window)
+#ifndef QMCG_MINB
+#define QMCG_MINB 3
+#endif
+#ifndef QMCG_GEN_UNROLL
+#define QMCG_GEN_UNROLL 1
+#endif
+constexpr int kTile = 8;  // dates per tile = warps per block (one date row per warp)
+constexpr int kGenUnroll = QMCG_GEN_UNROLL;
 constexpr int kRecCap = 64;   // per-warp ring of pending record evaluations
 constexpr uint32_t kNone = 0xffffffffu;
 
@@ -72,8 +81,16 @@ __device__ __forceinline__ double halton(uint32_t x, const DimParam& dp, const d
 // identical to the reference's `std::abs(y) <= 0.42` partition.
 __device__ __forceinline__ bool moro_is_tail(double y) {
   const unsigned long long a = static_cast<unsigned long long>(__double_as_longlong(y)) & 0x7fffffffffffffffull;
-  return a > static_cast<unsigned long long>(__double_as_longlong(0.42));
+  return a > 0x3fdae147ae147ae1ull;  // bits of 0.42
 }
+
+// Moro / Beasley-Springer coefficients in the constant bank so the DFMAs take
+// them as c[][] operands (no per-use materialisation).
+__constant__ double c_bs_a[4] = {2.50662823884, -18.61500062529, 41.39119773534, -25.44106049637};
+__constant__ double c_bs_b[4] = {-8.47351093090, 23.08336743743, -21.06224101826, 3.13082909833};
+__constant__ double c_moro_c[9] = {0.3374754822726147, 0.9761690190917186, 0.1607979714918209,
+                                   0.0276438810333863, 0.0038405729373609, 0.0003951896511919,
+                                   0.0000321767881768, 0.0000002888167364, 0.0000003960315187};
 
 __device__ __forceinline__ double rcp_nr(double x) {
   double r;
@@ -88,24 +105,83 @@ __device__ __forceinline__ double rcp_nr(double x) {
 // the drift offset alpha folded into the final FMA.
 __device__ __forceinline__ double moro_central_plus(double y, double alpha) {
   const double r = y * y;
-  const double A = fma(fma(fma(-25.44106049637, r, 41.39119773534), r, -18.61500062529), r, 2.50662823884);
-  const double B = fma(fma(fma(fma(3.13082909833, r, -21.06224101826), r, 23.08336743743), r,
-                           -8.47351093090), r, 1.0);
+  const double A = fma(fma(fma(c_bs_a[3], r, c_bs_a[2]), r, c_bs_a[1]), r, c_bs_a[0]);
+  const double B = fma(fma(fma(fma(c_bs_b[3], r, c_bs_b[2]), r, c_bs_b[1]), r, c_bs_b[0]), r, 1.0);
   return fma(y * A, rcp_nr(B), alpha);
 }
 
+__constant__ double2 c_log_table[128];
+__constant__ double c_log_consts[2] = {0x1.0000000000400p+52 /* 2^52 + 1024 */, 0x1.62e42fefa39efp-1 /* ln 2 */};
+
+// Shared-memory accessors on 32-bit shared-window addresses (keeps the
+// compiler from rebuilding generic->shared windows inside the hot loops).
+__device__ __forceinline__ uint32_t lds_u32(uint32_t a) {
+  uint32_t v;
+  asm("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint32_t lds_u8(uint32_t a) {
+  uint32_t v;
+  asm("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ double lds_f64(uint32_t a) {
+  double v;
+  asm("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ double2 lds_v2f64(uint32_t a) {
+  double2 v;
+  asm("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void sts_f64(uint32_t a, double v) {
+  asm volatile("st.shared.f64 [%0], %1;" ::"r"(a), "d"(v) : "memory");
+}
+__device__ __forceinline__ void sts_u32(uint32_t a, uint32_t v) {
+  asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+__device__ __forceinline__ void sts_u8(uint32_t a, uint32_t v) {
+  asm volatile("st.shared.u8 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+__device__ __forceinline__ void sts_v2f64(uint32_t a, double2 v) {
+  asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(a), "d"(v.x), "d"(v.y) : "memory");
+}
+
+// Natural log for positive normal x: x = 2^e * m, m = c_i (1 + f) with the
+// 128-entry table {1/c_i, -log(1/c_i)} (log_table.h) in shared memory at
+// `tab`, |f| <= 2^-8, log1p(f) by a degree-6 polynomial. ~11 FP64 operations,
+// error about 1 ulp of the result (CUDA's log() costs ~3x the issue slots).
+__device__ __forceinline__ double dev_log(double x, uint32_t tab) {
+  const int hi = __double2hiint(x);
+  const int lo = __double2loint(x);
+  const int e = (hi >> 20) - 1023;
+  const double2 t = lds_v2f64(tab + (static_cast<uint32_t>(hi >> 9) & 0x7f0u));
+  const double m = __hiloint2double((hi & 0x000fffff) | 0x3ff00000, lo);
+  const double f = fma(m, t.x, -1.0);
+  double q = fma(f, -0x1.5555555555555p-3, 0x1.999999999999ap-3);
+  q = fma(f, q, -0.25);
+  q = fma(f, q, 0x1.5555555555555p-2);
+  q = fma(f, q, -0.5);
+  const double p = fma(f * f, q, f);
+  const double de = __dadd_rn(__hiloint2double(0x43300000, e + 1024), -c_log_consts[0]);
+  return fma(de, c_log_consts[1], t.y + p);
+}
+
 // Moro log-log tail polynomial (analytic.cpp:95-99) for w = u or 1-u.
+__device__ __forceinline__ double moro_tail_poly(double w, uint32_t tab) {
+  const double z = dev_log(-dev_log(w, tab), tab);
+  double x = c_moro_c[8];
+#pragma unroll
+  for (int i = 7; i >= 0; --i) x = fma(x, z, c_moro_c[i]);
+  return x;
+}
+
 __device__ __forceinline__ double moro_tail_poly(double w) {
   const double z = log(-log(w));
-  double x = 0.0000003960315187;
-  x = fma(x, z, 0.0000002888167364);
-  x = fma(x, z, 0.0000321767881768);
-  x = fma(x, z, 0.0003951896511919);
-  x = fma(x, z, 0.0038405729373609);
-  x = fma(x, z, 0.0276438810333863);
-  x = fma(x, z, 0.1607979714918209);
-  x = fma(x, z, 0.9761690190917186);
-  x = fma(x, z, 0.3374754822726147);
+  double x = c_moro_c[8];
+#pragma unroll
+  for (int i = 7; i >= 0; --i) x = fma(x, z, c_moro_c[i]);
   return x;
 }
 
@@ -153,41 +229,139 @@ __device__ double cnd_dev(double d) {
   return d > 0.0 ? 1.0 - tail : tail;
 }
 
-__device__ __forceinline__ uint32_t ldg_stream(const uint32_t* p) {
-  uint32_t v;
-  asm volatile("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(v) : "l"(p));
-  return v;
-}
-
 __device__ __forceinline__ unsigned lanemask_lt() {
   unsigned m;
   asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
   return m;
 }
 
-struct WarpSmem {
-  double tail_w[kTile * 32];
-  double zres[kTile * 32];
-  double rq_v[kRecCap];
-  unsigned long long best[32];
-  uint32_t rq_code[kRecCap];
-  unsigned char tail_owner[kTile * 32];
-};
+// ---- radical inverse with the digit count fixed per date (warp-uniform) ----
+template <bool WIDE>
+__device__ __forceinline__ uint32_t divp(uint32_t x, uint32_t magic, uint32_t shift, uint64_t m64) {
+  if (WIDE) return static_cast<uint32_t>(__umul64hi(x, m64));
+  return __umulhi(x, magic) >> shift;
+}
+
+template <bool WIDE>
+__device__ __forceinline__ double halton_digits(uint32_t x, uint32_t p, uint32_t magic, uint32_t shift, uint64_t m64,
+                                                int D, const double2* __restrict__ sn) {
+  // D digits, least significant first; the last digit is the remaining quotient.
+  if (D == 3) {
+    const double2 s0 = sn[0], s1 = sn[1], s2 = sn[2];
+    const uint32_t q1 = divp<WIDE>(x, magic, shift, m64);
+    const uint32_t q2 = divp<WIDE>(q1, magic, shift, m64);
+    double v = digit_term(x - q1 * p, s0.x, s0.y);
+    v = __dadd_rn(v, digit_term(q1 - q2 * p, s1.x, s1.y));
+    return __dadd_rn(v, digit_term(q2, s2.x, s2.y));
+  }
+  if (D == 2) {
+    const double2 s0 = sn[0], s1 = sn[1];
+    const uint32_t q1 = divp<WIDE>(x, magic, shift, m64);
+    const double v = digit_term(x - q1 * p, s0.x, s0.y);
+    return __dadd_rn(v, digit_term(q1, s1.x, s1.y));
+  }
+  if (D == 4) {
+    const double2 s0 = sn[0], s1 = sn[1], s2 = sn[2], s3 = sn[3];
+    const uint32_t q1 = divp<WIDE>(x, magic, shift, m64);
+    const uint32_t q2 = divp<WIDE>(q1, magic, shift, m64);
+    const uint32_t q3 = divp<WIDE>(q2, magic, shift, m64);
+    double v = digit_term(x - q1 * p, s0.x, s0.y);
+    v = __dadd_rn(v, digit_term(q1 - q2 * p, s1.x, s1.y));
+    v = __dadd_rn(v, digit_term(q2 - q3 * p, s2.x, s2.y));
+    return __dadd_rn(v, digit_term(q3, s3.x, s3.y));
+  }
+  if (D == 1) {
+    const double2 s0 = sn[0];
+    return digit_term(x, s0.x, s0.y);
+  }
+  uint32_t q = divp<WIDE>(x, magic, shift, m64);
+  double2 s = sn[0];
+  double v = digit_term(x - q * p, s.x, s.y);
+  x = q;
+  for (int j = 1; j < D - 1; ++j) {
+    q = divp<WIDE>(x, magic, shift, m64);
+    s = sn[j];
+    v = __dadd_rn(v, digit_term(x - q * p, s.x, s.y));
+    x = q;
+  }
+  s = sn[D - 1];
+  return __dadd_rn(v, digit_term(x, s.x, s.y));
+}
+
+__device__ __forceinline__ double clamp_endpoints(double v) {  // quasi_rng.cpp:80-81
+  if (v < 1e-12) v = 1e-12;
+  if (v > 1.0 - 1e-12) v = 1.0 - 1e-12;
+  return v;
+}
+
+// ---- bulk-copy staging (cp.async.bulk + mbarrier) ----
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// Shared memory of one 256-path block (byte offsets from the dynamic base):
+//   perm[2][kTile][256] u32   permutation entries, bulk-copied, double-buffered
+//   zt[2][kTile][256]   f64   z_k + alpha per (date, path); reused for V_k in the walk
+//   logtab[128]         f64x2 log reduction table
+//   bar[2]              mbarriers of the two perm buffers
+//   per warp: tail_w[128] f64 | rq_v[64] f64 | best[32] u64 | rq_code[64] u32 | tail_idx[128] u8
+constexpr uint32_t kTailCap = 128;  // flushed when more than kTailCap - 32 are pending
+constexpr uint32_t kPermOff = 0;
+constexpr uint32_t kPermBuf = kTile * kThreads * 4;
+constexpr uint32_t kZtOff = kPermOff + 2 * kPermBuf;
+constexpr uint32_t kZtBuf = kTile * kThreads * 8;
+constexpr uint32_t kLogOff = kZtOff + 2 * kZtBuf;
+constexpr uint32_t kBarOff = kLogOff + 128 * 16;
+constexpr uint32_t kWarpOff = kBarOff + 128;
+constexpr uint32_t kWTail = 0;
+constexpr uint32_t kWRqV = kWTail + kTailCap * 8;
+constexpr uint32_t kWBest = kWRqV + kRecCap * 8;
+constexpr uint32_t kWRqCode = kWBest + 32 * 8;
+constexpr uint32_t kWTailIdx = kWRqCode + kRecCap * 4;
+constexpr uint32_t kWarpBytes = kWTailIdx + kTailCap;
+constexpr uint32_t kSmemBytes = kWarpOff + kWarps * kWarpBytes;
 
 template <int KIND, bool RNEG>
-__device__ __forceinline__ void process_records(const PriceParams& P, WarpSmem& S, uint32_t head,
-                                                uint32_t count, int lane) {
+__device__ __noinline__ void process_records(const PriceParams& P, uint32_t ws, uint32_t head, uint32_t count,
+                                             int lane) {
   if (static_cast<uint32_t>(lane) < count) {
     const uint32_t slot = (head + lane) & (kRecCap - 1);
-    const double v = S.rq_v[slot];
-    const uint32_t code = S.rq_code[slot];
+    const double v = lds_f64(ws + kWRqV + slot * 8);
+    const uint32_t code = lds_u32(ws + kWRqCode + slot * 4);
     const int d = static_cast<int>(code >> 5);
-    const int owner = static_cast<int>(code & 31u);
+    const uint32_t owner = code & 31u;
     const double s = exp(fma(P.b, v, P.X0));
     double intr = KIND == 0 ? s - P.strike : P.strike - s;
     intr = intr > 0.0 ? intr : 0.0;
     const double term = intr * __ldg(P.dpow + d + 1);
-    atomicMax(&S.best[owner], static_cast<unsigned long long>(__double_as_longlong(term)));
+    asm volatile("atom.shared.max.u64 _, [%0], %1;" ::"r"(ws + kWBest + owner * 8),
+                 "l"(static_cast<unsigned long long>(__double_as_longlong(term)))
+                 : "memory");
   }
 }
 
@@ -201,157 +375,334 @@ __device__ __forceinline__ double rneg_threshold(const PriceParams& P, double be
   return room > 0.0 ? (log(room) - P.X0) / P.b : -INFINITY;
 }
 
-// One thread = one path. Dates are processed in tiles of kTile: the uniforms
-// and central normals of a tile are computed lane-parallel, the Moro tail
-// evaluations (16% of points, two logs each) are compacted across the warp,
-// then the log-price walk V_k = sum (z_j + alpha) runs over the tile. A date k
-// can only set the foresight maximum max_k disc^k * I_k if I_k exceeds every
-// earlier intrinsic (disc <= 1), i.e. V_k sets a new running extreme; those
-// "records" are queued per warp and evaluated 32 at a time (exp + discount).
+// Issue the bulk copies of tile `k` (dates [k*kTile, ...)) into buffer b.
+__device__ __forceinline__ void issue_tile(const PriceParams& P, uint32_t sbase, int k, int b, int64_t col0,
+                                           uint32_t bytes) {
+  const int d0 = k * kTile;
+  const int rows = min(kTile, P.m - d0);
+  const uint32_t bar = sbase + kBarOff + b * 8;
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
+               "r"(static_cast<uint32_t>(rows) * bytes)
+               : "memory");
+  for (int t = 0; t < rows; ++t) {
+    const uint32_t dst = sbase + kPermOff + b * kPermBuf + t * kThreads * 4;
+    const uint32_t* src = P.perm + static_cast<int64_t>(d0 + t) * P.ld + col0;
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+        "l"(src), "r"(bytes), "r"(bar)
+        : "memory");
+  }
+}
+
+__device__ __forceinline__ void mbar_wait_u32(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+
+// Evaluate the queued Moro-tail points of one date row, 32 per round:
+// u -> y = u - 0.5 (exact as the reference), w = u or 1 - u, z = +-P8(log(-log w)).
+__device__ __noinline__ void flush_tail(uint32_t ws, uint32_t zrow, uint32_t ntail, uint32_t logtab, double alpha,
+                                        int lane) {
+  __syncwarp();
+  for (uint32_t r = 0; r < ntail; r += 32) {
+    const uint32_t q = r + lane;
+    if (q < ntail) {
+      const double u = lds_f64(ws + kWTail + q * 8);
+      const double y = __dadd_rn(u, -0.5);
+      const double x = moro_tail_poly(y > 0.0 ? __dadd_rn(1.0, -u) : u, logtab);
+      sts_f64(zrow + lds_u8(ws + kWTailIdx + q) * 8, (y > 0.0 ? x : -x) + alpha);
+    }
+  }
+  __syncwarp();
+}
+
+// One point of a date row: tail test, predicated push of a tail point, central
+// normal + alpha into the row (overwritten later for tail points).
+template <bool CLAMP>
+__device__ __forceinline__ void finish_point(uint32_t ws, uint32_t zslot, uint32_t idx, double u, bool clamp,
+                                             double alpha, unsigned lt, uint32_t& ntail) {
+  if (CLAMP && clamp) u = clamp_endpoints(u);
+  const double y = __dadd_rn(u, -0.5);
+  const bool tail = fabs(y) > 0.42;
+  const unsigned tb = __ballot_sync(kFull, tail);
+  const uint32_t pos = ntail + __popc(tb & lt);
+  if (tail) {
+    sts_f64(ws + kWTail + pos * 8, u);
+    sts_u8(ws + kWTailIdx + pos, idx);
+  }
+  ntail += __popc(tb);
+  sts_f64(zslot, moro_central_plus(y, alpha));
+}
+
+// Generation phase for one date row: warp w turns the 256 permutation
+// entries of date d into z + alpha. Date constants are loaded once per row
+// and reused for the 8 chunks of 32 paths (fully unrolled, immediate smem
+// offsets); the Moro tail points of the row are compacted into a warp queue
+// and evaluated 32 at a time.
+template <bool WIDE>
+__device__ __forceinline__ double halton_any(uint32_t x, const uint4& dp, uint64_t m64, const double2* sn) {
+  return halton_digits<WIDE>(x, dp.x, dp.y, dp.z & 0xffu, m64, static_cast<int>((dp.z >> 8) & 0xffu), sn);
+}
+
+template <int D>
+__device__ __forceinline__ double halton_fixed(uint32_t x, uint32_t magic, uint32_t shift, uint32_t negp,
+                                               const double2 (&sc)[4]) {
+  // D digits, least significant first; the last digit is the remaining quotient.
+  double u;
+  uint32_t r = x;
+#pragma unroll
+  for (int j = 0; j < D; ++j) {
+    double term;
+    uint32_t q = 0;
+    if (j < D - 1) {
+      q = __umulhi(r, magic) >> shift;
+      term = digit_term(q * negp + r, sc[j].x, sc[j].y);
+    } else {
+      term = digit_term(r, sc[j].x, sc[j].y);
+    }
+    u = j == 0 ? term : __dadd_rn(u, term);
+    r = q;
+  }
+  return u;
+}
+
+template <int D>
+__device__ __forceinline__ void generate_row_fixed(const double2* sn, uint32_t magic, uint32_t shift, uint32_t negp,
+                                                   uint32_t ws, uint32_t prow, uint32_t zrow, uint32_t logtab,
+                                                   int nchunks, int lane, unsigned lt, double alpha) {
+  double2 sc[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) sc[j] = j < D ? __ldg(sn + j) : make_double2(0.0, 0.0);
+  uint32_t ntail = 0;
+#pragma unroll 1
+  for (int ch = 0; ch < nchunks; ++ch) {
+    const uint32_t x = lds_u32(prow + ch * 128) + 1u;
+    const double u = halton_fixed<D>(x, magic, shift, negp, sc);
+    finish_point<false>(ws, zrow + ch * 256, ch * 32 + lane, u, false, alpha, lt, ntail);
+    if (ntail > kTailCap - 32) {
+      flush_tail(ws, zrow - lane * 8, ntail, logtab, alpha, lane);
+      ntail = 0;
+    }
+  }
+  if (ntail) flush_tail(ws, zrow - lane * 8, ntail, logtab, alpha, lane);
+}
+
+template <bool SLOW>
+__device__ __forceinline__ void generate_row(const PriceParams& P, uint32_t ws, int d, uint32_t prow, uint32_t zrow,
+                                             uint32_t logtab, int nchunks, int lane, unsigned lt) {
+  const uint4 dp = __ldg(reinterpret_cast<const uint4*>(P.dims) + d);
+  const uint32_t magic = dp.y, shift = dp.z & 0xffu, negp = 0u - dp.x;
+  const int D = static_cast<int>((dp.z >> 8) & 0xffu);
+  const double2* sn = P.scnc + dp.w;
+  const double alpha = P.alpha;
+  prow += lane * 4;
+  zrow += lane * 8;
+  if (!SLOW) {
+    if (D == 3) return generate_row_fixed<3>(sn, magic, shift, negp, ws, prow, zrow, logtab, nchunks, lane, lt, alpha);
+    if (D == 2) return generate_row_fixed<2>(sn, magic, shift, negp, ws, prow, zrow, logtab, nchunks, lane, lt, alpha);
+    if (D == 4) return generate_row_fixed<4>(sn, magic, shift, negp, ws, prow, zrow, logtab, nchunks, lane, lt, alpha);
+  }
+  const bool clamp = SLOW && ((dp.z >> 16) & DIM_CLAMP);
+  const bool wide = SLOW && ((dp.z >> 16) & DIM_WIDE);
+  const uint64_t m64 = wide ? __ldg(P.magic64 + d) : 0ull;
+  uint32_t ntail = 0;
+  for (int ch = 0; ch < nchunks; ++ch) {
+    const uint32_t x = lds_u32(prow + ch * 128) + 1u;
+    const double u = wide ? halton_any<true>(x, dp, m64, sn) : halton_any<false>(x, dp, m64, sn);
+    finish_point<SLOW>(ws, zrow + ch * 256, ch * 32 + lane, u, clamp, alpha, lt, ntail);
+    if (ntail > kTailCap - 32) {
+      flush_tail(ws, zrow - lane * 8, ntail, logtab, alpha, lane);
+      ntail = 0;
+    }
+  }
+  if (ntail) flush_tail(ws, zrow - lane * 8, ntail, logtab, alpha, lane);
+}
+
 template <int KIND, bool RNEG>
-__global__ void __launch_bounds__(kThreads, 2) price_kernel(const PriceParams P) {
-  __shared__ WarpSmem smem[kWarps];
-  WarpSmem& S = smem[threadIdx.x >> 5];
+__device__ __forceinline__ void push_record(uint32_t ws, const PriceParams& P, bool push, double v, int d, int lane,
+                                            unsigned lt, uint32_t& rq_head, uint32_t& rq_tail) {
+  const unsigned pb = __ballot_sync(kFull, push);
+  if (pb) {
+    if (push) {
+      const uint32_t slot = (rq_tail + __popc(pb & lt)) & (kRecCap - 1);
+      sts_f64(ws + kWRqV + slot * 8, v);
+      sts_u32(ws + kWRqCode + slot * 4, (static_cast<uint32_t>(d) << 5) | static_cast<uint32_t>(lane));
+    }
+    rq_tail += __popc(pb);
+    if (rq_tail - rq_head >= 32) {
+      __syncwarp();
+      process_records<KIND, RNEG>(P, ws, rq_head, 32, lane);
+      rq_head += 32;
+      __syncwarp();
+    }
+  }
+}
+
+// One block = 256 consecutive paths; thread i walks path i. Per tile of
+// kTile dates: (1) the permutation rows arrive by cp.async.bulk; (2) warp w
+// generates date row w of the tile (uniform -> normal, bit-exact uniforms);
+// (3) every thread walks its path through the tile: V_k = sum (z_j + alpha)
+// is the log-price in units of b, X_k = X0 + b V_k. A date k can only set the
+// foresight maximum max_k disc^k I_k if I_k exceeds every earlier intrinsic
+// (disc <= 1), i.e. V_k sets a new running extreme ("record"). Each record
+// replaces the lane's pending record; the pending record j is dropped when
+// the new record k dominates it (S_k disc^(k-j) >= S_j, i.e. key_k >= key_j
+// with key = V - slope*date, slope = r*dt/b, calls), otherwise j is queued
+// for exact evaluation (exp + discount) in warp-wide batches of 32.
+// SLOW = any of: volatility 0, range checks, 64-bit magic, endpoint clamp.
+template <int KIND, bool RNEG, bool SLOW>
+__global__ void __launch_bounds__(kThreads, QMCG_MINB) price_kernel(const PriceParams P) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const uint32_t sbase = smem_u32(smem_raw);
+  const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+  const uint32_t ws = sbase + kWarpOff + warp * kWarpBytes;
+  const uint32_t logtab = sbase + kLogOff;
   const unsigned lt = lanemask_lt();
-  const int64_t pi = static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x;
+  const int64_t block_first = static_cast<int64_t>(blockIdx.x) * kThreads;
+  const int64_t pi = block_first + threadIdx.x;
   const bool active = pi < P.path_count;
-  const int64_t col = active ? P.path_begin + pi - P.col_begin : 0;
-  const uint32_t* colp = P.perm + col;
-  const int64_t ld = P.ld;
   const int m = P.m;
   const int mrec = m - 1;
-  const bool det = P.deterministic != 0;
+  const bool det = SLOW && P.deterministic != 0;
+  const bool check = SLOW && P.check_range != 0;
+  const int ntiles = (m + kTile - 1) / kTile;
+  const int64_t block_paths = min(static_cast<int64_t>(kThreads), P.path_count - block_first);
+  const int nchunks = static_cast<int>((block_paths + 31) / 32);
+  // columns of this block in the table (16-byte aligned: path_begin - col_begin and ld are multiples of 4)
+  const int64_t col0 = P.path_begin - P.col_begin + block_first;
+  const uint32_t bytes = static_cast<uint32_t>(((block_paths + 3) / 4) * 16);
+  const double slope = P.dom_slope;
 
-  S.best[lane] = static_cast<unsigned long long>(__double_as_longlong(P.best0));
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sbase + kBarOff));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sbase + kBarOff + 8));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  asm volatile("st.shared.u64 [%0], %1;" ::"r"(ws + kWBest + lane * 8),
+               "l"(static_cast<unsigned long long>(__double_as_longlong(P.best0)))
+               : "memory");
+  if (threadIdx.x < 128) sts_v2f64(logtab + threadIdx.x * 16, c_log_table[threadIdx.x]);
+  __syncthreads();
+  if (threadIdx.x == 0 && !det) {
+    issue_tile(P, sbase, 0, 0, col0, bytes);
+    if (ntiles > 1) issue_tile(P, sbase, 1, 1, col0, bytes);
+  }
+
   double V = 0.0;
   double c = P.c0;
+  double pend_key = 0.0;  // pending (not yet evaluated) record: key = V - slope * d
+  int pend_d = -1;
   uint32_t rq_head = 0, rq_tail = 0;
   uint32_t err = 0;
-  __syncwarp();
 
-  uint32_t nxt[kTile];
-#pragma unroll
-  for (int t = 0; t < kTile; ++t)
-    nxt[t] = (active && !det && t < m) ? ldg_stream(colp + static_cast<int64_t>(t) * ld) : 0u;
-
-  for (int k0 = 0; k0 < m; k0 += kTile) {
-    uint32_t cur[kTile];
-#pragma unroll
-    for (int t = 0; t < kTile; ++t) cur[t] = nxt[t];
-#pragma unroll
-    for (int t = 0; t < kTile; ++t) {
-      const int d = k0 + kTile + t;
-      nxt[t] = (active && !det && d < m) ? ldg_stream(colp + static_cast<int64_t>(d) * ld) : 0u;
+  for (int k = 0; k < ntiles; ++k) {
+    const int k0 = k * kTile;
+    const int b = k & 1;
+    const uint32_t zcol = sbase + kZtOff + b * kZtBuf + threadIdx.x * 8;
+    if (!det) {
+      mbar_wait_u32(sbase + kBarOff + b * 8, static_cast<uint32_t>((k >> 1) & 1));
+      if (k0 + warp < m)
+        generate_row<SLOW>(P, ws, k0 + warp, sbase + kPermOff + b * kPermBuf + warp * kThreads * 4,
+                           sbase + kZtOff + b * kZtBuf + warp * kThreads * 8, logtab, nchunks, lane, lt);
+      __syncthreads();  // z tile complete; perm buffer b consumed
+      if (threadIdx.x == 0 && k + 2 < ntiles) issue_tile(P, sbase, k + 2, b, col0, bytes);
     }
-
-    double zq[kTile];
-    if (det) {
+    // ---- walk ----
+    const double sk0 = slope * static_cast<double>(k0);
+    if (!SLOW && !RNEG && k0 + kTile <= mrec) {
 #pragma unroll
-      for (int t = 0; t < kTile; ++t) zq[t] = P.alpha;
+      for (int t = 0; t < kTile; ++t) {
+        V = __dadd_rn(V, lds_f64(zcol + t * kThreads * 8));
+        const bool rec = KIND == 0 ? V > c : V < c;
+        c = rec ? V : c;
+        const double key = V - fma(slope, static_cast<double>(t), sk0);
+        const bool push = rec && pend_d >= 0 && !(KIND == 0 && key >= pend_key);
+        const double pv = fma(slope, static_cast<double>(pend_d), pend_key);
+        const int pd = pend_d;
+        pend_key = rec ? key : pend_key;
+        pend_d = rec ? k0 + t : pend_d;
+        push_record<KIND, RNEG>(ws, P, push, pv, pd, lane, lt, rq_head, rq_tail);
+      }
     } else {
-      uint32_t tail_base = 0;
-      uint32_t tmask = 0;
 #pragma unroll
       for (int t = 0; t < kTile; ++t) {
         const int d = k0 + t;
-        zq[t] = 0.0;
         if (d < m) {
-          const DimParam dp = P.dims[d];
-          const double u = active ? halton(cur[t] + 1u, dp, P.sc, P.nc) : 0.5;
-          const double y = __dadd_rn(u, -0.5);
-          const bool tail = moro_is_tail(y);
-          const unsigned tb = __ballot_sync(kFull, tail);
-          if (tail) {
-            const uint32_t pos = tail_base + __popc(tb & lt);
-            // sign carries the branch: negative <=> y > 0 (use 1-u).
-            S.tail_w[pos] = y > 0.0 ? -__dadd_rn(1.0, -u) : u;
-            S.tail_owner[pos] = static_cast<unsigned char>(t * 32 + lane);
-            tmask |= 1u << t;
+          V = __dadd_rn(V, det ? P.alpha : lds_f64(zcol + t * kThreads * 8));
+          if (check && active) {
+            const double X = fma(P.b, V, P.X0);
+            if (X < -745.1332191019412) err |= ERR_SPOT_NONPOSITIVE;
+            if (X > 709.782712893384) err |= ERR_SPOT_NONFINITE;
           }
-          tail_base += __popc(tb);
-          zq[t] = moro_central_plus(y, P.alpha);
-        }
-      }
-      if (tail_base) {
-        __syncwarp();
-        for (uint32_t r = 0; r < tail_base; r += 32) {
-          const uint32_t q = r + lane;
-          if (q < tail_base) {
-            const double ws = S.tail_w[q];
-            const double x = moro_tail_poly(fabs(ws));
-            S.zres[S.tail_owner[q]] = (ws < 0.0 ? x : -x) + P.alpha;
-          }
-        }
-        __syncwarp();
-#pragma unroll
-        for (int t = 0; t < kTile; ++t)
-          if (tmask & (1u << t)) zq[t] = S.zres[t * 32 + lane];
-      }
-    }
-
-#pragma unroll
-    for (int t = 0; t < kTile; ++t) {
-      const int d = k0 + t;
-      if (d < m) {
-        V = __dadd_rn(V, zq[t]);
-        if (P.check_range && active) {
-          const double X = fma(P.b, V, P.X0);
-          if (X < -745.1332191019412) err |= ERR_SPOT_NONPOSITIVE;
-          if (X > 709.782712893384) err |= ERR_SPOT_NONFINITE;
-        }
-        if (d < mrec) {
-          const bool rec = active && (KIND == 0 ? V > c : V < c);
-          const unsigned rb = __ballot_sync(kFull, rec);
-          if (rb) {
-            if (rec) {
-              const uint32_t slot = (rq_tail + __popc(rb & lt)) & (kRecCap - 1);
-              S.rq_v[slot] = V;
-              S.rq_code[slot] = (static_cast<uint32_t>(d) << 5) | static_cast<uint32_t>(lane);
-              if (!RNEG) c = V;
-            }
-            rq_tail += __popc(rb);
-            if (rq_tail - rq_head >= 32) {
-              __syncwarp();
-              process_records<KIND, RNEG>(P, S, rq_head, 32, lane);
-              rq_head += 32;
-              __syncwarp();
-              if (RNEG) c = rneg_threshold<KIND>(P, __longlong_as_double(static_cast<long long>(S.best[lane])));
+          if (d < mrec) {
+            const bool rec = KIND == 0 ? V > c : V < c;
+            if (RNEG) {
+              // every candidate is evaluated; the threshold follows the evaluated best
+              const uint32_t before = rq_head;
+              push_record<KIND, RNEG>(ws, P, rec, V, d, lane, lt, rq_head, rq_tail);
+              if (rq_head != before) {
+                unsigned long long bb;
+                asm volatile("ld.shared.u64 %0, [%1];" : "=l"(bb) : "r"(ws + kWBest + lane * 8));
+                c = rneg_threshold<KIND>(P, __longlong_as_double(static_cast<long long>(bb)));
+              }
+            } else {
+              c = rec ? V : c;
+              const double key = V - slope * static_cast<double>(d);
+              const bool push = rec && pend_d >= 0 && !(KIND == 0 && key >= pend_key);
+              const double pv = fma(slope, static_cast<double>(pend_d), pend_key);
+              const int pd = pend_d;
+              pend_key = rec ? key : pend_key;
+              pend_d = rec ? d : pend_d;
+              push_record<KIND, RNEG>(ws, P, push, pv, pd, lane, lt, rq_head, rq_tail);
             }
           }
         }
       }
     }
   }
+  if (!RNEG) {  // the last pending record of every path
+    push_record<KIND, RNEG>(ws, P, pend_d >= 0, fma(slope, static_cast<double>(pend_d), pend_key), pend_d, lane, lt,
+                            rq_head, rq_tail);
+  }
   if (rq_tail != rq_head) {
     __syncwarp();
-    process_records<KIND, RNEG>(P, S, rq_head, rq_tail - rq_head, lane);
+    process_records<KIND, RNEG>(P, ws, rq_head, rq_tail - rq_head, lane);
   }
   __syncwarp();
 
   // Date m: max(intrinsic, Black-Scholes of the final interval), american.cpp:43-52.
   const double X = fma(P.b, V, P.X0);
-  const double sm = exp(X);
+  const double sm_last = exp(X);
   double cont;
   if (P.bs_v_zero) {
-    const double fwd = sm * P.bs_fwd_growth;
+    const double fwd = sm_last * P.bs_fwd_growth;
     double iv = KIND == 0 ? fwd - P.strike : P.strike - fwd;
     cont = P.bs_disc * (iv > 0.0 ? iv : 0.0);
   } else {
     const double d1 = (X - P.log_strike + P.bs_mu_t) / P.bs_vsqrt;
     const double d2 = d1 - P.bs_vsqrt;
-    const double price = KIND == 0 ? sm * cnd_dev(d1) - P.bs_kdisc * cnd_dev(d2)
-                                   : P.bs_kdisc * cnd_dev(-d2) - sm * cnd_dev(-d1);
+    const double price = KIND == 0 ? sm_last * cnd_dev(d1) - P.bs_kdisc * cnd_dev(d2)
+                                   : P.bs_kdisc * cnd_dev(-d2) - sm_last * cnd_dev(-d1);
     cont = price > 0.0 ? price : 0.0;
   }
-  double intr = KIND == 0 ? sm - P.strike : P.strike - sm;
+  double intr = KIND == 0 ? sm_last - P.strike : P.strike - sm_last;
   intr = intr > 0.0 ? intr : 0.0;
   const double cm = intr > cont ? intr : cont;
   const double term_m = cm * __ldg(P.dpow + m);
-  const double best = __longlong_as_double(static_cast<long long>(S.best[lane]));
+  unsigned long long bb;
+  asm volatile("ld.shared.u64 %0, [%1];" : "=l"(bb) : "r"(ws + kWBest + lane * 8));
+  const double best = __longlong_as_double(static_cast<long long>(bb));
   if (active) {
-    if (!(sm > 0.0)) err |= ERR_SPOT_NONPOSITIVE;
-    if (!isfinite(sm)) err |= ERR_SPOT_NONFINITE;
+    if (!(sm_last > 0.0)) err |= ERR_SPOT_NONPOSITIVE;
+    if (!isfinite(sm_last)) err |= ERR_SPOT_NONFINITE;
     if (err) atomicOr(P.err, err);
     P.values[pi] = best > term_m ? best : term_m;
   }
@@ -519,17 +870,41 @@ int leaf_depth(int64_t len) {
 
 }  // namespace
 
+template <int KIND, bool RNEG, bool SLOW>
+cudaError_t launch_price_t(const PriceParams& P, cudaStream_t s) {
+  const int64_t blocks = (P.path_count + kThreads - 1) / kThreads;
+  const size_t smem = kSmemBytes;
+  auto kern = price_kernel<KIND, RNEG, SLOW>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  if (e != cudaSuccess) return e;
+  kern<<<static_cast<unsigned>(blocks), kThreads, smem, s>>>(P);
+  return cudaGetLastError();
+}
+
+template <int KIND, bool RNEG>
+cudaError_t launch_price_k(const PriceParams& P, cudaStream_t s) {
+  const bool slow = P.any_wide || P.any_clamp || P.deterministic || P.check_range;
+  return slow ? launch_price_t<KIND, RNEG, true>(P, s) : launch_price_t<KIND, RNEG, false>(P, s);
+}
+
+cudaError_t ensure_log_table(cudaStream_t s) {
+  static bool done[64] = {};
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (dev < 64 && done[dev]) return cudaSuccess;
+  e = cudaMemcpyToSymbolAsync(c_log_table, kLogTable, sizeof(kLogTable), 0, cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e == cudaSuccess && dev < 64) done[dev] = true;
+  return e;
+}
+
 cudaError_t launch_price(const PriceParams& P, cudaStream_t s) {
   if (P.path_count <= 0) return cudaSuccess;
-  const int64_t blocks = (P.path_count + kThreads - 1) / kThreads;
-  if (P.kind == 0) {
-    if (P.rate_negative) price_kernel<0, true><<<static_cast<unsigned>(blocks), kThreads, 0, s>>>(P);
-    else price_kernel<0, false><<<static_cast<unsigned>(blocks), kThreads, 0, s>>>(P);
-  } else {
-    if (P.rate_negative) price_kernel<1, true><<<static_cast<unsigned>(blocks), kThreads, 0, s>>>(P);
-    else price_kernel<1, false><<<static_cast<unsigned>(blocks), kThreads, 0, s>>>(P);
-  }
-  return cudaGetLastError();
+  cudaError_t e = ensure_log_table(s);
+  if (e != cudaSuccess) return e;
+  if (P.kind == 0) return P.rate_negative ? launch_price_k<0, true>(P, s) : launch_price_k<0, false>(P, s);
+  return P.rate_negative ? launch_price_k<1, true>(P, s) : launch_price_k<1, false>(P, s);
 }
 
 cudaError_t launch_uniforms(const uint32_t* perm_row, int64_t count, DimParam dp, const double* sc,

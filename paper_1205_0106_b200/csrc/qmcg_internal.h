@@ -21,6 +21,11 @@ struct DimParam {
   uint32_t flags;    // DIM_CLAMP: endpoint clamp can trigger; DIM_WIDE: 64-bit magic
   uint64_t magic64;  // ceil(2^64 / p) for DIM_WIDE
 };
+// Kernel-side packed form: {p, magic, shift | ndig << 8 | flags << 16, doff}
+// (one 16-byte uniform load per date) and interleaved {sc[j], nc[j]} pairs.
+struct DimPack {
+  uint32_t p, magic, meta, doff;
+};
 enum : uint32_t { DIM_CLAMP = 1u, DIM_WIDE = 2u };
 
 // Error bits raised by the pricing kernel (mapped to the reference's
@@ -35,9 +40,11 @@ struct PriceParams {
   int64_t path_count;    // paths in this launch
   int32_t m;             // exercise dates (dims used: 0..m-1)
   int32_t kind;          // 0 call, 1 put
-  const DimParam* dims;
-  const double* sc;
-  const double* nc;
+  const DimPack* dims;
+  const double2* scnc;     // {sc[j], nc[j]} per digit, indexed by DimPack::doff
+  const uint64_t* magic64; // per dimension, used when any dimension needs it
+  int32_t any_wide;        // some dimension needs the 64-bit magic division
+  int32_t any_clamp;       // some dimension can hit the endpoint clamp
   const double* dpow;    // dpow[k] = disc^k as the host's rounded chain, k = 0..m
   double X0;             // log(spot)
   double b;              // log-price scale: X_k = X0 + b * V_k
@@ -47,6 +54,7 @@ struct PriceParams {
   double best0;          // intrinsic value at t0 (date 0 term)
   double log_strike;
   double dmax_inv;       // 1 / max_k disc^k  (only for rate < 0)
+  double dom_slope;      // r*dt / b: record dominance slope in V units (calls)
   // Black-Scholes of the last interval (reference sweep_impl, american.cpp:45-52)
   double bs_vsqrt;       // v*sqrt(dt)
   double bs_mu_t;        // (r + 0.5*v*v)*dt
@@ -71,6 +79,12 @@ cudaError_t launch_perm_build(uint64_t seed64, int64_t n, uint32_t* out, void* s
 // Copy columns [c0, c1) of a freshly built permutation into a table row.
 cudaError_t launch_uniforms(const uint32_t* perm_row, int64_t count, DimParam dp, const double* sc,
                             const double* nc, int normals, double* out, cudaStream_t s);
+// Row stride (in paths) of the permutation table: padded so every row starts
+// 16-byte aligned for the bulk-copy staging of K2.
+inline int64_t table_ld(int64_t cols) { return (cols + 63) / 64 * 64; }
+// Extra elements allocated after the last row (bulk copies of a partial block
+// may read up to one block past the end of a row).
+constexpr int64_t kTablePad = 256;
 // Pairwise-tree sums of v and v*v over `len` values (reference pairwise_sum
 // with 64-element leaves). out2[0] = sum, out2[1] = sum of squares.
 size_t reduce_scratch_doubles(int64_t len);

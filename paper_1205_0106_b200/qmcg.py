@@ -21,7 +21,7 @@ from typing import Optional, Sequence
 
 import numpy as np
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libqmcg.so")
+LIB_PATH = os.environ.get("QMCG_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "libqmcg.so")
 
 OK, INVALID_ARGUMENT, LENGTH_ERROR, CUDA_ERROR, NCCL_ERROR, UNSUPPORTED, OUT_OF_MEMORY = range(7)
 FLAG_ALLOW_PUT = 1
