@@ -135,6 +135,12 @@ qmcg_status qmcg_time_perm_build(qmcg_ctx* ctx, int64_t n_paths, uint64_t seed, 
                                  double* ms);
 /* Number of kernels the last qmcg_price_american* call launched. */
 int64_t qmcg_last_launch_count(qmcg_ctx* ctx);
+/* The context's CUDA stream (a cudaStream_t) so a caller can record its own
+ * events around a sequence of calls. */
+void* qmcg_get_stream(qmcg_ctx* ctx);
+/* Measured FP64 FMA issue rate of this device (instructions/s), from a
+ * dependent-chain-free DFMA kernel run for about `ms` milliseconds. */
+qmcg_status qmcg_fp64_peak(qmcg_ctx* ctx, double ms, double* inst_per_s);
 
 #ifdef __cplusplus
 }

@@ -823,4 +823,29 @@ qmcg_status qmcg_time_perm_build(qmcg_ctx* c, int64_t n, uint64_t seed, int64_t 
 
 int64_t qmcg_last_launch_count(qmcg_ctx* c) { return c ? c->launches : 0; }
 
+void* qmcg_get_stream(qmcg_ctx* c) { return c ? static_cast<void*>(c->stream) : nullptr; }
+
+qmcg_status qmcg_fp64_peak(qmcg_ctx* c, double ms, double* inst_per_s) {
+  if (!c || !inst_per_s || !(ms > 0.0)) return fail(QMCG_INVALID_ARGUMENT, "qmcg_fp64_peak: bad argument");
+  std::lock_guard<std::mutex> lock(c->mu);
+  DeviceGuard g(c->device);
+  int sms = 0;
+  QMCG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device));
+  const int blocks = sms * 8;
+  QMCG_CUDA(c->d_values.reserve(static_cast<size_t>(blocks) * 256));
+  int iters = 64;
+  float f = 0.f;
+  for (int rep = 0; rep < 8; ++rep) {  // grow until the launch lasts about `ms`
+    QMCG_CUDA(cudaEventRecord(c->ev[0], c->stream));
+    QMCG_CUDA(qmcg::launch_dfma_probe(c->d_values.ptr, blocks, iters, c->stream));
+    QMCG_CUDA(cudaEventRecord(c->ev[1], c->stream));
+    QMCG_CUDA(cudaEventSynchronize(c->ev[1]));
+    QMCG_CUDA(cudaEventElapsedTime(&f, c->ev[0], c->ev[1]));
+    if (f >= 0.5 * ms) break;
+    iters = static_cast<int>(iters * std::min(16.0, std::max(2.0, ms / std::max(f, 1e-3f))));
+  }
+  *inst_per_s = static_cast<double>(blocks) * 256.0 * iters * 128.0 / (f * 1e-3);
+  return QMCG_OK;
+}
+
 }  // extern "C"

@@ -887,6 +887,30 @@ cudaError_t launch_price_k(const PriceParams& P, cudaStream_t s) {
   return slow ? launch_price_t<KIND, RNEG, true>(P, s) : launch_price_t<KIND, RNEG, false>(P, s);
 }
 
+namespace {
+__global__ void __launch_bounds__(256) dfma_probe_kernel(double* out, int iters, double a, double b) {
+  double x[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) x[k] = threadIdx.x * 1e-3 + k;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) x[k] = fma(x[k], a, b);
+    }
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) s += x[k];
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+}  // namespace
+
+cudaError_t launch_dfma_probe(double* out, int blocks, int iters, cudaStream_t s) {
+  dfma_probe_kernel<<<blocks, 256, 0, s>>>(out, iters, 0.9999, 1e-3);
+  return cudaGetLastError();
+}
+
 cudaError_t ensure_log_table(cudaStream_t s) {
   static bool done[64] = {};
   int dev = 0;

@@ -85,6 +85,8 @@ inline int64_t table_ld(int64_t cols) { return (cols + 63) / 64 * 64; }
 // Extra elements allocated after the last row (bulk copies of a partial block
 // may read up to one block past the end of a row).
 constexpr int64_t kTablePad = 256;
+// DFMA throughput probe: blocks x 256 threads x iters x 128 independent DFMAs.
+cudaError_t launch_dfma_probe(double* out, int blocks, int iters, cudaStream_t s);
 // Pairwise-tree sums of v and v*v over `len` values (reference pairwise_sum
 // with 64-element leaves). out2[0] = sum, out2[1] = sum of squares.
 size_t reduce_scratch_doubles(int64_t len);

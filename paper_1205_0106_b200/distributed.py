@@ -1,0 +1,84 @@
+"""Multi-GPU path sharding (one process per GPU, torch.distributed for plumbing).
+
+Paths are independent end to end (the foresight rule is per path, reference
+proj/src/american.cpp:32-68), so the only exchange is the final reduction.
+The reference reduces with a fixed pairwise tree (pairwise_sum,
+proj/src/path_engine.cpp:37-47); ranks own whole subtrees of that tree -- the
+nodes at depth ceil(log2 world) -- and compute their subtree sums (sum v,
+sum v^2) on their GPU. The node table is all-gathered (16 bytes per node, no
+arithmetic in the collective) and every rank folds it up the same tree on the
+host (qmcg_combine_nodes). The result is therefore bit-identical for any
+world size, exactly as the reference is for any lane count.
+"""
+from __future__ import annotations
+
+import math
+from typing import Callable, List, Optional, Tuple
+
+import numpy as np
+
+from . import qmcg
+
+
+def tree_depth(n_paths: int, world_size: int) -> int:
+    """Smallest depth with at least world_size nodes whose ancestors are all split (> 64 paths)."""
+    want = 0 if world_size <= 1 else math.ceil(math.log2(world_size))
+    depth = 0
+    while depth < want:
+        # nodes at depth+1 exist only if every node at `depth` is larger than a leaf (64)
+        smallest = n_paths >> depth  # floor(n / 2^depth) is the smallest node size at this depth
+        if smallest <= 64:
+            break
+        depth += 1
+    return depth
+
+
+def node_owner(depth: int, world_size: int) -> List[int]:
+    """Contiguous assignment of the 2^depth nodes to ranks (rank r owns a contiguous path range)."""
+    nodes = 1 << depth
+    return [min(world_size - 1, (i * world_size) // nodes) for i in range(nodes)]
+
+
+def rank_nodes(depth: int, world_size: int, rank: int) -> List[int]:
+    return [i for i, r in enumerate(node_owner(depth, world_size)) if r == rank]
+
+
+def combine(n_paths: int, depth: int, table: np.ndarray) -> Tuple[float, float]:
+    """Fold the (2^depth, 2) node table up the reference tree -> (price, std_error)."""
+    return qmcg.combine_nodes(n_paths, depth, table)
+
+
+def price_american_sharded(spec: "qmcg.OptionSpec", m: int, n_paths: int, seed: int, *,
+                           ctx: Optional["qmcg.Context"] = None,
+                           node_sums_fn: Optional[Callable[[int, int], np.ndarray]] = None,
+                           allow_put: bool = False, group=None) -> Tuple[float, float, int]:
+    """Price one option with the paths sharded over the ranks of `group`.
+
+    node_sums_fn(depth, node) -> [sum v, sum v^2] defaults to the GPU kernel on
+    `ctx` (qmcg_price_american_node). Returns (price, std_error, depth).
+    """
+    import torch
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    depth = tree_depth(n_paths, world)
+    if node_sums_fn is None:
+        if ctx is None:
+            raise ValueError("price_american_sharded: pass ctx or node_sums_fn")
+        node_sums_fn = lambda d, node: ctx.price_american_node(spec, m, n_paths, seed, d, node,  # noqa: E731
+                                                               allow_put=allow_put)
+    table = np.zeros((1 << depth, 2), dtype=np.float64)
+    for node in rank_nodes(depth, world, rank):
+        table[node] = node_sums_fn(depth, node)
+    if world > 1:
+        backend = dist.get_backend(group)
+        dev = torch.device("cuda", torch.cuda.current_device()) if backend == "nccl" else torch.device("cpu")
+        local = torch.from_numpy(table).to(dev)
+        gathered = [torch.empty_like(local) for _ in range(world)]
+        dist.all_gather(gathered, local, group=group)
+        owners = node_owner(depth, world)
+        rows = [gathered[r].cpu().numpy() for r in range(world)]
+        table = np.stack([rows[owners[i]][i] for i in range(1 << depth)])
+    price, se = combine(n_paths, depth, table)
+    return price, se, depth

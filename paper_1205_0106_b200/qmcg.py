@@ -33,7 +33,7 @@ EXPORTS = (
     "qmcg_price_american_batch", "qmcg_price_american_node", "qmcg_tree_node_range",
     "qmcg_combine_nodes", "qmcg_warm", "qmcg_clear_cache", "qmcg_permutation", "qmcg_uniforms",
     "qmcg_normals", "qmcg_path_values", "qmcg_time_device", "qmcg_time_perm_build",
-    "qmcg_last_launch_count",
+    "qmcg_last_launch_count", "qmcg_get_stream", "qmcg_fp64_peak",
 )
 
 
@@ -123,6 +123,9 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
         L.qmcg_time_perm_build.argtypes = [P, I64, U64, I64, PD]
         L.qmcg_last_launch_count.argtypes = [P]
         L.qmcg_last_launch_count.restype = I64
+        L.qmcg_get_stream.argtypes = [P]
+        L.qmcg_get_stream.restype = P
+        L.qmcg_fp64_peak.argtypes = [P, D, PD]
         _lib = L
         return L
 
@@ -254,6 +257,16 @@ class Context:
 
     def last_launch_count(self) -> int:
         return int(self._lib.qmcg_last_launch_count(self._h))
+
+    def stream_ptr(self) -> int:
+        """The context's cudaStream_t (wrap with torch.cuda.ExternalStream to record events)."""
+        return int(self._lib.qmcg_get_stream(self._h) or 0)
+
+    def fp64_peak(self, ms: float = 50.0) -> float:
+        """Measured DFMA issue rate of the device, instructions per second."""
+        out = C.c_double()
+        _check(self._lib.qmcg_fp64_peak(self._h, float(ms), C.byref(out)))
+        return out.value
 
 
 def tree_node_range(n_paths: int, depth: int, node: int):

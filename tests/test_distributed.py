@@ -1,0 +1,64 @@
+"""The multi-GPU sharding host logic on CPU: world_size 2 (and 3, 4) over gloo.
+Each rank owns whole subtrees of the reference's pairwise tree; the per-node
+sums come from the oracle's per-path values here (on the GPU box they come from
+the kernel, qmcg_price_american_node). The result must be bit-identical to the
+single-process reduce_stats, like the reference across lane counts."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.multiprocessing as mp
+
+SPEC = (100.0, 100.0, 0.05, 0.2, 1.0)
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _worker(rank, world, port, n, m, out):
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import torch.distributed as dist
+    import oracle
+    import paper_1205_0106_b200 as q
+    from paper_1205_0106_b200 import distributed
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    O = oracle.Oracle()
+    _, _, vals = O.price_american(*SPEC, m, n, 42, want_values=True)
+    calls = []
+
+    def node_sums(depth, node):
+        b, e = q.tree_node_range(n, depth, node)
+        calls.append((b, e))
+        return np.array([O.pairwise_sum(vals[b:e]), O.pairwise_sum(vals[b:e] ** 2)])
+
+    spec = q.OptionSpec(*SPEC)
+    price, se, depth = distributed.price_american_sharded(spec, m, n, 42, node_sums_fn=node_sums)
+    out[rank] = (price, se, depth, calls)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3, 4])
+def test_sharded_reduction_bit_identical(world, oracle_lib):
+    n, m = 3001, 12
+    ref_price, ref_se = oracle_lib.price_american(*SPEC, m, n, 42)
+    manager = mp.Manager()
+    out = manager.dict()
+    mp.spawn(_worker, args=(world, _free_port(), n, m, out), nprocs=world, join=True)
+    covered = sorted(r for rank in range(world) for r in out[rank][3])
+    assert covered[0][0] == 0 and covered[-1][1] == n
+    assert all(a[1] == b[0] for a, b in zip(covered, covered[1:]))  # disjoint, contiguous cover
+    for rank in range(world):
+        price, se, depth, _ = out[rank]
+        assert (price, se) == (ref_price, ref_se)
+        assert (1 << depth) >= world
