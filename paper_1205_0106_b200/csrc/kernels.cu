@@ -346,23 +346,46 @@ constexpr uint32_t kWTailIdx = kWRqCode + kRecCap * 4;
 constexpr uint32_t kWarpBytes = kWTailIdx + kTailCap;
 constexpr uint32_t kSmemBytes = kWarpOff + kWarps * kWarpBytes;
 
-template <int KIND, bool RNEG>
-__device__ __noinline__ void process_records(const PriceParams& P, uint32_t ws, uint32_t head, uint32_t count,
-                                             int lane) {
+// Exact evaluation of up to 32 queued records: term = disc^date * intrinsic(exp(X0 + b V)),
+// folded into the owner lane's running maximum (doubles >= 0 order like their bits).
+template <int KIND>
+__device__ __forceinline__ void eval_records(double b, double X0, double strike, const double* __restrict__ dpow,
+                                             uint32_t ws, uint32_t head, uint32_t count, int lane) {
   if (static_cast<uint32_t>(lane) < count) {
     const uint32_t slot = (head + lane) & (kRecCap - 1);
     const double v = lds_f64(ws + kWRqV + slot * 8);
     const uint32_t code = lds_u32(ws + kWRqCode + slot * 4);
     const int d = static_cast<int>(code >> 5);
     const uint32_t owner = code & 31u;
-    const double s = exp(fma(P.b, v, P.X0));
-    double intr = KIND == 0 ? s - P.strike : P.strike - s;
+    const double s = exp(fma(b, v, X0));
+    double intr = KIND == 0 ? s - strike : strike - s;
     intr = intr > 0.0 ? intr : 0.0;
-    const double term = intr * __ldg(P.dpow + d + 1);
+    const double term = intr * __ldg(dpow + d + 1);
     asm volatile("atom.shared.max.u64 _, [%0], %1;" ::"r"(ws + kWBest + owner * 8),
                  "l"(static_cast<unsigned long long>(__double_as_longlong(term)))
                  : "memory");
   }
+}
+
+// Out-of-line copy for the rare call sites (ring overflow inside a tile, end of
+// path). Scalars only: a reference to the kernel parameters would force a
+// per-thread local copy of them.
+template <int KIND>
+__device__ __noinline__ void eval_records_call(double b, double X0, double strike, const double* dpow, uint32_t ws,
+                                               uint32_t head, uint32_t count, int lane) {
+  eval_records<KIND>(b, X0, strike, dpow, ws, head, count, lane);
+}
+
+template <int KIND, bool RNEG>
+__device__ __forceinline__ void process_records_inline(const PriceParams& P, uint32_t ws, uint32_t head,
+                                                       uint32_t count, int lane) {
+  eval_records<KIND>(P.b, P.X0, P.strike, P.dpow, ws, head, count, lane);
+}
+
+template <int KIND, bool RNEG>
+__device__ __forceinline__ void process_records(const PriceParams& P, uint32_t ws, uint32_t head, uint32_t count,
+                                                int lane) {
+  eval_records_call<KIND>(P.b, P.X0, P.strike, P.dpow, ws, head, count, lane);
 }
 
 // Threshold in V units below/above which a date cannot beat `best` when
@@ -408,8 +431,8 @@ __device__ __forceinline__ void mbar_wait_u32(uint32_t bar, uint32_t parity) {
 
 // Evaluate the queued Moro-tail points of one date row, 32 per round:
 // u -> y = u - 0.5 (exact as the reference), w = u or 1 - u, z = +-P8(log(-log w)).
-__device__ __noinline__ void flush_tail(uint32_t ws, uint32_t zrow, uint32_t ntail, uint32_t logtab, double alpha,
-                                        int lane) {
+__device__ __forceinline__ void flush_tail_inline(uint32_t ws, uint32_t zrow, uint32_t ntail, uint32_t logtab,
+                                                  double alpha, int lane) {
   __syncwarp();
   for (uint32_t r = 0; r < ntail; r += 32) {
     const uint32_t q = r + lane;
@@ -421,6 +444,12 @@ __device__ __noinline__ void flush_tail(uint32_t ws, uint32_t zrow, uint32_t nta
     }
   }
   __syncwarp();
+}
+
+// Out-of-line variant for the rare mid-row overflow of the queue.
+__device__ __noinline__ void flush_tail(uint32_t ws, uint32_t zrow, uint32_t ntail, uint32_t logtab, double alpha,
+                                        int lane) {
+  flush_tail_inline(ws, zrow, ntail, logtab, alpha, lane);
 }
 
 // One point of a date row: tail test, predicated push of a tail point, central
@@ -474,24 +503,51 @@ __device__ __forceinline__ double halton_fixed(uint32_t x, uint32_t magic, uint3
 }
 
 template <int D>
-__device__ __forceinline__ void generate_row_fixed(const double2* sn, uint32_t magic, uint32_t shift, uint32_t negp,
-                                                   uint32_t ws, uint32_t prow, uint32_t zrow, uint32_t logtab,
-                                                   int nchunks, int lane, unsigned lt, double alpha) {
+__device__ __forceinline__ uint32_t generate_row_fixed(const double2* sn, uint32_t magic, uint32_t shift,
+                                                       uint32_t negp, uint32_t ws, uint32_t prow, uint32_t zrow,
+                                                       uint32_t logtab, int nchunks, int lane, unsigned lt,
+                                                       double alpha) {
   double2 sc[4];
 #pragma unroll
   for (int j = 0; j < 4; ++j) sc[j] = j < D ? __ldg(sn + j) : make_double2(0.0, 0.0);
   uint32_t ntail = 0;
+  int ch = 0;
 #pragma unroll 1
-  for (int ch = 0; ch < nchunks; ++ch) {
-    const uint32_t x = lds_u32(prow + ch * 128) + 1u;
-    const double u = halton_fixed<D>(x, magic, shift, negp, sc);
-    finish_point<false>(ws, zrow + ch * 256, ch * 32 + lane, u, false, alpha, lt, ntail);
-    if (ntail > kTailCap - 32) {
+  for (; ch + 1 < nchunks; ch += 2) {  // two independent chunks in flight
+    const uint32_t xa = lds_u32(prow + ch * 128) + 1u;
+    const uint32_t xb = lds_u32(prow + ch * 128 + 128) + 1u;
+    const double ua = halton_fixed<D>(xa, magic, shift, negp, sc);
+    const double ub = halton_fixed<D>(xb, magic, shift, negp, sc);
+    const double ya = __dadd_rn(ua, -0.5);
+    const double yb = __dadd_rn(ub, -0.5);
+    const double za = moro_central_plus(ya, alpha);
+    const double zb = moro_central_plus(yb, alpha);
+    const bool ta = fabs(ya) > 0.42, tb = fabs(yb) > 0.42;
+    const unsigned ba = __ballot_sync(kFull, ta), bb = __ballot_sync(kFull, tb);
+    const uint32_t pa = ntail + __popc(ba & lt);
+    const uint32_t pb = ntail + __popc(ba) + __popc(bb & lt);
+    if (ta) {
+      sts_f64(ws + kWTail + pa * 8, ua);
+      sts_u8(ws + kWTailIdx + pa, ch * 32 + lane);
+    }
+    if (tb) {
+      sts_f64(ws + kWTail + pb * 8, ub);
+      sts_u8(ws + kWTailIdx + pb, ch * 32 + 32 + lane);
+    }
+    ntail += __popc(ba) + __popc(bb);
+    sts_f64(zrow + ch * 256, za);
+    sts_f64(zrow + ch * 256 + 256, zb);
+    if (ntail > kTailCap - 64) {
       flush_tail(ws, zrow - lane * 8, ntail, logtab, alpha, lane);
       ntail = 0;
     }
   }
-  if (ntail) flush_tail(ws, zrow - lane * 8, ntail, logtab, alpha, lane);
+  if (ch < nchunks) {
+    const uint32_t x = lds_u32(prow + ch * 128) + 1u;
+    const double u = halton_fixed<D>(x, magic, shift, negp, sc);
+    finish_point<false>(ws, zrow + ch * 256, ch * 32 + lane, u, false, alpha, lt, ntail);
+  }
+  return ntail;
 }
 
 template <bool SLOW>
@@ -502,27 +558,31 @@ __device__ __forceinline__ void generate_row(const PriceParams& P, uint32_t ws, 
   const int D = static_cast<int>((dp.z >> 8) & 0xffu);
   const double2* sn = P.scnc + dp.w;
   const double alpha = P.alpha;
+  const uint32_t zrow0 = zrow;
   prow += lane * 4;
   zrow += lane * 8;
-  if (!SLOW) {
-    if (D == 3) return generate_row_fixed<3>(sn, magic, shift, negp, ws, prow, zrow, logtab, nchunks, lane, lt, alpha);
-    if (D == 2) return generate_row_fixed<2>(sn, magic, shift, negp, ws, prow, zrow, logtab, nchunks, lane, lt, alpha);
-    if (D == 4) return generate_row_fixed<4>(sn, magic, shift, negp, ws, prow, zrow, logtab, nchunks, lane, lt, alpha);
-  }
-  const bool clamp = SLOW && ((dp.z >> 16) & DIM_CLAMP);
-  const bool wide = SLOW && ((dp.z >> 16) & DIM_WIDE);
-  const uint64_t m64 = wide ? __ldg(P.magic64 + d) : 0ull;
   uint32_t ntail = 0;
-  for (int ch = 0; ch < nchunks; ++ch) {
-    const uint32_t x = lds_u32(prow + ch * 128) + 1u;
-    const double u = wide ? halton_any<true>(x, dp, m64, sn) : halton_any<false>(x, dp, m64, sn);
-    finish_point<SLOW>(ws, zrow + ch * 256, ch * 32 + lane, u, clamp, alpha, lt, ntail);
-    if (ntail > kTailCap - 32) {
-      flush_tail(ws, zrow - lane * 8, ntail, logtab, alpha, lane);
-      ntail = 0;
+  if (!SLOW && D == 3) {
+    ntail = generate_row_fixed<3>(sn, magic, shift, negp, ws, prow, zrow, logtab, nchunks, lane, lt, alpha);
+  } else if (!SLOW && D == 4) {
+    ntail = generate_row_fixed<4>(sn, magic, shift, negp, ws, prow, zrow, logtab, nchunks, lane, lt, alpha);
+  } else if (!SLOW && D == 2) {
+    ntail = generate_row_fixed<2>(sn, magic, shift, negp, ws, prow, zrow, logtab, nchunks, lane, lt, alpha);
+  } else {
+    const bool clamp = SLOW && ((dp.z >> 16) & DIM_CLAMP);
+    const bool wide = SLOW && ((dp.z >> 16) & DIM_WIDE);
+    const uint64_t m64 = wide ? __ldg(P.magic64 + d) : 0ull;
+    for (int ch = 0; ch < nchunks; ++ch) {
+      const uint32_t x = lds_u32(prow + ch * 128) + 1u;
+      const double u = wide ? halton_any<true>(x, dp, m64, sn) : halton_any<false>(x, dp, m64, sn);
+      finish_point<SLOW>(ws, zrow + ch * 256, ch * 32 + lane, u, clamp, alpha, lt, ntail);
+      if (ntail > kTailCap - 32) {
+        flush_tail(ws, zrow0, ntail, logtab, alpha, lane);
+        ntail = 0;
+      }
     }
   }
-  if (ntail) flush_tail(ws, zrow - lane * 8, ntail, logtab, alpha, lane);
+  if (ntail) flush_tail_inline(ws, zrow0, ntail, logtab, alpha, lane);
 }
 
 template <int KIND, bool RNEG>
@@ -536,7 +596,7 @@ __device__ __forceinline__ void push_record(uint32_t ws, const PriceParams& P, b
       sts_u32(ws + kWRqCode + slot * 4, (static_cast<uint32_t>(d) << 5) | static_cast<uint32_t>(lane));
     }
     rq_tail += __popc(pb);
-    if (rq_tail - rq_head >= 32) {
+    if (rq_tail - rq_head > 32) {  // rare: the ring (64) must keep room for one more date
       __syncwarp();
       process_records<KIND, RNEG>(P, ws, rq_head, 32, lane);
       rq_head += 32;
@@ -665,6 +725,17 @@ __global__ void __launch_bounds__(kThreads, QMCG_MINB) price_kernel(const PriceP
             }
           }
         }
+      }
+    }
+    if (rq_tail - rq_head >= 32) {  // the common evaluation site, once per tile at most
+      __syncwarp();
+      process_records_inline<KIND, RNEG>(P, ws, rq_head, 32, lane);
+      rq_head += 32;
+      __syncwarp();
+      if (RNEG) {
+        unsigned long long bb;
+        asm volatile("ld.shared.u64 %0, [%1];" : "=l"(bb) : "r"(ws + kWBest + lane * 8));
+        c = rneg_threshold<KIND>(P, __longlong_as_double(static_cast<long long>(bb)));
       }
     }
   }
