@@ -24,7 +24,11 @@ namespace qmcg {
 namespace {
 
 constexpr unsigned kFull = 0xffffffffu;
-constexpr int kThreads = 256;
+#ifndef QMCG_THREADS
+#define QMCG_THREADS 256
+#endif
+constexpr int kThreads = QMCG_THREADS;  // paths per block (one per thread)
+static_assert(kThreads % 32 == 0 && kThreads <= 256, "tail queue indices are 8-bit");
 constexpr int kWarps = kThreads / 32;
 #ifndef QMCG_MINB
 #define QMCG_MINB 3
@@ -32,7 +36,7 @@ constexpr int kWarps = kThreads / 32;
 #ifndef QMCG_GEN_UNROLL
 #define QMCG_GEN_UNROLL 1
 #endif
-constexpr int kTile = 8;  // dates per tile = warps per block (one date row per warp)
+constexpr int kTile = kWarps;  // dates per tile = warps per block (one date row per warp)
 constexpr int kGenUnroll = QMCG_GEN_UNROLL;
 constexpr int kRecCap = 64;   // per-warp ring of pending record evaluations
 constexpr uint32_t kNone = 0xffffffffu;
@@ -329,8 +333,10 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 //   zt[2][kTile][256]   f64   z_k + alpha per (date, path); reused for V_k in the walk
 //   logtab[128]         f64x2 log reduction table
 //   bar[2]              mbarriers of the two perm buffers
-//   per warp: tail_w[128] f64 | rq_v[64] f64 | best[32] u64 | rq_code[64] u32 | tail_idx[128] u8
-constexpr uint32_t kTailCap = 128;  // flushed when more than kTailCap - 32 are pending
+//   per warp: rq_v[64] f64 | best[32] u64 | rq_code[64] u32 | tail_idx[256 + 32] u8
+// A Moro-tail point keeps its uniform u in its z slot until the row's tail queue
+// (indices only) is evaluated and overwrites it with z.
+constexpr uint32_t kTailCap = kThreads;  // a whole date row can be queued: no mid-row flush
 constexpr uint32_t kPermOff = 0;
 constexpr uint32_t kPermBuf = kTile * kThreads * 4;
 constexpr uint32_t kZtOff = kPermOff + 2 * kPermBuf;
@@ -338,12 +344,11 @@ constexpr uint32_t kZtBuf = kTile * kThreads * 8;
 constexpr uint32_t kLogOff = kZtOff + 2 * kZtBuf;
 constexpr uint32_t kBarOff = kLogOff + 128 * 16;
 constexpr uint32_t kWarpOff = kBarOff + 128;
-constexpr uint32_t kWTail = 0;
-constexpr uint32_t kWRqV = kWTail + kTailCap * 8;
+constexpr uint32_t kWRqV = 0;
 constexpr uint32_t kWBest = kWRqV + kRecCap * 8;
 constexpr uint32_t kWRqCode = kWBest + 32 * 8;
 constexpr uint32_t kWTailIdx = kWRqCode + kRecCap * 4;
-constexpr uint32_t kWarpBytes = kWTailIdx + kTailCap;
+constexpr uint32_t kWarpBytes = kWTailIdx + kTailCap + 32;  // + 32 dummy slots for non-tail lanes
 constexpr uint32_t kSmemBytes = kWarpOff + kWarps * kWarpBytes;
 
 // Exact evaluation of up to 32 queued records: term = disc^date * intrinsic(exp(X0 + b V)),
@@ -430,51 +435,41 @@ __device__ __forceinline__ void mbar_wait_u32(uint32_t bar, uint32_t parity) {
 }
 
 // Evaluate the queued Moro-tail points of one date row, 32 per round:
-// u -> y = u - 0.5 (exact as the reference), w = u or 1 - u, z = +-P8(log(-log w)).
-__device__ __forceinline__ void flush_tail_inline(uint32_t ws, uint32_t zrow, uint32_t ntail, uint32_t logtab,
-                                                  double alpha, int lane) {
+// u (parked in the point's z slot) -> y = u - 0.5 (exact as the reference),
+// w = u or 1 - u, z = +-P8(log(-log w)) + alpha written back to the slot.
+__device__ __forceinline__ void flush_tail(uint32_t ws, uint32_t zrow, uint32_t ntail, uint32_t logtab, double alpha,
+                                           int lane) {
   __syncwarp();
   for (uint32_t r = 0; r < ntail; r += 32) {
     const uint32_t q = r + lane;
     if (q < ntail) {
-      const double u = lds_f64(ws + kWTail + q * 8);
+      const uint32_t slot = zrow + lds_u8(ws + kWTailIdx + q) * 8;
+      const double u = lds_f64(slot);
       const double y = __dadd_rn(u, -0.5);
       const double x = moro_tail_poly(y > 0.0 ? __dadd_rn(1.0, -u) : u, logtab);
-      sts_f64(zrow + lds_u8(ws + kWTailIdx + q) * 8, (y > 0.0 ? x : -x) + alpha);
+      sts_f64(slot, (y > 0.0 ? x : -x) + alpha);
     }
   }
   __syncwarp();
 }
 
-// Out-of-line variant for the rare mid-row overflow of the queue.
-__device__ __noinline__ void flush_tail(uint32_t ws, uint32_t zrow, uint32_t ntail, uint32_t logtab, double alpha,
-                                        int lane) {
-  flush_tail_inline(ws, zrow, ntail, logtab, alpha, lane);
-}
-
-// One point of a date row: tail test, predicated push of a tail point, central
-// normal + alpha into the row (overwritten later for tail points).
+// One point of a date row: tail test; a tail point parks u in its z slot and
+// queues its index (branch-free: other lanes write a dummy slot); otherwise
+// the central normal + alpha goes to the slot.
 template <bool CLAMP>
 __device__ __forceinline__ void finish_point(uint32_t ws, uint32_t zslot, uint32_t idx, double u, bool clamp,
-                                             double alpha, unsigned lt, uint32_t& ntail) {
+                                             double alpha, int lane, unsigned lt, uint32_t& ntail) {
   if (CLAMP && clamp) u = clamp_endpoints(u);
   const double y = __dadd_rn(u, -0.5);
   const bool tail = fabs(y) > 0.42;
   const unsigned tb = __ballot_sync(kFull, tail);
-  const uint32_t pos = ntail + __popc(tb & lt);
-  if (tail) {
-    sts_f64(ws + kWTail + pos * 8, u);
-    sts_u8(ws + kWTailIdx + pos, idx);
-  }
+  const uint32_t pos = tail ? ntail + __popc(tb & lt) : kTailCap + lane;
+  sts_u8(ws + kWTailIdx + pos, idx);
   ntail += __popc(tb);
-  sts_f64(zslot, moro_central_plus(y, alpha));
+  const double z = moro_central_plus(y, alpha);
+  sts_f64(zslot, tail ? u : z);
 }
 
-// Generation phase for one date row: warp w turns the 256 permutation
-// entries of date d into z + alpha. Date constants are loaded once per row
-// and reused for the 8 chunks of 32 paths (fully unrolled, immediate smem
-// offsets); the Moro tail points of the row are compacted into a warp queue
-// and evaluated 32 at a time.
 template <bool WIDE>
 __device__ __forceinline__ double halton_any(uint32_t x, const uint4& dp, uint64_t m64, const double2* sn) {
   return halton_digits<WIDE>(x, dp.x, dp.y, dp.z & 0xffu, m64, static_cast<int>((dp.z >> 8) & 0xffu), sn);
@@ -505,8 +500,7 @@ __device__ __forceinline__ double halton_fixed(uint32_t x, uint32_t magic, uint3
 template <int D>
 __device__ __forceinline__ uint32_t generate_row_fixed(const double2* sn, uint32_t magic, uint32_t shift,
                                                        uint32_t negp, uint32_t ws, uint32_t prow, uint32_t zrow,
-                                                       uint32_t logtab, int nchunks, int lane, unsigned lt,
-                                                       double alpha) {
+                                                       int nchunks, int lane, unsigned lt, double alpha) {
   double2 sc[4];
 #pragma unroll
   for (int j = 0; j < 4; ++j) sc[j] = j < D ? __ldg(sn + j) : make_double2(0.0, 0.0);
@@ -524,28 +518,19 @@ __device__ __forceinline__ uint32_t generate_row_fixed(const double2* sn, uint32
     const double zb = moro_central_plus(yb, alpha);
     const bool ta = fabs(ya) > 0.42, tb = fabs(yb) > 0.42;
     const unsigned ba = __ballot_sync(kFull, ta), bb = __ballot_sync(kFull, tb);
-    const uint32_t pa = ntail + __popc(ba & lt);
-    const uint32_t pb = ntail + __popc(ba) + __popc(bb & lt);
-    if (ta) {
-      sts_f64(ws + kWTail + pa * 8, ua);
-      sts_u8(ws + kWTailIdx + pa, ch * 32 + lane);
-    }
-    if (tb) {
-      sts_f64(ws + kWTail + pb * 8, ub);
-      sts_u8(ws + kWTailIdx + pb, ch * 32 + 32 + lane);
-    }
-    ntail += __popc(ba) + __popc(bb);
-    sts_f64(zrow + ch * 256, za);
-    sts_f64(zrow + ch * 256 + 256, zb);
-    if (ntail > kTailCap - 64) {
-      flush_tail(ws, zrow - lane * 8, ntail, logtab, alpha, lane);
-      ntail = 0;
-    }
+    const uint32_t na = __popc(ba);
+    const uint32_t pa = ta ? ntail + __popc(ba & lt) : kTailCap + lane;
+    const uint32_t pb = tb ? ntail + na + __popc(bb & lt) : kTailCap + lane;
+    sts_u8(ws + kWTailIdx + pa, ch * 32 + lane);
+    sts_u8(ws + kWTailIdx + pb, ch * 32 + 32 + lane);
+    ntail += na + __popc(bb);
+    sts_f64(zrow + ch * 256, ta ? ua : za);
+    sts_f64(zrow + ch * 256 + 256, tb ? ub : zb);
   }
   if (ch < nchunks) {
     const uint32_t x = lds_u32(prow + ch * 128) + 1u;
     const double u = halton_fixed<D>(x, magic, shift, negp, sc);
-    finish_point<false>(ws, zrow + ch * 256, ch * 32 + lane, u, false, alpha, lt, ntail);
+    finish_point<false>(ws, zrow + ch * 256, ch * 32 + lane, u, false, alpha, lane, lt, ntail);
   }
   return ntail;
 }
@@ -558,31 +543,26 @@ __device__ __forceinline__ void generate_row(const PriceParams& P, uint32_t ws, 
   const int D = static_cast<int>((dp.z >> 8) & 0xffu);
   const double2* sn = P.scnc + dp.w;
   const double alpha = P.alpha;
-  const uint32_t zrow0 = zrow;
-  prow += lane * 4;
-  zrow += lane * 8;
+  const uint32_t pl = prow + lane * 4;
+  const uint32_t zl = zrow + lane * 8;
   uint32_t ntail = 0;
   if (!SLOW && D == 3) {
-    ntail = generate_row_fixed<3>(sn, magic, shift, negp, ws, prow, zrow, logtab, nchunks, lane, lt, alpha);
+    ntail = generate_row_fixed<3>(sn, magic, shift, negp, ws, pl, zl, nchunks, lane, lt, alpha);
   } else if (!SLOW && D == 4) {
-    ntail = generate_row_fixed<4>(sn, magic, shift, negp, ws, prow, zrow, logtab, nchunks, lane, lt, alpha);
+    ntail = generate_row_fixed<4>(sn, magic, shift, negp, ws, pl, zl, nchunks, lane, lt, alpha);
   } else if (!SLOW && D == 2) {
-    ntail = generate_row_fixed<2>(sn, magic, shift, negp, ws, prow, zrow, logtab, nchunks, lane, lt, alpha);
+    ntail = generate_row_fixed<2>(sn, magic, shift, negp, ws, pl, zl, nchunks, lane, lt, alpha);
   } else {
     const bool clamp = SLOW && ((dp.z >> 16) & DIM_CLAMP);
     const bool wide = SLOW && ((dp.z >> 16) & DIM_WIDE);
     const uint64_t m64 = wide ? __ldg(P.magic64 + d) : 0ull;
     for (int ch = 0; ch < nchunks; ++ch) {
-      const uint32_t x = lds_u32(prow + ch * 128) + 1u;
+      const uint32_t x = lds_u32(pl + ch * 128) + 1u;
       const double u = wide ? halton_any<true>(x, dp, m64, sn) : halton_any<false>(x, dp, m64, sn);
-      finish_point<SLOW>(ws, zrow + ch * 256, ch * 32 + lane, u, clamp, alpha, lt, ntail);
-      if (ntail > kTailCap - 32) {
-        flush_tail(ws, zrow0, ntail, logtab, alpha, lane);
-        ntail = 0;
-      }
+      finish_point<SLOW>(ws, zl + ch * 256, ch * 32 + lane, u, clamp, alpha, lane, lt, ntail);
     }
   }
-  if (ntail) flush_tail_inline(ws, zrow0, ntail, logtab, alpha, lane);
+  if (ntail) flush_tail(ws, zrow, ntail, logtab, alpha, lane);
 }
 
 template <int KIND, bool RNEG>
@@ -658,8 +638,8 @@ __global__ void __launch_bounds__(kThreads, QMCG_MINB) price_kernel(const PriceP
 
   double V = 0.0;
   double c = P.c0;
-  double pend_key = 0.0;  // pending (not yet evaluated) record: key = V - slope * d
-  int pend_d = -1;
+  double cd = 0.0;  // dominance threshold of the pending record (see the walk)
+  int pend_d = -1;  // date of the pending (not yet evaluated) record, -1 = none
   uint32_t rq_head = 0, rq_tail = 0;
   uint32_t err = 0;
 
@@ -676,18 +656,20 @@ __global__ void __launch_bounds__(kThreads, QMCG_MINB) price_kernel(const PriceP
       if (threadIdx.x == 0 && k + 2 < ntiles) issue_tile(P, sbase, k + 2, b, col0, bytes);
     }
     // ---- walk ----
-    const double sk0 = slope * static_cast<double>(k0);
+    // c = V of the last record (= the pending record when pend_d >= 0);
+    // cd = c + slope * (date - pend_d): the pending record j is dominated by a
+    // record at date k iff V_k >= cd (S_k disc^(k-j) >= S_j, calls).
     if (!SLOW && !RNEG && k0 + kTile <= mrec) {
 #pragma unroll
       for (int t = 0; t < kTile; ++t) {
         V = __dadd_rn(V, lds_f64(zcol + t * kThreads * 8));
+        cd = __dadd_rn(cd, slope);
         const bool rec = KIND == 0 ? V > c : V < c;
-        c = rec ? V : c;
-        const double key = V - fma(slope, static_cast<double>(t), sk0);
-        const bool push = rec && pend_d >= 0 && !(KIND == 0 && key >= pend_key);
-        const double pv = fma(slope, static_cast<double>(pend_d), pend_key);
+        const bool push = rec && pend_d >= 0 && !(KIND == 0 && V >= cd);
+        const double pv = c;
         const int pd = pend_d;
-        pend_key = rec ? key : pend_key;
+        c = rec ? V : c;
+        cd = rec ? V : cd;
         pend_d = rec ? k0 + t : pend_d;
         push_record<KIND, RNEG>(ws, P, push, pv, pd, lane, lt, rq_head, rq_tail);
       }
@@ -697,6 +679,7 @@ __global__ void __launch_bounds__(kThreads, QMCG_MINB) price_kernel(const PriceP
         const int d = k0 + t;
         if (d < m) {
           V = __dadd_rn(V, det ? P.alpha : lds_f64(zcol + t * kThreads * 8));
+          cd = __dadd_rn(cd, slope);
           if (check && active) {
             const double X = fma(P.b, V, P.X0);
             if (X < -745.1332191019412) err |= ERR_SPOT_NONPOSITIVE;
@@ -706,20 +689,13 @@ __global__ void __launch_bounds__(kThreads, QMCG_MINB) price_kernel(const PriceP
             const bool rec = KIND == 0 ? V > c : V < c;
             if (RNEG) {
               // every candidate is evaluated; the threshold follows the evaluated best
-              const uint32_t before = rq_head;
               push_record<KIND, RNEG>(ws, P, rec, V, d, lane, lt, rq_head, rq_tail);
-              if (rq_head != before) {
-                unsigned long long bb;
-                asm volatile("ld.shared.u64 %0, [%1];" : "=l"(bb) : "r"(ws + kWBest + lane * 8));
-                c = rneg_threshold<KIND>(P, __longlong_as_double(static_cast<long long>(bb)));
-              }
             } else {
-              c = rec ? V : c;
-              const double key = V - slope * static_cast<double>(d);
-              const bool push = rec && pend_d >= 0 && !(KIND == 0 && key >= pend_key);
-              const double pv = fma(slope, static_cast<double>(pend_d), pend_key);
+              const bool push = rec && pend_d >= 0 && !(KIND == 0 && V >= cd);
+              const double pv = c;
               const int pd = pend_d;
-              pend_key = rec ? key : pend_key;
+              c = rec ? V : c;
+              cd = rec ? V : cd;
               pend_d = rec ? d : pend_d;
               push_record<KIND, RNEG>(ws, P, push, pv, pd, lane, lt, rq_head, rq_tail);
             }
@@ -740,8 +716,7 @@ __global__ void __launch_bounds__(kThreads, QMCG_MINB) price_kernel(const PriceP
     }
   }
   if (!RNEG) {  // the last pending record of every path
-    push_record<KIND, RNEG>(ws, P, pend_d >= 0, fma(slope, static_cast<double>(pend_d), pend_key), pend_d, lane, lt,
-                            rq_head, rq_tail);
+    push_record<KIND, RNEG>(ws, P, pend_d >= 0, c, pend_d, lane, lt, rq_head, rq_tail);
   }
   if (rq_tail != rq_head) {
     __syncwarp();
