@@ -226,6 +226,8 @@ struct qmcg_ctx {
   DevBuf<uint64_t> d_m64;
   DevBuf<double> d_sc, d_nc, d_scnc, d_dpow;
   DevBuf<double> d_values, d_red, d_sums;
+  DevBuf<double> d_z, d_bvalues, d_bred, d_bsums;  // batch: shared normal table, per-contract values
+  DevBuf<qmcg::ContractParams> d_cparams;
   DevBuf<uint32_t> d_err, d_fullperm;
   DevBuf<char> d_permscratch;
   double* h_pinned = nullptr;  // [0..1] sums, [2] err as double bits
@@ -525,6 +527,11 @@ void qmcg_destroy(qmcg_ctx* c) {
   c->d_dpow.release();
   c->d_values.release();
   c->d_red.release();
+  c->d_z.release();
+  c->d_bvalues.release();
+  c->d_bred.release();
+  c->d_bsums.release();
+  c->d_cparams.release();
   c->d_sums.release();
   c->d_err.release();
   c->d_fullperm.release();
@@ -669,21 +676,84 @@ qmcg_status qmcg_price_american_batch(qmcg_ctx* c, const qmcg_option_spec* specs
   if (st) return st;
   st = prepare_scratch(c, static_cast<size_t>(n_specs));
   if (st) return st;
-  // all contracts share m -> one dpow upload per contract (cheap), launched back to back
+  // discount chains of every contract in one upload
   QMCG_CUDA(c->d_dpow.reserve(static_cast<size_t>(m + 1) * static_cast<size_t>(n_specs)));
-  for (int64_t i = 0; i < n_specs; ++i) {
-    CallPlan& plan = plans[static_cast<size_t>(i)];
-    double* dp = c->d_dpow.ptr + static_cast<size_t>(i) * static_cast<size_t>(m + 1);
-    QMCG_CUDA(cudaMemcpyAsync(dp, plan.dpow.data(), plan.dpow.size() * sizeof(double), cudaMemcpyHostToDevice,
+  {
+    std::vector<double> all(static_cast<size_t>(m + 1) * static_cast<size_t>(n_specs));
+    for (int64_t i = 0; i < n_specs; ++i)
+      std::copy(plans[static_cast<size_t>(i)].dpow.begin(), plans[static_cast<size_t>(i)].dpow.end(),
+                all.begin() + i * (m + 1));
+    QMCG_CUDA(cudaMemcpyAsync(c->d_dpow.ptr, all.data(), all.size() * sizeof(double), cudaMemcpyHostToDevice,
                               c->stream));
-    attach_dims(c, plan.P);
-    plan.P.dpow = dp;
-    st = enqueue_price(c, plan, 0, n, static_cast<int>(i), nullptr);
+    QMCG_CUDA(cudaStreamSynchronize(c->stream));
+  }
+  // Contracts on the plain path share one normal table (generated once, inside
+  // this call) and are walked kCpt per thread; the rest use the fused kernel.
+  std::vector<int64_t> shared_idx[2], single_idx;
+  for (int64_t i = 0; i < n_specs; ++i) {
+    const PriceParams& P = plans[static_cast<size_t>(i)].P;
+    attach_dims(c, plans[static_cast<size_t>(i)].P);
+    plans[static_cast<size_t>(i)].P.dpow = c->d_dpow.ptr + static_cast<size_t>(i) * static_cast<size_t>(m + 1);
+    if (!P.deterministic && !P.check_range && !P.rate_negative) shared_idx[P.kind].push_back(i);
+    else single_idx.push_back(i);
+  }
+  const bool use_shared = shared_idx[0].size() + shared_idx[1].size() >= 2;
+  if (!use_shared)
+    for (int k = 0; k < 2; ++k) single_idx.insert(single_idx.end(), shared_idx[k].begin(), shared_idx[k].end());
+  for (int64_t i : single_idx) {
+    st = enqueue_price(c, plans[static_cast<size_t>(i)], 0, n, static_cast<int>(i), nullptr);
     if (st) return st;
+  }
+  std::vector<double> shared_sums[2];
+  if (use_shared) {
+    QMCG_CUDA(c->d_z.reserve(static_cast<size_t>(m) * static_cast<size_t>(n)));
+    PriceParams G = plans[static_cast<size_t>(shared_idx[0].empty() ? shared_idx[1][0] : shared_idx[0][0])].P;
+    G.perm = c->table;
+    G.ld = qmcg::table_ld(c->col_end - c->col_begin);
+    G.col_begin = c->col_begin;
+    G.path_begin = 0;
+    G.path_count = n;
+    G.alpha = 0.0;
+    QMCG_CUDA(qmcg::launch_gen_z(G, c->d_z.ptr, n, c->stream));
+    c->launches += 1;
+    for (int k = 0; k < 2; ++k) {
+      const size_t cnt = shared_idx[k].size();
+      if (!cnt) continue;
+      std::vector<qmcg::ContractParams> cps(cnt);
+      for (size_t j = 0; j < cnt; ++j) {
+        const PriceParams& P = plans[static_cast<size_t>(shared_idx[k][j])].P;
+        cps[j] = qmcg::ContractParams{P.dpow, P.X0, P.b, P.alpha, P.c0, P.strike, P.best0, P.log_strike,
+                                      P.dom_slope, P.bs_vsqrt, P.bs_mu_t, P.bs_kdisc, P.bs_fwd_growth, P.bs_disc,
+                                      P.bs_v_zero, 0};
+      }
+      QMCG_CUDA(c->d_cparams.reserve(cnt));
+      QMCG_CUDA(cudaMemcpyAsync(c->d_cparams.ptr, cps.data(), cnt * sizeof(qmcg::ContractParams),
+                                cudaMemcpyHostToDevice, c->stream));
+      QMCG_CUDA(c->d_bvalues.reserve(cnt * static_cast<size_t>(n)));
+      QMCG_CUDA(c->d_bred.reserve(cnt * qmcg::reduce_scratch_doubles(n)));
+      QMCG_CUDA(c->d_bsums.reserve(2 * cnt));
+      qmcg::BatchParams B{c->d_z.ptr, n, n, static_cast<int32_t>(m), static_cast<int32_t>(cnt), c->d_cparams.ptr,
+                          c->d_bvalues.ptr};
+      QMCG_CUDA(qmcg::launch_walk_batch(B, k, c->stream));
+      int launches = 1;
+      QMCG_CUDA(qmcg::launch_pairwise_batched(c->d_bvalues.ptr, n, static_cast<int>(cnt), c->d_bred.ptr,
+                                              c->d_bsums.ptr, c->stream, &launches));
+      c->launches += launches;
+      shared_sums[k].resize(2 * cnt);
+      QMCG_CUDA(cudaMemcpyAsync(shared_sums[k].data(), c->d_bsums.ptr, 2 * cnt * sizeof(double),
+                                cudaMemcpyDeviceToHost, c->stream));
+      QMCG_CUDA(cudaStreamSynchronize(c->stream));  // d_cparams / d_bsums are reused by the next kind
+    }
   }
   std::vector<double> sums;
   st = sync_results(c, static_cast<size_t>(n_specs), sums);
   if (st) return st;
+  if (use_shared)
+    for (int k = 0; k < 2; ++k)
+      for (size_t j = 0; j < shared_idx[k].size(); ++j) {
+        sums[2 * static_cast<size_t>(shared_idx[k][j])] = shared_sums[k][2 * j];
+        sums[2 * static_cast<size_t>(shared_idx[k][j]) + 1] = shared_sums[k][2 * j + 1];
+      }
   const double el = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   for (int64_t i = 0; i < n_specs; ++i) {
     double mean, se;

@@ -754,6 +754,207 @@ __global__ void __launch_bounds__(kThreads, QMCG_MINB) price_kernel(const PriceP
   }
 }
 
+// Generation only (batches): the QMC normal table z[d][p] = moro_inv_cnd of the
+// bit-exact scrambled-Halton uniform, for all dates of this block's 256 paths.
+// Same tile staging and generation as price_kernel; rows are then streamed to
+// HBM (coalesced, 2 KB per warp-row).
+template <bool SLOW>
+__global__ void __launch_bounds__(kThreads, QMCG_MINB) gen_z_kernel(const PriceParams P, double* __restrict__ z,
+                                                                    int64_t ldz) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const uint32_t sbase = smem_u32(smem_raw);
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const uint32_t ws = sbase + kWarpOff + warp * kWarpBytes;
+  const uint32_t logtab = sbase + kLogOff;
+  const unsigned lt = lanemask_lt();
+  const int64_t block_first = static_cast<int64_t>(blockIdx.x) * kThreads;
+  const int m = P.m;
+  const int ntiles = (m + kTile - 1) / kTile;
+  const int64_t block_paths = min(static_cast<int64_t>(kThreads), P.path_count - block_first);
+  const int nchunks = static_cast<int>((block_paths + 31) / 32);
+  const int64_t col0 = P.path_begin - P.col_begin + block_first;
+  const uint32_t bytes = static_cast<uint32_t>(((block_paths + 3) / 4) * 16);
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sbase + kBarOff));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sbase + kBarOff + 8));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (threadIdx.x < 128) sts_v2f64(logtab + threadIdx.x * 16, c_log_table[threadIdx.x]);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    issue_tile(P, sbase, 0, 0, col0, bytes);
+    if (ntiles > 1) issue_tile(P, sbase, 1, 1, col0, bytes);
+  }
+  for (int k = 0; k < ntiles; ++k) {
+    const int k0 = k * kTile;
+    const int b = k & 1;
+    mbar_wait_u32(sbase + kBarOff + b * 8, static_cast<uint32_t>((k >> 1) & 1));
+    const uint32_t zrow = sbase + kZtOff + b * kZtBuf + warp * kThreads * 8;
+    if (k0 + warp < m) {
+      generate_row<SLOW>(P, ws, k0 + warp, sbase + kPermOff + b * kPermBuf + warp * kThreads * 4, zrow, logtab,
+                         nchunks, lane, lt);
+      __syncwarp();
+      double* dst = z + static_cast<int64_t>(k0 + warp) * ldz + P.path_begin + block_first;
+      for (int ch = 0; ch < nchunks; ++ch) {
+        const int idx = ch * 32 + lane;
+        if (idx < block_paths) __stcs(dst + idx, lds_f64(zrow + idx * 8));
+      }
+    }
+    __syncthreads();  // perm buffer b consumed, z tile b stored
+    if (threadIdx.x == 0 && k + 2 < ntiles) issue_tile(P, sbase, k + 2, b, col0, bytes);
+  }
+}
+
+// Batch walk over a shared normal table: thread = path, CPT contracts of one
+// kind per thread (z loaded once, used CPT times). Per contract the same
+// foresight walk as price_kernel: V_c,k = Z_k + (k+1) alpha_c with
+// Z_k = sum_{j<=k} z_j, records filtered by the running extreme and the
+// pending-record dominance test, survivors evaluated 32 per warp.
+// blockIdx.x = contract group (fastest), so the 256-path z block of
+// blockIdx.y stays in L2 while every contract group reads it.
+constexpr int kCpt = 4;
+constexpr uint32_t kBWarpBytes = kCpt * (kRecCap * 12 + 32 * 8);
+
+template <int KIND>
+__global__ void __launch_bounds__(kThreads, 2) walk_batch_kernel(const BatchParams B) {
+  __shared__ __align__(16) unsigned char sm[kWarps * kBWarpBytes];
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const unsigned lt = lanemask_lt();
+  const uint32_t wbase = smem_u32(sm) + warp * kBWarpBytes;
+  const int64_t p = static_cast<int64_t>(blockIdx.y) * kThreads + threadIdx.x;
+  const bool active = p < B.n;
+  const int c_first = blockIdx.x * kCpt;
+  const int m = B.m;
+  const int mrec = m - 1;
+  // per-contract state
+  double c[kCpt], cd[kCpt], alpha[kCpt], slope[kCpt];
+  int pend_d[kCpt];
+  uint32_t rq_head[kCpt], rq_tail[kCpt];
+  const ContractParams* cp[kCpt];
+#pragma unroll
+  for (int i = 0; i < kCpt; ++i) {
+    const int ci = min(c_first + i, B.count - 1);
+    cp[i] = B.cp + ci;
+    c[i] = cp[i]->c0;
+    cd[i] = 0.0;
+    alpha[i] = cp[i]->alpha;
+    slope[i] = cp[i]->dom_slope;
+    pend_d[i] = -1;
+    rq_head[i] = rq_tail[i] = 0;
+    const uint32_t ws = wbase + i * (kRecCap * 12 + 32 * 8);
+    asm volatile("st.shared.u64 [%0], %1;" ::"r"(ws + kRecCap * 12 + lane * 8),
+                 "l"(static_cast<unsigned long long>(__double_as_longlong(cp[i]->best0)))
+                 : "memory");
+  }
+  __syncwarp();
+  const double* zc = B.z + (active ? p : 0);
+  double Z = 0.0, kd = 0.0;
+  for (int d = 0; d < m; ++d) {
+    const double zv = __ldg(zc + static_cast<int64_t>(d) * B.ldz);
+    Z = __dadd_rn(Z, zv);
+    kd = __dadd_rn(kd, 1.0);
+    if (d < mrec) {
+#pragma unroll
+      for (int i = 0; i < kCpt; ++i) {
+        const double V = fma(alpha[i], kd, Z);
+        cd[i] = __dadd_rn(cd[i], slope[i]);
+        const bool rec = KIND == 0 ? V > c[i] : V < c[i];
+        const bool push = active && rec && pend_d[i] >= 0 && !(KIND == 0 && V >= cd[i]);
+        const double pv = c[i];
+        const int pd = pend_d[i];
+        c[i] = rec ? V : c[i];
+        cd[i] = rec ? V : cd[i];
+        pend_d[i] = rec ? d : pend_d[i];
+        const unsigned pb = __ballot_sync(kFull, push);
+        if (pb) {
+          const uint32_t ws = wbase + i * (kRecCap * 12 + 32 * 8);
+          if (push) {
+            const uint32_t slot = (rq_tail[i] + __popc(pb & lt)) & (kRecCap - 1);
+            sts_f64(ws + slot * 8, pv);
+            sts_u32(ws + kRecCap * 8 + slot * 4, (static_cast<uint32_t>(pd) << 5) | static_cast<uint32_t>(lane));
+          }
+          rq_tail[i] += __popc(pb);
+          if (rq_tail[i] - rq_head[i] >= 32) {
+            __syncwarp();
+            const ContractParams& q = *cp[i];
+            if (true) {
+              const uint32_t slot = (rq_head[i] + lane) & (kRecCap - 1);
+              const double v = lds_f64(ws + slot * 8);
+              const uint32_t code = lds_u32(ws + kRecCap * 8 + slot * 4);
+              const double sv = exp(fma(q.b, v, q.X0));
+              double intr = KIND == 0 ? sv - q.strike : q.strike - sv;
+              intr = intr > 0.0 ? intr : 0.0;
+              const double term = intr * __ldg(q.dpow + (code >> 5) + 1);
+              asm volatile("atom.shared.max.u64 _, [%0], %1;" ::"r"(ws + kRecCap * 12 + (code & 31u) * 8),
+                           "l"(static_cast<unsigned long long>(__double_as_longlong(term)))
+                           : "memory");
+            }
+            rq_head[i] += 32;
+            __syncwarp();
+          }
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < kCpt; ++i) {
+    const ContractParams& q = *cp[i];
+    const uint32_t ws = wbase + i * (kRecCap * 12 + 32 * 8);
+    const bool push = active && pend_d[i] >= 0;
+    const unsigned pb = __ballot_sync(kFull, push);
+    if (push) {
+      const uint32_t slot = (rq_tail[i] + __popc(pb & lt)) & (kRecCap - 1);
+      sts_f64(ws + slot * 8, c[i]);
+      sts_u32(ws + kRecCap * 8 + slot * 4, (static_cast<uint32_t>(pend_d[i]) << 5) | static_cast<uint32_t>(lane));
+    }
+    rq_tail[i] += __popc(pb);
+    __syncwarp();
+    while (rq_tail[i] != rq_head[i]) {
+      const uint32_t cnt = min(32u, rq_tail[i] - rq_head[i]);
+      if (static_cast<uint32_t>(lane) < cnt) {
+        const uint32_t slot = (rq_head[i] + lane) & (kRecCap - 1);
+        const double v = lds_f64(ws + slot * 8);
+        const uint32_t code = lds_u32(ws + kRecCap * 8 + slot * 4);
+        const double sv = exp(fma(q.b, v, q.X0));
+        double intr = KIND == 0 ? sv - q.strike : q.strike - sv;
+        intr = intr > 0.0 ? intr : 0.0;
+        const double term = intr * __ldg(q.dpow + (code >> 5) + 1);
+        asm volatile("atom.shared.max.u64 _, [%0], %1;" ::"r"(ws + kRecCap * 12 + (code & 31u) * 8),
+                     "l"(static_cast<unsigned long long>(__double_as_longlong(term)))
+                     : "memory");
+      }
+      rq_head[i] += cnt;
+      __syncwarp();
+    }
+    // date m
+    const double V = fma(alpha[i], kd, Z);
+    const double X = fma(q.b, V, q.X0);
+    const double sl = exp(X);
+    double cont;
+    if (q.bs_v_zero) {
+      const double fwd = sl * q.bs_fwd_growth;
+      const double iv = KIND == 0 ? fwd - q.strike : q.strike - fwd;
+      cont = q.bs_disc * (iv > 0.0 ? iv : 0.0);
+    } else {
+      const double d1 = (X - q.log_strike + q.bs_mu_t) / q.bs_vsqrt;
+      const double d2 = d1 - q.bs_vsqrt;
+      const double price = KIND == 0 ? sl * cnd_dev(d1) - q.bs_kdisc * cnd_dev(d2)
+                                     : q.bs_kdisc * cnd_dev(-d2) - sl * cnd_dev(-d1);
+      cont = price > 0.0 ? price : 0.0;
+    }
+    double intr = KIND == 0 ? sl - q.strike : q.strike - sl;
+    intr = intr > 0.0 ? intr : 0.0;
+    const double cm = intr > cont ? intr : cont;
+    const double term_m = cm * __ldg(q.dpow + m);
+    unsigned long long bb;
+    asm volatile("ld.shared.u64 %0, [%1];" : "=l"(bb) : "r"(ws + kRecCap * 12 + lane * 8));
+    const double best = __longlong_as_double(static_cast<long long>(bb));
+    if (active && c_first + i < B.count) B.values[static_cast<int64_t>(c_first + i) * B.n + p] = best > term_m ? best : term_m;
+  }
+}
+
 // D1: uniforms (or Moro normals) of one dimension for `count` paths.
 __global__ void uniforms_kernel(const uint32_t* __restrict__ perm_row, int64_t count, DimParam dp,
                                 const double* __restrict__ sc, const double* __restrict__ nc,
@@ -864,7 +1065,9 @@ __device__ __forceinline__ void seq_sum(const double* __restrict__ v, int64_t of
 }
 
 __global__ void pairwise_leaves_kernel(const double* __restrict__ v, int64_t len, int depth,
-                                       double* __restrict__ out) {
+                                       double* __restrict__ out, int64_t out_stride) {
+  v += static_cast<int64_t>(blockIdx.y) * len;
+  out += static_cast<int64_t>(blockIdx.y) * out_stride;
   const int64_t node = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (node >= (int64_t{1} << depth)) return;
   int64_t off, size;
@@ -886,8 +1089,10 @@ __global__ void pairwise_leaves_kernel(const double* __restrict__ v, int64_t len
 
 // Reduces groups of `group` (power of two <= 1024) consecutive node pairs.
 __global__ void pairwise_tree_kernel(const double* __restrict__ in, int64_t count, int group,
-                                     double* __restrict__ out) {
+                                     double* __restrict__ out, int64_t in_stride, int64_t out_stride) {
   __shared__ double s[1024], s2[1024];
+  in += static_cast<int64_t>(blockIdx.y) * in_stride;
+  out += static_cast<int64_t>(blockIdx.y) * out_stride;
   const int64_t base = static_cast<int64_t>(blockIdx.x) * group;
   for (int i = threadIdx.x; i < group; i += blockDim.x) {
     s[i] = in[2 * (base + i)];
@@ -954,6 +1159,29 @@ __global__ void __launch_bounds__(256) dfma_probe_kernel(double* out, int iters,
 
 cudaError_t launch_dfma_probe(double* out, int blocks, int iters, cudaStream_t s) {
   dfma_probe_kernel<<<blocks, 256, 0, s>>>(out, iters, 0.9999, 1e-3);
+  return cudaGetLastError();
+}
+
+cudaError_t ensure_log_table(cudaStream_t s);
+
+cudaError_t launch_gen_z(const PriceParams& P, double* z, int64_t ldz, cudaStream_t s) {
+  if (P.path_count <= 0) return cudaSuccess;
+  cudaError_t e = ensure_log_table(s);
+  if (e != cudaSuccess) return e;
+  const int64_t blocks = (P.path_count + kThreads - 1) / kThreads;
+  const bool slow = P.any_wide || P.any_clamp;
+  auto kern = slow ? gen_z_kernel<true> : gen_z_kernel<false>;
+  e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmemBytes));
+  if (e != cudaSuccess) return e;
+  kern<<<static_cast<unsigned>(blocks), kThreads, kSmemBytes, s>>>(P, z, ldz);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_walk_batch(const BatchParams& B, int kind, cudaStream_t s) {
+  if (B.count <= 0 || B.n <= 0) return cudaSuccess;
+  const dim3 grid(static_cast<unsigned>((B.count + kCpt - 1) / kCpt), static_cast<unsigned>((B.n + kThreads - 1) / kThreads));
+  if (kind == 0) walk_batch_kernel<0><<<grid, kThreads, 0, s>>>(B);
+  else walk_batch_kernel<1><<<grid, kThreads, 0, s>>>(B);
   return cudaGetLastError();
 }
 
@@ -1048,31 +1276,42 @@ size_t reduce_scratch_doubles(int64_t len) {
   const int L = leaf_depth(len);
   const int D = L > 0 ? L - 1 : 0;
   const int64_t nodes = int64_t{1} << D;
-  return static_cast<size_t>(2 * nodes + 2 * ((nodes + 1023) / 1024) + 4);
+  return static_cast<size_t>(2 * nodes + 2 * ((nodes + 1023) / 1024));
 }
 
-cudaError_t launch_pairwise(const double* v, int64_t len, double* scratch, double* out2, cudaStream_t s,
-                            int* launches) {
+cudaError_t launch_pairwise_batched(const double* v, int64_t len, int count, double* scratch, double* out2,
+                                    cudaStream_t s, int* launches) {
   const int L = leaf_depth(len);
   const int D = L > 0 ? L - 1 : 0;
   int64_t nodes = int64_t{1} << D;
+  // per contract: 2*nodes (level A) + 2*ceil(nodes/1024) (level B) doubles of scratch
+  const int64_t strideA = 2 * nodes, strideB = 2 * ((nodes + 1023) / 1024);
   double* a = scratch;
-  double* b = scratch + 2 * nodes;
+  double* b = scratch + strideA * count;
+  int64_t sa = strideA, sb = strideB;
   {
-    const int64_t blocks = (nodes + 255) / 256;
-    pairwise_leaves_kernel<<<static_cast<unsigned>(blocks), 256, 0, s>>>(v, len, D, nodes == 1 ? out2 : a);
+    const dim3 grid(static_cast<unsigned>((nodes + 255) / 256), static_cast<unsigned>(count));
+    pairwise_leaves_kernel<<<grid, 256, 0, s>>>(v, len, D, nodes == 1 ? out2 : a, nodes == 1 ? 2 : sa);
     if (launches) ++*launches;
   }
   while (nodes > 1) {
     const int group = static_cast<int>(std::min<int64_t>(nodes, 1024));
     const int64_t blocks = nodes / group;
-    double* dst = blocks == 1 ? out2 : b;
-    pairwise_tree_kernel<<<static_cast<unsigned>(blocks), 256, 0, s>>>(a, nodes, group, dst);
+    const bool last = blocks == 1;
+    double* dst = last ? out2 : b;
+    const dim3 grid(static_cast<unsigned>(blocks), static_cast<unsigned>(count));
+    pairwise_tree_kernel<<<grid, 256, 0, s>>>(a, nodes, group, dst, sa, last ? 2 : sb);
     if (launches) ++*launches;
     nodes = blocks;
     std::swap(a, b);
+    std::swap(sa, sb);
   }
   return cudaGetLastError();
+}
+
+cudaError_t launch_pairwise(const double* v, int64_t len, double* scratch, double* out2, cudaStream_t s,
+                            int* launches) {
+  return launch_pairwise_batched(v, len, 1, scratch, out2, s, launches);
 }
 
 }  // namespace qmcg

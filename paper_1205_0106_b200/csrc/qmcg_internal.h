@@ -69,7 +69,33 @@ struct PriceParams {
   uint32_t* err;
 };
 
+// Per-contract constants of a batch walk (same meaning as in PriceParams).
+struct ContractParams {
+  const double* dpow;
+  double X0, b, alpha, c0, strike, best0, log_strike, dom_slope;
+  double bs_vsqrt, bs_mu_t, bs_kdisc, bs_fwd_growth, bs_disc;
+  int32_t bs_v_zero, pad;
+};
+
+// Batch pricing over a shared normal table z[m][ldz] (z = Moro normal, no drift).
+struct BatchParams {
+  const double* z;
+  int64_t ldz;
+  int64_t n;                  // paths
+  int32_t m;                  // dates
+  int32_t count;              // contracts in this launch (all of one kind)
+  const ContractParams* cp;   // count entries
+  double* values;             // [count][n]
+};
+
 // ---- launchers (kernels.cu) ----
+// Generation only: the QMC normal table z[d][p] (d < m, p in [path_begin, +path_count)) of the
+// context's permutation table (PriceParams fields perm/ld/col_begin/dims/... ; alpha ignored).
+cudaError_t launch_gen_z(const PriceParams& P, double* z, int64_t ldz, cudaStream_t s);
+cudaError_t launch_walk_batch(const BatchParams& B, int kind, cudaStream_t s);
+// Pairwise sums of `count` contiguous vectors v[c*len .. (c+1)*len) into out2[2c, 2c+1].
+cudaError_t launch_pairwise_batched(const double* v, int64_t len, int count, double* scratch, double* out2,
+                                    cudaStream_t s, int* launches);
 cudaError_t launch_price(const PriceParams& P, cudaStream_t s);
 // K1: Fisher-Yates permutation of length n for LCG seed `seed64` into out[0..n).
 // scratch must hold perm_scratch_bytes(n) bytes.

@@ -141,11 +141,32 @@ def test_node_decomposition_bit_identical(ctx, qmcg):
 
 
 def test_batch_matches_single(ctx, qmcg):
+    """Batch pricing (shared normal table generated once + multi-contract walk) against
+    single calls: the same numbers up to the order of the log-price additions."""
     specs = [spec_of(qmcg, (100.0, 80 + 4 * i, 0.05, 0.1 + 0.05 * i, 1.0), kind=i % 2) for i in range(6)]
-    batch = ctx.price_american_batch(specs, 24, 1 << 14, 42, allow_put=True)
+    specs.append(spec_of(qmcg, (100.0, 100.0, -0.01, 0.2, 1.0)))   # r < 0: fused path inside the batch
+    specs.append(spec_of(qmcg, (100.0, 100.0, 0.05, 0.0, 1.0)))    # sigma = 0: fused path inside the batch
+    batch = ctx.price_american_batch(specs, 24, (1 << 14) + 77, 42, allow_put=True)
     for s, r in zip(specs, batch):
-        one = ctx.price_american(s, 24, 1 << 14, 42, allow_put=True)
-        assert (one.price, one.std_error) == (r.price, r.std_error)
+        one = ctx.price_american(s, 24, (1 << 14) + 77, 42, allow_put=True)
+        assert abs(one.price - r.price) <= 1e-12 * max(one.price, 1e-300), (s, one.price, r.price)
+        assert abs(one.std_error - r.std_error) <= 1e-9 * one.std_error + 1e-12
+
+
+def test_config4_grid_vs_oracle(ctx, qmcg, oracle_lib):
+    """Config 4's contract grid (32 strikes x 32 vols, calls for even i+j) at a reduced size:
+    every contract of an 8 x 8 sub-grid against the C restatement."""
+    specs, raw = [], []
+    for i in range(0, 32, 4):
+        for j in range(0, 32, 4):
+            sp = (100.0, 80 + 40 * i / 31, 0.05, 0.10 + 0.40 * j / 31, 1.0)
+            kind = (i + j) % 2
+            specs.append(spec_of(qmcg, sp, kind))
+            raw.append((sp, kind))
+    batch = ctx.price_american_batch(specs, 16, 3000, 42, allow_put=True)
+    for (sp, kind), r in zip(raw, batch):
+        p, se = oracle_lib.price_american(*sp, 16, 3000, 42, kind=kind, allow_put=True)
+        assert abs(r.price - p) <= PRICE_RTOL * max(p, 1e-12), (sp, kind, r.price, p)
 
 
 def test_convergence_curve(ctx, qmcg):
