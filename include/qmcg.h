@@ -119,6 +119,9 @@ qmcg_status qmcg_permutation(qmcg_ctx* ctx, int64_t n, uint64_t seed64, uint32_t
 qmcg_status qmcg_uniforms(qmcg_ctx* ctx, int64_t n, uint64_t seed, int64_t dim, double* out_host);
 /* moro_inv_cnd of the same uniforms (quasi_rng.cpp:103-105), as the pricing kernel computes it. */
 qmcg_status qmcg_normals(qmcg_ctx* ctx, int64_t n, uint64_t seed, int64_t dim, double* out_host);
+/* The normal table z[d][p] = moro_inv_cnd(uniform_at(p, d)) for d < dims, as the batch
+ * path generates it (row-major [dims][n_paths]). */
+qmcg_status qmcg_normal_table(qmcg_ctx* ctx, int64_t n_paths, uint64_t seed, int64_t dims, double* out_host);
 /* Per-path t0 values of the foresight sweep (american.cpp:119-124). */
 qmcg_status qmcg_path_values(qmcg_ctx* ctx, const qmcg_option_spec* spec, int64_t m,
                              int64_t n_paths, uint64_t seed, uint32_t flags, double* out_host);

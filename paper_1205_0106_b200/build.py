@@ -58,7 +58,8 @@ def build(force: bool = False, verbose: bool = False, defines: tuple = (), lib: 
         objs.append(o)
         if force or _stale(o, [s] + headers):
             cmd = ["g++", "-std=c++17", "-O2", "-fPIC", "-ffp-contract=off", "-Wall",
-                   "-I", INCLUDE, "-I", CSRC, "-I", "/usr/local/cuda/include", "-c", s, "-o", o]
+                   "-I", INCLUDE, "-I", CSRC, "-I", "/usr/local/cuda/include", *[f"-D{d}" for d in defines],
+                   "-c", s, "-o", o]
             if verbose:
                 print(" ".join(cmd))
             _run(cmd)

@@ -12,6 +12,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <mutex>
@@ -369,7 +370,8 @@ qmcg_status plan_call(const qmcg_option_spec& s, int64_t m, int64_t n, uint32_t 
   plan.dpow[0] = 1.0;
   for (int64_t k = 1; k <= m; ++k) plan.dpow[static_cast<size_t>(k)] = plan.dpow[static_cast<size_t>(k - 1)] * disc;
   P.rate_negative = disc > 1.0;
-  P.dom_slope = (r * dt) / P.b;
+  P.dom_slope = s.kind == QMCG_CALL ? (r * dt) / P.b : r * dt;
+  P.x0mk = 1.0 + P.X0 - P.log_strike;
   if (!P.rate_negative) {
     const double edge = s.kind == QMCG_CALL ? std::max(s.strike, s.spot) : std::min(s.strike, s.spot);
     P.c0 = (std::log(edge) - P.X0) / P.b;
@@ -706,7 +708,7 @@ qmcg_status qmcg_price_american_batch(qmcg_ctx* c, const qmcg_option_spec* specs
   }
   std::vector<double> shared_sums[2];
   if (use_shared) {
-    QMCG_CUDA(c->d_z.reserve(static_cast<size_t>(m) * static_cast<size_t>(n)));
+    QMCG_CUDA(c->d_z.reserve(static_cast<size_t>(m + 8) * static_cast<size_t>(n)));  // + 8 prefetch rows
     PriceParams G = plans[static_cast<size_t>(shared_idx[0].empty() ? shared_idx[1][0] : shared_idx[0][0])].P;
     G.perm = c->table;
     G.ld = qmcg::table_ld(c->col_end - c->col_begin);
@@ -724,12 +726,15 @@ qmcg_status qmcg_price_american_batch(qmcg_ctx* c, const qmcg_option_spec* specs
         const PriceParams& P = plans[static_cast<size_t>(shared_idx[k][j])].P;
         cps[j] = qmcg::ContractParams{P.dpow, P.X0, P.b, P.alpha, P.c0, P.strike, P.best0, P.log_strike,
                                       P.dom_slope, P.bs_vsqrt, P.bs_mu_t, P.bs_kdisc, P.bs_fwd_growth, P.bs_disc,
-                                      P.bs_v_zero, 0};
+                                      P.x0mk, P.bs_v_zero, 0};
       }
       QMCG_CUDA(c->d_cparams.reserve(cnt));
       QMCG_CUDA(cudaMemcpyAsync(c->d_cparams.ptr, cps.data(), cnt * sizeof(qmcg::ContractParams),
                                 cudaMemcpyHostToDevice, c->stream));
-      QMCG_CUDA(c->d_bvalues.reserve(cnt * static_cast<size_t>(n)));
+      QMCG_CUDA(c->d_bvalues.reserve(cnt * static_cast<size_t>(n) + 16));
+#ifdef QMCG_COUNT_PUSHES
+      QMCG_CUDA(cudaMemsetAsync(c->d_bvalues.ptr + cnt * static_cast<size_t>(n), 0, 16, c->stream));
+#endif
       QMCG_CUDA(c->d_bred.reserve(cnt * qmcg::reduce_scratch_doubles(n)));
       QMCG_CUDA(c->d_bsums.reserve(2 * cnt));
       qmcg::BatchParams B{c->d_z.ptr, n, n, static_cast<int32_t>(m), static_cast<int32_t>(cnt), c->d_cparams.ptr,
@@ -739,6 +744,15 @@ qmcg_status qmcg_price_american_batch(qmcg_ctx* c, const qmcg_option_spec* specs
       QMCG_CUDA(qmcg::launch_pairwise_batched(c->d_bvalues.ptr, n, static_cast<int>(cnt), c->d_bred.ptr,
                                               c->d_bsums.ptr, c->stream, &launches));
       c->launches += launches;
+#ifdef QMCG_COUNT_PUSHES
+      {
+        unsigned long long cntr[2];
+        cudaStreamSynchronize(c->stream);
+        cudaMemcpy(cntr, c->d_bvalues.ptr + cnt * static_cast<size_t>(n), 16, cudaMemcpyDeviceToHost);
+        std::fprintf(stderr, "kind %d: pushes %llu records %llu (per path-contract %.3f / %.3f)\n", k, cntr[0], cntr[1],
+                     cntr[0] / double(cnt * n), cntr[1] / double(cnt * n));
+      }
+#endif
       shared_sums[k].resize(2 * cnt);
       QMCG_CUDA(cudaMemcpyAsync(shared_sums[k].data(), c->d_bsums.ptr, 2 * cnt * sizeof(double),
                                 cudaMemcpyDeviceToHost, c->stream));
@@ -812,6 +826,33 @@ qmcg_status qmcg_uniforms(qmcg_ctx* c, int64_t n, uint64_t seed, int64_t dim, do
 
 qmcg_status qmcg_normals(qmcg_ctx* c, int64_t n, uint64_t seed, int64_t dim, double* out_host) {
   return export_dim(c, n, seed, dim, 1, out_host);
+}
+
+qmcg_status qmcg_normal_table(qmcg_ctx* c, int64_t n, uint64_t seed, int64_t dims, double* out_host) {
+  if (!c || !out_host || n < 1 || dims < 1) return fail(QMCG_INVALID_ARGUMENT, "qmcg_normal_table: bad argument");
+  std::lock_guard<std::mutex> lock(c->mu);
+  DeviceGuard g(c->device);
+  qmcg_option_spec s{100.0, 100.0, 0.05, 0.2, 1.0, QMCG_CALL};
+  CallPlan plan;
+  qmcg_status st = plan_call(s, dims, n < 2 ? 2 : n, 0, plan);
+  if (st) return st;
+  st = upload_plan(c, plan, n);
+  if (st) return st;
+  st = ensure_perms(c, seed, n, 0, n, dims, false);
+  if (st) return st;
+  QMCG_CUDA(c->d_z.reserve(static_cast<size_t>(dims) * static_cast<size_t>(n)));
+  PriceParams G = plan.P;
+  G.perm = c->table;
+  G.ld = qmcg::table_ld(c->col_end - c->col_begin);
+  G.col_begin = c->col_begin;
+  G.path_begin = 0;
+  G.path_count = n;
+  G.alpha = 0.0;
+  QMCG_CUDA(qmcg::launch_gen_z(G, c->d_z.ptr, n, c->stream));
+  QMCG_CUDA(cudaMemcpyAsync(out_host, c->d_z.ptr, static_cast<size_t>(dims) * static_cast<size_t>(n) * sizeof(double),
+                            cudaMemcpyDeviceToHost, c->stream));
+  QMCG_CUDA(cudaStreamSynchronize(c->stream));
+  return QMCG_OK;
 }
 
 qmcg_status qmcg_path_values(qmcg_ctx* c, const qmcg_option_spec* spec, int64_t m, int64_t n, uint64_t seed,

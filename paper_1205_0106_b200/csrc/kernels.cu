@@ -121,17 +121,17 @@ __constant__ double c_log_consts[2] = {0x1.0000000000400p+52 /* 2^52 + 1024 */, 
 // compiler from rebuilding generic->shared windows inside the hot loops).
 __device__ __forceinline__ uint32_t lds_u32(uint32_t a) {
   uint32_t v;
-  asm("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
   return v;
 }
 __device__ __forceinline__ uint32_t lds_u8(uint32_t a) {
   uint32_t v;
-  asm("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+  asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
   return v;
 }
 __device__ __forceinline__ double lds_f64(uint32_t a) {
   double v;
-  asm("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a) : "memory");
+  asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a) : "memory");
   return v;
 }
 __device__ __forceinline__ double2 lds_v2f64(uint32_t a) {
@@ -565,6 +565,23 @@ __device__ __forceinline__ void generate_row(const PriceParams& P, uint32_t ws, 
   if (ntail) flush_tail(ws, zrow, ntail, logtab, alpha, lane);
 }
 
+// Dominance of the lane's pending record j by a new record k (then j can never
+// be the maximum and needs no exp()):
+//   calls: acc = V_j + slope (k - j) in V units; k dominates j iff V_k >= acc
+//          (S_k disc^(k-j) >= S_j);
+//   puts:  acc = delta = r dt (k - j); k dominates j iff
+//          w (1 - e^-(delta + Delta)) >= 1 - e^-delta, w = S_j / K, Delta = b (V_j - V_k);
+//          sufficient (exact-safe lower/upper bounds, no exp): with u = ln w,
+//          (1 + u) s (1 - s/2) >= delta, s = delta + Delta, 1 + u > 0, s < 2.
+// x0mk = 1 + X0 - ln K (puts only).
+template <int KIND>
+__device__ __forceinline__ bool record_dominates(double V, double c, double acc, double b, double x0mk) {
+  if (KIND == 0) return V >= acc;
+  const double u1 = fma(b, c, x0mk);
+  const double s = fma(b, c - V, acc);
+  return u1 > 0.0 && s < 2.0 && u1 * s * fma(-0.5, s, 1.0) >= acc * (1.0 + 1e-12);
+}
+
 template <int KIND, bool RNEG>
 __device__ __forceinline__ void push_record(uint32_t ws, const PriceParams& P, bool push, double v, int d, int lane,
                                             unsigned lt, uint32_t& rq_head, uint32_t& rq_tail) {
@@ -657,19 +674,18 @@ __global__ void __launch_bounds__(kThreads, QMCG_MINB) price_kernel(const PriceP
     }
     // ---- walk ----
     // c = V of the last record (= the pending record when pend_d >= 0);
-    // cd = c + slope * (date - pend_d): the pending record j is dominated by a
-    // record at date k iff V_k >= cd (S_k disc^(k-j) >= S_j, calls).
+    // cd = the dominance accumulator of the pending record (record_dominates).
     if (!SLOW && !RNEG && k0 + kTile <= mrec) {
 #pragma unroll
       for (int t = 0; t < kTile; ++t) {
         V = __dadd_rn(V, lds_f64(zcol + t * kThreads * 8));
         cd = __dadd_rn(cd, slope);
         const bool rec = KIND == 0 ? V > c : V < c;
-        const bool push = rec && pend_d >= 0 && !(KIND == 0 && V >= cd);
+        const bool push = rec && pend_d >= 0 && !record_dominates<KIND>(V, c, cd, P.b, P.x0mk);
         const double pv = c;
         const int pd = pend_d;
         c = rec ? V : c;
-        cd = rec ? V : cd;
+        cd = rec ? (KIND == 0 ? V : 0.0) : cd;
         pend_d = rec ? k0 + t : pend_d;
         push_record<KIND, RNEG>(ws, P, push, pv, pd, lane, lt, rq_head, rq_tail);
       }
@@ -691,11 +707,11 @@ __global__ void __launch_bounds__(kThreads, QMCG_MINB) price_kernel(const PriceP
               // every candidate is evaluated; the threshold follows the evaluated best
               push_record<KIND, RNEG>(ws, P, rec, V, d, lane, lt, rq_head, rq_tail);
             } else {
-              const bool push = rec && pend_d >= 0 && !(KIND == 0 && V >= cd);
+              const bool push = rec && pend_d >= 0 && !record_dominates<KIND>(V, c, cd, P.b, P.x0mk);
               const double pv = c;
               const int pd = pend_d;
               c = rec ? V : c;
-              cd = rec ? V : cd;
+              cd = rec ? (KIND == 0 ? V : 0.0) : cd;
               pend_d = rec ? d : pend_d;
               push_record<KIND, RNEG>(ws, P, push, pv, pd, lane, lt, rq_head, rq_tail);
             }
@@ -806,153 +822,149 @@ __global__ void __launch_bounds__(kThreads, QMCG_MINB) gen_z_kernel(const PriceP
   }
 }
 
-// Batch walk over a shared normal table: thread = path, CPT contracts of one
-// kind per thread (z loaded once, used CPT times). Per contract the same
-// foresight walk as price_kernel: V_c,k = Z_k + (k+1) alpha_c with
-// Z_k = sum_{j<=k} z_j, records filtered by the running extreme and the
+// Batch walk over a shared normal table. Block = 8 warps = 8 contracts of one
+// kind x the same 32 paths (lane = path): every warp walks its contract over
+// the block's 32-path column of z (read once from HBM/L2, then L1 hits for the
+// other 7 warps). Per contract the same foresight walk as price_kernel:
+// V_k = sum (z_j + alpha_c), records filtered by the running extreme and the
 // pending-record dominance test, survivors evaluated 32 per warp.
-// blockIdx.x = contract group (fastest), so the 256-path z block of
-// blockIdx.y stays in L2 while every contract group reads it.
-constexpr int kCpt = 4;
-constexpr uint32_t kBWarpBytes = kCpt * (kRecCap * 12 + 32 * 8);
+constexpr int kBCw = 8;  // contracts (warps) per block
+constexpr uint32_t kBWarpBytes = kRecCap * 12 + 32 * 8;
 
 template <int KIND>
-__global__ void __launch_bounds__(kThreads, 2) walk_batch_kernel(const BatchParams B) {
-  __shared__ __align__(16) unsigned char sm[kWarps * kBWarpBytes];
+__global__ void __launch_bounds__(kBCw * 32) walk_batch_kernel(const BatchParams B) {
+  __shared__ __align__(16) unsigned char sm[kBCw * kBWarpBytes];
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const unsigned lt = lanemask_lt();
-  const uint32_t wbase = smem_u32(sm) + warp * kBWarpBytes;
-  const int64_t p = static_cast<int64_t>(blockIdx.y) * kThreads + threadIdx.x;
+  const uint32_t ws = smem_u32(sm) + warp * kBWarpBytes;
+  const uint32_t rq_code_off = kRecCap * 8, best_off = kRecCap * 12;
+  const int64_t p = static_cast<int64_t>(blockIdx.y) * 32 + lane;
   const bool active = p < B.n;
-  const int c_first = blockIdx.x * kCpt;
-  const int m = B.m;
-  const int mrec = m - 1;
-  // per-contract state
-  double c[kCpt], cd[kCpt], alpha[kCpt], slope[kCpt];
-  int pend_d[kCpt];
-  uint32_t rq_head[kCpt], rq_tail[kCpt];
-  const ContractParams* cp[kCpt];
-#pragma unroll
-  for (int i = 0; i < kCpt; ++i) {
-    const int ci = min(c_first + i, B.count - 1);
-    cp[i] = B.cp + ci;
-    c[i] = cp[i]->c0;
-    cd[i] = 0.0;
-    alpha[i] = cp[i]->alpha;
-    slope[i] = cp[i]->dom_slope;
-    pend_d[i] = -1;
-    rq_head[i] = rq_tail[i] = 0;
-    const uint32_t ws = wbase + i * (kRecCap * 12 + 32 * 8);
-    asm volatile("st.shared.u64 [%0], %1;" ::"r"(ws + kRecCap * 12 + lane * 8),
-                 "l"(static_cast<unsigned long long>(__double_as_longlong(cp[i]->best0)))
-                 : "memory");
-  }
+  const int ci = blockIdx.x * kBCw + warp;
+  if (ci >= B.count) return;  // warp-uniform; no block barrier below
+  const ContractParams& q = B.cp[ci];
+  const double alpha = q.alpha, slope = q.dom_slope;
+  double c = q.c0, cd = 0.0, V = 0.0;
+  int pend_d = -1;
+  uint32_t rq_head = 0, rq_tail = 0;
+  asm volatile("st.shared.u64 [%0], %1;" ::"r"(ws + best_off + lane * 8),
+               "l"(static_cast<unsigned long long>(__double_as_longlong(q.best0)))
+               : "memory");
   __syncwarp();
   const double* zc = B.z + (active ? p : 0);
-  double Z = 0.0, kd = 0.0;
-  for (int d = 0; d < m; ++d) {
-    const double zv = __ldg(zc + static_cast<int64_t>(d) * B.ldz);
-    Z = __dadd_rn(Z, zv);
-    kd = __dadd_rn(kd, 1.0);
-    if (d < mrec) {
-#pragma unroll
-      for (int i = 0; i < kCpt; ++i) {
-        const double V = fma(alpha[i], kd, Z);
-        cd[i] = __dadd_rn(cd[i], slope[i]);
-        const bool rec = KIND == 0 ? V > c[i] : V < c[i];
-        const bool push = active && rec && pend_d[i] >= 0 && !(KIND == 0 && V >= cd[i]);
-        const double pv = c[i];
-        const int pd = pend_d[i];
-        c[i] = rec ? V : c[i];
-        cd[i] = rec ? V : cd[i];
-        pend_d[i] = rec ? d : pend_d[i];
-        const unsigned pb = __ballot_sync(kFull, push);
-        if (pb) {
-          const uint32_t ws = wbase + i * (kRecCap * 12 + 32 * 8);
-          if (push) {
-            const uint32_t slot = (rq_tail[i] + __popc(pb & lt)) & (kRecCap - 1);
-            sts_f64(ws + slot * 8, pv);
-            sts_u32(ws + kRecCap * 8 + slot * 4, (static_cast<uint32_t>(pd) << 5) | static_cast<uint32_t>(lane));
-          }
-          rq_tail[i] += __popc(pb);
-          if (rq_tail[i] - rq_head[i] >= 32) {
-            __syncwarp();
-            const ContractParams& q = *cp[i];
-            if (true) {
-              const uint32_t slot = (rq_head[i] + lane) & (kRecCap - 1);
-              const double v = lds_f64(ws + slot * 8);
-              const uint32_t code = lds_u32(ws + kRecCap * 8 + slot * 4);
-              const double sv = exp(fma(q.b, v, q.X0));
-              double intr = KIND == 0 ? sv - q.strike : q.strike - sv;
-              intr = intr > 0.0 ? intr : 0.0;
-              const double term = intr * __ldg(q.dpow + (code >> 5) + 1);
-              asm volatile("atom.shared.max.u64 _, [%0], %1;" ::"r"(ws + kRecCap * 12 + (code & 31u) * 8),
-                           "l"(static_cast<unsigned long long>(__double_as_longlong(term)))
-                           : "memory");
-            }
-            rq_head[i] += 32;
-            __syncwarp();
-          }
-        }
+  const int m = B.m;
+  const int mrec = m - 1;
+  auto eval = [&](uint32_t head, uint32_t cnt) {
+    if (static_cast<uint32_t>(lane) < cnt) {
+      const uint32_t slot = (head + lane) & (kRecCap - 1);
+      const double v = lds_f64(ws + slot * 8);
+      const uint32_t code = lds_u32(ws + rq_code_off + slot * 4);
+      const double sv = exp(fma(q.b, v, q.X0));
+      double intr = KIND == 0 ? sv - q.strike : q.strike - sv;
+      intr = intr > 0.0 ? intr : 0.0;
+      const double term = intr * __ldg(q.dpow + (code >> 5) + 1);
+      asm volatile("atom.shared.max.u64 _, [%0], %1;" ::"r"(ws + best_off + (code & 31u) * 8),
+                   "l"(static_cast<unsigned long long>(__double_as_longlong(term)))
+                   : "memory");
+    }
+  };
+#ifdef QMCG_COUNT_PUSHES
+  unsigned long long* dbg_counter = reinterpret_cast<unsigned long long*>(B.values + static_cast<int64_t>(B.count) * B.n);
+#endif
+  auto step = [&](int d, double zv) {
+    V = __dadd_rn(V, __dadd_rn(zv, alpha));
+    cd = __dadd_rn(cd, slope);
+    const bool rec = KIND == 0 ? V > c : V < c;
+    const bool push = active && rec && pend_d >= 0 && !record_dominates<KIND>(V, c, cd, q.b, q.x0mk);
+#ifdef QMCG_COUNT_PUSHES
+    if (push) atomicAdd(dbg_counter, 1ull);
+    if (rec && active) atomicAdd(dbg_counter + 1, 1ull);
+#endif
+    const double pv = c;
+    const int pd = pend_d;
+    c = rec ? V : c;
+    cd = rec ? (KIND == 0 ? V : 0.0) : cd;
+    pend_d = rec ? d : pend_d;
+    const unsigned pb = __ballot_sync(kFull, push);
+    if (pb) {
+      if (push) {
+        const uint32_t slot = (rq_tail + __popc(pb & lt)) & (kRecCap - 1);
+        sts_f64(ws + slot * 8, pv);
+        sts_u32(ws + rq_code_off + slot * 4, (static_cast<uint32_t>(pd) << 5) | static_cast<uint32_t>(lane));
+      }
+      rq_tail += __popc(pb);
+      if (rq_tail - rq_head >= 32) {
+        __syncwarp();
+        eval(rq_head, 32);
+        rq_head += 32;
+        __syncwarp();
       }
     }
-  }
+  };
+  // z is read 8 dates ahead of use (the walk itself is a serial chain per path)
+  constexpr int kPf = 8;
+  double zbuf[kPf];
 #pragma unroll
-  for (int i = 0; i < kCpt; ++i) {
-    const ContractParams& q = *cp[i];
-    const uint32_t ws = wbase + i * (kRecCap * 12 + 32 * 8);
-    const bool push = active && pend_d[i] >= 0;
+  for (int t = 0; t < kPf; ++t) zbuf[t] = t < mrec ? __ldg(zc + static_cast<int64_t>(t) * B.ldz) : 0.0;
+  for (int d0 = 0; d0 < mrec; d0 += kPf) {
+    double cur[kPf];
+#pragma unroll
+    for (int t = 0; t < kPf; ++t) {
+      cur[t] = zbuf[t];
+      const int dn = d0 + kPf + t;
+      zbuf[t] = dn < mrec ? __ldg(zc + static_cast<int64_t>(dn) * B.ldz) : 0.0;
+    }
+    if (d0 + kPf <= mrec) {
+#pragma unroll
+      for (int t = 0; t < kPf; ++t) step(d0 + t, cur[t]);
+    } else {
+#pragma unroll
+      for (int t = 0; t < kPf; ++t)
+        if (d0 + t < mrec) step(d0 + t, cur[t]);
+    }
+  }
+  V = __dadd_rn(V, __dadd_rn(__ldg(zc + static_cast<int64_t>(mrec) * B.ldz), alpha));
+  {
+    const bool push = active && pend_d >= 0;
     const unsigned pb = __ballot_sync(kFull, push);
     if (push) {
-      const uint32_t slot = (rq_tail[i] + __popc(pb & lt)) & (kRecCap - 1);
-      sts_f64(ws + slot * 8, c[i]);
-      sts_u32(ws + kRecCap * 8 + slot * 4, (static_cast<uint32_t>(pend_d[i]) << 5) | static_cast<uint32_t>(lane));
+      const uint32_t slot = (rq_tail + __popc(pb & lt)) & (kRecCap - 1);
+      sts_f64(ws + slot * 8, c);
+      sts_u32(ws + rq_code_off + slot * 4, (static_cast<uint32_t>(pend_d) << 5) | static_cast<uint32_t>(lane));
     }
-    rq_tail[i] += __popc(pb);
+    rq_tail += __popc(pb);
     __syncwarp();
-    while (rq_tail[i] != rq_head[i]) {
-      const uint32_t cnt = min(32u, rq_tail[i] - rq_head[i]);
-      if (static_cast<uint32_t>(lane) < cnt) {
-        const uint32_t slot = (rq_head[i] + lane) & (kRecCap - 1);
-        const double v = lds_f64(ws + slot * 8);
-        const uint32_t code = lds_u32(ws + kRecCap * 8 + slot * 4);
-        const double sv = exp(fma(q.b, v, q.X0));
-        double intr = KIND == 0 ? sv - q.strike : q.strike - sv;
-        intr = intr > 0.0 ? intr : 0.0;
-        const double term = intr * __ldg(q.dpow + (code >> 5) + 1);
-        asm volatile("atom.shared.max.u64 _, [%0], %1;" ::"r"(ws + kRecCap * 12 + (code & 31u) * 8),
-                     "l"(static_cast<unsigned long long>(__double_as_longlong(term)))
-                     : "memory");
-      }
-      rq_head[i] += cnt;
+    while (rq_tail != rq_head) {
+      const uint32_t cnt = min(32u, rq_tail - rq_head);
+      eval(rq_head, cnt);
+      rq_head += cnt;
       __syncwarp();
     }
-    // date m
-    const double V = fma(alpha[i], kd, Z);
-    const double X = fma(q.b, V, q.X0);
-    const double sl = exp(X);
-    double cont;
-    if (q.bs_v_zero) {
-      const double fwd = sl * q.bs_fwd_growth;
-      const double iv = KIND == 0 ? fwd - q.strike : q.strike - fwd;
-      cont = q.bs_disc * (iv > 0.0 ? iv : 0.0);
-    } else {
-      const double d1 = (X - q.log_strike + q.bs_mu_t) / q.bs_vsqrt;
-      const double d2 = d1 - q.bs_vsqrt;
-      const double price = KIND == 0 ? sl * cnd_dev(d1) - q.bs_kdisc * cnd_dev(d2)
-                                     : q.bs_kdisc * cnd_dev(-d2) - sl * cnd_dev(-d1);
-      cont = price > 0.0 ? price : 0.0;
-    }
-    double intr = KIND == 0 ? sl - q.strike : q.strike - sl;
-    intr = intr > 0.0 ? intr : 0.0;
-    const double cm = intr > cont ? intr : cont;
-    const double term_m = cm * __ldg(q.dpow + m);
-    unsigned long long bb;
-    asm volatile("ld.shared.u64 %0, [%1];" : "=l"(bb) : "r"(ws + kRecCap * 12 + lane * 8));
-    const double best = __longlong_as_double(static_cast<long long>(bb));
-    if (active && c_first + i < B.count) B.values[static_cast<int64_t>(c_first + i) * B.n + p] = best > term_m ? best : term_m;
   }
+  // date m
+  const double X = fma(q.b, V, q.X0);
+  const double sl = exp(X);
+  double cont;
+  if (q.bs_v_zero) {
+    const double fwd = sl * q.bs_fwd_growth;
+    const double iv = KIND == 0 ? fwd - q.strike : q.strike - fwd;
+    cont = q.bs_disc * (iv > 0.0 ? iv : 0.0);
+  } else {
+    const double d1 = (X - q.log_strike + q.bs_mu_t) / q.bs_vsqrt;
+    const double d2 = d1 - q.bs_vsqrt;
+    const double price = KIND == 0 ? sl * cnd_dev(d1) - q.bs_kdisc * cnd_dev(d2)
+                                   : q.bs_kdisc * cnd_dev(-d2) - sl * cnd_dev(-d1);
+    cont = price > 0.0 ? price : 0.0;
+  }
+  double intr = KIND == 0 ? sl - q.strike : q.strike - sl;
+  intr = intr > 0.0 ? intr : 0.0;
+  const double cm = intr > cont ? intr : cont;
+  const double term_m = cm * __ldg(q.dpow + m);
+  unsigned long long bb;
+  asm volatile("ld.shared.u64 %0, [%1];" : "=l"(bb) : "r"(ws + best_off + lane * 8));
+  const double best = __longlong_as_double(static_cast<long long>(bb));
+  if (active) B.values[static_cast<int64_t>(ci) * B.n + p] = best > term_m ? best : term_m;
 }
 
 // D1: uniforms (or Moro normals) of one dimension for `count` paths.
@@ -1099,10 +1111,27 @@ __global__ void pairwise_tree_kernel(const double* __restrict__ in, int64_t coun
     s2[i] = in[2 * (base + i) + 1];
   }
   __syncthreads();
+  // level by level, s[i] = s[2i] + s[2i+1] (the reference's pairing). The sums
+  // of a level are formed in registers and written after a barrier: in place,
+  // a warp could otherwise overwrite entries another warp has yet to read.
   for (int w = group / 2; w >= 1; w /= 2) {
-    for (int i = threadIdx.x; i < w; i += blockDim.x) {
-      s[i] = __dadd_rn(s[2 * i], s[2 * i + 1]);
-      s2[i] = __dadd_rn(s2[2 * i], s2[2 * i + 1]);
+    double a[4], a2[4];  // w <= 512, blockDim 256 -> at most 2 per thread
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int i = threadIdx.x + r * blockDim.x;
+      if (i < w) {
+        a[r] = __dadd_rn(s[2 * i], s[2 * i + 1]);
+        a2[r] = __dadd_rn(s2[2 * i], s2[2 * i + 1]);
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int i = threadIdx.x + r * blockDim.x;
+      if (i < w) {
+        s[i] = a[r];
+        s2[i] = a2[r];
+      }
     }
     __syncthreads();
   }
@@ -1179,9 +1208,9 @@ cudaError_t launch_gen_z(const PriceParams& P, double* z, int64_t ldz, cudaStrea
 
 cudaError_t launch_walk_batch(const BatchParams& B, int kind, cudaStream_t s) {
   if (B.count <= 0 || B.n <= 0) return cudaSuccess;
-  const dim3 grid(static_cast<unsigned>((B.count + kCpt - 1) / kCpt), static_cast<unsigned>((B.n + kThreads - 1) / kThreads));
-  if (kind == 0) walk_batch_kernel<0><<<grid, kThreads, 0, s>>>(B);
-  else walk_batch_kernel<1><<<grid, kThreads, 0, s>>>(B);
+  const dim3 grid(static_cast<unsigned>((B.count + kBCw - 1) / kBCw), static_cast<unsigned>((B.n + 31) / 32));
+  if (kind == 0) walk_batch_kernel<0><<<grid, kBCw * 32, 0, s>>>(B);
+  else walk_batch_kernel<1><<<grid, kBCw * 32, 0, s>>>(B);
   return cudaGetLastError();
 }
 

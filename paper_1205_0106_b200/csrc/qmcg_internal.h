@@ -54,7 +54,8 @@ struct PriceParams {
   double best0;          // intrinsic value at t0 (date 0 term)
   double log_strike;
   double dmax_inv;       // 1 / max_k disc^k  (only for rate < 0)
-  double dom_slope;      // r*dt / b: record dominance slope in V units (calls)
+  double dom_slope;      // per-date step of the dominance accumulator: calls r*dt/b, puts r*dt
+  double x0mk;           // 1 + X0 - log K (put dominance test)
   // Black-Scholes of the last interval (reference sweep_impl, american.cpp:45-52)
   double bs_vsqrt;       // v*sqrt(dt)
   double bs_mu_t;        // (r + 0.5*v*v)*dt
@@ -74,6 +75,7 @@ struct ContractParams {
   const double* dpow;
   double X0, b, alpha, c0, strike, best0, log_strike, dom_slope;
   double bs_vsqrt, bs_mu_t, bs_kdisc, bs_fwd_growth, bs_disc;
+  double x0mk;
   int32_t bs_v_zero, pad;
 };
 

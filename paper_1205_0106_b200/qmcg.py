@@ -32,7 +32,7 @@ EXPORTS = (
     "qmcg_create", "qmcg_destroy", "qmcg_last_error", "qmcg_version", "qmcg_price_american",
     "qmcg_price_american_batch", "qmcg_price_american_node", "qmcg_tree_node_range",
     "qmcg_combine_nodes", "qmcg_warm", "qmcg_clear_cache", "qmcg_permutation", "qmcg_uniforms",
-    "qmcg_normals", "qmcg_path_values", "qmcg_time_device", "qmcg_time_perm_build",
+    "qmcg_normals", "qmcg_normal_table", "qmcg_path_values", "qmcg_time_device", "qmcg_time_perm_build",
     "qmcg_last_launch_count", "qmcg_get_stream", "qmcg_fp64_peak",
 )
 
@@ -119,6 +119,7 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
         L.qmcg_uniforms.argtypes = [P, I64, U64, I64, P]
         L.qmcg_normals.argtypes = [P, I64, U64, I64, P]
         L.qmcg_path_values.argtypes = [P, C.POINTER(_CSpec), I64, I64, U64, U32, P]
+        L.qmcg_normal_table.argtypes = [P, I64, U64, I64, P]
         L.qmcg_time_device.argtypes = [P, C.POINTER(_CSpec), I64, I64, U64, U32, C.c_int, PD, PD, PD]
         L.qmcg_time_perm_build.argtypes = [P, I64, U64, I64, PD]
         L.qmcg_last_launch_count.argtypes = [P]
@@ -230,6 +231,11 @@ class Context:
     def normals(self, n: int, seed: int, dim: int) -> np.ndarray:
         out = np.zeros(int(n), dtype=np.float64)
         _check(self._lib.qmcg_normals(self._h, int(n), int(seed), int(dim), out.ctypes.data))
+        return out
+
+    def normal_table(self, n: int, seed: int, dims: int) -> np.ndarray:
+        out = np.zeros((int(dims), int(n)), dtype=np.float64)
+        _check(self._lib.qmcg_normal_table(self._h, int(n), int(seed), int(dims), out.ctypes.data))
         return out
 
     def path_values(self, spec: OptionSpec, m: int, n_paths: int, seed: int, allow_put: bool = False) -> np.ndarray:
