@@ -68,6 +68,10 @@ PricingResult price_american(const OptionSpec& spec, Index m, Index n_paths, std
 ConvergenceCurve convergence_curve(const OptionSpec& spec, const std::vector<Index>& m_values,
                                    Index n_paths, std::uint64_t seed, const ExecPolicy& exec = {});
 
+// One-step QMC European price; reference proj/src/mc_european.cpp:11-46.
+PricingResult mc_european_price(const OptionSpec& spec, Index n_paths, std::uint64_t seed,
+                                const ExecPolicy& exec = {});
+
 namespace b200 {
 // Extension (no reference counterpart): the same foresight rule for puts.
 PricingResult price_american_put_extension(const OptionSpec& spec, Index m, Index n_paths,

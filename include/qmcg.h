@@ -84,6 +84,13 @@ qmcg_status qmcg_price_american(qmcg_ctx* ctx, const qmcg_option_spec* spec, int
                                 int64_t n_paths, uint64_t seed, uint32_t flags,
                                 qmcg_pricing_result* out);
 
+/* qmc::mc_european_price (proj/src/mc_european.cpp:11-46): one-step QMC
+ * European price from the dimension-0 scrambled-Halton normals (puts allowed,
+ * as in the reference); volatility 0 or maturity 0 returns the discounted
+ * deterministic payoff exactly. method = QMCG_METHOD_EUROPEAN_MC. */
+qmcg_status qmcg_mc_european_price(qmcg_ctx* ctx, const qmcg_option_spec* spec, int64_t n_paths, uint64_t seed,
+                                   uint32_t flags, qmcg_pricing_result* out);
+
 /* The same pricing for n_specs contracts sharing (m, n_paths, seed): one
  * permutation-table set, one launch per contract group. No reference
  * counterpart (the reference loops price_american). */

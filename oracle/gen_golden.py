@@ -156,6 +156,16 @@ def main() -> None:
            "gbm_step": [[hexf(R.gbm_step(100, 0.25, 1.0, 0.05, 0.2))]]}
     write("analytic.json", ana)
 
+    # ---- European QMC (mc_european_price), calls and puts ----
+    eur = []
+    for sp, kind, n in [(REF_SPEC, 0, 1 << 20), (REF_SPEC, 0, 1_000_000), (REF_SPEC, 1, 1 << 18),
+                        ((90.0, 100.0, 0.03, 0.3, 0.5), 0, 3001), ((110.0, 100.0, 0.08, 0.15, 2.0), 1, 65536),
+                        ((100.0, 90.0, 0.05, 0.0, 1.0), 0, 1000), ((110.0, 100.0, 0.05, 0.2, 0.0), 0, 64),
+                        ((100.0, 120.0, -0.01, 0.4, 1.5), 1, 1 << 16)]:
+        p, se, _ = R.mc_european_price(*sp, n, SEED, kind=kind, lanes=lanes)
+        eur.append({"spec": list(sp), "kind": kind, "n": n, "seed": SEED, "price": hexf(p), "std_error": hexf(se)})
+    write("european.json", {"source": "oracle/_ref mc_european_price", "cases": eur})
+
     # ---- CRR American call (reference oracles.cpp) for dominance checks ----
     crr = []
     for sp in [REF_SPEC] + extra_specs[:5]:

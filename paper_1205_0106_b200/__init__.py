@@ -7,8 +7,9 @@ ctypes binding with the reference's names.
 """
 from .qmcg import (  # noqa: F401
     Context, ExecPolicy, Method, OptionKind, OptionSpec, PricingResult, combine_nodes,
-    convergence_curve, load_library, price_american, tree_node_range,
+    convergence_curve, load_library, mc_european_price, price_american, tree_node_range,
 )
 
 __all__ = ["Context", "ExecPolicy", "Method", "OptionKind", "OptionSpec", "PricingResult",
-           "combine_nodes", "convergence_curve", "load_library", "price_american", "tree_node_range"]
+           "combine_nodes", "convergence_curve", "load_library", "mc_european_price", "price_american",
+           "tree_node_range"]

@@ -638,6 +638,55 @@ qmcg_status qmcg_price_american(qmcg_ctx* c, const qmcg_option_spec* spec, int64
   return QMCG_OK;
 }
 
+qmcg_status qmcg_mc_european_price(qmcg_ctx* c, const qmcg_option_spec* spec, int64_t n, uint64_t seed,
+                                   uint32_t flags, qmcg_pricing_result* out) {
+  if (!c || !spec || !out) return fail(QMCG_INVALID_ARGUMENT, "qmcg_mc_european_price: null argument");
+  const auto t0 = std::chrono::steady_clock::now();
+  std::lock_guard<std::mutex> lock(c->mu);
+  DeviceGuard g(c->device);
+  c->launches = 0;
+  (void)flags;
+  qmcg_status st = validate(*spec);
+  if (st) return st;
+  if (n < 2) return fail(QMCG_INVALID_ARGUMENT, "mc_european_price: n_paths must be >= 2");
+  const double r = spec->rate, v = spec->volatility, T = spec->maturity;
+  out->n_paths = n;
+  out->method = QMCG_METHOD_EUROPEAN_MC;
+  out->seed = seed;
+  if (v == 0.0 || T == 0.0) {  // mc_european.cpp:20-28, exact host arithmetic
+    const double disc = std::exp(-r * T);
+    const double forward = spec->spot * std::exp(r * T);
+    out->price = disc * intrinsic(spec->kind, forward, spec->strike);
+    out->std_error = 0.0;
+    out->elapsed_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    return QMCG_OK;
+  }
+  if (static_cast<uint64_t>(n) > 0xffffffffULL)
+    return fail(QMCG_LENGTH_ERROR, "permutation_indices: n exceeds the 2^32-1 supported maximum");
+  st = ensure_dim_tables(c, n, 1);
+  if (st) return st;
+  st = ensure_perms(c, seed, n, 0, n, 1, false);  // dimension 0 only (reuses a larger cached set)
+  if (st) return st;
+  st = prepare_scratch(c, 1);
+  if (st) return st;
+  QMCG_CUDA(c->d_values.reserve(static_cast<size_t>(n)));
+  QMCG_CUDA(c->d_red.reserve(qmcg::reduce_scratch_doubles(n)));
+  const double a = (r - 0.5 * v * v) * T;  // gbm_step with dt = T
+  const double bsd = v * std::sqrt(T);
+  const double disc = std::exp(-r * T);
+  QMCG_CUDA(qmcg::launch_european(c->table, n, c->dt.dims[0], c->d_sc.ptr, c->d_nc.ptr, spec->spot, a, bsd,
+                                  spec->strike, disc, spec->kind, c->d_values.ptr, c->stream));
+  int launches = 1;
+  QMCG_CUDA(qmcg::launch_pairwise(c->d_values.ptr, n, c->d_red.ptr, c->d_sums.ptr, c->stream, &launches));
+  c->launches += launches;
+  std::vector<double> sums;
+  st = sync_results(c, 1, sums);
+  if (st) return st;
+  finish_stats(n, sums[0], sums[1], out->price, out->std_error);
+  out->elapsed_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  return QMCG_OK;
+}
+
 qmcg_status qmcg_price_american_node(qmcg_ctx* c, const qmcg_option_spec* spec, int64_t m, int64_t n,
                                      uint64_t seed, uint32_t flags, int depth, int64_t node, double out_sums[2]) {
   if (!c || !spec || !out_sums) return fail(QMCG_INVALID_ARGUMENT, "qmcg_price_american_node: null argument");

@@ -89,6 +89,18 @@ ConvergenceCurve convergence_curve(const OptionSpec& spec, const std::vector<Ind
   return curve;
 }
 
+PricingResult mc_european_price(const OptionSpec& spec, Index n_paths, std::uint64_t seed, const ExecPolicy& exec) {
+  if (exec.lanes < 1) throw std::invalid_argument("parallel_for_chunks: lanes must be >= 1");
+  if (exec.chunk < 1) throw std::invalid_argument("parallel_for_chunks: chunk must be >= 1");
+  const qmcg_option_spec cs = to_c(spec);
+  qmcg_pricing_result r{};
+  const qmcg_status st = qmcg_mc_european_price(context(), &cs, n_paths, seed, 0u, &r);
+  if (st != QMCG_OK) rethrow(st);
+  PricingResult out = from_c(r);
+  out.method = Method::EuropeanMC;
+  return out;
+}
+
 namespace b200 {
 
 PricingResult price_american_put_extension(const OptionSpec& spec, Index m, Index n_paths, std::uint64_t seed) {

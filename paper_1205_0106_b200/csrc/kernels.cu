@@ -967,6 +967,20 @@ __global__ void __launch_bounds__(kBCw * 32) walk_batch_kernel(const BatchParams
   if (active) B.values[static_cast<int64_t>(ci) * B.n + p] = best > term_m ? best : term_m;
 }
 
+// European pricing (reference mc_european_price, mc_european.cpp:11-46, with
+// simulate_terminal, path_engine.cpp:154-172): one GBM step of width T from the
+// dimension-0 scrambled-Halton normal, discounted intrinsic per path.
+__global__ void european_kernel(const uint32_t* __restrict__ perm_row, int64_t count, DimParam dp,
+                                const double* __restrict__ sc, const double* __restrict__ nc, double s0, double a,
+                                double bsd, double strike, double disc, int kind, double* __restrict__ out) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= count) return;
+  const double z = moro_full(halton(perm_row[i] + 1u, dp, sc, nc));
+  const double st = s0 * exp(fma(bsd, z, a));
+  const double diff = kind == 0 ? st - strike : strike - st;
+  out[i] = disc * (diff > 0.0 ? diff : 0.0);
+}
+
 // D1: uniforms (or Moro normals) of one dimension for `count` paths.
 __global__ void uniforms_kernel(const uint32_t* __restrict__ perm_row, int64_t count, DimParam dp,
                                 const double* __restrict__ sc, const double* __restrict__ nc,
@@ -1232,6 +1246,15 @@ cudaError_t launch_price(const PriceParams& P, cudaStream_t s) {
   if (e != cudaSuccess) return e;
   if (P.kind == 0) return P.rate_negative ? launch_price_k<0, true>(P, s) : launch_price_k<0, false>(P, s);
   return P.rate_negative ? launch_price_k<1, true>(P, s) : launch_price_k<1, false>(P, s);
+}
+
+cudaError_t launch_european(const uint32_t* perm_row, int64_t count, DimParam dp, const double* sc, const double* nc,
+                            double s0, double a, double bsd, double strike, double disc, int kind, double* out,
+                            cudaStream_t s) {
+  const int64_t blocks = (count + 255) / 256;
+  european_kernel<<<static_cast<unsigned>(blocks), 256, 0, s>>>(perm_row, count, dp, sc, nc, s0, a, bsd, strike, disc,
+                                                                kind, out);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_uniforms(const uint32_t* perm_row, int64_t count, DimParam dp, const double* sc,

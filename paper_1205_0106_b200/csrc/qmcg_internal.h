@@ -95,6 +95,9 @@ struct BatchParams {
 // context's permutation table (PriceParams fields perm/ld/col_begin/dims/... ; alpha ignored).
 cudaError_t launch_gen_z(const PriceParams& P, double* z, int64_t ldz, cudaStream_t s);
 cudaError_t launch_walk_batch(const BatchParams& B, int kind, cudaStream_t s);
+cudaError_t launch_european(const uint32_t* perm_row, int64_t count, DimParam dp, const double* sc, const double* nc,
+                            double s0, double a, double bsd, double strike, double disc, int kind, double* out,
+                            cudaStream_t s);
 // Pairwise sums of `count` contiguous vectors v[c*len .. (c+1)*len) into out2[2c, 2c+1].
 cudaError_t launch_pairwise_batched(const double* v, int64_t len, int count, double* scratch, double* out2,
                                     cudaStream_t s, int* launches);

@@ -30,6 +30,7 @@ FLAG_NO_CACHE = 2
 # every symbol include/qmcg.h declares (checked by tests/test_abi.py)
 EXPORTS = (
     "qmcg_create", "qmcg_destroy", "qmcg_last_error", "qmcg_version", "qmcg_price_american",
+    "qmcg_mc_european_price",
     "qmcg_price_american_batch", "qmcg_price_american_node", "qmcg_tree_node_range",
     "qmcg_combine_nodes", "qmcg_warm", "qmcg_clear_cache", "qmcg_permutation", "qmcg_uniforms",
     "qmcg_normals", "qmcg_normal_table", "qmcg_path_values", "qmcg_time_device", "qmcg_time_perm_build",
@@ -109,6 +110,7 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
         L.qmcg_last_error.restype = C.c_char_p
         L.qmcg_version.restype = C.c_char_p
         L.qmcg_price_american.argtypes = [P, C.POINTER(_CSpec), I64, I64, U64, U32, C.POINTER(_CResult)]
+        L.qmcg_mc_european_price.argtypes = [P, C.POINTER(_CSpec), I64, U64, U32, C.POINTER(_CResult)]
         L.qmcg_price_american_batch.argtypes = [P, C.POINTER(_CSpec), I64, I64, I64, U64, U32, C.POINTER(_CResult)]
         L.qmcg_price_american_node.argtypes = [P, C.POINTER(_CSpec), I64, I64, U64, U32, C.c_int, I64, PD]
         L.qmcg_tree_node_range.argtypes = [I64, C.c_int, I64, C.POINTER(I64), C.POINTER(I64)]
@@ -191,6 +193,16 @@ class Context:
         flags = (FLAG_ALLOW_PUT if allow_put else 0) | (FLAG_NO_CACHE if no_cache else 0)
         s, r = _cspec(spec), _CResult()
         _check(self._lib.qmcg_price_american(self._h, C.byref(s), int(m), int(n_paths), int(seed), flags, C.byref(r)))
+        return _result(r)
+
+    def mc_european_price(self, spec: OptionSpec, n_paths: int, seed: int,
+                          exec: Optional[ExecPolicy] = None) -> PricingResult:
+        """qmc::mc_european_price (reference proj/src/mc_european.cpp:11-46)."""
+        if exec is not None and (exec.lanes < 1 or exec.chunk < 1):
+            raise ValueError("parallel_for_chunks: lanes must be >= 1" if exec.lanes < 1
+                             else "parallel_for_chunks: chunk must be >= 1")
+        s, r = _cspec(spec), _CResult()
+        _check(self._lib.qmcg_mc_european_price(self._h, C.byref(s), int(n_paths), int(seed), 0, C.byref(r)))
         return _result(r)
 
     def price_american_batch(self, specs: Sequence[OptionSpec], m: int, n_paths: int, seed: int,
@@ -307,6 +319,11 @@ def price_american(spec: OptionSpec, m: int, n_paths: int, seed: int,
                    exec: Optional[ExecPolicy] = None) -> PricingResult:
     """qmc::price_american (reference proj/src/american.cpp:103-131) on the default device."""
     return default_context().price_american(spec, m, n_paths, seed, exec)
+
+
+def mc_european_price(spec: OptionSpec, n_paths: int, seed: int, exec: Optional[ExecPolicy] = None) -> PricingResult:
+    """qmc::mc_european_price (reference proj/src/mc_european.cpp:11-46) on the default device."""
+    return default_context().mc_european_price(spec, n_paths, seed, exec)
 
 
 def convergence_curve(spec: OptionSpec, m_values: Sequence[int], n_paths: int, seed: int,

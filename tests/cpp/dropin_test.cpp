@@ -110,6 +110,21 @@ int main() {
     std::snprintf(buf, sizeof buf, "%.6g", r.price);
     CHECK(std::strcmp(buf, "14.9587") == 0);
   }
+  // mc_european_price (test_mc_european.cpp:24-40): zero volatility / maturity are exact
+  {
+    const OptionSpec spec{100.0, 90.0, 0.05, 0.0, 1.0, OptionKind::Call};
+    const double expected = std::exp(-0.05) * (100.0 * std::exp(0.05) - 90.0);
+    for (const Index n : {Index{2}, Index{1000}, Index{4096}}) {
+      const auto r = qmc::mc_european_price(spec, n, 1, ExecPolicy{2, 128});
+      CHECK(r.price == expected);
+      CHECK(r.std_error == 0.0);
+    }
+    const OptionSpec t0{110.0, 100.0, 0.05, 0.2, 0.0, OptionKind::Call};
+    CHECK(qmc::mc_european_price(t0, 64, 1, ExecPolicy{}).price == 10.0);
+    const auto mc = qmc::mc_european_price(kRef, Index{1} << 16, 42, ExecPolicy{2, 4096});
+    CHECK(std::fabs(mc.price - bs_call(kRef)) < 3.0 * mc.std_error);
+    CHECK(mc.method == qmc::Method::EuropeanMC);
+  }
   // put extension (no reference counterpart)
   {
     const auto r = qmc::b200::price_american_put_extension(put, 20, 1 << 14, 42);

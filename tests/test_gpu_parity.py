@@ -191,3 +191,22 @@ def test_config3_2p24_x_256(ctx, qmcg, golden):
     if g24:
         assert abs(r.price - fx(g24[0]["price"])) <= PRICE_RTOL * fx(g24[0]["price"])
     ctx.clear_cache()
+
+
+def test_mc_european_vs_reference_goldens(ctx, qmcg, golden):
+    """mc_european_price (reference mc_european.cpp:11-46; the §8f-next sibling of the hot path)."""
+    for c in golden["european"]["cases"]:
+        r = ctx.mc_european_price(spec_of(qmcg, c["spec"], c["kind"]), c["n"], c["seed"])
+        p, se = fx(c["price"]), fx(c["std_error"])
+        if se == 0.0:  # volatility or maturity 0: the reference's exact host formula
+            assert r.price == p and r.std_error == 0.0, c
+        else:
+            assert abs(r.price - p) <= PRICE_RTOL * p, (c, r.price)
+            assert abs(r.std_error - se) <= PRICE_RTOL * se, (c, r.std_error)
+        assert r.method == qmcg.Method.EuropeanMC
+    # proj/test_output.txt:29,33 -- 10.4505 at 2^20 paths, 10.4503 at 1e6
+    assert f"{ctx.mc_european_price(qmcg.OptionSpec(*REF), 1 << 20, 42).price:.6g}" == "10.4505"
+    assert f"{ctx.mc_european_price(qmcg.OptionSpec(*REF), 1_000_000, 42).price:.6g}" == "10.4503"
+    with pytest.raises(ValueError) as e:
+        ctx.mc_european_price(qmcg.OptionSpec(*REF), 1, 42)
+    assert str(e.value) == "mc_european_price: n_paths must be >= 2"
