@@ -31,14 +31,14 @@ constexpr int kThreads = QMCG_THREADS;  // paths per block (one per thread)
 static_assert(kThreads % 32 == 0 && kThreads <= 256, "tail queue indices are 8-bit");
 constexpr int kWarps = kThreads / 32;
 #ifndef QMCG_MINB
-#define QMCG_MINB 3
+#define QMCG_MINB 4
 #endif
 #ifndef QMCG_GEN_UNROLL
 #define QMCG_GEN_UNROLL 1
 #endif
 constexpr int kTile = kWarps;  // dates per tile = warps per block (one date row per warp)
 constexpr int kGenUnroll = QMCG_GEN_UNROLL;
-constexpr int kRecCap = 64;   // per-warp ring of pending record evaluations
+constexpr int kRecCap = 128;  // per-warp ring of pending record evaluations (mostly drained at path end)
 constexpr uint32_t kNone = 0xffffffffu;
 
 // ---------------------------------------------------------------------------
@@ -341,7 +341,13 @@ constexpr uint32_t kPermOff = 0;
 constexpr uint32_t kPermBuf = kTile * kThreads * 4;
 constexpr uint32_t kZtOff = kPermOff + 2 * kPermBuf;
 constexpr uint32_t kZtBuf = kTile * kThreads * 8;
-constexpr uint32_t kLogOff = kZtOff + 2 * kZtBuf;
+#ifndef QMCG_ZT_BUFFERS
+#define QMCG_ZT_BUFFERS 1
+#endif
+// 2: double-buffered z tiles (one block barrier per tile); 1: single buffer and a
+// second barrier after the walk (smaller shared footprint).
+constexpr int kZtBuffers = QMCG_ZT_BUFFERS;
+constexpr uint32_t kLogOff = kZtOff + kZtBuffers * kZtBuf;
 constexpr uint32_t kBarOff = kLogOff + 128 * 16;
 constexpr uint32_t kWarpOff = kBarOff + 128;
 constexpr uint32_t kWRqV = 0;
@@ -593,7 +599,7 @@ __device__ __forceinline__ void push_record(uint32_t ws, const PriceParams& P, b
       sts_u32(ws + kWRqCode + slot * 4, (static_cast<uint32_t>(d) << 5) | static_cast<uint32_t>(lane));
     }
     rq_tail += __popc(pb);
-    if (rq_tail - rq_head > 32) {  // rare: the ring (64) must keep room for one more date
+    if (rq_tail - rq_head > kRecCap - 32) {  // rare: the ring must keep room for one more date
       __syncwarp();
       process_records<KIND, RNEG>(P, ws, rq_head, 32, lane);
       rq_head += 32;
@@ -663,12 +669,13 @@ __global__ void __launch_bounds__(kThreads, QMCG_MINB) price_kernel(const PriceP
   for (int k = 0; k < ntiles; ++k) {
     const int k0 = k * kTile;
     const int b = k & 1;
-    const uint32_t zcol = sbase + kZtOff + b * kZtBuf + threadIdx.x * 8;
+    const uint32_t zb = kZtBuffers == 2 ? b : 0;
+    const uint32_t zcol = sbase + kZtOff + zb * kZtBuf + threadIdx.x * 8;
     if (!det) {
       mbar_wait_u32(sbase + kBarOff + b * 8, static_cast<uint32_t>((k >> 1) & 1));
       if (k0 + warp < m)
         generate_row<SLOW>(P, ws, k0 + warp, sbase + kPermOff + b * kPermBuf + warp * kThreads * 4,
-                           sbase + kZtOff + b * kZtBuf + warp * kThreads * 8, logtab, nchunks, lane, lt);
+                           sbase + kZtOff + zb * kZtBuf + warp * kThreads * 8, logtab, nchunks, lane, lt);
       __syncthreads();  // z tile complete; perm buffer b consumed
       if (threadIdx.x == 0 && k + 2 < ntiles) issue_tile(P, sbase, k + 2, b, col0, bytes);
     }
@@ -719,24 +726,36 @@ __global__ void __launch_bounds__(kThreads, QMCG_MINB) price_kernel(const PriceP
         }
       }
     }
-    if (rq_tail - rq_head >= 32) {  // the common evaluation site, once per tile at most
+    if (kZtBuffers == 1) __syncthreads();  // the z tile is rewritten by the next generation
+#ifndef QMCG_DRAIN_AT_END
+#define QMCG_DRAIN_AT_END 1
+#endif
+    if (!RNEG && !QMCG_DRAIN_AT_END && rq_tail - rq_head >= 32) {
       __syncwarp();
       process_records_inline<KIND, RNEG>(P, ws, rq_head, 32, lane);
       rq_head += 32;
       __syncwarp();
-      if (RNEG) {
-        unsigned long long bb;
-        asm volatile("ld.shared.u64 %0, [%1];" : "=l"(bb) : "r"(ws + kWBest + lane * 8));
-        c = rneg_threshold<KIND>(P, __longlong_as_double(static_cast<long long>(bb)));
-      }
+    }
+    if (RNEG && rq_tail - rq_head >= 32) {  // r < 0: the threshold follows the evaluated best
+      __syncwarp();
+      process_records_inline<KIND, RNEG>(P, ws, rq_head, 32, lane);
+      rq_head += 32;
+      __syncwarp();
+      unsigned long long bb;
+      asm volatile("ld.shared.u64 %0, [%1];" : "=l"(bb) : "r"(ws + kWBest + lane * 8));
+      c = rneg_threshold<KIND>(P, __longlong_as_double(static_cast<long long>(bb)));
     }
   }
   if (!RNEG) {  // the last pending record of every path
     push_record<KIND, RNEG>(ws, P, pend_d >= 0, c, pend_d, lane, lt, rq_head, rq_tail);
   }
-  if (rq_tail != rq_head) {
+  // The queued evaluations are drained after the last block barrier, so their
+  // uneven distribution over warps never stalls the other warps of the block.
+  while (rq_tail != rq_head) {
     __syncwarp();
-    process_records<KIND, RNEG>(P, ws, rq_head, rq_tail - rq_head, lane);
+    const uint32_t cnt = min(32u, rq_tail - rq_head);
+    process_records_inline<KIND, RNEG>(P, ws, rq_head, cnt, lane);
+    rq_head += cnt;
   }
   __syncwarp();
 
@@ -806,7 +825,7 @@ __global__ void __launch_bounds__(kThreads, QMCG_MINB) gen_z_kernel(const PriceP
     const int k0 = k * kTile;
     const int b = k & 1;
     mbar_wait_u32(sbase + kBarOff + b * 8, static_cast<uint32_t>((k >> 1) & 1));
-    const uint32_t zrow = sbase + kZtOff + b * kZtBuf + warp * kThreads * 8;
+    const uint32_t zrow = sbase + kZtOff + (kZtBuffers == 2 ? b : 0) * kZtBuf + warp * kThreads * 8;
     if (k0 + warp < m) {
       generate_row<SLOW>(P, ws, k0 + warp, sbase + kPermOff + b * kPermBuf + warp * kThreads * 4, zrow, logtab,
                          nchunks, lane, lt);
