@@ -46,6 +46,7 @@ enum { QMCG_METHOD_CLOSED_FORM = 0, QMCG_METHOD_EUROPEAN_MC = 1, QMCG_METHOD_AME
 enum {
   QMCG_FLAG_ALLOW_PUT = 1u << 0, /* opt-in put extension (reference rejects puts: american.cpp:106-109) */
   QMCG_FLAG_NO_CACHE = 1u << 1,  /* rebuild the permutation tables for this call (cold timing) */
+  QMCG_FLAG_FP32 = 1u << 2,      /* FP32 normals + walk (uniforms stay bit-exact FP64); price within QMC error */
 };
 
 /* reference OptionSpec, proj/include/qmc/types.hpp:24-31 */

@@ -394,6 +394,7 @@ qmcg_status plan_call(const qmcg_option_spec& s, int64_t m, int64_t n, uint32_t 
   // |X0| + m (|a| + b |z|max) stays inside exp's range (|z| <= 7.04 for u in [1e-12, 1-1e-12])
   const double reach = std::fabs(P.X0) + static_cast<double>(m) * (std::fabs(a) + bdiff * 7.05) + 1.0;
   P.check_range = reach > 700.0;
+  P.fp32 = (flags & QMCG_FLAG_FP32) != 0;
   return QMCG_OK;
 }
 

@@ -181,6 +181,30 @@ __device__ __forceinline__ double moro_tail_poly(double w, uint32_t tab) {
   return x;
 }
 
+// FP32 variant (QMCG_FLAG_FP32): Moro in single precision on the exact FP64
+// uniform (the branch partition is still decided in FP64).
+__device__ __forceinline__ float moro_central_f32(float y, float alpha) {
+  const float r = y * y;
+  const float A = fmaf(fmaf(fmaf(-25.44106049637f, r, 41.39119773534f), r, -18.61500062529f), r, 2.50662823884f);
+  const float B = fmaf(fmaf(fmaf(fmaf(3.13082909833f, r, -21.06224101826f), r, 23.08336743743f), r, -8.47351093090f),
+                       r, 1.0f);
+  return fmaf(y * A, __frcp_rn(B), alpha);
+}
+
+__device__ __forceinline__ float moro_tail_poly_f32(float w) {
+  const float z = __logf(-__logf(w));
+  float x = 0.0000003960315187f;
+  x = fmaf(x, z, 0.0000002888167364f);
+  x = fmaf(x, z, 0.0000321767881768f);
+  x = fmaf(x, z, 0.0003951896511919f);
+  x = fmaf(x, z, 0.0038405729373609f);
+  x = fmaf(x, z, 0.0276438810333863f);
+  x = fmaf(x, z, 0.1607979714918209f);
+  x = fmaf(x, z, 0.9761690190917186f);
+  x = fmaf(x, z, 0.3374754822726147f);
+  return x;
+}
+
 __device__ __forceinline__ double moro_tail_poly(double w) {
   const double z = log(-log(w));
   double x = c_moro_c[8];
@@ -440,20 +464,67 @@ __device__ __forceinline__ void mbar_wait_u32(uint32_t bar, uint32_t parity) {
       : "memory");
 }
 
+__device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ float add_rn(float a, float b) { return __fadd_rn(a, b); }
+
+// z-tile slot access: FP64 (8 B) or, for the FP32 variant, FP32 (4 B).
+template <bool F32> struct ZSlot;
+template <> struct ZSlot<false> {
+  using T = double;
+  static constexpr uint32_t kSize = 8;
+  static __device__ __forceinline__ T load(uint32_t a) { return lds_f64(a); }
+  static __device__ __forceinline__ void store(uint32_t a, T v) { sts_f64(a, v); }
+};
+template <> struct ZSlot<true> {
+  using T = float;
+  static constexpr uint32_t kSize = 4;
+  static __device__ __forceinline__ T load(uint32_t a) {
+    float v;
+    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a) : "memory");
+    return v;
+  }
+  static __device__ __forceinline__ void store(uint32_t a, T v) {
+    asm volatile("st.shared.f32 [%0], %1;" ::"r"(a), "f"(v) : "memory");
+  }
+};
+
+// The value a tail point parks in its slot until flush_tail: FP64 mode the
+// uniform u itself; FP32 mode the exact FP64 w = u or 1 - u rounded to FP32,
+// negative when y > 0 (w = 1 - u).
+template <bool F32>
+__device__ __forceinline__ typename ZSlot<F32>::T tail_park(double u, double y) {
+  if (F32) return static_cast<float>(y > 0.0 ? -__dadd_rn(1.0, -u) : u);
+  return u;
+}
+
+template <bool F32>
+__device__ __forceinline__ typename ZSlot<F32>::T central_z(double y, double alpha) {
+  if (F32) return moro_central_f32(static_cast<float>(y), static_cast<float>(alpha));
+  return moro_central_plus(y, alpha);
+}
+
 // Evaluate the queued Moro-tail points of one date row, 32 per round:
 // u (parked in the point's z slot) -> y = u - 0.5 (exact as the reference),
 // w = u or 1 - u, z = +-P8(log(-log w)) + alpha written back to the slot.
+template <bool F32>
 __device__ __forceinline__ void flush_tail(uint32_t ws, uint32_t zrow, uint32_t ntail, uint32_t logtab, double alpha,
                                            int lane) {
+  using Z = ZSlot<F32>;
   __syncwarp();
   for (uint32_t r = 0; r < ntail; r += 32) {
     const uint32_t q = r + lane;
     if (q < ntail) {
-      const uint32_t slot = zrow + lds_u8(ws + kWTailIdx + q) * 8;
-      const double u = lds_f64(slot);
-      const double y = __dadd_rn(u, -0.5);
-      const double x = moro_tail_poly(y > 0.0 ? __dadd_rn(1.0, -u) : u, logtab);
-      sts_f64(slot, (y > 0.0 ? x : -x) + alpha);
+      const uint32_t slot = zrow + lds_u8(ws + kWTailIdx + q) * Z::kSize;
+      if (F32) {
+        const float wsg = Z::load(slot);
+        const float x = moro_tail_poly_f32(fabsf(wsg));
+        Z::store(slot, (wsg < 0.0f ? x : -x) + static_cast<float>(alpha));
+      } else {
+        const double u = Z::load(slot);
+        const double y = __dadd_rn(u, -0.5);
+        const double x = moro_tail_poly(y > 0.0 ? __dadd_rn(1.0, -u) : u, logtab);
+        Z::store(slot, (y > 0.0 ? x : -x) + alpha);
+      }
     }
   }
   __syncwarp();
@@ -462,7 +533,7 @@ __device__ __forceinline__ void flush_tail(uint32_t ws, uint32_t zrow, uint32_t 
 // One point of a date row: tail test; a tail point parks u in its z slot and
 // queues its index (branch-free: other lanes write a dummy slot); otherwise
 // the central normal + alpha goes to the slot.
-template <bool CLAMP>
+template <bool CLAMP, bool F32>
 __device__ __forceinline__ void finish_point(uint32_t ws, uint32_t zslot, uint32_t idx, double u, bool clamp,
                                              double alpha, int lane, unsigned lt, uint32_t& ntail) {
   if (CLAMP && clamp) u = clamp_endpoints(u);
@@ -472,8 +543,8 @@ __device__ __forceinline__ void finish_point(uint32_t ws, uint32_t zslot, uint32
   const uint32_t pos = tail ? ntail + __popc(tb & lt) : kTailCap + lane;
   sts_u8(ws + kWTailIdx + pos, idx);
   ntail += __popc(tb);
-  const double z = moro_central_plus(y, alpha);
-  sts_f64(zslot, tail ? u : z);
+  const auto z = central_z<F32>(y, alpha);
+  ZSlot<F32>::store(zslot, tail ? tail_park<F32>(u, y) : z);
 }
 
 template <bool WIDE>
@@ -503,10 +574,12 @@ __device__ __forceinline__ double halton_fixed(uint32_t x, uint32_t magic, uint3
   return u;
 }
 
-template <int D>
+template <int D, bool F32>
 __device__ __forceinline__ uint32_t generate_row_fixed(const double2* sn, uint32_t magic, uint32_t shift,
                                                        uint32_t negp, uint32_t ws, uint32_t prow, uint32_t zrow,
                                                        int nchunks, int lane, unsigned lt, double alpha) {
+  using Z = ZSlot<F32>;
+  constexpr uint32_t kCh = 32 * Z::kSize;  // bytes per 32-path chunk of a row
   double2 sc[4];
 #pragma unroll
   for (int j = 0; j < 4; ++j) sc[j] = j < D ? __ldg(sn + j) : make_double2(0.0, 0.0);
@@ -520,8 +593,8 @@ __device__ __forceinline__ uint32_t generate_row_fixed(const double2* sn, uint32
     const double ub = halton_fixed<D>(xb, magic, shift, negp, sc);
     const double ya = __dadd_rn(ua, -0.5);
     const double yb = __dadd_rn(ub, -0.5);
-    const double za = moro_central_plus(ya, alpha);
-    const double zb = moro_central_plus(yb, alpha);
+    const auto za = central_z<F32>(ya, alpha);
+    const auto zb = central_z<F32>(yb, alpha);
     const bool ta = fabs(ya) > 0.42, tb = fabs(yb) > 0.42;
     const unsigned ba = __ballot_sync(kFull, ta), bb = __ballot_sync(kFull, tb);
     const uint32_t na = __popc(ba);
@@ -530,34 +603,35 @@ __device__ __forceinline__ uint32_t generate_row_fixed(const double2* sn, uint32
     sts_u8(ws + kWTailIdx + pa, ch * 32 + lane);
     sts_u8(ws + kWTailIdx + pb, ch * 32 + 32 + lane);
     ntail += na + __popc(bb);
-    sts_f64(zrow + ch * 256, ta ? ua : za);
-    sts_f64(zrow + ch * 256 + 256, tb ? ub : zb);
+    Z::store(zrow + ch * kCh, ta ? tail_park<F32>(ua, ya) : za);
+    Z::store(zrow + ch * kCh + kCh, tb ? tail_park<F32>(ub, yb) : zb);
   }
   if (ch < nchunks) {
     const uint32_t x = lds_u32(prow + ch * 128) + 1u;
     const double u = halton_fixed<D>(x, magic, shift, negp, sc);
-    finish_point<false>(ws, zrow + ch * 256, ch * 32 + lane, u, false, alpha, lane, lt, ntail);
+    finish_point<false, F32>(ws, zrow + ch * kCh, ch * 32 + lane, u, false, alpha, lane, lt, ntail);
   }
   return ntail;
 }
 
-template <bool SLOW>
+template <bool SLOW, bool F32>
 __device__ __forceinline__ void generate_row(const PriceParams& P, uint32_t ws, int d, uint32_t prow, uint32_t zrow,
                                              uint32_t logtab, int nchunks, int lane, unsigned lt) {
+  using Z = ZSlot<F32>;
   const uint4 dp = __ldg(reinterpret_cast<const uint4*>(P.dims) + d);
   const uint32_t magic = dp.y, shift = dp.z & 0xffu, negp = 0u - dp.x;
   const int D = static_cast<int>((dp.z >> 8) & 0xffu);
   const double2* sn = P.scnc + dp.w;
   const double alpha = P.alpha;
   const uint32_t pl = prow + lane * 4;
-  const uint32_t zl = zrow + lane * 8;
+  const uint32_t zl = zrow + lane * Z::kSize;
   uint32_t ntail = 0;
   if (!SLOW && D == 3) {
-    ntail = generate_row_fixed<3>(sn, magic, shift, negp, ws, pl, zl, nchunks, lane, lt, alpha);
+    ntail = generate_row_fixed<3, F32>(sn, magic, shift, negp, ws, pl, zl, nchunks, lane, lt, alpha);
   } else if (!SLOW && D == 4) {
-    ntail = generate_row_fixed<4>(sn, magic, shift, negp, ws, pl, zl, nchunks, lane, lt, alpha);
+    ntail = generate_row_fixed<4, F32>(sn, magic, shift, negp, ws, pl, zl, nchunks, lane, lt, alpha);
   } else if (!SLOW && D == 2) {
-    ntail = generate_row_fixed<2>(sn, magic, shift, negp, ws, pl, zl, nchunks, lane, lt, alpha);
+    ntail = generate_row_fixed<2, F32>(sn, magic, shift, negp, ws, pl, zl, nchunks, lane, lt, alpha);
   } else {
     const bool clamp = SLOW && ((dp.z >> 16) & DIM_CLAMP);
     const bool wide = SLOW && ((dp.z >> 16) & DIM_WIDE);
@@ -565,10 +639,10 @@ __device__ __forceinline__ void generate_row(const PriceParams& P, uint32_t ws, 
     for (int ch = 0; ch < nchunks; ++ch) {
       const uint32_t x = lds_u32(pl + ch * 128) + 1u;
       const double u = wide ? halton_any<true>(x, dp, m64, sn) : halton_any<false>(x, dp, m64, sn);
-      finish_point<SLOW>(ws, zl + ch * 256, ch * 32 + lane, u, clamp, alpha, lane, lt, ntail);
+      finish_point<SLOW, F32>(ws, zl + ch * 32 * Z::kSize, ch * 32 + lane, u, clamp, alpha, lane, lt, ntail);
     }
   }
-  if (ntail) flush_tail(ws, zrow, ntail, logtab, alpha, lane);
+  if (ntail) flush_tail<F32>(ws, zrow, ntail, logtab, alpha, lane);
 }
 
 // Dominance of the lane's pending record j by a new record k (then j can never
@@ -580,12 +654,14 @@ __device__ __forceinline__ void generate_row(const PriceParams& P, uint32_t ws, 
 //          sufficient (exact-safe lower/upper bounds, no exp): with u = ln w,
 //          (1 + u) s (1 - s/2) >= delta, s = delta + Delta, 1 + u > 0, s < 2.
 // x0mk = 1 + X0 - ln K (puts only).
-template <int KIND>
-__device__ __forceinline__ bool record_dominates(double V, double c, double acc, double b, double x0mk) {
+template <int KIND, typename T>
+__device__ __forceinline__ bool record_dominates(T V, T c, T acc, T b, T x0mk) {
   if (KIND == 0) return V >= acc;
-  const double u1 = fma(b, c, x0mk);
-  const double s = fma(b, c - V, acc);
-  return u1 > 0.0 && s < 2.0 && u1 * s * fma(-0.5, s, 1.0) >= acc * (1.0 + 1e-12);
+  // FP32 variant: the bound is taken with a relative margin far above its rounding
+  const T margin = sizeof(T) == 8 ? T(1e-12) : T(1e-4);
+  const T u1 = fma(b, c, x0mk);
+  const T s = fma(b, c - V, acc);
+  return u1 > T(0) && s < T(2) && u1 * s * fma(T(-0.5), s, T(1)) >= acc * (T(1) + margin);
 }
 
 template <int KIND, bool RNEG>
@@ -620,7 +696,7 @@ __device__ __forceinline__ void push_record(uint32_t ws, const PriceParams& P, b
 // with key = V - slope*date, slope = r*dt/b, calls), otherwise j is queued
 // for exact evaluation (exp + discount) in warp-wide batches of 32.
 // SLOW = any of: volatility 0, range checks, 64-bit magic, endpoint clamp.
-template <int KIND, bool RNEG, bool SLOW>
+template <int KIND, bool RNEG, bool SLOW, bool F32>
 __global__ void __launch_bounds__(kThreads, QMCG_MINB) price_kernel(const PriceParams P) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const uint32_t sbase = smem_u32(smem_raw);
@@ -642,7 +718,10 @@ __global__ void __launch_bounds__(kThreads, QMCG_MINB) price_kernel(const PriceP
   // columns of this block in the table (16-byte aligned: path_begin - col_begin and ld are multiples of 4)
   const int64_t col0 = P.path_begin - P.col_begin + block_first;
   const uint32_t bytes = static_cast<uint32_t>(((block_paths + 3) / 4) * 16);
-  const double slope = P.dom_slope;
+  using Z = ZSlot<F32>;
+  using T = typename Z::T;
+  const T slope = static_cast<T>(P.dom_slope);
+  const T bT = static_cast<T>(P.b), x0mkT = static_cast<T>(P.x0mk);
 
   if (threadIdx.x == 0) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sbase + kBarOff));
@@ -659,9 +738,9 @@ __global__ void __launch_bounds__(kThreads, QMCG_MINB) price_kernel(const PriceP
     if (ntiles > 1) issue_tile(P, sbase, 1, 1, col0, bytes);
   }
 
-  double V = 0.0;
-  double c = P.c0;
-  double cd = 0.0;  // dominance threshold of the pending record (see the walk)
+  T V = T(0);
+  T c = static_cast<T>(P.c0);
+  T cd = T(0);  // dominance threshold of the pending record (see the walk)
   int pend_d = -1;  // date of the pending (not yet evaluated) record, -1 = none
   uint32_t rq_head = 0, rq_tail = 0;
   uint32_t err = 0;
@@ -670,12 +749,12 @@ __global__ void __launch_bounds__(kThreads, QMCG_MINB) price_kernel(const PriceP
     const int k0 = k * kTile;
     const int b = k & 1;
     const uint32_t zb = kZtBuffers == 2 ? b : 0;
-    const uint32_t zcol = sbase + kZtOff + zb * kZtBuf + threadIdx.x * 8;
+    const uint32_t zcol = sbase + kZtOff + zb * kZtBuf + threadIdx.x * Z::kSize;
     if (!det) {
       mbar_wait_u32(sbase + kBarOff + b * 8, static_cast<uint32_t>((k >> 1) & 1));
       if (k0 + warp < m)
-        generate_row<SLOW>(P, ws, k0 + warp, sbase + kPermOff + b * kPermBuf + warp * kThreads * 4,
-                           sbase + kZtOff + zb * kZtBuf + warp * kThreads * 8, logtab, nchunks, lane, lt);
+        generate_row<SLOW, F32>(P, ws, k0 + warp, sbase + kPermOff + b * kPermBuf + warp * kThreads * 4,
+                                sbase + kZtOff + zb * kZtBuf + warp * kThreads * Z::kSize, logtab, nchunks, lane, lt);
       __syncthreads();  // z tile complete; perm buffer b consumed
       if (threadIdx.x == 0 && k + 2 < ntiles) issue_tile(P, sbase, k + 2, b, col0, bytes);
     }
@@ -685,14 +764,14 @@ __global__ void __launch_bounds__(kThreads, QMCG_MINB) price_kernel(const PriceP
     if (!SLOW && !RNEG && k0 + kTile <= mrec) {
 #pragma unroll
       for (int t = 0; t < kTile; ++t) {
-        V = __dadd_rn(V, lds_f64(zcol + t * kThreads * 8));
-        cd = __dadd_rn(cd, slope);
+        V = add_rn(V, Z::load(zcol + t * kThreads * Z::kSize));
+        cd = add_rn(cd, slope);
         const bool rec = KIND == 0 ? V > c : V < c;
-        const bool push = rec && pend_d >= 0 && !record_dominates<KIND>(V, c, cd, P.b, P.x0mk);
+        const bool push = rec && pend_d >= 0 && !record_dominates<KIND>(V, c, cd, bT, x0mkT);
         const double pv = c;
         const int pd = pend_d;
         c = rec ? V : c;
-        cd = rec ? (KIND == 0 ? V : 0.0) : cd;
+        cd = rec ? (KIND == 0 ? V : T(0)) : cd;
         pend_d = rec ? k0 + t : pend_d;
         push_record<KIND, RNEG>(ws, P, push, pv, pd, lane, lt, rq_head, rq_tail);
       }
@@ -701,10 +780,10 @@ __global__ void __launch_bounds__(kThreads, QMCG_MINB) price_kernel(const PriceP
       for (int t = 0; t < kTile; ++t) {
         const int d = k0 + t;
         if (d < m) {
-          V = __dadd_rn(V, det ? P.alpha : lds_f64(zcol + t * kThreads * 8));
-          cd = __dadd_rn(cd, slope);
+          V = add_rn(V, det ? static_cast<T>(P.alpha) : Z::load(zcol + t * kThreads * Z::kSize));
+          cd = add_rn(cd, slope);
           if (check && active) {
-            const double X = fma(P.b, V, P.X0);
+            const double X = fma(P.b, static_cast<double>(V), P.X0);
             if (X < -745.1332191019412) err |= ERR_SPOT_NONPOSITIVE;
             if (X > 709.782712893384) err |= ERR_SPOT_NONFINITE;
           }
@@ -714,11 +793,11 @@ __global__ void __launch_bounds__(kThreads, QMCG_MINB) price_kernel(const PriceP
               // every candidate is evaluated; the threshold follows the evaluated best
               push_record<KIND, RNEG>(ws, P, rec, V, d, lane, lt, rq_head, rq_tail);
             } else {
-              const bool push = rec && pend_d >= 0 && !record_dominates<KIND>(V, c, cd, P.b, P.x0mk);
+              const bool push = rec && pend_d >= 0 && !record_dominates<KIND>(V, c, cd, bT, x0mkT);
               const double pv = c;
               const int pd = pend_d;
               c = rec ? V : c;
-              cd = rec ? (KIND == 0 ? V : 0.0) : cd;
+              cd = rec ? (KIND == 0 ? V : T(0)) : cd;
               pend_d = rec ? d : pend_d;
               push_record<KIND, RNEG>(ws, P, push, pv, pd, lane, lt, rq_head, rq_tail);
             }
@@ -743,7 +822,7 @@ __global__ void __launch_bounds__(kThreads, QMCG_MINB) price_kernel(const PriceP
       __syncwarp();
       unsigned long long bb;
       asm volatile("ld.shared.u64 %0, [%1];" : "=l"(bb) : "r"(ws + kWBest + lane * 8));
-      c = rneg_threshold<KIND>(P, __longlong_as_double(static_cast<long long>(bb)));
+      c = static_cast<T>(rneg_threshold<KIND>(P, __longlong_as_double(static_cast<long long>(bb))));
     }
   }
   if (!RNEG) {  // the last pending record of every path
@@ -760,7 +839,7 @@ __global__ void __launch_bounds__(kThreads, QMCG_MINB) price_kernel(const PriceP
   __syncwarp();
 
   // Date m: max(intrinsic, Black-Scholes of the final interval), american.cpp:43-52.
-  const double X = fma(P.b, V, P.X0);
+  const double X = fma(P.b, static_cast<double>(V), P.X0);
   const double sm_last = exp(X);
   double cont;
   if (P.bs_v_zero) {
@@ -827,7 +906,7 @@ __global__ void __launch_bounds__(kThreads, QMCG_MINB) gen_z_kernel(const PriceP
     mbar_wait_u32(sbase + kBarOff + b * 8, static_cast<uint32_t>((k >> 1) & 1));
     const uint32_t zrow = sbase + kZtOff + (kZtBuffers == 2 ? b : 0) * kZtBuf + warp * kThreads * 8;
     if (k0 + warp < m) {
-      generate_row<SLOW>(P, ws, k0 + warp, sbase + kPermOff + b * kPermBuf + warp * kThreads * 4, zrow, logtab,
+      generate_row<SLOW, false>(P, ws, k0 + warp, sbase + kPermOff + b * kPermBuf + warp * kThreads * 4, zrow, logtab,
                          nchunks, lane, lt);
       __syncwarp();
       double* dst = z + static_cast<int64_t>(k0 + warp) * ldz + P.path_begin + block_first;
@@ -1183,11 +1262,11 @@ int leaf_depth(int64_t len) {
 
 }  // namespace
 
-template <int KIND, bool RNEG, bool SLOW>
+template <int KIND, bool RNEG, bool SLOW, bool F32>
 cudaError_t launch_price_t(const PriceParams& P, cudaStream_t s) {
   const int64_t blocks = (P.path_count + kThreads - 1) / kThreads;
   const size_t smem = kSmemBytes;
-  auto kern = price_kernel<KIND, RNEG, SLOW>;
+  auto kern = price_kernel<KIND, RNEG, SLOW, F32>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   if (e != cudaSuccess) return e;
   kern<<<static_cast<unsigned>(blocks), kThreads, smem, s>>>(P);
@@ -1197,7 +1276,9 @@ cudaError_t launch_price_t(const PriceParams& P, cudaStream_t s) {
 template <int KIND, bool RNEG>
 cudaError_t launch_price_k(const PriceParams& P, cudaStream_t s) {
   const bool slow = P.any_wide || P.any_clamp || P.deterministic || P.check_range;
-  return slow ? launch_price_t<KIND, RNEG, true>(P, s) : launch_price_t<KIND, RNEG, false>(P, s);
+  if (P.fp32)
+    return slow ? launch_price_t<KIND, RNEG, true, true>(P, s) : launch_price_t<KIND, RNEG, false, true>(P, s);
+  return slow ? launch_price_t<KIND, RNEG, true, false>(P, s) : launch_price_t<KIND, RNEG, false, false>(P, s);
 }
 
 namespace {

@@ -66,6 +66,8 @@ struct PriceParams {
   int32_t deterministic; // volatility == 0: z never affects the path
   int32_t check_range;   // per-date overflow/underflow checks needed
   int32_t rate_negative; // disc > 1: running-max filter invalid, use best-based filter
+  int32_t fp32;          // QMCG_FLAG_FP32: single-precision normals and walk
+  int32_t pad0;
   double* values;        // per-path t0 values, index = path - path_begin
   uint32_t* err;
 };

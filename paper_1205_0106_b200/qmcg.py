@@ -26,6 +26,11 @@ LIB_PATH = os.environ.get("QMCG_LIB") or os.path.join(os.path.dirname(os.path.ab
 OK, INVALID_ARGUMENT, LENGTH_ERROR, CUDA_ERROR, NCCL_ERROR, UNSUPPORTED, OUT_OF_MEMORY = range(7)
 FLAG_ALLOW_PUT = 1
 FLAG_NO_CACHE = 2
+FLAG_FP32 = 4  # single-precision normals + walk (uniforms stay bit-exact FP64)
+
+
+def _flags(allow_put: bool = False, no_cache: bool = False, fp32: bool = False) -> int:
+    return (FLAG_ALLOW_PUT if allow_put else 0) | (FLAG_NO_CACHE if no_cache else 0) | (FLAG_FP32 if fp32 else 0)
 
 # every symbol include/qmcg.h declares (checked by tests/test_abi.py)
 EXPORTS = (
@@ -184,13 +189,13 @@ class Context:
     # -- the hot path --
     def price_american(self, spec: OptionSpec, m: int, n_paths: int, seed: int,
                        exec: Optional[ExecPolicy] = None, allow_put: bool = False,
-                       no_cache: bool = False) -> PricingResult:
+                       no_cache: bool = False, fp32: bool = False) -> PricingResult:
         if exec is not None:
             if exec.lanes < 1:
                 raise ValueError("parallel_for_chunks: lanes must be >= 1")
             if exec.chunk < 1:
                 raise ValueError("parallel_for_chunks: chunk must be >= 1")
-        flags = (FLAG_ALLOW_PUT if allow_put else 0) | (FLAG_NO_CACHE if no_cache else 0)
+        flags = _flags(allow_put, no_cache, fp32)
         s, r = _cspec(spec), _CResult()
         _check(self._lib.qmcg_price_american(self._h, C.byref(s), int(m), int(n_paths), int(seed), flags, C.byref(r)))
         return _result(r)
@@ -250,21 +255,22 @@ class Context:
         _check(self._lib.qmcg_normal_table(self._h, int(n), int(seed), int(dims), out.ctypes.data))
         return out
 
-    def path_values(self, spec: OptionSpec, m: int, n_paths: int, seed: int, allow_put: bool = False) -> np.ndarray:
+    def path_values(self, spec: OptionSpec, m: int, n_paths: int, seed: int, allow_put: bool = False,
+                    fp32: bool = False) -> np.ndarray:
         out = np.zeros(int(n_paths), dtype=np.float64)
         s = _cspec(spec)
         _check(self._lib.qmcg_path_values(self._h, C.byref(s), int(m), int(n_paths), int(seed),
-                                          FLAG_ALLOW_PUT if allow_put else 0, out.ctypes.data))
+                                          _flags(allow_put, fp32=fp32), out.ctypes.data))
         return out
 
     # -- measurement hooks --
     def time_device(self, spec: OptionSpec, m: int, n_paths: int, seed: int, reps: int,
-                    allow_put: bool = False):
+                    allow_put: bool = False, fp32: bool = False):
         k, st = C.c_double(), C.c_double()
         ps = np.zeros(2, dtype=np.float64)
         s = _cspec(spec)
         _check(self._lib.qmcg_time_device(self._h, C.byref(s), int(m), int(n_paths), int(seed),
-                                          FLAG_ALLOW_PUT if allow_put else 0, int(reps), C.byref(k), C.byref(st),
+                                          _flags(allow_put, fp32=fp32), int(reps), C.byref(k), C.byref(st),
                                           ps.ctypes.data_as(C.POINTER(C.c_double))))
         return k.value, st.value, float(ps[0]), float(ps[1])
 

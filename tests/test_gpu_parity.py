@@ -210,3 +210,23 @@ def test_mc_european_vs_reference_goldens(ctx, qmcg, golden):
     with pytest.raises(ValueError) as e:
         ctx.mc_european_price(qmcg.OptionSpec(*REF), 1, 42)
     assert str(e.value) == "mc_european_price: n_paths must be >= 2"
+
+
+@pytest.mark.parametrize("s,kind,m,n", [(REF, 0, 16, 1 << 14), (REF, 0, 256, 1 << 18),
+                                        ((110.0, 100.0, 0.05, 0.3, 2.0), 0, 100, 1 << 16),
+                                        (REF, 1, 50, 1 << 16), ((90.0, 100.0, 0.03, 0.3, 0.5), 1, 365, 1 << 15),
+                                        ((100.0, 110.0, -0.02, 0.3, 1.0), 0, 33, 1 << 14)])
+def test_fp32_variant_within_qmc_error(ctx, qmcg, s, kind, m, n):
+    """FP32 variant (north star: 'within the QMC standard error for an FP32 variant'):
+    uniforms stay bit-exact FP64; normals and the walk run in FP32, exercise values in FP64.
+    Bar: |price32 - price64| <= 0.05 se, and every path value within 1e-4 relative."""
+    sp = spec_of(qmcg, s, kind)
+    put = kind == 1
+    r64 = ctx.price_american(sp, m, n, 42, allow_put=put)
+    r32 = ctx.price_american(sp, m, n, 42, allow_put=put, fp32=True)
+    assert abs(r32.price - r64.price) <= 0.05 * r64.std_error, (r32.price, r64.price, r64.std_error)
+    assert abs(r32.std_error - r64.std_error) <= 1e-3 * r64.std_error
+    v64 = ctx.path_values(sp, m, n, 42, allow_put=put)
+    v32 = ctx.path_values(sp, m, n, 42, allow_put=put, fp32=True)
+    rel = np.abs(v32 - v64) / np.maximum(np.abs(v64), 1e-3 * s[1])
+    assert rel.max() <= 1e-4, rel.max()
