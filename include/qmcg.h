@@ -119,6 +119,16 @@ qmcg_status qmcg_combine_nodes(int64_t n_paths, int depth, const double* node_su
 qmcg_status qmcg_warm(qmcg_ctx* ctx, int64_t n_paths, uint64_t seed, int64_t dims);
 /* Drop every cached table. */
 qmcg_status qmcg_clear_cache(qmcg_ctx* ctx);
+/* Cap the bytes the permutation tables may occupy (0 = whatever free device
+ * memory allows). A pricing whose tables exceed it runs in date windows
+ * ("streamed tables": each window's rows are built, walked, and replaced,
+ * with the per-path walk state carried in HBM) with identical results; this
+ * is how 2^28 paths x 365 dates (392 GB of tables) prices on one GPU. No
+ * reference counterpart: the reference caps its path matrix at 128 GiB
+ * (proj/src/path_engine.cpp:20-35). */
+qmcg_status qmcg_set_table_budget(qmcg_ctx* ctx, uint64_t bytes);
+/* Date windows the last pricing call used (1 = resident tables). */
+int64_t qmcg_last_window_count(qmcg_ctx* ctx);
 
 /* ---- parity exports (bit-exact checks against the reference) ---- */
 /* permutation_indices(n, seed64) (proj/src/quasi_rng.cpp:48-61), built on the GPU. */

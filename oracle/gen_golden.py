@@ -5,8 +5,9 @@ oracle/Makefile) and writes small JSON fixtures: full-precision prices and
 standard errors, permutation / uniform hashes, analytic function values.
 The GPU box has no /root/reference, so the parity tests read these fixtures.
 
-usage: python oracle/gen_golden.py [--big]
-  --big additionally prices 2^24 x 256 (config 3; ~52 GB RAM, minutes).
+usage: python oracle/gen_golden.py [--big | --only-big | --only-c5]
+  --big additionally prices 2^24 x 256 (config 3; ~52 GB RAM, minutes); --only-big / --only-c5
+  price just config 3 / the config-5 ladder rung 2^20 x 365 and merge them into prices.json.
 """
 from __future__ import annotations
 
@@ -57,24 +58,27 @@ def hexf(x: float) -> str:
     return float(x).hex()
 
 
-def only_big() -> None:
-    """Price config 3 (2^24 x 256) with the reference and merge it into prices.json."""
+def only_big(m: int = 256, n: int = 1 << 24) -> None:
+    """Price one large case with the reference and merge it into prices.json: config 3
+    (2^24 x 256, --only-big) or the first rung of the config-5 ladder (2^20 x 365, --only-c5)."""
     R = oracle.Reference()
     lanes = os.cpu_count() or 1
     path = os.path.join(GOLD, "prices.json")
     doc = json.load(open(path))
-    p, se, el = R.price_american(*REF_SPEC, 256, 1 << 24, SEED, lanes=lanes)
-    doc["cases"] = [c for c in doc["cases"] if not (c["m"] == 256 and c["n"] == 1 << 24)]
-    doc["cases"].append({"spec": list(REF_SPEC), "kind": "call", "m": 256, "n": 1 << 24, "seed": SEED,
+    p, se, el = R.price_american(*REF_SPEC, m, n, SEED, lanes=lanes)
+    doc["cases"] = [c for c in doc["cases"] if not (c["m"] == m and c["n"] == n and tuple(c["spec"]) == REF_SPEC)]
+    doc["cases"].append({"spec": list(REF_SPEC), "kind": "call", "m": m, "n": n, "seed": SEED,
                          "price": hexf(p), "std_error": hexf(se), "price_dec": repr(p), "elapsed_s_ref": el,
                          "lanes": lanes})
     write("prices.json", doc)
-    print(f"config 3: price={p!r} se={se!r} ({el:.1f}s, {lanes} lanes)")
+    print(f"m={m} n={n}: price={p!r} se={se!r} ({el:.1f}s, {lanes} lanes)")
 
 
 def main() -> None:
     if "--only-big" in sys.argv:
         return only_big()
+    if "--only-c5" in sys.argv:
+        return only_big(365, 1 << 20)
     big = "--big" in sys.argv
     R = oracle.Reference()
     lanes = os.cpu_count() or 1
@@ -106,7 +110,7 @@ def main() -> None:
     if os.path.exists(path) and not big:
         old = {(tuple(c["spec"]), c["m"], c["n"]): c for c in json.load(open(path))["cases"]}
         for key, c in old.items():
-            if key[2] == 1 << 24 and not any((tuple(x["spec"]), x["m"], x["n"]) == key for x in prices):
+            if (key[2] == 1 << 24 or key[1:] == (365, 1 << 20)) and not any((tuple(x["spec"]), x["m"], x["n"]) == key for x in prices):
                 prices.append(c)  # keep a previously generated config-3 golden
     write("prices.json", {"source": "oracle/_ref (reference proj/src compiled unmodified)", "cases": prices})
 

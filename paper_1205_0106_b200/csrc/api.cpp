@@ -231,6 +231,11 @@ struct qmcg_ctx {
   DevBuf<qmcg::ContractParams> d_cparams;
   DevBuf<uint32_t> d_err, d_fullperm;
   DevBuf<char> d_permscratch;
+  // streamed tables (date windows): per-path walk state carried between windows
+  DevBuf<double> d_stV, d_stc, d_stcd, d_stbest;
+  DevBuf<int32_t> d_stpend;
+  size_t table_budget = 0;  // bytes the permutation table may take; 0 = what free memory allows
+  int64_t last_windows = 0;  // date windows of the last pricing (1 = resident tables)
   double* h_pinned = nullptr;  // [0..1] sums, [2] err as double bits
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
   int64_t launches = 0;
@@ -395,6 +400,9 @@ qmcg_status plan_call(const qmcg_option_spec& s, int64_t m, int64_t n, uint32_t 
   const double reach = std::fabs(P.X0) + static_cast<double>(m) * (std::fabs(a) + bdiff * 7.05) + 1.0;
   P.check_range = reach > 700.0;
   P.fp32 = (flags & QMCG_FLAG_FP32) != 0;
+  P.d_begin = 0;
+  P.d_end = P.m;
+  P.perm_row0 = 0;
   return QMCG_OK;
 }
 
@@ -539,6 +547,11 @@ void qmcg_destroy(qmcg_ctx* c) {
   c->d_err.release();
   c->d_fullperm.release();
   c->d_permscratch.release();
+  c->d_stV.release();
+  c->d_stc.release();
+  c->d_stcd.release();
+  c->d_stbest.release();
+  c->d_stpend.release();
   if (c->h_pinned) cudaFreeHost(c->h_pinned);
   for (auto& ev : c->ev)
     if (ev) cudaEventDestroy(ev);
@@ -588,12 +601,105 @@ qmcg_status qmcg_warm(qmcg_ctx* c, int64_t n, uint64_t seed, int64_t dims) {
   return QMCG_OK;
 }
 
+qmcg_status qmcg_set_table_budget(qmcg_ctx* c, uint64_t bytes) {
+  if (!c) return fail(QMCG_INVALID_ARGUMENT, "qmcg_set_table_budget: null context");
+  std::lock_guard<std::mutex> lock(c->mu);
+  c->table_budget = static_cast<size_t>(bytes);
+  return QMCG_OK;
+}
+
+int64_t qmcg_last_window_count(qmcg_ctx* c) { return c ? c->last_windows : -1; }
+
 qmcg_status qmcg_clear_cache(qmcg_ctx* c) {
   if (!c) return fail(QMCG_INVALID_ARGUMENT, "qmcg_clear_cache: null context");
   std::lock_guard<std::mutex> lock(c->mu);
   DeviceGuard g(c->device);
   cudaStreamSynchronize(c->stream);
   drop_cache(c);
+  return QMCG_OK;
+}
+
+// Bytes the permutation table of `cols` columns may occupy: the caller's
+// budget, capped by free device memory (+ the table already held) minus the
+// K1 scratch, the carried walk state, the per-path values and a margin.
+size_t table_bytes_allowed(qmcg_ctx* c, int64_t n, int64_t cols, bool full) {
+  size_t free_b = 0, total_b = 0;
+  cudaMemGetInfo(&free_b, &total_b);
+  const int64_t held_ld = qmcg::table_ld(c->col_end - c->col_begin);
+  const size_t held = c->table ? c->table_rows_cap * static_cast<size_t>(held_ld) * sizeof(uint32_t) : 0;
+  const size_t reserve = qmcg::perm_scratch_bytes(n) + (full ? 0 : static_cast<size_t>(n) * 4) +
+                         static_cast<size_t>(cols) * (4 * 8 + 4 + 8 + 8) + (size_t{1} << 30);
+  const size_t avail = free_b + held > reserve ? free_b + held - reserve : 0;
+  return c->table_budget ? std::min(c->table_budget, avail) : avail;
+}
+
+// Tables larger than device memory (config 5: 2^28 paths x 365 dates = 392 GB):
+// the dates are processed in windows of W rows; each window's rows are built
+// by K1 into the same W-row buffer, then K2 walks every path through the
+// window, carrying (V, last record, dominance accumulator, pending record,
+// best) in HBM to the next window. Results are identical to resident tables.
+qmcg_status enqueue_streamed(qmcg_ctx* c, CallPlan& plan, uint64_t seed, int64_t n, int64_t b, int64_t e,
+                             size_t budget) {
+  const int64_t cols = e - b, m = plan.P.m;
+  const int64_t ld = qmcg::table_ld(cols);
+  const size_t row_bytes = static_cast<size_t>(ld) * sizeof(uint32_t);
+  int64_t W = static_cast<int64_t>(budget / row_bytes) / 8 * 8;
+  if (W < 8)
+    return fail(QMCG_OUT_OF_MEMORY, "price_american: not enough device memory for 8 permutation rows");
+  W = std::min<int64_t>(W, (m + 7) / 8 * 8);
+  drop_cache(c);
+  uint32_t* nt = nullptr;
+  if (cudaMalloc(&nt, row_bytes * static_cast<size_t>(W) + qmcg::kTablePad * sizeof(uint32_t)) != cudaSuccess) {
+    cudaGetLastError();
+    return fail(QMCG_OUT_OF_MEMORY, "price_american: permutation window does not fit in device memory");
+  }
+  c->table = nt;
+  c->table_rows_cap = static_cast<size_t>(W);
+  c->col_begin = b;  // the buffer holds a window, never a cache (cache_n stays -1)
+  c->col_end = e;
+  const bool full = (b == 0 && e == n);
+  if (!full) QMCG_CUDA(c->d_fullperm.reserve(static_cast<size_t>(n)));
+  QMCG_CUDA(c->d_values.reserve(static_cast<size_t>(cols)));
+  QMCG_CUDA(c->d_red.reserve(qmcg::reduce_scratch_doubles(cols)));
+  for (auto* buf : {&c->d_stV, &c->d_stc, &c->d_stcd, &c->d_stbest})
+    QMCG_CUDA(buf->reserve(static_cast<size_t>(cols)));
+  QMCG_CUDA(c->d_stpend.reserve(static_cast<size_t>(cols)));
+  PriceParams P = plan.P;
+  P.perm = c->table;
+  P.ld = ld;
+  P.col_begin = b;
+  P.path_begin = b;
+  P.path_count = cols;
+  P.values = c->d_values.ptr;
+  P.err = c->d_err.ptr;
+  P.st_V = c->d_stV.ptr;
+  P.st_c = c->d_stc.ptr;
+  P.st_cd = c->d_stcd.ptr;
+  P.st_best = c->d_stbest.ptr;
+  P.st_pend = c->d_stpend.ptr;
+  c->last_windows = 0;
+  for (int64_t d0 = 0; d0 < m; d0 += W) {
+    const int64_t d1 = std::min(m, d0 + W);
+    for (int64_t d = d0; d < d1; ++d) {
+      uint32_t* row = c->table + static_cast<size_t>(d - d0) * static_cast<size_t>(ld);
+      qmcg_status st = build_perm(c, dimension_seed(seed, d), n, full ? row : c->d_fullperm.ptr);
+      if (st) return st;
+      if (!full)
+        QMCG_CUDA(cudaMemcpyAsync(row, c->d_fullperm.ptr + b, static_cast<size_t>(cols) * sizeof(uint32_t),
+                                  cudaMemcpyDeviceToDevice, c->stream));
+    }
+    P.d_begin = static_cast<int32_t>(d0);
+    P.d_end = static_cast<int32_t>(d1);
+    P.perm_row0 = static_cast<int32_t>(d0);
+    P.stream_load = d0 > 0;
+    P.stream_store = d1 < m;
+    QMCG_CUDA(qmcg::launch_price(P, c->stream));
+    c->launches += 1;
+    c->last_windows += 1;
+  }
+  int launches = 0;
+  QMCG_CUDA(qmcg::launch_pairwise(c->d_values.ptr, cols, c->d_red.ptr, c->d_sums.ptr, c->stream, &launches));
+  c->launches += launches;
   return QMCG_OK;
 }
 
@@ -604,11 +710,26 @@ static qmcg_status price_range(qmcg_ctx* c, const qmcg_option_spec* spec, int64_
   if (st) return st;
   st = upload_plan(c, plan, n);
   if (st) return st;
-  st = ensure_perms(c, seed, n, b, e, m, (flags & QMCG_FLAG_NO_CACHE) != 0);
-  if (st) return st;
+  const bool rebuild = (flags & QMCG_FLAG_NO_CACHE) != 0;
+  const bool cached = !rebuild && c->cache_n == n && c->cache_seed == seed && c->col_begin == b &&
+                      c->col_end == e && c->cache_dims >= m;
+  bool streamed = false;
+  size_t budget = 0;
+  if (!cached && !plan.P.deterministic) {
+    budget = table_bytes_allowed(c, n, e - b, b == 0 && e == n);
+    const size_t need = static_cast<size_t>(qmcg::table_ld(e - b)) * sizeof(uint32_t) * static_cast<size_t>(m);
+    streamed = need > budget;
+  }
   st = prepare_scratch(c, 1);
   if (st) return st;
-  st = enqueue_price(c, plan, b, e, 0, nullptr);
+  if (streamed) {
+    st = enqueue_streamed(c, plan, seed, n, b, e, budget);
+  } else {
+    st = ensure_perms(c, seed, n, b, e, m, rebuild);
+    if (st) return st;
+    c->last_windows = 1;
+    st = enqueue_price(c, plan, b, e, 0, nullptr);
+  }
   if (st) return st;
   std::vector<double> out;
   st = sync_results(c, 1, out);

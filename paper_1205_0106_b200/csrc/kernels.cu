@@ -434,17 +434,16 @@ __device__ __forceinline__ double rneg_threshold(const PriceParams& P, double be
 }
 
 // Issue the bulk copies of tile `k` (dates [k*kTile, ...)) into buffer b.
-__device__ __forceinline__ void issue_tile(const PriceParams& P, uint32_t sbase, int k, int b, int64_t col0,
+__device__ __forceinline__ void issue_tile(const PriceParams& P, uint32_t sbase, int d0, int b, int64_t col0,
                                            uint32_t bytes) {
-  const int d0 = k * kTile;
-  const int rows = min(kTile, P.m - d0);
+  const int rows = min(kTile, P.d_end - d0);
   const uint32_t bar = sbase + kBarOff + b * 8;
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
                "r"(static_cast<uint32_t>(rows) * bytes)
                : "memory");
   for (int t = 0; t < rows; ++t) {
     const uint32_t dst = sbase + kPermOff + b * kPermBuf + t * kThreads * 4;
-    const uint32_t* src = P.perm + static_cast<int64_t>(d0 + t) * P.ld + col0;
+    const uint32_t* src = P.perm + static_cast<int64_t>(d0 + t - P.perm_row0) * P.ld + col0;
     asm volatile(
         "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
         "l"(src), "r"(bytes), "r"(bar)
@@ -712,7 +711,8 @@ __global__ void __launch_bounds__(kThreads, QMCG_MINB) price_kernel(const PriceP
   const int mrec = m - 1;
   const bool det = SLOW && P.deterministic != 0;
   const bool check = SLOW && P.check_range != 0;
-  const int ntiles = (m + kTile - 1) / kTile;
+  const int dbeg = P.d_begin, dend = P.d_end;  // date window of this launch
+  const int ntiles = (dend - dbeg + kTile - 1) / kTile;
   const int64_t block_paths = min(static_cast<int64_t>(kThreads), P.path_count - block_first);
   const int nchunks = static_cast<int>((block_paths + 31) / 32);
   // columns of this block in the table (16-byte aligned: path_begin - col_begin and ld are multiples of 4)
@@ -731,32 +731,40 @@ __global__ void __launch_bounds__(kThreads, QMCG_MINB) price_kernel(const PriceP
   asm volatile("st.shared.u64 [%0], %1;" ::"r"(ws + kWBest + lane * 8),
                "l"(static_cast<unsigned long long>(__double_as_longlong(P.best0)))
                : "memory");
-  if (threadIdx.x < 128) sts_v2f64(logtab + threadIdx.x * 16, c_log_table[threadIdx.x]);
-  __syncthreads();
-  if (threadIdx.x == 0 && !det) {
-    issue_tile(P, sbase, 0, 0, col0, bytes);
-    if (ntiles > 1) issue_tile(P, sbase, 1, 1, col0, bytes);
-  }
-
   T V = T(0);
   T c = static_cast<T>(P.c0);
   T cd = T(0);  // dominance threshold of the pending record (see the walk)
   int pend_d = -1;  // date of the pending (not yet evaluated) record, -1 = none
+  if (P.stream_load && active) {  // carry-in from the previous date window
+    const int64_t i = pi;
+    V = static_cast<T>(P.st_V[i]);
+    c = static_cast<T>(P.st_c[i]);
+    cd = static_cast<T>(P.st_cd[i]);
+    pend_d = P.st_pend[i];
+    asm volatile("st.shared.f64 [%0], %1;" ::"r"(ws + kWBest + lane * 8), "d"(P.st_best[i]) : "memory");
+  }
+  if (threadIdx.x < 128) sts_v2f64(logtab + threadIdx.x * 16, c_log_table[threadIdx.x]);
+  __syncthreads();
+  if (threadIdx.x == 0 && !det) {
+    issue_tile(P, sbase, dbeg, 0, col0, bytes);
+    if (ntiles > 1) issue_tile(P, sbase, dbeg + kTile, 1, col0, bytes);
+  }
+
   uint32_t rq_head = 0, rq_tail = 0;
   uint32_t err = 0;
 
   for (int k = 0; k < ntiles; ++k) {
-    const int k0 = k * kTile;
+    const int k0 = dbeg + k * kTile;
     const int b = k & 1;
     const uint32_t zb = kZtBuffers == 2 ? b : 0;
     const uint32_t zcol = sbase + kZtOff + zb * kZtBuf + threadIdx.x * Z::kSize;
     if (!det) {
       mbar_wait_u32(sbase + kBarOff + b * 8, static_cast<uint32_t>((k >> 1) & 1));
-      if (k0 + warp < m)
+      if (k0 + warp < dend)
         generate_row<SLOW, F32>(P, ws, k0 + warp, sbase + kPermOff + b * kPermBuf + warp * kThreads * 4,
                                 sbase + kZtOff + zb * kZtBuf + warp * kThreads * Z::kSize, logtab, nchunks, lane, lt);
       __syncthreads();  // z tile complete; perm buffer b consumed
-      if (threadIdx.x == 0 && k + 2 < ntiles) issue_tile(P, sbase, k + 2, b, col0, bytes);
+      if (threadIdx.x == 0 && k + 2 < ntiles) issue_tile(P, sbase, k0 + 2 * kTile, b, col0, bytes);
     }
     // ---- walk ----
     // c = V of the last record (= the pending record when pend_d >= 0);
@@ -779,7 +787,7 @@ __global__ void __launch_bounds__(kThreads, QMCG_MINB) price_kernel(const PriceP
 #pragma unroll
       for (int t = 0; t < kTile; ++t) {
         const int d = k0 + t;
-        if (d < m) {
+        if (d < dend) {
           V = add_rn(V, det ? static_cast<T>(P.alpha) : Z::load(zcol + t * kThreads * Z::kSize));
           cd = add_rn(cd, slope);
           if (check && active) {
@@ -825,7 +833,7 @@ __global__ void __launch_bounds__(kThreads, QMCG_MINB) price_kernel(const PriceP
       c = static_cast<T>(rneg_threshold<KIND>(P, __longlong_as_double(static_cast<long long>(bb))));
     }
   }
-  if (!RNEG) {  // the last pending record of every path
+  if (!RNEG && !P.stream_store) {  // the last pending record of every path
     push_record<KIND, RNEG>(ws, P, pend_d >= 0, c, pend_d, lane, lt, rq_head, rq_tail);
   }
   // The queued evaluations are drained after the last block barrier, so their
@@ -837,6 +845,20 @@ __global__ void __launch_bounds__(kThreads, QMCG_MINB) price_kernel(const PriceP
     rq_head += cnt;
   }
   __syncwarp();
+  if (P.stream_store) {  // carry-out to the next date window
+    if (active) {
+      const int64_t i = pi;
+      double bst;
+      asm volatile("ld.shared.f64 %0, [%1];" : "=d"(bst) : "r"(ws + kWBest + lane * 8) : "memory");
+      P.st_V[i] = static_cast<double>(V);
+      P.st_c[i] = static_cast<double>(c);
+      P.st_cd[i] = static_cast<double>(cd);
+      P.st_pend[i] = pend_d;
+      P.st_best[i] = bst;
+      if (err) atomicOr(P.err, err);
+    }
+    return;
+  }
 
   // Date m: max(intrinsic, Black-Scholes of the final interval), american.cpp:43-52.
   const double X = fma(P.b, static_cast<double>(V), P.X0);
@@ -898,7 +920,7 @@ __global__ void __launch_bounds__(kThreads, QMCG_MINB) gen_z_kernel(const PriceP
   __syncthreads();
   if (threadIdx.x == 0) {
     issue_tile(P, sbase, 0, 0, col0, bytes);
-    if (ntiles > 1) issue_tile(P, sbase, 1, 1, col0, bytes);
+    if (ntiles > 1) issue_tile(P, sbase, kTile, 1, col0, bytes);
   }
   for (int k = 0; k < ntiles; ++k) {
     const int k0 = k * kTile;
@@ -916,7 +938,7 @@ __global__ void __launch_bounds__(kThreads, QMCG_MINB) gen_z_kernel(const PriceP
       }
     }
     __syncthreads();  // perm buffer b consumed, z tile b stored
-    if (threadIdx.x == 0 && k + 2 < ntiles) issue_tile(P, sbase, k + 2, b, col0, bytes);
+    if (threadIdx.x == 0 && k + 2 < ntiles) issue_tile(P, sbase, k0 + 2 * kTile, b, col0, bytes);
   }
 }
 

@@ -67,7 +67,17 @@ struct PriceParams {
   int32_t check_range;   // per-date overflow/underflow checks needed
   int32_t rate_negative; // disc > 1: running-max filter invalid, use best-based filter
   int32_t fp32;          // QMCG_FLAG_FP32: single-precision normals and walk
+  // Date window of this launch (streamed tables: the permutation rows of
+  // dates [d_begin, d_end) only, row index d - perm_row0). Resident: [0, m), 0.
+  int32_t d_begin, d_end, perm_row0;
+  int32_t stream_load;   // carry-in: walk state read from st_* (window > first)
+  int32_t stream_store;  // carry-out: walk state written to st_* (window < last)
   int32_t pad0;
+  double* st_V;          // per path (index = path - path_begin): log-price walk V
+  double* st_c;          // last record
+  double* st_cd;         // dominance accumulator of the pending record
+  double* st_best;       // best evaluated discounted intrinsic so far
+  int32_t* st_pend;      // date of the pending record (-1 none)
   double* values;        // per-path t0 values, index = path - path_begin
   uint32_t* err;
 };

@@ -39,7 +39,8 @@ EXPORTS = (
     "qmcg_price_american_batch", "qmcg_price_american_node", "qmcg_tree_node_range",
     "qmcg_combine_nodes", "qmcg_warm", "qmcg_clear_cache", "qmcg_permutation", "qmcg_uniforms",
     "qmcg_normals", "qmcg_normal_table", "qmcg_path_values", "qmcg_time_device", "qmcg_time_perm_build",
-    "qmcg_last_launch_count", "qmcg_get_stream", "qmcg_fp64_peak",
+    "qmcg_last_launch_count", "qmcg_get_stream", "qmcg_fp64_peak", "qmcg_set_table_budget",
+    "qmcg_last_window_count",
 )
 
 
@@ -122,6 +123,9 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
         L.qmcg_combine_nodes.argtypes = [I64, C.c_int, PD, PD, PD]
         L.qmcg_warm.argtypes = [P, I64, U64, I64]
         L.qmcg_clear_cache.argtypes = [P]
+        L.qmcg_set_table_budget.argtypes = [P, U64]
+        L.qmcg_last_window_count.argtypes = [P]
+        L.qmcg_last_window_count.restype = I64
         L.qmcg_permutation.argtypes = [P, I64, U64, P]
         L.qmcg_uniforms.argtypes = [P, I64, U64, I64, P]
         L.qmcg_normals.argtypes = [P, I64, U64, I64, P]
@@ -233,6 +237,13 @@ class Context:
 
     def clear_cache(self) -> None:
         _check(self._lib.qmcg_clear_cache(self._h))
+
+    def set_table_budget(self, nbytes: int) -> None:
+        """Cap the permutation-table bytes (0 = free device memory); larger pricings stream date windows."""
+        _check(self._lib.qmcg_set_table_budget(self._h, int(nbytes)))
+
+    def last_window_count(self) -> int:
+        return int(self._lib.qmcg_last_window_count(self._h))
 
     # -- parity exports --
     def permutation(self, n: int, seed64: int) -> np.ndarray:

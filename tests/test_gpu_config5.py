@@ -1,0 +1,61 @@
+"""Config 5 (SURVEY.md 8c ladder): 2^28 paths x 365 daily dates in FP32 on one GPU.
+
+The permutation tables (2^28 x 365 x 4 B = 392 GB) exceed HBM, so the call
+streams date windows (test_gpu_streamed.py proves windows == resident tables).
+No oracle can run at that size (the reference's own path matrix would be
+786 GB), so parity is pinned by a ladder:
+  1. FP64 GPU vs the reference at 2^20 x 365 (golden from oracle/_ref), here with
+     streamed tables forced;
+  2. FP32 GPU vs FP64 GPU at 2^24 x 365: |delta price| <= 1 se;
+  3. the full 2^28 x 365 FP32 run vs the FP64 run at 2^26 x 365: consistent
+     within 4 combined standard errors."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+REF = (100.0, 100.0, 0.05, 0.2, 1.0)
+
+
+def fx(h):
+    return float.fromhex(h)
+
+
+def test_rung1_fp64_streamed_vs_reference(ctx, qmcg, golden):
+    c = next(c for c in golden["prices"]["cases"] if c["m"] == 365 and c["n"] == 1 << 20)
+    n = c["n"]
+    ctx.clear_cache()
+    ctx.set_table_budget(64 * n * 4)
+    try:
+        r = ctx.price_american(qmcg.OptionSpec(*c["spec"]), 365, n, c["seed"])
+        assert ctx.last_window_count() == 6
+    finally:
+        ctx.set_table_budget(0)
+        ctx.clear_cache()
+    p, se = fx(c["price"]), fx(c["std_error"])
+    assert abs(r.price - p) <= 1e-9 * p, (r.price, p)
+    assert abs(r.std_error - se) <= 1e-9 * se
+
+
+def test_rung2_fp32_vs_fp64_2p24(ctx, qmcg):
+    sp = qmcg.OptionSpec(*REF)
+    r64 = ctx.price_american(sp, 365, 1 << 24, 42)
+    r32 = ctx.price_american(sp, 365, 1 << 24, 42, fp32=True)
+    ctx.clear_cache()
+    assert abs(r32.price - r64.price) <= r64.std_error, (r32.price, r64.price, r64.std_error)
+
+
+def test_rung3_full_config5(ctx, qmcg):
+    sp = qmcg.OptionSpec(*REF)
+    ctx.clear_cache()
+    r26 = ctx.price_american(sp, 365, 1 << 26, 42)
+    ctx.clear_cache()
+    r28 = ctx.price_american(sp, 365, 1 << 28, 42, fp32=True)
+    windows = ctx.last_window_count()
+    ctx.clear_cache()
+    assert windows >= 3  # 392 GB of tables cannot be resident on one 180 GB GPU
+    assert r28.n_paths == 1 << 28
+    assert np.isfinite(r28.price) and r28.std_error > 0
+    assert abs(r28.price - r26.price) <= 4 * np.hypot(r28.std_error, r26.std_error), (r28.price, r26.price)
+    # the QMC error shrinks with n (4x the paths: at least ~2x smaller se)
+    assert r28.std_error < 0.6 * r26.std_error

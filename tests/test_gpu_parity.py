@@ -219,7 +219,8 @@ def test_mc_european_vs_reference_goldens(ctx, qmcg, golden):
 def test_fp32_variant_within_qmc_error(ctx, qmcg, s, kind, m, n):
     """FP32 variant (north star: 'within the QMC standard error for an FP32 variant'):
     uniforms stay bit-exact FP64; normals and the walk run in FP32, exercise values in FP64.
-    Bar: |price32 - price64| <= 0.05 se, and every path value within 1e-4 relative."""
+    Bar: |price32 - price64| <= 0.05 se, and every path value within 5e-5 * spot (FP32 log-price
+    walk: ~sqrt(m) ulp(V) * b of error in X, i.e. ~1e-7 relative in S per path)."""
     sp = spec_of(qmcg, s, kind)
     put = kind == 1
     r64 = ctx.price_american(sp, m, n, 42, allow_put=put)
@@ -228,5 +229,5 @@ def test_fp32_variant_within_qmc_error(ctx, qmcg, s, kind, m, n):
     assert abs(r32.std_error - r64.std_error) <= 1e-3 * r64.std_error
     v64 = ctx.path_values(sp, m, n, 42, allow_put=put)
     v32 = ctx.path_values(sp, m, n, 42, allow_put=put, fp32=True)
-    rel = np.abs(v32 - v64) / np.maximum(np.abs(v64), 1e-3 * s[1])
-    assert rel.max() <= 1e-4, rel.max()
+    err = np.abs(v32 - v64).max()
+    assert err <= 5e-5 * s[0], err
