@@ -40,6 +40,11 @@ constexpr int kTile = kWarps;  // dates per tile = warps per block (one date row
 constexpr int kGenUnroll = QMCG_GEN_UNROLL;
 constexpr int kRecCap = 128;  // per-warp ring of pending record evaluations (mostly drained at path end)
 constexpr uint32_t kNone = 0xffffffffu;
+constexpr int kBins = 256;             // K1 binned scatter (== the bin kernel's block size)
+constexpr int kCursorStride = 32;      // one 128-byte line per bin cursor (spreads the atomics over L2 slices)
+#ifndef QMCG_K1_BIN_MIN
+#define QMCG_K1_BIN_MIN (1 << 25)      // n from which K1 scatters through bins (measured: 2^24 faster direct)
+#endif
 
 // ---------------------------------------------------------------------------
 // Scrambled Halton uniform, bit-exact with radical_inverse():
@@ -1156,8 +1161,9 @@ __global__ void fy_draws_kernel(uint64_t seed, int64_t n, uint64_t stride_mult, 
 }
 
 __global__ void fy_first_kernel(const uint32_t* __restrict__ sk, const uint32_t* __restrict__ sv, int64_t n,
-                                uint32_t* __restrict__ F) {
+                                uint32_t* __restrict__ F, uint32_t* __restrict__ cursor, int bin_shift) {
   const int64_t q = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (cursor && q < kBins) cursor[q * kCursorStride] = static_cast<uint32_t>(q) << bin_shift;
   if (q >= n) return;
   const uint32_t x = sk[q], i = sv[q];
   if (i > x) {
@@ -1166,8 +1172,13 @@ __global__ void fy_first_kernel(const uint32_t* __restrict__ sk, const uint32_t*
   }
 }
 
+// perm[i] for the sorted entry q. With `pairs`, the result is written in
+// sorted order as (i, perm[i]) for the binned scatter below (large n, where a
+// direct perm[i] store is a random 4-byte write: a read-modify-write of a
+// whole DRAM burst); otherwise it is stored directly.
 __global__ void fy_assign_kernel(const uint32_t* __restrict__ sk, const uint32_t* __restrict__ sv, int64_t n,
-                                 const uint32_t* __restrict__ F, uint32_t* __restrict__ perm) {
+                                 const uint32_t* __restrict__ F, uint32_t* __restrict__ perm,
+                                 uint2* __restrict__ pairs) {
   const int64_t q = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (q >= n) return;
   const uint32_t x = sk[q], i = sv[q];
@@ -1177,7 +1188,82 @@ __global__ void fy_assign_kernel(const uint32_t* __restrict__ sk, const uint32_t
     for (uint32_t f = F[y]; f != kNone; f = F[y]) y = f;
     out = y;
   }
-  perm[i] = out;
+#ifdef QMCG_K1_COALESCED_PROBE
+  perm[q] = out + i;  // timing probe only: coalesced store (wrong result)
+#else
+  if (pairs) pairs[q] = make_uint2(i, out);
+  else perm[i] = out;
+#endif
+}
+
+// Binned scatter, pass 1: partition the (i, perm[i]) pairs by i >> bin_shift
+// into kBins bins. Bin b holds exactly the i in [b << shift, (b+1) << shift),
+// so its region starts at b << shift; blocks reserve their run in each bin
+// with one atomic per bin (order inside a bin is irrelevant). The tile is
+// first ordered by bin in shared memory so that every warp store is a
+// contiguous run of one bin (few TLB pages and full sectors per store).
+constexpr int kBinThreads = 256, kBinPer = 16, kBinTile = kBinThreads * kBinPer;
+__global__ void __launch_bounds__(kBinThreads) fy_bin_kernel(const uint2* __restrict__ in, int64_t n,
+                                                            int bin_shift, uint32_t* __restrict__ cursor,
+                                                            uint2* __restrict__ out) {
+  __shared__ uint32_t cnt[kBins], start[kBins], base[kBins];
+  __shared__ uint2 staged[kBinTile];
+  for (int b = threadIdx.x; b < kBins; b += kBinThreads) cnt[b] = 0;
+  __syncthreads();
+  const int64_t tile = static_cast<int64_t>(blockIdx.x) * kBinTile;
+  const int valid = static_cast<int>(min(static_cast<int64_t>(kBinTile), n - tile));
+  uint2 v[kBinPer];
+  uint32_t rank[kBinPer];
+#pragma unroll
+  for (int e = 0; e < kBinPer; ++e) {
+    const int k = e * kBinThreads + threadIdx.x;
+    if (k < valid) {
+      v[e] = in[tile + k];
+      rank[e] = atomicAdd(&cnt[v[e].x >> bin_shift], 1u);
+    }
+  }
+  __syncthreads();
+  // exclusive scan of cnt (kBins == kBinThreads: one bin per thread)
+  {
+    const int b = threadIdx.x;
+    const uint32_t c = cnt[b];
+    uint32_t x = c;
+    const int lane = b & 31, w = b >> 5;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(kFull, x, o);
+      if (lane >= o) x += y;
+    }
+    __shared__ uint32_t wsum[kBinThreads / 32];
+    if (lane == 31) wsum[w] = x;
+    __syncthreads();
+    uint32_t off = 0;
+    for (int k = 0; k < w; ++k) off += wsum[k];
+    start[b] = off + x - c;
+    if (c) base[b] = atomicAdd(cursor + b * kCursorStride, c);
+  }
+  __syncthreads();
+#pragma unroll
+  for (int e = 0; e < kBinPer; ++e) {
+    const int k = e * kBinThreads + threadIdx.x;
+    if (k < valid) staged[start[v[e].x >> bin_shift] + rank[e]] = v[e];
+  }
+  __syncthreads();
+  for (int k = threadIdx.x; k < valid; k += kBinThreads) {
+    const uint2 p = staged[k];
+    const uint32_t b = p.x >> bin_shift;
+    out[base[b] + (k - start[b])] = p;
+  }
+}
+
+// Pass 2: perm[i] = p for the binned pairs. Consecutive blocks cover
+// consecutive bins, so the destination window in flight is a few bins
+// (<< L2) and every 32-byte sector is completed in L2 before write-back.
+__global__ void fy_scatter_kernel(const uint2* __restrict__ in, int64_t n, uint32_t* __restrict__ perm) {
+  const int64_t q = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (q >= n) return;
+  const uint2 v = in[q];
+  perm[v.x] = v.y;
 }
 
 // ---------------------------------------------------------------------------
@@ -1388,7 +1474,7 @@ cudaError_t launch_uniforms(const uint32_t* perm_row, int64_t count, DimParam dp
 
 namespace {
 struct PermScratchLayout {
-  size_t keys, vals, skeys, svals, F, temp, temp_bytes, total;
+  size_t keys, vals, skeys, svals, F, cursor, temp, temp_bytes, total;
 };
 PermScratchLayout perm_layout(int64_t n) {
   auto align = [](size_t x) { return (x + 255) & ~size_t{255}; };
@@ -1403,7 +1489,8 @@ PermScratchLayout perm_layout(int64_t n) {
   L.skeys = L.vals + arr;
   L.svals = L.skeys + arr;
   L.F = L.svals + arr;
-  L.temp = L.F + arr;
+  L.cursor = L.F + arr;
+  L.temp = L.cursor + align(kBins * kCursorStride * sizeof(uint32_t));
   L.temp_bytes = align(temp_bytes);
   L.total = L.temp + L.temp_bytes;
   return L;
@@ -1440,9 +1527,23 @@ cudaError_t launch_perm_build(uint64_t seed64, int64_t n, uint32_t* out, void* s
   e = cudaMemsetAsync(F, 0xff, static_cast<size_t>(n) * sizeof(uint32_t), s);
   if (e != cudaSuccess) return e;
   const int64_t eb = (n + threads - 1) / threads;
-  fy_first_kernel<<<static_cast<unsigned>(eb), threads, 0, s>>>(skeys, svals, n, F);
-  fy_assign_kernel<<<static_cast<unsigned>(eb), threads, 0, s>>>(skeys, svals, n, F, out);
-  if (launches) *launches += 4 + 1;  // draws, sort (>=1), first, assign (+ memset)
+  const bool binned = n >= QMCG_K1_BIN_MIN;
+  int shift = 0;
+  while (shift < 32 && (static_cast<uint64_t>(n - 1) >> shift) >= static_cast<uint64_t>(kBins)) ++shift;
+  auto* cursor = reinterpret_cast<uint32_t*>(base + L.cursor);
+  // keys+vals (free after the sort) hold the pairs; skeys+svals (free after assign) the bins
+  auto* pairs = reinterpret_cast<uint2*>(base + L.keys);
+  auto* binned_pairs = reinterpret_cast<uint2*>(base + L.skeys);
+  fy_first_kernel<<<static_cast<unsigned>(eb), threads, 0, s>>>(skeys, svals, n, F, binned ? cursor : nullptr,
+                                                                 shift);
+  fy_assign_kernel<<<static_cast<unsigned>(eb), threads, 0, s>>>(skeys, svals, n, F, out,
+                                                                  binned ? pairs : nullptr);
+  if (binned) {
+    const int64_t bb = (n + kBinThreads * kBinPer - 1) / (kBinThreads * kBinPer);
+    fy_bin_kernel<<<static_cast<unsigned>(bb), kBinThreads, 0, s>>>(pairs, n, shift, cursor, binned_pairs);
+    fy_scatter_kernel<<<static_cast<unsigned>(eb), threads, 0, s>>>(binned_pairs, n, out);
+  }
+  if (launches) *launches += 4 + 1 + (binned ? 2 : 0);  // draws, sort (>=1), first, assign (+ memset) [+ bin, scatter]
   return cudaGetLastError();
 }
 

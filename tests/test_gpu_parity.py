@@ -231,3 +231,11 @@ def test_fp32_variant_within_qmc_error(ctx, qmcg, s, kind, m, n):
     v32 = ctx.path_values(sp, m, n, 42, allow_put=put, fp32=True)
     err = np.abs(v32 - v64).max()
     assert err <= 5e-5 * s[0], err
+
+
+@pytest.mark.parametrize("n", [(1 << 25) + 3, 1 << 26])
+def test_permutations_binned_scatter_bit_exact(ctx, oracle_lib, n):
+    """K1 from 2^25 entries scatters through 256 i-bins (QMCG_K1_BIN_MIN); same table as the
+    serial Fisher-Yates of the C restatement."""
+    s = 0x9E3779B97F4A7C15 ^ n
+    assert np.array_equal(ctx.permutation(n, s)[:n], oracle_lib.permutation_indices(n, s)[:n])
