@@ -157,6 +157,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-batch", action="store_true")
+    ap.add_argument("--no-c5", action="store_true", help="skip the config-5 stress line (2^28 x 365 FP32)")
     ap.add_argument("--paths-log2", type=int, default=24, help="(debug) smaller path count")
     args = ap.parse_args()
     rank, world = env_int("RANK", 0), env_int("WORLD_SIZE", 1)
@@ -188,8 +189,7 @@ def main():
         cold_perm_ms = ctx.time_perm_build(n_paths, SEED, M_DATES)
     else:
         t0 = time.perf_counter()
-        for node in my_nodes:
-            ctx.price_american_node(call, M_DATES, n_paths, SEED, depth, node)
+        ctx.price_american_nodes(call, M_DATES, n_paths, SEED, depth, my_nodes[0], len(my_nodes))
         cold_perm_ms = 1e3 * (time.perf_counter() - t0)
 
     def one_step(spec, allow_put=False):
@@ -243,31 +243,75 @@ def main():
         kernel_ms = None
     fp64_peak = ctx.fp64_peak(100.0)
 
-    # ---- config 4 (one GPU): 1024 contracts, 32 strikes x 32 vols, calls/puts alternating,
-    # 2^18 paths x 128 dates, one shared permutation set; contract-path-steps/s ----
+    # ---- config 4: 1024 contracts, 32 strikes x 32 vols, calls/puts alternating, 2^18 paths x
+    # 128 dates, one shared permutation set; contracts sharded over the ranks (N > 1) with an
+    # all-gather of the (price, se) rows; contract-path-steps/s, max over ranks ----
     batch = None
-    if world == 1 and not args.no_batch:
+    if not args.no_batch:
         bspecs = [q.OptionSpec(100.0, 80 + 40 * i / 31, 0.05, 0.10 + 0.40 * j / 31, 1.0, q.OptionKind((i + j) % 2))
                   for i in range(32) for j in range(32)]
         bn, bm = 1 << 18, 128
+
+        def batch_step():
+            if world == 1:
+                return np.array([(r.price, r.std_error)
+                                 for r in ctx.price_american_batch(bspecs, bm, bn, SEED, allow_put=True)])
+            return distributed.price_american_batch_sharded(bspecs, bm, bn, SEED, ctx=ctx, allow_put=True)
+
         ctx.warm(bn, SEED, bm)
-        ctx.price_american_batch(bspecs, bm, bn, SEED, allow_put=True)
+        batch_step()
+        if dist:
+            dist.barrier()
         torch.cuda.synchronize()
         be0, be1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         breps = 3
         t0 = time.perf_counter()
         be0.record(stream)
         for _ in range(breps):
-            bres = ctx.price_american_batch(bspecs, bm, bn, SEED, allow_put=True)
+            bres = batch_step()
         be1.record(stream)
         torch.cuda.synchronize()
         bwall = (time.perf_counter() - t0) / breps
         bms = be0.elapsed_time(be1) / breps
+        if dist:
+            t = torch.tensor([bms, bwall], dtype=torch.float64, device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            bms, bwall = float(t[0]), float(t[1])
         batch = {"workload": "config 4: 1024 contracts (K = 80..120 x sigma = 0.10..0.50, calls for even i+j), "
-                             "2^18 paths x 128 dates, seed 42, one call of qmcg_price_american_batch",
+                             "2^18 paths x 128 dates, seed 42, qmcg_price_american_batch"
+                             + (f" on {world} ranks (contiguous contract blocks + all_gather)" if world > 1 else ""),
                  "value": len(bspecs) * bn * bm / (bms * 1e-3), "unit": "contract-path-steps/s",
                  "ms_per_batch": bms, "e2e_ms_per_batch": 1e3 * bwall, "us_per_contract": 1e3 * bms / len(bspecs),
-                 "price_first": bres[0].price, "price_last": bres[-1].price}
+                 "price_first": float(bres[0][0]), "price_last": float(bres[-1][0])}
+        ctx.clear_cache()
+
+    # ---- config 5 (stress): 2^28 paths x 365 dates, FP32 walk, tables rebuilt by K1 in date
+    # windows when they exceed HBM (392 GB on one GPU; 49 GB per GPU at 8); one cold call ----
+    c5 = None
+    if not args.no_c5 and args.paths_log2 == 24:
+        ctx.clear_cache()
+        n5, m5 = 1 << 28, 365
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0 = time.perf_counter()
+        c0.record(stream)
+        p5, se5, _ = distributed.price_american_sharded(call, m5, n5, SEED, ctx=ctx, fp32=True)
+        c1.record(stream)
+        torch.cuda.synchronize()
+        w5 = time.perf_counter() - t0
+        ms5 = c0.elapsed_time(c1)
+        windows = ctx.last_window_count()
+        if dist:
+            t = torch.tensor([ms5, w5], dtype=torch.float64, device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms5, w5 = float(t[0]), float(t[1])
+        c5 = {"workload": "config 5: 2^28 paths x 365 dates, FP32 normals + walk (bit-exact FP64 uniforms), call, "
+                          "seed 42, cold (K1 rebuilds every table)",
+              "value": n5 * m5 / (ms5 * 1e-3), "unit": "path-steps/s", "ms_per_option": ms5,
+              "e2e_ms_per_option": 1e3 * w5, "date_windows_rank0": windows,
+              "tables": "streamed date windows" if windows > 1 else "resident", "price": p5, "std_error": se5}
         ctx.clear_cache()
 
     path_steps = n_paths * M_DATES
@@ -323,7 +367,8 @@ def main():
                          "ms_per_option_cold": cold_perm_ms + ms_call,
                          "note": "K1 rebuilds all 256 Fisher-Yates tables (the reference's QuasiStream "
                                  "construction, included in its elapsed_s)"},
-                "kernel_ms": kernel_ms, "device_step_ms": step_ms, "batch_config4": batch}
+                "kernel_ms": kernel_ms, "device_step_ms": step_ms, "batch_config4": batch,
+                "stress_config5": c5}
         print(json.dumps(line), flush=True)
     if dist:
         dist.barrier()

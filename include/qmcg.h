@@ -107,6 +107,13 @@ qmcg_status qmcg_price_american_batch(qmcg_ctx* ctx, const qmcg_option_spec* spe
 qmcg_status qmcg_price_american_node(qmcg_ctx* ctx, const qmcg_option_spec* spec, int64_t m,
                                      int64_t n_paths, uint64_t seed, uint32_t flags, int depth,
                                      int64_t node, double out_sums[2]);
+/* The same for `node_count` consecutive nodes [node_begin, node_begin + node_count) at
+ * `depth` in one pass (one kernel over their contiguous path range, one cached table
+ * slice): out_sums[2k], out_sums[2k+1] = (sum v, sum v^2) of node node_begin + k. A rank
+ * of a multi-GPU job calls this once for all the nodes it owns. */
+qmcg_status qmcg_price_american_nodes(qmcg_ctx* ctx, const qmcg_option_spec* spec, int64_t m,
+                                      int64_t n_paths, uint64_t seed, uint32_t flags, int depth,
+                                      int64_t node_begin, int64_t node_count, double* out_sums);
 /* Path range [begin, end) of pairwise-tree node `node` at `depth`. */
 qmcg_status qmcg_tree_node_range(int64_t n_paths, int depth, int64_t node, int64_t* begin,
                                  int64_t* end);

@@ -434,7 +434,8 @@ qmcg_status map_err(uint32_t err) {
 
 // Enqueue pricing of paths [b, e) and the pairwise reduction of that range
 // into d_sums[slot*2 .. slot*2+1]. Tables must be resident.
-qmcg_status enqueue_price(qmcg_ctx* c, CallPlan& plan, int64_t b, int64_t e, int slot, cudaEvent_t after_kernel) {
+// Launch the pricing kernel over paths [b, e) (tables resident) into d_values.
+qmcg_status enqueue_values(qmcg_ctx* c, CallPlan& plan, int64_t b, int64_t e, cudaEvent_t after_kernel = nullptr) {
   const int64_t cnt = e - b;
   QMCG_CUDA(c->d_values.reserve(static_cast<size_t>(cnt)));
   QMCG_CUDA(c->d_red.reserve(qmcg::reduce_scratch_doubles(cnt)));
@@ -450,8 +451,15 @@ qmcg_status enqueue_price(qmcg_ctx* c, CallPlan& plan, int64_t b, int64_t e, int
   QMCG_CUDA(qmcg::launch_price(P, c->stream));
   c->launches += 1;
   if (after_kernel) QMCG_CUDA(cudaEventRecord(after_kernel, c->stream));
+  return QMCG_OK;
+}
+
+// Kernel over [b, e) + the pairwise sums of all its paths into d_sums[slot].
+qmcg_status enqueue_price(qmcg_ctx* c, CallPlan& plan, int64_t b, int64_t e, int slot, cudaEvent_t after_kernel) {
+  qmcg_status st = enqueue_values(c, plan, b, e, after_kernel);
+  if (st) return st;
   int launches = 0;
-  QMCG_CUDA(qmcg::launch_pairwise(c->d_values.ptr, cnt, c->d_red.ptr, c->d_sums.ptr + 2 * slot, c->stream,
+  QMCG_CUDA(qmcg::launch_pairwise(c->d_values.ptr, e - b, c->d_red.ptr, c->d_sums.ptr + 2 * slot, c->stream,
                                   &launches));
   c->launches += launches;
   return QMCG_OK;
@@ -697,14 +705,19 @@ qmcg_status enqueue_streamed(qmcg_ctx* c, CallPlan& plan, uint64_t seed, int64_t
     c->launches += 1;
     c->last_windows += 1;
   }
-  int launches = 0;
-  QMCG_CUDA(qmcg::launch_pairwise(c->d_values.ptr, cols, c->d_red.ptr, c->d_sums.ptr, c->stream, &launches));
-  c->launches += launches;
   return QMCG_OK;
 }
 
-static qmcg_status price_range(qmcg_ctx* c, const qmcg_option_spec* spec, int64_t m, int64_t n, uint64_t seed,
-                               uint32_t flags, int64_t b, int64_t e, double sums[2]) {
+// Per-path values of paths [b, e) into d_values (resident tables from the
+// cache, or streamed date windows when the tables exceed the budget), then
+// the pairwise sums of each of the `count` consecutive tree nodes
+// [node0, node0 + count) at `depth` (which must tile [b, e)) into d_sums.
+static qmcg_status price_nodes(qmcg_ctx* c, const qmcg_option_spec* spec, int64_t m, int64_t n, uint64_t seed,
+                               uint32_t flags, int depth, int64_t node0, int64_t count, double* sums) {
+  int64_t b, e, off, size;
+  tree_node(n, depth, node0, b, size);
+  tree_node(n, depth, node0 + count - 1, off, size);
+  e = off + size;
   CallPlan plan;
   qmcg_status st = plan_call(*spec, m, n, flags, plan);
   if (st) return st;
@@ -720,23 +733,35 @@ static qmcg_status price_range(qmcg_ctx* c, const qmcg_option_spec* spec, int64_
     const size_t need = static_cast<size_t>(qmcg::table_ld(e - b)) * sizeof(uint32_t) * static_cast<size_t>(m);
     streamed = need > budget;
   }
-  st = prepare_scratch(c, 1);
+  st = prepare_scratch(c, static_cast<size_t>(count));
   if (st) return st;
   if (streamed) {
     st = enqueue_streamed(c, plan, seed, n, b, e, budget);
+    if (st) return st;
   } else {
     st = ensure_perms(c, seed, n, b, e, m, rebuild);
     if (st) return st;
     c->last_windows = 1;
-    st = enqueue_price(c, plan, b, e, 0, nullptr);
+    st = enqueue_values(c, plan, b, e);
+    if (st) return st;
   }
-  if (st) return st;
+  for (int64_t k = 0; k < count; ++k) {
+    tree_node(n, depth, node0 + k, off, size);
+    int launches = 0;
+    QMCG_CUDA(qmcg::launch_pairwise(c->d_values.ptr + (off - b), size, c->d_red.ptr, c->d_sums.ptr + 2 * k,
+                                    c->stream, &launches));
+    c->launches += launches;
+  }
   std::vector<double> out;
-  st = sync_results(c, 1, out);
+  st = sync_results(c, static_cast<size_t>(count), out);
   if (st) return st;
-  sums[0] = out[0];
-  sums[1] = out[1];
+  std::copy(out.begin(), out.end(), sums);
   return QMCG_OK;
+}
+
+static qmcg_status price_range(qmcg_ctx* c, const qmcg_option_spec* spec, int64_t m, int64_t n, uint64_t seed,
+                               uint32_t flags, double sums[2]) {
+  return price_nodes(c, spec, m, n, seed, flags, 0, 0, 1, sums);
 }
 
 qmcg_status qmcg_price_american(qmcg_ctx* c, const qmcg_option_spec* spec, int64_t m, int64_t n, uint64_t seed,
@@ -747,7 +772,7 @@ qmcg_status qmcg_price_american(qmcg_ctx* c, const qmcg_option_spec* spec, int64
   DeviceGuard g(c->device);
   c->launches = 0;
   double sums[2];
-  qmcg_status st = price_range(c, spec, m, n, seed, flags, 0, n, sums);
+  qmcg_status st = price_range(c, spec, m, n, seed, flags, sums);
   if (st) return st;
   double mean, se;
   finish_stats(n, sums[0], sums[1], mean, se);
@@ -827,7 +852,27 @@ qmcg_status qmcg_price_american_node(qmcg_ctx* c, const qmcg_option_spec* spec, 
       if (asize <= 64) return fail(QMCG_INVALID_ARGUMENT, "qmcg_price_american_node: node below a leaf of the tree");
     }
   }
-  return price_range(c, spec, m, n, seed, flags, off, off + size, out_sums);
+  return price_nodes(c, spec, m, n, seed, flags, depth, node, 1, out_sums);
+}
+
+qmcg_status qmcg_price_american_nodes(qmcg_ctx* c, const qmcg_option_spec* spec, int64_t m, int64_t n,
+                                      uint64_t seed, uint32_t flags, int depth, int64_t node_begin,
+                                      int64_t node_count, double* out_sums) {
+  if (!c || !spec || !out_sums) return fail(QMCG_INVALID_ARGUMENT, "qmcg_price_american_nodes: null argument");
+  std::lock_guard<std::mutex> lock(c->mu);
+  DeviceGuard g(c->device);
+  c->launches = 0;
+  if (depth < 0 || depth > 30 || node_count < 1 || node_begin < 0 ||
+      node_begin + node_count > (int64_t{1} << depth))
+    return fail(QMCG_INVALID_ARGUMENT, "qmcg_price_american_nodes: bad node range");
+  int64_t aoff, asize;
+  for (int64_t k = node_begin; k < node_begin + node_count; ++k)
+    for (int d = 0; d < depth; ++d) {
+      tree_node(n, d, k >> (depth - d), aoff, asize);
+      if (asize <= 64)
+        return fail(QMCG_INVALID_ARGUMENT, "qmcg_price_american_nodes: node below a leaf of the tree");
+    }
+  return price_nodes(c, spec, m, n, seed, flags, depth, node_begin, node_count, out_sums);
 }
 
 qmcg_status qmcg_price_american_batch(qmcg_ctx* c, const qmcg_option_spec* specs, int64_t n_specs, int64_t m,
@@ -1032,7 +1077,7 @@ qmcg_status qmcg_path_values(qmcg_ctx* c, const qmcg_option_spec* spec, int64_t 
   std::lock_guard<std::mutex> lock(c->mu);
   DeviceGuard g(c->device);
   double sums[2];
-  qmcg_status st = price_range(c, spec, m, n, seed, flags, 0, n, sums);
+  qmcg_status st = price_range(c, spec, m, n, seed, flags, sums);
   if (st) return st;
   QMCG_CUDA(cudaMemcpyAsync(out_host, c->d_values.ptr, static_cast<size_t>(n) * sizeof(double),
                             cudaMemcpyDeviceToHost, c->stream));

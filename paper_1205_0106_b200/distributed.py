@@ -13,7 +13,7 @@ world size, exactly as the reference is for any lane count.
 from __future__ import annotations
 
 import math
-from typing import Callable, List, Optional, Tuple
+from typing import Callable, List, Optional, Sequence, Tuple
 
 import numpy as np
 
@@ -48,37 +48,87 @@ def combine(n_paths: int, depth: int, table: np.ndarray) -> Tuple[float, float]:
     return qmcg.combine_nodes(n_paths, depth, table)
 
 
+def _all_gather_rows(table: np.ndarray, group=None) -> List[np.ndarray]:
+    """all_gather of an equally-shaped float64 array from every rank (NCCL on GPU, gloo on CPU)."""
+    import torch
+    import torch.distributed as dist
+
+    if not dist.is_initialized() or dist.get_world_size(group) == 1:
+        return [table]
+    backend = dist.get_backend(group)
+    dev = torch.device("cuda", torch.cuda.current_device()) if backend == "nccl" else torch.device("cpu")
+    local = torch.from_numpy(np.ascontiguousarray(table)).to(dev)
+    gathered = [torch.empty_like(local) for _ in range(dist.get_world_size(group))]
+    dist.all_gather(gathered, local, group=group)
+    return [g.cpu().numpy() for g in gathered]
+
+
 def price_american_sharded(spec: "qmcg.OptionSpec", m: int, n_paths: int, seed: int, *,
                            ctx: Optional["qmcg.Context"] = None,
                            node_sums_fn: Optional[Callable[[int, int], np.ndarray]] = None,
-                           allow_put: bool = False, group=None) -> Tuple[float, float, int]:
+                           allow_put: bool = False, fp32: bool = False, group=None) -> Tuple[float, float, int]:
     """Price one option with the paths sharded over the ranks of `group`.
 
-    node_sums_fn(depth, node) -> [sum v, sum v^2] defaults to the GPU kernel on
-    `ctx` (qmcg_price_american_node). Returns (price, std_error, depth).
+    Each rank prices the contiguous path range of the tree nodes it owns in one
+    kernel pass (qmcg_price_american_nodes); node_sums_fn(depth, node) ->
+    [sum v, sum v^2] replaces that (CPU tests). Returns (price, std_error, depth).
     """
-    import torch
     import torch.distributed as dist
 
     world = dist.get_world_size(group) if dist.is_initialized() else 1
     rank = dist.get_rank(group) if dist.is_initialized() else 0
     depth = tree_depth(n_paths, world)
-    if node_sums_fn is None:
-        if ctx is None:
-            raise ValueError("price_american_sharded: pass ctx or node_sums_fn")
-        node_sums_fn = lambda d, node: ctx.price_american_node(spec, m, n_paths, seed, d, node,  # noqa: E731
-                                                               allow_put=allow_put)
+    mine = rank_nodes(depth, world, rank)
     table = np.zeros((1 << depth, 2), dtype=np.float64)
-    for node in rank_nodes(depth, world, rank):
-        table[node] = node_sums_fn(depth, node)
+    if mine:
+        if node_sums_fn is not None:
+            for node in mine:
+                table[node] = node_sums_fn(depth, node)
+        else:
+            if ctx is None:
+                raise ValueError("price_american_sharded: pass ctx or node_sums_fn")
+            table[mine[0]:mine[-1] + 1] = ctx.price_american_nodes(spec, m, n_paths, seed, depth, mine[0],
+                                                                  len(mine), allow_put=allow_put, fp32=fp32)
     if world > 1:
-        backend = dist.get_backend(group)
-        dev = torch.device("cuda", torch.cuda.current_device()) if backend == "nccl" else torch.device("cpu")
-        local = torch.from_numpy(table).to(dev)
-        gathered = [torch.empty_like(local) for _ in range(world)]
-        dist.all_gather(gathered, local, group=group)
+        rows = _all_gather_rows(table, group)
         owners = node_owner(depth, world)
-        rows = [gathered[r].cpu().numpy() for r in range(world)]
         table = np.stack([rows[owners[i]][i] for i in range(1 << depth)])
     price, se = combine(n_paths, depth, table)
     return price, se, depth
+
+
+def contract_range(n_contracts: int, world: int, rank: int) -> Tuple[int, int]:
+    """Contiguous block of contracts owned by `rank` (config 4: contracts shard, paths do not)."""
+    return (n_contracts * rank) // world, (n_contracts * (rank + 1)) // world
+
+
+def price_american_batch_sharded(specs: Sequence["qmcg.OptionSpec"], m: int, n_paths: int, seed: int, *,
+                                 ctx: Optional["qmcg.Context"] = None,
+                                 batch_fn: Optional[Callable[[Sequence], np.ndarray]] = None,
+                                 allow_put: bool = False, group=None) -> np.ndarray:
+    """Config 4 over the ranks of `group`: rank r prices contracts contract_range(C, world, r)
+    over all paths (its own copy of the shared permutation tables), then the (price, std_error)
+    rows are all-gathered. Every contract is independent, so the result equals the single-GPU
+    batch bit for bit. batch_fn(specs) -> (len, 2) replaces the GPU call (CPU tests)."""
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    C = len(specs)
+    per = -(-C // world)
+    b, e = contract_range(C, world, rank)
+    local = np.zeros((per, 2), dtype=np.float64)
+    if e > b:
+        if batch_fn is not None:
+            local[: e - b] = batch_fn(specs[b:e])
+        else:
+            if ctx is None:
+                raise ValueError("price_american_batch_sharded: pass ctx or batch_fn")
+            res = ctx.price_american_batch(list(specs[b:e]), m, n_paths, seed, allow_put=allow_put)
+            local[: e - b] = [(r.price, r.std_error) for r in res]
+    rows = _all_gather_rows(local, group)
+    out = np.zeros((C, 2), dtype=np.float64)
+    for r in range(world):
+        rb, re_ = contract_range(C, world, r)
+        out[rb:re_] = rows[r][: re_ - rb]
+    return out

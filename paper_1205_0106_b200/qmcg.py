@@ -40,7 +40,7 @@ EXPORTS = (
     "qmcg_combine_nodes", "qmcg_warm", "qmcg_clear_cache", "qmcg_permutation", "qmcg_uniforms",
     "qmcg_normals", "qmcg_normal_table", "qmcg_path_values", "qmcg_time_device", "qmcg_time_perm_build",
     "qmcg_last_launch_count", "qmcg_get_stream", "qmcg_fp64_peak", "qmcg_set_table_budget",
-    "qmcg_last_window_count",
+    "qmcg_last_window_count", "qmcg_price_american_nodes",
 )
 
 
@@ -119,6 +119,7 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
         L.qmcg_mc_european_price.argtypes = [P, C.POINTER(_CSpec), I64, U64, U32, C.POINTER(_CResult)]
         L.qmcg_price_american_batch.argtypes = [P, C.POINTER(_CSpec), I64, I64, I64, U64, U32, C.POINTER(_CResult)]
         L.qmcg_price_american_node.argtypes = [P, C.POINTER(_CSpec), I64, I64, U64, U32, C.c_int, I64, PD]
+        L.qmcg_price_american_nodes.argtypes = [P, C.POINTER(_CSpec), I64, I64, U64, U32, C.c_int, I64, I64, PD]
         L.qmcg_tree_node_range.argtypes = [I64, C.c_int, I64, C.POINTER(I64), C.POINTER(I64)]
         L.qmcg_combine_nodes.argtypes = [I64, C.c_int, PD, PD, PD]
         L.qmcg_warm.argtypes = [P, I64, U64, I64]
@@ -224,12 +225,23 @@ class Context:
         return [_result(r) for r in res]
 
     def price_american_node(self, spec: OptionSpec, m: int, n_paths: int, seed: int, depth: int, node: int,
-                            allow_put: bool = False) -> np.ndarray:
+                            allow_put: bool = False, fp32: bool = False) -> np.ndarray:
         out = np.zeros(2, dtype=np.float64)
         s = _cspec(spec)
         _check(self._lib.qmcg_price_american_node(self._h, C.byref(s), int(m), int(n_paths), int(seed),
-                                                   FLAG_ALLOW_PUT if allow_put else 0, int(depth), int(node),
+                                                   _flags(allow_put, fp32=fp32), int(depth), int(node),
                                                    out.ctypes.data_as(C.POINTER(C.c_double))))
+        return out
+
+    def price_american_nodes(self, spec: OptionSpec, m: int, n_paths: int, seed: int, depth: int,
+                             node_begin: int, node_count: int, allow_put: bool = False,
+                             fp32: bool = False) -> np.ndarray:
+        """(node_count, 2) table of (sum v, sum v^2) for consecutive tree nodes, one kernel pass."""
+        out = np.zeros((int(node_count), 2), dtype=np.float64)
+        s = _cspec(spec)
+        _check(self._lib.qmcg_price_american_nodes(self._h, C.byref(s), int(m), int(n_paths), int(seed),
+                                                    _flags(allow_put, fp32=fp32), int(depth), int(node_begin),
+                                                    int(node_count), out.ctypes.data_as(C.POINTER(C.c_double))))
         return out
 
     def warm(self, n_paths: int, seed: int, dims: int) -> None:

@@ -62,3 +62,43 @@ def test_sharded_reduction_bit_identical(world, oracle_lib):
         price, se, depth, _ = out[rank]
         assert (price, se) == (ref_price, ref_se)
         assert (1 << depth) >= world
+
+
+def _batch_worker(rank, world, port, specs, m, n, out):
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import torch.distributed as dist
+    import oracle
+    import paper_1205_0106_b200 as q
+    from paper_1205_0106_b200 import distributed
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    O = oracle.Oracle()
+    seen = []
+
+    def batch_fn(sub):
+        seen.extend(tuple(s) for s in sub)
+        return np.array([O.price_american(*s[:5], m, n, 42, kind=s[5], allow_put=True)[:2] for s in sub])
+
+    res = distributed.price_american_batch_sharded(specs, m, n, 42, batch_fn=batch_fn)
+    out[rank] = (res, seen)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_batch_contract_sharding(world, oracle_lib):
+    """Config 4 over ranks: contiguous contract blocks, all-gathered (price, se) rows equal the
+    single-process batch exactly; every contract priced by exactly one rank."""
+    specs = [(100.0, 80.0 + 5 * i, 0.05, 0.1 + 0.05 * i, 1.0, i % 2) for i in range(7)]
+    m, n = 9, 700
+    ref = np.array([oracle_lib.price_american(*s[:5], m, n, 42, kind=s[5], allow_put=True)[:2] for s in specs])
+    manager = mp.Manager()
+    out = manager.dict()
+    mp.spawn(_batch_worker, args=(world, _free_port(), specs, m, n, out), nprocs=world, join=True)
+    seen = sorted(x for r in range(world) for x in out[r][1])
+    assert seen == sorted(specs)
+    for r in range(world):
+        assert np.array_equal(out[r][0], ref)

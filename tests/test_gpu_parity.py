@@ -239,3 +239,18 @@ def test_permutations_binned_scatter_bit_exact(ctx, oracle_lib, n):
     serial Fisher-Yates of the C restatement."""
     s = 0x9E3779B97F4A7C15 ^ n
     assert np.array_equal(ctx.permutation(n, s)[:n], oracle_lib.permutation_indices(n, s)[:n])
+
+
+def test_price_nodes_one_pass(ctx, qmcg):
+    """qmcg_price_american_nodes (one kernel over a rank's contiguous nodes) == per-node calls,
+    and the folded table == the single call, bit for bit; also for the FP32 variant."""
+    sp = spec_of(qmcg, REF)
+    n, m, depth = 50003, 30, 3
+    for fp32 in (False, True):
+        single = ctx.price_american(sp, m, n, 42, fp32=fp32)
+        per = np.array([ctx.price_american_node(sp, m, n, 42, depth, k, fp32=fp32) for k in range(8)])
+        lo = ctx.price_american_nodes(sp, m, n, 42, depth, 0, 3, fp32=fp32)
+        hi = ctx.price_american_nodes(sp, m, n, 42, depth, 3, 5, fp32=fp32)
+        table = np.concatenate([lo, hi])
+        assert np.array_equal(table, per)
+        assert qmcg.combine_nodes(n, depth, table) == (single.price, single.std_error)
