@@ -274,12 +274,14 @@ qmcg_status ensure_dim_tables(qmcg_ctx* c, int64_t n, int64_t m) {
 }
 
 // Build one full permutation (length n) for dimension `dim` into dst (n u32).
-qmcg_status build_perm(qmcg_ctx* c, uint64_t seed64, int64_t n, uint32_t* dst) {
+// K1 into dst. Pricing tables hold perm + 1 (add = 1): the Halton index of
+// uniform_at (quasi_rng.cpp:96-101), saving the increment per point in K2.
+qmcg_status build_perm(qmcg_ctx* c, uint64_t seed64, int64_t n, uint32_t* dst, uint32_t add = 1) {
   const size_t need = qmcg::perm_scratch_bytes(n);
   QMCG_CUDA(c->d_permscratch.reserve(need));
   int launches = 0;
   QMCG_CUDA(qmcg::launch_perm_build(seed64, n, dst, c->d_permscratch.ptr, c->d_permscratch.cap, c->stream,
-                                    &launches));
+                                    &launches, add));
   c->launches += launches;
   return QMCG_OK;
 }
@@ -1006,7 +1008,7 @@ qmcg_status qmcg_permutation(qmcg_ctx* c, int64_t n, uint64_t seed64, uint32_t* 
   std::lock_guard<std::mutex> lock(c->mu);
   DeviceGuard g(c->device);
   QMCG_CUDA(c->d_fullperm.reserve(static_cast<size_t>(n)));
-  qmcg_status st = build_perm(c, seed64, n, c->d_fullperm.ptr);
+  qmcg_status st = build_perm(c, seed64, n, c->d_fullperm.ptr, 0);
   if (st) return st;
   QMCG_CUDA(cudaMemcpyAsync(out_host, c->d_fullperm.ptr, static_cast<size_t>(n) * sizeof(uint32_t),
                             cudaMemcpyDeviceToHost, c->stream));

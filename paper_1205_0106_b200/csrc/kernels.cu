@@ -30,6 +30,9 @@ constexpr unsigned kFull = 0xffffffffu;
 constexpr int kThreads = QMCG_THREADS;  // paths per block (one per thread)
 static_assert(kThreads % 32 == 0 && kThreads <= 256, "tail queue indices are 8-bit");
 constexpr int kWarps = kThreads / 32;
+#ifndef QMCG_WALK_V
+#define QMCG_WALK_V 0
+#endif
 #ifndef QMCG_MINB
 #define QMCG_MINB 4
 #endif
@@ -101,13 +104,15 @@ __constant__ double c_moro_c[9] = {0.3374754822726147, 0.9761690190917186, 0.160
                                    0.0276438810333863, 0.0038405729373609, 0.0003951896511919,
                                    0.0000321767881768, 0.0000002888167364, 0.0000003960315187};
 
+// 1/x from the MUFU estimate r0 with one cubic step: with e = 1 - x r0,
+// 1/x = r0 (1 + e + e^2 + e^3 + ...), so r0 + r0 (e + e^2) leaves a relative
+// error ~e^3 (< 2^-60 for the ~2^-20 estimate) plus the final rounding:
+// 3 DFMAs instead of the 4 of two Newton steps.
 __device__ __forceinline__ double rcp_nr(double x) {
   double r;
   asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
-  double e = fma(-x, r, 1.0);
-  r = fma(r, e, r);
-  e = fma(-x, r, 1.0);
-  return fma(r, e, r);
+  const double e = fma(-x, r, 1.0);
+  return fma(r, fma(e, e, e), r);
 }
 
 // Beasley-Springer central region of moro_inv_cnd (analytic.cpp:82-94), plus
@@ -507,6 +512,39 @@ __device__ __forceinline__ typename ZSlot<F32>::T central_z(double y, double alp
   return moro_central_plus(y, alpha);
 }
 
+// Store one generated point: z in its slot; a tail point (|u - 1/2| > 0.42, the
+// reference's branch on the bit-exact uniform) then overwrites the slot with its
+// parked value and queues its index at ntail + rank. One predicate feeds the
+// ballot and both predicated stores (no selects, no dummy queue slots).
+template <bool F32>
+__device__ __forceinline__ void park_point(uint32_t zslot, uint32_t qbase, uint32_t idx,
+                                           typename ZSlot<F32>::T z, typename ZSlot<F32>::T park, double y,
+                                           unsigned lt, uint32_t& ntail) {
+  unsigned b;
+  if constexpr (F32) {
+    asm volatile(
+        "{\n .reg .pred p;\n .reg .f64 ay;\n .reg .b32 m, a;\n"
+        " abs.f64 ay, %4;\n setp.gt.f64 p, ay, 0d3FDAE147AE147AE1;\n"
+        " vote.sync.ballot.b32 %0, p, 0xffffffff;\n"
+        " st.shared.f32 [%1], %2;\n @p st.shared.f32 [%1], %3;\n"
+        " and.b32 m, %0, %5;\n popc.b32 m, m;\n add.u32 a, %6, m;\n @p st.shared.u8 [a], %7;\n}"
+        : "=r"(b)
+        : "r"(zslot), "f"(z), "f"(park), "d"(y), "r"(lt), "r"(qbase + ntail), "r"(idx)
+        : "memory");
+  } else {
+    asm volatile(
+        "{\n .reg .pred p;\n .reg .f64 ay;\n .reg .b32 m, a;\n"
+        " abs.f64 ay, %4;\n setp.gt.f64 p, ay, 0d3FDAE147AE147AE1;\n"
+        " vote.sync.ballot.b32 %0, p, 0xffffffff;\n"
+        " st.shared.f64 [%1], %2;\n @p st.shared.f64 [%1], %3;\n"
+        " and.b32 m, %0, %5;\n popc.b32 m, m;\n add.u32 a, %6, m;\n @p st.shared.u8 [a], %7;\n}"
+        : "=r"(b)
+        : "r"(zslot), "d"(z), "d"(park), "d"(y), "r"(lt), "r"(qbase + ntail), "r"(idx)
+        : "memory");
+  }
+  ntail += __popc(b);
+}
+
 // Evaluate the queued Moro-tail points of one date row, 32 per round:
 // u (parked in the point's z slot) -> y = u - 0.5 (exact as the reference),
 // w = u or 1 - u, z = +-P8(log(-log w)) + alpha written back to the slot.
@@ -542,13 +580,7 @@ __device__ __forceinline__ void finish_point(uint32_t ws, uint32_t zslot, uint32
                                              double alpha, int lane, unsigned lt, uint32_t& ntail) {
   if (CLAMP && clamp) u = clamp_endpoints(u);
   const double y = __dadd_rn(u, -0.5);
-  const bool tail = fabs(y) > 0.42;
-  const unsigned tb = __ballot_sync(kFull, tail);
-  const uint32_t pos = tail ? ntail + __popc(tb & lt) : kTailCap + lane;
-  sts_u8(ws + kWTailIdx + pos, idx);
-  ntail += __popc(tb);
-  const auto z = central_z<F32>(y, alpha);
-  ZSlot<F32>::store(zslot, tail ? tail_park<F32>(u, y) : z);
+  park_point<F32>(zslot, ws + kWTailIdx, idx, central_z<F32>(y, alpha), tail_park<F32>(u, y), y, lt, ntail);
 }
 
 template <bool WIDE>
@@ -591,27 +623,20 @@ __device__ __forceinline__ uint32_t generate_row_fixed(const double2* sn, uint32
   int ch = 0;
 #pragma unroll 1
   for (; ch + 1 < nchunks; ch += 2) {  // two independent chunks in flight
-    const uint32_t xa = lds_u32(prow + ch * 128) + 1u;
-    const uint32_t xb = lds_u32(prow + ch * 128 + 128) + 1u;
+    const uint32_t xa = lds_u32(prow + ch * 128);  // tables hold perm + 1 (the Halton index)
+    const uint32_t xb = lds_u32(prow + ch * 128 + 128);
     const double ua = halton_fixed<D>(xa, magic, shift, negp, sc);
     const double ub = halton_fixed<D>(xb, magic, shift, negp, sc);
     const double ya = __dadd_rn(ua, -0.5);
     const double yb = __dadd_rn(ub, -0.5);
     const auto za = central_z<F32>(ya, alpha);
     const auto zb = central_z<F32>(yb, alpha);
-    const bool ta = fabs(ya) > 0.42, tb = fabs(yb) > 0.42;
-    const unsigned ba = __ballot_sync(kFull, ta), bb = __ballot_sync(kFull, tb);
-    const uint32_t na = __popc(ba);
-    const uint32_t pa = ta ? ntail + __popc(ba & lt) : kTailCap + lane;
-    const uint32_t pb = tb ? ntail + na + __popc(bb & lt) : kTailCap + lane;
-    sts_u8(ws + kWTailIdx + pa, ch * 32 + lane);
-    sts_u8(ws + kWTailIdx + pb, ch * 32 + 32 + lane);
-    ntail += na + __popc(bb);
-    Z::store(zrow + ch * kCh, ta ? tail_park<F32>(ua, ya) : za);
-    Z::store(zrow + ch * kCh + kCh, tb ? tail_park<F32>(ub, yb) : zb);
+    park_point<F32>(zrow + ch * kCh, ws + kWTailIdx, ch * 32 + lane, za, tail_park<F32>(ua, ya), ya, lt, ntail);
+    park_point<F32>(zrow + ch * kCh + kCh, ws + kWTailIdx, ch * 32 + 32 + lane, zb, tail_park<F32>(ub, yb), yb, lt,
+                    ntail);
   }
   if (ch < nchunks) {
-    const uint32_t x = lds_u32(prow + ch * 128) + 1u;
+    const uint32_t x = lds_u32(prow + ch * 128);
     const double u = halton_fixed<D>(x, magic, shift, negp, sc);
     finish_point<false, F32>(ws, zrow + ch * kCh, ch * 32 + lane, u, false, alpha, lane, lt, ntail);
   }
@@ -641,7 +666,7 @@ __device__ __forceinline__ void generate_row(const PriceParams& P, uint32_t ws, 
     const bool wide = SLOW && ((dp.z >> 16) & DIM_WIDE);
     const uint64_t m64 = wide ? __ldg(P.magic64 + d) : 0ull;
     for (int ch = 0; ch < nchunks; ++ch) {
-      const uint32_t x = lds_u32(pl + ch * 128) + 1u;
+      const uint32_t x = lds_u32(pl + ch * 128);
       const double u = wide ? halton_any<true>(x, dp, m64, sn) : halton_any<false>(x, dp, m64, sn);
       finish_point<SLOW, F32>(ws, zl + ch * 32 * Z::kSize, ch * 32 + lane, u, clamp, alpha, lane, lt, ntail);
     }
@@ -671,8 +696,8 @@ __device__ __forceinline__ bool record_dominates(T V, T c, T acc, T b, T x0mk) {
 template <int KIND, bool RNEG>
 __device__ __forceinline__ void push_record(uint32_t ws, const PriceParams& P, bool push, double v, int d, int lane,
                                             unsigned lt, uint32_t& rq_head, uint32_t& rq_tail) {
-  const unsigned pb = __ballot_sync(kFull, push);
-  if (pb) {
+  if (__any_sync(kFull, push)) {
+    const unsigned pb = __ballot_sync(kFull, push);
     if (push) {
       const uint32_t slot = (rq_tail + __popc(pb & lt)) & (kRecCap - 1);
       sts_f64(ws + kWRqV + slot * 8, v);
@@ -725,7 +750,8 @@ __global__ void __launch_bounds__(kThreads, QMCG_MINB) price_kernel(const PriceP
   const uint32_t bytes = static_cast<uint32_t>(((block_paths + 3) / 4) * 16);
   using Z = ZSlot<F32>;
   using T = typename Z::T;
-  const T slope = static_cast<T>(P.dom_slope);
+  T slope = static_cast<T>(P.dom_slope);
+  if constexpr (!F32) asm volatile("mov.b64 %0, %0;" : "+d"(slope));  // keep it in a register (no per-date reload)
   const T bT = static_cast<T>(P.b), x0mkT = static_cast<T>(P.x0mk);
 
   if (threadIdx.x == 0) {
@@ -738,7 +764,9 @@ __global__ void __launch_bounds__(kThreads, QMCG_MINB) price_kernel(const PriceP
                : "memory");
   T V = T(0);
   T c = static_cast<T>(P.c0);
-  T cd = T(0);  // dominance threshold of the pending record (see the walk)
+  // dominance threshold of the pending record (see the walk); for calls -inf
+  // while no record is pending, so that no new record is ever pushed against it
+  T cd = KIND == 0 ? T(-INFINITY) : T(0);
   int pend_d = -1;  // date of the pending (not yet evaluated) record, -1 = none
   if (P.stream_load && active) {  // carry-in from the previous date window
     const int64_t i = pi;
@@ -775,19 +803,30 @@ __global__ void __launch_bounds__(kThreads, QMCG_MINB) price_kernel(const PriceP
     // c = V of the last record (= the pending record when pend_d >= 0);
     // cd = the dominance accumulator of the pending record (record_dominates).
     if (!SLOW && !RNEG && k0 + kTile <= mrec) {
+      // pending date kept tile-relative (the select takes t as an immediate);
+      // calls need no "pending exists" test: cd = -inf until the first record
+      int pl = pend_d - k0;
 #pragma unroll
       for (int t = 0; t < kTile; ++t) {
         V = add_rn(V, Z::load(zcol + t * kThreads * Z::kSize));
         cd = add_rn(cd, slope);
         const bool rec = KIND == 0 ? V > c : V < c;
-        const bool push = rec && pend_d >= 0 && !record_dominates<KIND>(V, c, cd, bT, x0mkT);
-        const double pv = c;
-        const int pd = pend_d;
+        const bool push = rec && (KIND == 0 || pl + k0 >= 0) && !record_dominates<KIND>(V, c, cd, bT, x0mkT);
+#if QMCG_WALK_V == 1
+        push_record<KIND, RNEG>(ws, P, push, c, k0 + pl, lane, lt, rq_head, rq_tail);
         c = rec ? V : c;
         cd = rec ? (KIND == 0 ? V : T(0)) : cd;
-        pend_d = rec ? k0 + t : pend_d;
-        push_record<KIND, RNEG>(ws, P, push, pv, pd, lane, lt, rq_head, rq_tail);
+        pl = rec ? t : pl;
+#else
+        const double pv = c;
+        const int pdl = pl;
+        c = rec ? V : c;
+        cd = rec ? (KIND == 0 ? V : T(0)) : cd;
+        pl = rec ? t : pl;
+        push_record<KIND, RNEG>(ws, P, push, pv, k0 + pdl, lane, lt, rq_head, rq_tail);
+#endif
       }
+      pend_d = k0 + pl;
     } else {
 #pragma unroll
       for (int t = 0; t < kTile; ++t) {
@@ -1100,7 +1139,7 @@ __global__ void european_kernel(const uint32_t* __restrict__ perm_row, int64_t c
                                 double bsd, double strike, double disc, int kind, double* __restrict__ out) {
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= count) return;
-  const double z = moro_full(halton(perm_row[i] + 1u, dp, sc, nc));
+  const double z = moro_full(halton(perm_row[i], dp, sc, nc));  // table entry = perm + 1
   const double st = s0 * exp(fma(bsd, z, a));
   const double diff = kind == 0 ? st - strike : strike - st;
   out[i] = disc * (diff > 0.0 ? diff : 0.0);
@@ -1112,7 +1151,7 @@ __global__ void uniforms_kernel(const uint32_t* __restrict__ perm_row, int64_t c
                                 int normals, double* __restrict__ out) {
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= count) return;
-  const double u = halton(perm_row[i] + 1u, dp, sc, nc);
+  const double u = halton(perm_row[i], dp, sc, nc);  // table entry = perm + 1
   out[i] = normals ? moro_full(u) : u;
 }
 
@@ -1178,7 +1217,7 @@ __global__ void fy_first_kernel(const uint32_t* __restrict__ sk, const uint32_t*
 // whole DRAM burst); otherwise it is stored directly.
 __global__ void fy_assign_kernel(const uint32_t* __restrict__ sk, const uint32_t* __restrict__ sv, int64_t n,
                                  const uint32_t* __restrict__ F, uint32_t* __restrict__ perm,
-                                 uint2* __restrict__ pairs) {
+                                 uint2* __restrict__ pairs, uint32_t add) {
   const int64_t q = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (q >= n) return;
   const uint32_t x = sk[q], i = sv[q];
@@ -1191,8 +1230,8 @@ __global__ void fy_assign_kernel(const uint32_t* __restrict__ sk, const uint32_t
 #ifdef QMCG_K1_COALESCED_PROBE
   perm[q] = out + i;  // timing probe only: coalesced store (wrong result)
 #else
-  if (pairs) pairs[q] = make_uint2(i, out);
-  else perm[i] = out;
+  if (pairs) pairs[q] = make_uint2(i, out + add);
+  else perm[i] = out + add;
 #endif
 }
 
@@ -1255,6 +1294,8 @@ __global__ void __launch_bounds__(kBinThreads) fy_bin_kernel(const uint2* __rest
     out[base[b] + (k - start[b])] = p;
   }
 }
+
+__global__ void fill_u32_kernel(uint32_t* out, uint32_t v) { *out = v; }
 
 // Pass 2: perm[i] = p for the binned pairs. Consecutive blocks cover
 // consecutive bins, so the destination window in flight is a few bins
@@ -1500,7 +1541,7 @@ PermScratchLayout perm_layout(int64_t n) {
 size_t perm_scratch_bytes(int64_t n) { return perm_layout(n).total; }
 
 cudaError_t launch_perm_build(uint64_t seed64, int64_t n, uint32_t* out, void* scratch, size_t scratch_bytes,
-                              cudaStream_t s, int* launches) {
+                              cudaStream_t s, int* launches, uint32_t add) {
   const PermScratchLayout L = perm_layout(n);
   if (scratch_bytes < L.total) return cudaErrorInvalidValue;
   char* base = static_cast<char*>(scratch);
@@ -1510,7 +1551,8 @@ cudaError_t launch_perm_build(uint64_t seed64, int64_t n, uint32_t* out, void* s
   auto* svals = reinterpret_cast<uint32_t*>(base + L.svals);
   auto* F = reinterpret_cast<uint32_t*>(base + L.F);
   if (n == 1) {
-    return cudaMemsetAsync(out, 0, sizeof(uint32_t), s);
+    fill_u32_kernel<<<1, 1, 0, s>>>(out, add);
+    return cudaGetLastError();
   }
   int bits = 1;
   while (bits < 32 && (static_cast<uint64_t>(n - 1) >> bits) != 0) ++bits;
@@ -1537,7 +1579,7 @@ cudaError_t launch_perm_build(uint64_t seed64, int64_t n, uint32_t* out, void* s
   fy_first_kernel<<<static_cast<unsigned>(eb), threads, 0, s>>>(skeys, svals, n, F, binned ? cursor : nullptr,
                                                                  shift);
   fy_assign_kernel<<<static_cast<unsigned>(eb), threads, 0, s>>>(skeys, svals, n, F, out,
-                                                                  binned ? pairs : nullptr);
+                                                                  binned ? pairs : nullptr, add);
   if (binned) {
     const int64_t bb = (n + kBinThreads * kBinPer - 1) / (kBinThreads * kBinPer);
     fy_bin_kernel<<<static_cast<unsigned>(bb), kBinThreads, 0, s>>>(pairs, n, shift, cursor, binned_pairs);

@@ -118,7 +118,7 @@ cudaError_t launch_price(const PriceParams& P, cudaStream_t s);
 // scratch must hold perm_scratch_bytes(n) bytes.
 size_t perm_scratch_bytes(int64_t n);
 cudaError_t launch_perm_build(uint64_t seed64, int64_t n, uint32_t* out, void* scratch,
-                              size_t scratch_bytes, cudaStream_t s, int* launches);
+                              size_t scratch_bytes, cudaStream_t s, int* launches, uint32_t add);
 // Copy columns [c0, c1) of a freshly built permutation into a table row.
 cudaError_t launch_uniforms(const uint32_t* perm_row, int64_t count, DimParam dp, const double* sc,
                             const double* nc, int normals, double* out, cudaStream_t s);
