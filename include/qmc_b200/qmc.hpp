@@ -15,6 +15,7 @@
 
 #include <cstddef>
 #include <cstdint>
+#include <optional>
 #include <string>
 #include <vector>
 
@@ -71,6 +72,41 @@ ConvergenceCurve convergence_curve(const OptionSpec& spec, const std::vector<Ind
 // One-step QMC European price; reference proj/src/mc_european.cpp:11-46.
 PricingResult mc_european_price(const OptionSpec& spec, Index n_paths, std::uint64_t seed,
                                 const ExecPolicy& exec = {});
+
+// ExerciseSchedule / make_schedule; reference proj/include/qmc/path_engine.hpp:15-22,
+// proj/src/path_engine.cpp:63-76 (t_i = i dt for i = 1..m, then T; dt = T / (m+1)).
+struct ExerciseSchedule {
+  Index m = 0;
+  double maturity = 0.0;
+  double dt = 0.0;
+  std::vector<double> times;  // m + 1 entries
+  Index points() const { return m + 1; }
+};
+ExerciseSchedule make_schedule(Index m, double maturity);
+
+// PathBatch / simulate_batch; reference path_engine.hpp:26-31, path_engine.cpp:124-152.
+// prices is the reference's row-major [n_paths x points] matrix, generated on the GPU.
+struct PathBatch {
+  std::vector<double> prices;
+  Index n_paths = 0;
+  OptionSpec spec;
+  ExerciseSchedule schedule;
+  std::uint64_t seed = 0;
+  double operator()(Index p, Index k) const { return prices[static_cast<std::size_t>(p * schedule.points() + k)]; }
+};
+PathBatch simulate_batch(const OptionSpec& spec, const ExerciseSchedule& schedule, Index n_paths,
+                         std::uint64_t seed, const ExecPolicy& exec = {});
+
+// SweepTrace / backward_sweep / sweep_value; reference proj/include/qmc/american.hpp:13-41.
+// The reference takes Eigen::Ref<const RowVector>; pass path.data(), path.size().
+struct SweepTrace {
+  std::vector<double> values;             // t_0..t_m, then the payoff at T (m + 2 entries)
+  std::optional<Index> exercise_point;    // earliest index where intrinsic beat continuation
+};
+SweepTrace backward_sweep(const double* path, Index path_len, const OptionSpec& spec,
+                          const ExerciseSchedule& schedule);
+double sweep_value(const double* path, Index path_len, const OptionSpec& spec,
+                   const ExerciseSchedule& schedule);
 
 namespace b200 {
 // Extension (no reference counterpart): the same foresight rule for puts.

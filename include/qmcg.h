@@ -151,6 +151,31 @@ qmcg_status qmcg_normal_table(qmcg_ctx* ctx, int64_t n_paths, uint64_t seed, int
 qmcg_status qmcg_path_values(qmcg_ctx* ctx, const qmcg_option_spec* spec, int64_t m,
                              int64_t n_paths, uint64_t seed, uint32_t flags, double* out_host);
 
+/* ---- path matrix and sweeps (diagnostics; the pricing kernels never store paths) ---- */
+enum { QMCG_LAYOUT_PATH_MAJOR = 0, /* prices[p * (m+1) + k]: reference PathBatch::prices (row-major) */
+       QMCG_LAYOUT_POINT_MAJOR = 1 /* prices[k * n + p]: the device layout */ };
+/* simulate_batch(spec, make_schedule(m, T), n_paths, seed) (proj/src/path_engine.cpp:124-152):
+ * S at t_1..t_m, T for every path, generated on the GPU from the same tables as the pricer.
+ * Errors as the reference (make_schedule, validate, n_paths >= 1, check_capacity's 128 GiB
+ * length_error with the computed size, gbm_step's s_prev > 0). out_host == NULL only validates
+ * (ctx may then be NULL too), so a caller can size its buffer after the reference's checks. */
+qmcg_status qmcg_simulate_batch(qmcg_ctx* ctx, const qmcg_option_spec* spec, int64_t m,
+                                int64_t n_paths, uint64_t seed, uint32_t flags, int layout,
+                                double* out_host);
+/* sweep_value and the earliest exercise point of backward_sweep (american.cpp:19-101) for
+ * every simulated path, on the GPU over the point-major matrix: values_host[p] = t_0 value,
+ * exercise_host[p] = earliest index in 0..m where intrinsic beat continuation, -1 if never. */
+qmcg_status qmcg_sweep_batch(qmcg_ctx* ctx, const qmcg_option_spec* spec, int64_t m,
+                             int64_t n_paths, uint64_t seed, uint32_t flags, double* values_host,
+                             int32_t* exercise_host);
+/* backward_sweep(path, spec, make_schedule(m, T)) for one caller-provided path (host; the
+ * reference's per-path diagnostic, american.cpp:88-95): values_out[0..m] = value at t_0..t_m,
+ * values_out[m+1] = realised payoff at T; *exercise_point = earliest exercise index or -1.
+ * path holds m+1 prices (t_1..t_m, T). */
+qmcg_status qmcg_backward_sweep(const double* path, int64_t path_len, const qmcg_option_spec* spec,
+                                int64_t m, uint32_t flags, double* values_out,
+                                int64_t* exercise_point);
+
 /* ---- measurement hooks (bench.py) ---- */
 /* Launch the pricing of `spec` reps times on the context stream with the
  * tables resident, and report the device time of the pricing kernel alone and

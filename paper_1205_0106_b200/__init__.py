@@ -6,10 +6,11 @@ hand-written sm_100a CUDA kernels behind the C ABI in ``include/qmcg.h``
 ctypes binding with the reference's names.
 """
 from .qmcg import (  # noqa: F401
-    Context, ExecPolicy, Method, OptionKind, OptionSpec, PricingResult, combine_nodes,
-    convergence_curve, load_library, mc_european_price, price_american, tree_node_range,
+    Context, ExecPolicy, Method, OptionKind, OptionSpec, PricingResult, backward_sweep, combine_nodes,
+    convergence_curve, load_library, mc_european_price, price_american, sweep_value, tree_node_range,
+    validate_simulation,
 )
 
-__all__ = ["Context", "ExecPolicy", "Method", "OptionKind", "OptionSpec", "PricingResult",
+__all__ = ["Context", "ExecPolicy", "Method", "OptionKind", "OptionSpec", "PricingResult", "backward_sweep",
            "combine_nodes", "convergence_curve", "load_library", "mc_european_price", "price_american",
-           "tree_node_range"]
+           "sweep_value", "tree_node_range", "validate_simulation"]

@@ -224,6 +224,9 @@ struct qmcg_ctx {
   // host-side dimension constants mirrored on the device
   DimTables dt;
   DevBuf<qmcg::DimPack> d_pack;
+  DevBuf<DimParam> d_dimp;           // per-dimension digit parameters (path-matrix export)
+  DevBuf<double> d_path, d_path_t;   // path matrix [point][path] (+ path-major transpose)
+  DevBuf<int32_t> d_ex;              // per-path exercise points
   DevBuf<uint64_t> d_m64;
   DevBuf<double> d_sc, d_nc, d_scnc, d_dpow;
   DevBuf<double> d_values, d_red, d_sums;
@@ -255,6 +258,9 @@ qmcg_status ensure_dim_tables(qmcg_ctx* c, int64_t n, int64_t m) {
   if (c->dt.n == n && c->dt.m >= m) return QMCG_OK;
   build_dim_tables(n, std::max<int64_t>(m, c->dt.n == n ? c->dt.m : 0), c->dt);
   QMCG_CUDA(c->d_pack.reserve(c->dt.pack.size()));
+  QMCG_CUDA(c->d_dimp.reserve(c->dt.dims.size()));
+  QMCG_CUDA(cudaMemcpyAsync(c->d_dimp.ptr, c->dt.dims.data(), c->dt.dims.size() * sizeof(DimParam),
+                            cudaMemcpyHostToDevice, c->stream));
   QMCG_CUDA(c->d_m64.reserve(c->dt.magic64.size()));
   QMCG_CUDA(c->d_sc.reserve(c->dt.sc.size()));
   QMCG_CUDA(c->d_nc.reserve(c->dt.nc.size()));
@@ -557,6 +563,10 @@ void qmcg_destroy(qmcg_ctx* c) {
   c->d_err.release();
   c->d_fullperm.release();
   c->d_permscratch.release();
+  c->d_dimp.release();
+  c->d_path.release();
+  c->d_path_t.release();
+  c->d_ex.release();
   c->d_stV.release();
   c->d_stc.release();
   c->d_stcd.release();
@@ -1178,3 +1188,208 @@ qmcg_status qmcg_fp64_peak(qmcg_ctx* c, double ms, double* inst_per_s) {
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------
+// Path matrix export and per-path sweeps: the reference's
+// simulate_batch (path_engine.cpp:124-152) and backward_sweep / sweep_value
+// (american.cpp:70-101). The pricing kernel never materialises paths; these are
+// the diagnostics that need them.
+// ---------------------------------------------------------------------------
+namespace {
+
+// check_capacity (path_engine.cpp:20-35): the reference's 128 GiB matrix cap and message.
+qmcg_status check_capacity(int64_t n, int64_t points, const char* who) {
+  const long double bytes = static_cast<long double>(n) * static_cast<long double>(points) * 8.0L;
+  const long double cap = static_cast<long double>(uint64_t{1} << 37);
+  if (bytes > cap) {
+    char msg[512];
+    std::snprintf(msg, sizeof msg, "%s: requested %lld paths x %lld points = %g bytes, above the supported maximum of %g bytes",
+                  who, static_cast<long long>(n), static_cast<long long>(points), static_cast<double>(bytes),
+                  static_cast<double>(cap));
+    return fail(QMCG_LENGTH_ERROR, msg);
+  }
+  return QMCG_OK;
+}
+
+// The reference's checks, in its order, for simulate_batch(spec, make_schedule(m, T), n, seed).
+qmcg_status validate_simulation(const qmcg_option_spec& s, int64_t m, int64_t n) {
+  if (m < 1) return fail(QMCG_INVALID_ARGUMENT, "make_schedule: m must be >= 1");
+  if (!(s.maturity > 0.0)) return fail(QMCG_INVALID_ARGUMENT, "make_schedule: maturity must be > 0");
+  qmcg_status st = validate(s);
+  if (st) return st;
+  if (n < 1) return fail(QMCG_INVALID_ARGUMENT, "simulate_batch: n_paths must be >= 1");
+  st = check_capacity(n, m + 1, "simulate_batch");
+  if (st) return st;
+  if (static_cast<uint64_t>(n) > 0xffffffffULL)
+    return fail(QMCG_LENGTH_ERROR, "permutation_indices: n exceeds the 2^32-1 supported maximum");
+  if (m + 1 > (int64_t{1} << 26)) return fail(QMCG_LENGTH_ERROR, "simulate_batch: m exceeds the 2^26 supported maximum");
+  return QMCG_OK;
+}
+
+// The matrix of paths [0, n) at points t_1..t_m, T into c->d_path ([point][path]).
+qmcg_status simulate_device(qmcg_ctx* c, const qmcg_option_spec& s, int64_t m, int64_t n, uint64_t seed) {
+  if (m < 1) return fail(QMCG_INVALID_ARGUMENT, "make_schedule: m must be >= 1");
+  if (!(s.maturity > 0.0)) return fail(QMCG_INVALID_ARGUMENT, "make_schedule: maturity must be > 0");
+  qmcg_status st = validate(s);
+  if (st) return st;
+  if (n < 1) return fail(QMCG_INVALID_ARGUMENT, "simulate_batch: n_paths must be >= 1");
+  const int64_t points = m + 1;
+  st = check_capacity(n, points, "simulate_batch");
+  if (st) return st;
+  if (static_cast<uint64_t>(n) > 0xffffffffULL)
+    return fail(QMCG_LENGTH_ERROR, "permutation_indices: n exceeds the 2^32-1 supported maximum");
+  if (points > (int64_t{1} << 26)) return fail(QMCG_LENGTH_ERROR, "simulate_batch: m exceeds the 2^26 supported maximum");
+  st = ensure_dim_tables(c, n, points);
+  if (st) return st;
+  st = ensure_perms(c, seed, n, 0, n, points, false);
+  if (st) return st;
+  QMCG_CUDA(c->d_path.reserve(static_cast<size_t>(n) * static_cast<size_t>(points)));
+  QMCG_CUDA(c->d_err.reserve(1));
+  QMCG_CUDA(cudaMemsetAsync(c->d_err.ptr, 0, sizeof(uint32_t), c->stream));
+  const double dt = s.maturity / static_cast<double>(points);  // make_schedule
+  const double a = (s.rate - 0.5 * s.volatility * s.volatility) * dt;
+  const double bsd = s.volatility * std::sqrt(dt);
+  QMCG_CUDA(qmcg::launch_path_matrix(c->table, qmcg::table_ld(n), c->d_dimp.ptr, c->d_sc.ptr, c->d_nc.ptr, n,
+                                     static_cast<int>(points), s.spot, a, bsd, c->d_path.ptr, c->d_err.ptr,
+                                     c->stream));
+  c->launches += 1;
+  return QMCG_OK;
+}
+
+// cnd (analytic.cpp:33-72), restated for the host sweep.
+double cnd_host(double d) {
+  const double x = std::fabs(d);
+  double tail = 0.0;
+  if (x <= 37.0) {
+    const double e = std::exp(-0.5 * x * x);
+    if (x < 7.07106781186547) {
+      static const double P[7] = {3.52624965998911e-02, 0.700383064443688, 6.37396220353165, 33.912866078383,
+                                  112.079291497871,     221.213596169931,  220.206867912376};
+      static const double Q[8] = {8.83883476483184e-02, 1.75566716318264,  16.064177579207,  86.7807322029461,
+                                  296.564248779674,     637.333633378831,  793.826512519948, 440.413735824752};
+      double num = P[0], den = Q[0];
+      for (int i = 1; i < 7; ++i) num = num * x + P[i];
+      for (int i = 1; i < 8; ++i) den = den * x + Q[i];
+      tail = e * num / den;
+    } else {
+      double b = x + 0.65;
+      for (double k = 4.0; k >= 1.0; k -= 1.0) b = x + k / b;
+      tail = e / (b * 2.506628274631000502);
+    }
+  }
+  return d > 0.0 ? 1.0 - tail : tail;
+}
+
+// bs_price (analytic.cpp:102-124) for a spec already validated.
+double bs_price_host(double s, double x, double r, double v, double t, int kind) {
+  if (t == 0.0) return intrinsic(kind, s, x);
+  if (v == 0.0) return std::exp(-r * t) * intrinsic(kind, s * std::exp(r * t), x);
+  const double vst = v * std::sqrt(t);
+  const double d1 = (std::log(s / x) + (r + 0.5 * v * v) * t) / vst;
+  const double d2 = d1 - vst;
+  const double disc = std::exp(-r * t);
+  const double price = kind == QMCG_CALL ? s * cnd_host(d1) - x * disc * cnd_host(d2)
+                                         : x * disc * cnd_host(-d2) - s * cnd_host(-d1);
+  return price > 0.0 ? price : 0.0;
+}
+
+}  // namespace
+
+qmcg_status qmcg_simulate_batch(qmcg_ctx* c, const qmcg_option_spec* spec, int64_t m, int64_t n, uint64_t seed,
+                                uint32_t flags, int layout, double* out_host) {
+  if (!spec) return fail(QMCG_INVALID_ARGUMENT, "qmcg_simulate_batch: null argument");
+  if (layout != QMCG_LAYOUT_PATH_MAJOR && layout != QMCG_LAYOUT_POINT_MAJOR)
+    return fail(QMCG_INVALID_ARGUMENT, "qmcg_simulate_batch: bad layout");
+  if (!out_host) return validate_simulation(*spec, m, n);  // validation only (size the caller's buffer)
+  if (!c) return fail(QMCG_INVALID_ARGUMENT, "qmcg_simulate_batch: null argument");
+  (void)flags;
+  std::lock_guard<std::mutex> lock(c->mu);
+  DeviceGuard g(c->device);
+  c->launches = 0;
+  qmcg_status st = simulate_device(c, *spec, m, n, seed);
+  if (st) return st;
+  const int64_t points = m + 1;
+  const size_t count = static_cast<size_t>(n) * static_cast<size_t>(points);
+  const double* src = c->d_path.ptr;
+  if (layout == QMCG_LAYOUT_PATH_MAJOR) {
+    QMCG_CUDA(c->d_path_t.reserve(count));
+    QMCG_CUDA(qmcg::launch_transpose(c->d_path.ptr, points, n, c->d_path_t.ptr, c->stream));
+    c->launches += 1;
+    src = c->d_path_t.ptr;
+  }
+  uint32_t err = 0;
+  QMCG_CUDA(cudaMemcpyAsync(out_host, src, count * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  QMCG_CUDA(cudaMemcpyAsync(&err, c->d_err.ptr, sizeof(uint32_t), cudaMemcpyDeviceToHost, c->stream));
+  QMCG_CUDA(cudaStreamSynchronize(c->stream));
+  return map_err(err & qmcg::ERR_SPOT_NONPOSITIVE);
+}
+
+qmcg_status qmcg_sweep_batch(qmcg_ctx* c, const qmcg_option_spec* spec, int64_t m, int64_t n, uint64_t seed,
+                             uint32_t flags, double* values_host, int32_t* exercise_host) {
+  if (!c || !spec || !values_host || !exercise_host)
+    return fail(QMCG_INVALID_ARGUMENT, "qmcg_sweep_batch: null argument");
+  if (spec->kind != QMCG_CALL && !(flags & QMCG_FLAG_ALLOW_PUT))
+    return fail(QMCG_INVALID_ARGUMENT, "backward_sweep: not implemented for puts; the foresight algorithm is call-only");
+  std::lock_guard<std::mutex> lock(c->mu);
+  DeviceGuard g(c->device);
+  c->launches = 0;
+  qmcg_status st = simulate_device(c, *spec, m, n, seed);
+  if (st) return st;
+  QMCG_CUDA(c->d_values.reserve(static_cast<size_t>(n)));
+  QMCG_CUDA(c->d_ex.reserve(static_cast<size_t>(n)));
+  const double dt = spec->maturity / static_cast<double>(m + 1);
+  const double disc = std::exp(-spec->rate * dt);
+  QMCG_CUDA(qmcg::launch_sweep(c->d_path.ptr, n, static_cast<int>(m), spec->spot, spec->strike, spec->rate,
+                               spec->volatility, dt, disc, spec->kind, c->d_values.ptr, c->d_ex.ptr, c->stream));
+  c->launches += 1;
+  uint32_t err = 0;
+  QMCG_CUDA(cudaMemcpyAsync(values_host, c->d_values.ptr, static_cast<size_t>(n) * sizeof(double),
+                            cudaMemcpyDeviceToHost, c->stream));
+  QMCG_CUDA(cudaMemcpyAsync(exercise_host, c->d_ex.ptr, static_cast<size_t>(n) * sizeof(int32_t),
+                            cudaMemcpyDeviceToHost, c->stream));
+  QMCG_CUDA(cudaMemcpyAsync(&err, c->d_err.ptr, sizeof(uint32_t), cudaMemcpyDeviceToHost, c->stream));
+  QMCG_CUDA(cudaStreamSynchronize(c->stream));
+  return map_err(err & qmcg::ERR_SPOT_NONPOSITIVE);
+}
+
+qmcg_status qmcg_backward_sweep(const double* path, int64_t path_len, const qmcg_option_spec* spec, int64_t m,
+                                uint32_t flags, double* values_out, int64_t* exercise_point) {
+  if (!path || !spec || !values_out || !exercise_point)
+    return fail(QMCG_INVALID_ARGUMENT, "qmcg_backward_sweep: null argument");
+  if (m < 1) return fail(QMCG_INVALID_ARGUMENT, "make_schedule: m must be >= 1");
+  if (!(spec->maturity > 0.0)) return fail(QMCG_INVALID_ARGUMENT, "make_schedule: maturity must be > 0");
+  qmcg_status st = validate(*spec);  // check_sweep_inputs (american.cpp:70-85)
+  if (st) return st;
+  if (spec->kind != QMCG_CALL && !(flags & QMCG_FLAG_ALLOW_PUT))
+    return fail(QMCG_INVALID_ARGUMENT, "backward_sweep: not implemented for puts; the foresight algorithm is call-only");
+  if (path_len != m + 1)
+    return fail(QMCG_INVALID_ARGUMENT, "backward_sweep: path length does not match the schedule point count");
+  const int kind = spec->kind;
+  const double K = spec->strike;
+  const double dt = spec->maturity / static_cast<double>(m + 1);
+  const double disc = std::exp(-spec->rate * dt);
+  *exercise_point = -1;
+  values_out[m + 1] = intrinsic(kind, path[m], K);  // realised payoff at T
+  // last exercise point: intrinsic vs the closed form of the final interval
+  double value;
+  {
+    const double sm = path[m - 1];
+    // bs_price validates its OptionSpec{sm, K, r, v, dt} (analytic.cpp:18-31)
+    if (!std::isfinite(sm)) return fail(QMCG_INVALID_ARGUMENT, "OptionSpec: all fields must be finite");
+    if (!(sm > 0.0)) return fail(QMCG_INVALID_ARGUMENT, "OptionSpec: spot must be > 0");
+    const double cont = bs_price_host(sm, K, spec->rate, spec->volatility, dt, kind);
+    const double intr = intrinsic(kind, sm, K);
+    value = intr > cont ? intr : cont;
+    values_out[m] = value;
+    if (intr > cont) *exercise_point = m;
+  }
+  for (int64_t i = m - 1; i >= 0; --i) {  // i = 0: the spot (immediate exercise)
+    const double si = i >= 1 ? path[i - 1] : spec->spot;
+    const double cont = value * disc;
+    const double intr = intrinsic(kind, si, K);
+    value = intr > cont ? intr : cont;
+    values_out[i] = value;
+    if (intr > cont) *exercise_point = i;  // walking backward: the last write is the earliest point
+  }
+  return QMCG_OK;
+}

@@ -101,6 +101,66 @@ PricingResult mc_european_price(const OptionSpec& spec, Index n_paths, std::uint
   return out;
 }
 
+ExerciseSchedule make_schedule(Index m, double maturity) {
+  if (m < 1) throw std::invalid_argument("make_schedule: m must be >= 1");
+  if (!(maturity > 0.0)) throw std::invalid_argument("make_schedule: maturity must be > 0");
+  ExerciseSchedule s;
+  s.m = m;
+  s.maturity = maturity;
+  s.dt = maturity / static_cast<double>(m + 1);
+  s.times.resize(static_cast<std::size_t>(m) + 1);
+  for (Index i = 0; i < m; ++i) s.times[static_cast<std::size_t>(i)] = static_cast<double>(i + 1) * s.dt;
+  s.times[static_cast<std::size_t>(m)] = maturity;
+  return s;
+}
+
+namespace {
+void check_schedule(const ExerciseSchedule& schedule, const char* who) {
+  if (schedule.m < 1 || schedule.times.size() != static_cast<std::size_t>(schedule.m) + 1)
+    throw std::invalid_argument(std::string(who) + ": schedule is not initialized");
+}
+}  // namespace
+
+PathBatch simulate_batch(const OptionSpec& spec, const ExerciseSchedule& schedule, Index n_paths, std::uint64_t seed,
+                         const ExecPolicy& exec) {
+  if (exec.lanes < 1) throw std::invalid_argument("parallel_for_chunks: lanes must be >= 1");
+  if (exec.chunk < 1) throw std::invalid_argument("parallel_for_chunks: chunk must be >= 1");
+  check_schedule(schedule, "simulate_batch");
+  if (schedule.maturity != spec.maturity)
+    throw std::invalid_argument("simulate_batch: schedule maturity does not match spec maturity");
+  const qmcg_option_spec cs = to_c(spec);
+  PathBatch batch;
+  // validation (incl. the 128 GiB capacity check) happens before any allocation
+  qmcg_status st = qmcg_simulate_batch(context(), &cs, schedule.m, n_paths, seed, 0u, QMCG_LAYOUT_PATH_MAJOR, nullptr);
+  if (st != QMCG_OK) rethrow(st);
+  batch.prices.resize(static_cast<std::size_t>(n_paths) * static_cast<std::size_t>(schedule.points()));
+  st = qmcg_simulate_batch(context(), &cs, schedule.m, n_paths, seed, 0u, QMCG_LAYOUT_PATH_MAJOR,
+                           batch.prices.data());
+  if (st != QMCG_OK) rethrow(st);
+  batch.n_paths = n_paths;
+  batch.spec = spec;
+  batch.schedule = schedule;
+  batch.seed = seed;
+  return batch;
+}
+
+SweepTrace backward_sweep(const double* path, Index path_len, const OptionSpec& spec,
+                          const ExerciseSchedule& schedule) {
+  check_schedule(schedule, "backward_sweep");
+  const qmcg_option_spec cs = to_c(spec);
+  SweepTrace trace;
+  trace.values.assign(static_cast<std::size_t>(schedule.m) + 2, 0.0);
+  int64_t ex = -1;
+  const qmcg_status st = qmcg_backward_sweep(path, path_len, &cs, schedule.m, 0u, trace.values.data(), &ex);
+  if (st != QMCG_OK) rethrow(st);
+  if (ex >= 0) trace.exercise_point = static_cast<Index>(ex);
+  return trace;
+}
+
+double sweep_value(const double* path, Index path_len, const OptionSpec& spec, const ExerciseSchedule& schedule) {
+  return backward_sweep(path, path_len, spec, schedule).values[0];
+}
+
 namespace b200 {
 
 PricingResult price_american_put_extension(const OptionSpec& spec, Index m, Index n_paths, std::uint64_t seed) {

@@ -1513,6 +1513,122 @@ cudaError_t launch_uniforms(const uint32_t* perm_row, int64_t count, DimParam dp
   return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------------------
+// Path matrix and per-path sweep (reference simulate_batch, path_engine.cpp:124-152,
+// and sweep_impl with its trace recorder, american.cpp:19-68). Not on the pricing
+// path (K2 never materialises paths); these serve the diagnostics that need them.
+// ---------------------------------------------------------------------------
+namespace {
+// prices[k][p] (point-major, coalesced stores): S at t_1..t_m, T from
+// s = s * exp(a + bsd * z) with the reference's operation order (gbm_step,
+// path_engine.hpp:51-56: drift and diffusion rounded separately, no FMA).
+__global__ void path_matrix_kernel(const uint32_t* __restrict__ table, int64_t ld, const DimParam* __restrict__ dims,
+                                   const double* __restrict__ sc, const double* __restrict__ nc, int64_t n,
+                                   int points, double s0, double a, double bsd, double* __restrict__ out,
+                                   uint32_t* err) {
+  const int64_t p = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  double s = s0;
+  uint32_t e = 0;
+  for (int k = 0; k < points; ++k) {
+    const DimParam dp = dims[k];
+    const double z = moro_full(halton(table[k * ld + p], dp, sc, nc));  // table entry = perm + 1
+    if (!(s > 0.0)) e |= ERR_SPOT_NONPOSITIVE;  // gbm_step's s_prev check
+    s = __dmul_rn(s, exp(__dadd_rn(a, __dmul_rn(bsd, z))));
+    __stcs(out + k * n + p, s);
+  }
+  if (e) atomicOr(err, e);
+}
+
+// 32x32 tiled transpose [rows][cols] -> [cols][rows] (point-major -> the
+// reference's path-major PathBatch::prices).
+__global__ void transpose_kernel(const double* __restrict__ in, int64_t rows, int64_t cols,
+                                 double* __restrict__ out) {
+  __shared__ double tile[32][33];
+  const int64_t c0 = static_cast<int64_t>(blockIdx.x) * 32, r0 = static_cast<int64_t>(blockIdx.y) * 32;
+  for (int j = threadIdx.y; j < 32; j += blockDim.y) {
+    const int64_t r = r0 + j, c = c0 + threadIdx.x;
+    if (r < rows && c < cols) tile[j][threadIdx.x] = in[r * cols + c];
+  }
+  __syncthreads();
+  for (int j = threadIdx.y; j < 32; j += blockDim.y) {
+    const int64_t c = c0 + j, r = r0 + threadIdx.x;
+    if (r < rows && c < cols) out[c * rows + r] = tile[threadIdx.x][j];
+  }
+}
+
+__device__ double bs_price_dev(double s, double x, double r, double v, double t, int kind) {
+  // bs_price (analytic.cpp:102-124) for t > 0
+  if (v == 0.0) {
+    const double fwd = s * exp(r * t);
+    const double iv = kind == 0 ? fwd - x : x - fwd;
+    return exp(-r * t) * (iv > 0.0 ? iv : 0.0);
+  }
+  const double vst = __dmul_rn(v, sqrt(t));
+  const double d1 = __ddiv_rn(__dadd_rn(log(__ddiv_rn(s, x)), __dmul_rn(__dadd_rn(r, __dmul_rn(__dmul_rn(0.5, v), v)), t)),
+                              vst);
+  const double d2 = __dadd_rn(d1, -vst);
+  const double disc = exp(-r * t);
+  const double price = kind == 0 ? __dadd_rn(__dmul_rn(s, cnd_dev(d1)), -__dmul_rn(__dmul_rn(x, disc), cnd_dev(d2)))
+                                 : __dadd_rn(__dmul_rn(__dmul_rn(x, disc), cnd_dev(-d2)), -__dmul_rn(s, cnd_dev(-d1)));
+  return price > 0.0 ? price : 0.0;
+}
+
+// One thread per path over the point-major matrix: the reference's backward
+// recursion with its rounding (value * disc per point), the t_0 value and the
+// earliest exercise point (the last index written with intrinsic > continuation).
+__global__ void sweep_kernel(const double* __restrict__ prices, int64_t n, int m, double spot, double strike,
+                             double rate, double vol, double dt, double disc, int kind, double* __restrict__ values,
+                             int32_t* __restrict__ exercise) {
+  const int64_t p = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  auto intrinsic = [&](double s) {
+    const double d = kind == 0 ? s - strike : strike - s;
+    return d > 0.0 ? d : 0.0;
+  };
+  int32_t ex = -1;
+  double s = prices[static_cast<int64_t>(m - 1) * n + p];
+  double cont = bs_price_dev(s, strike, rate, vol, dt, kind);
+  double intr = intrinsic(s);
+  double value = intr > cont ? intr : cont;
+  if (intr > cont) ex = m;
+  for (int i = m - 1; i >= 1; --i) {
+    s = prices[static_cast<int64_t>(i - 1) * n + p];
+    cont = __dmul_rn(value, disc);
+    intr = intrinsic(s);
+    value = intr > cont ? intr : cont;
+    if (intr > cont) ex = i;
+  }
+  cont = __dmul_rn(value, disc);
+  intr = intrinsic(spot);
+  value = intr > cont ? intr : cont;
+  if (intr > cont) ex = 0;
+  values[p] = value;
+  exercise[p] = ex;
+}
+}  // namespace
+
+cudaError_t launch_path_matrix(const uint32_t* table, int64_t ld, const DimParam* dims, const double* sc,
+                               const double* nc, int64_t n, int points, double s0, double a, double bsd, double* out,
+                               uint32_t* err, cudaStream_t s) {
+  path_matrix_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(table, ld, dims, sc, nc, n, points, s0,
+                                                                             a, bsd, out, err);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_transpose(const double* in, int64_t rows, int64_t cols, double* out, cudaStream_t s) {
+  const dim3 grid(static_cast<unsigned>((cols + 31) / 32), static_cast<unsigned>((rows + 31) / 32));
+  transpose_kernel<<<grid, dim3(32, 8), 0, s>>>(in, rows, cols, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_sweep(const double* prices, int64_t n, int m, double spot, double strike, double rate, double vol,
+                         double dt, double disc, int kind, double* values, int32_t* exercise, cudaStream_t s) {
+  sweep_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(prices, n, m, spot, strike, rate, vol, dt, disc,
+                                                                       kind, values, exercise);
+  return cudaGetLastError();
+}
+
 namespace {
 struct PermScratchLayout {
   size_t keys, vals, skeys, svals, F, cursor, temp, temp_bytes, total;

@@ -117,6 +117,12 @@ cudaError_t launch_price(const PriceParams& P, cudaStream_t s);
 // K1: Fisher-Yates permutation of length n for LCG seed `seed64` into out[0..n).
 // scratch must hold perm_scratch_bytes(n) bytes.
 size_t perm_scratch_bytes(int64_t n);
+cudaError_t launch_path_matrix(const uint32_t* table, int64_t ld, const DimParam* dims, const double* sc,
+                               const double* nc, int64_t n, int points, double s0, double a, double bsd, double* out,
+                               uint32_t* err, cudaStream_t s);
+cudaError_t launch_transpose(const double* in, int64_t rows, int64_t cols, double* out, cudaStream_t s);
+cudaError_t launch_sweep(const double* prices, int64_t n, int m, double spot, double strike, double rate, double vol,
+                         double dt, double disc, int kind, double* values, int32_t* exercise, cudaStream_t s);
 cudaError_t launch_perm_build(uint64_t seed64, int64_t n, uint32_t* out, void* scratch,
                               size_t scratch_bytes, cudaStream_t s, int* launches, uint32_t add);
 // Copy columns [c0, c1) of a freshly built permutation into a table row.

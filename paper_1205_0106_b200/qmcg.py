@@ -40,7 +40,8 @@ EXPORTS = (
     "qmcg_combine_nodes", "qmcg_warm", "qmcg_clear_cache", "qmcg_permutation", "qmcg_uniforms",
     "qmcg_normals", "qmcg_normal_table", "qmcg_path_values", "qmcg_time_device", "qmcg_time_perm_build",
     "qmcg_last_launch_count", "qmcg_get_stream", "qmcg_fp64_peak", "qmcg_set_table_budget",
-    "qmcg_last_window_count", "qmcg_price_american_nodes",
+    "qmcg_last_window_count", "qmcg_price_american_nodes", "qmcg_simulate_batch", "qmcg_sweep_batch",
+    "qmcg_backward_sweep",
 )
 
 
@@ -125,6 +126,9 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
         L.qmcg_warm.argtypes = [P, I64, U64, I64]
         L.qmcg_clear_cache.argtypes = [P]
         L.qmcg_set_table_budget.argtypes = [P, U64]
+        L.qmcg_simulate_batch.argtypes = [P, C.POINTER(_CSpec), I64, I64, U64, U32, C.c_int, P]
+        L.qmcg_sweep_batch.argtypes = [P, C.POINTER(_CSpec), I64, I64, U64, U32, P, P]
+        L.qmcg_backward_sweep.argtypes = [P, I64, C.POINTER(_CSpec), I64, U32, P, C.POINTER(I64)]
         L.qmcg_last_window_count.argtypes = [P]
         L.qmcg_last_window_count.restype = I64
         L.qmcg_permutation.argtypes = [P, I64, U64, P]
@@ -244,6 +248,28 @@ class Context:
                                                     int(node_count), out.ctypes.data_as(C.POINTER(C.c_double))))
         return out
 
+    # -- path matrix and sweeps (reference simulate_batch / backward_sweep) --
+    def simulate_batch(self, spec: OptionSpec, m: int, n_paths: int, seed: int,
+                       point_major: bool = False) -> np.ndarray:
+        """simulate_batch(spec, make_schedule(m, T), n_paths, seed).prices (path_engine.cpp:124-152):
+        (n_paths, m+1) like the reference's row-major matrix, or (m+1, n_paths) with point_major."""
+        s = _cspec(spec)
+        _check(self._lib.qmcg_simulate_batch(None, C.byref(s), int(m), int(n_paths), int(seed), 0, 0, None))
+        shape = (int(m) + 1, int(n_paths)) if point_major else (int(n_paths), int(m) + 1)
+        out = np.zeros(shape, dtype=np.float64)
+        _check(self._lib.qmcg_simulate_batch(self._h, C.byref(s), int(m), int(n_paths), int(seed), 0,
+                                             1 if point_major else 0, out.ctypes.data))
+        return out
+
+    def sweep_batch(self, spec: OptionSpec, m: int, n_paths: int, seed: int, allow_put: bool = False):
+        """(t_0 values, earliest exercise points) of the reference's backward sweep over every simulated path."""
+        s = _cspec(spec)
+        vals = np.zeros(int(n_paths), dtype=np.float64)
+        ex = np.zeros(int(n_paths), dtype=np.int32)
+        _check(self._lib.qmcg_sweep_batch(self._h, C.byref(s), int(m), int(n_paths), int(seed),
+                                          _flags(allow_put), vals.ctypes.data, ex.ctypes.data))
+        return vals, ex
+
     def warm(self, n_paths: int, seed: int, dims: int) -> None:
         _check(self._lib.qmcg_warm(self._h, int(n_paths), int(seed), int(dims)))
 
@@ -321,6 +347,30 @@ def tree_node_range(n_paths: int, depth: int, node: int):
     b, e = C.c_int64(), C.c_int64()
     _check(L.qmcg_tree_node_range(int(n_paths), int(depth), int(node), C.byref(b), C.byref(e)))
     return b.value, e.value
+
+
+def backward_sweep(path, spec: OptionSpec, m: int, allow_put: bool = False):
+    """backward_sweep(path, spec, make_schedule(m, T)) (reference american.cpp:88-95), host-side:
+    returns (values[t_0..t_m, payoff at T], earliest exercise index or None)."""
+    L = load_library()
+    p = np.ascontiguousarray(path, dtype=np.float64)
+    values = np.zeros(int(m) + 2, dtype=np.float64)
+    ex = C.c_int64()
+    s = _cspec(spec)
+    _check(L.qmcg_backward_sweep(p.ctypes.data, p.size, C.byref(s), int(m), _flags(allow_put), values.ctypes.data,
+                                 C.byref(ex)))
+    return values, (None if ex.value < 0 else int(ex.value))
+
+
+def sweep_value(path, spec: OptionSpec, m: int) -> float:
+    return float(backward_sweep(path, spec, m)[0][0])
+
+
+def validate_simulation(spec: OptionSpec, m: int, n_paths: int) -> None:
+    """The reference's checks for simulate_batch (no GPU needed)."""
+    L = load_library()
+    s = _cspec(spec)
+    _check(L.qmcg_simulate_batch(None, C.byref(s), int(m), int(n_paths), 0, 0, 0, None))
 
 
 def combine_nodes(n_paths: int, depth: int, node_sums: np.ndarray):

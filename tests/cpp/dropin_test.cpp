@@ -5,7 +5,10 @@
 
 #include <cmath>
 #include <cstdio>
+#include <algorithm>
 #include <cstring>
+#include <string>
+#include <vector>
 #include <stdexcept>
 
 using qmc::ExecPolicy;
@@ -129,6 +132,44 @@ int main() {
   {
     const auto r = qmc::b200::price_american_put_extension(put, 20, 1 << 14, 42);
     CHECK(r.price > 0.0 && r.std_error > 0.0);
+  }
+  // backward_sweep / sweep_value (test_american.cpp:59-78, 94-103): hand 3-point sweep, terminal entry
+  {
+    const OptionSpec spec{100.0, 95.0, 0.0, 0.3, 1.0, OptionKind::Call};
+    const auto schedule = qmc::make_schedule(3, 1.0);
+    const std::vector<double> path{108.0, 91.0, 104.0, 97.0};
+    const double value = qmc::sweep_value(path.data(), static_cast<Index>(path.size()), spec, schedule);
+    CHECK(std::fabs(value - 13.0) <= 1e-15 * 13.0);
+    const auto trace = qmc::backward_sweep(path.data(), static_cast<Index>(path.size()), spec, schedule);
+    CHECK(trace.exercise_point.has_value() && *trace.exercise_point == 1);
+    CHECK(trace.values[0] == value);
+    const auto s2 = qmc::make_schedule(2, 1.0);
+    const std::vector<double> p2{104.0, 99.0, 117.5};
+    CHECK(qmc::backward_sweep(p2.data(), 3, kRef, s2).values.back() == 17.5);
+    CHECK_THROWS_AS(qmc::backward_sweep(p2.data(), 2, kRef, s2), std::invalid_argument);
+    CHECK_THROWS_AS(qmc::make_schedule(0, 1.0), std::invalid_argument);
+  }
+  // simulate_batch (test_path_engine.cpp:62-104): deterministic forward, lanes invariance, capacity
+  {
+    const OptionSpec spec{100.0, 100.0, 0.05, 0.0, 1.0, OptionKind::Call};
+    const auto b = qmc::simulate_batch(spec, qmc::make_schedule(1, 1.0), 1, 7, ExecPolicy{1, 16});
+    CHECK(b.prices.size() == 2);
+    CHECK(std::fabs(b(0, 0) - 100.0 * std::exp(0.025)) <= 1e-12 * b(0, 0));
+    CHECK(std::fabs(b(0, 1) - 100.0 * std::exp(0.05)) <= 1e-12 * b(0, 1));
+    const OptionSpec s5{100.0, 95.0, 0.03, 0.25, 2.0, OptionKind::Call};
+    const auto sched = qmc::make_schedule(5, 2.0);
+    const auto base = qmc::simulate_batch(s5, sched, 20000, 42, ExecPolicy{1, 4096});
+    const auto lanes8 = qmc::simulate_batch(s5, sched, 20000, 42, ExecPolicy{8, 777});
+    CHECK(base.prices == lanes8.prices);
+    CHECK(*std::min_element(base.prices.begin(), base.prices.end()) > 0.0);
+    bool threw = false;
+    try {
+      qmc::simulate_batch(kRef, qmc::make_schedule(1000, 1.0), Index{1} << 40, 1, ExecPolicy{});
+    } catch (const std::length_error& e) {
+      const std::string msg = e.what();
+      threw = msg.find("bytes") != std::string::npos && msg.find("1001") != std::string::npos;
+    }
+    CHECK(threw);
   }
   std::printf("%s (%d failures)\n", failures ? "FAILED" : "PASSED", failures);
   return failures ? 1 : 0;
