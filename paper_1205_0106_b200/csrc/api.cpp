@@ -9,6 +9,7 @@
 #include "qmcg_internal.h"
 
 #include <algorithm>
+#include <array>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -92,6 +93,12 @@ qmcg_status validate(const qmcg_option_spec& s) {
   if (!(s.maturity >= 0.0)) return fail(QMCG_INVALID_ARGUMENT, "OptionSpec: maturity must be >= 0");
   if (s.kind != QMCG_CALL && s.kind != QMCG_PUT) return fail(QMCG_INVALID_ARGUMENT, "OptionSpec: unknown kind");
   return QMCG_OK;
+}
+
+uint64_t bits_of(double x) {
+  uint64_t u;
+  std::memcpy(&u, &x, sizeof u);
+  return u;
 }
 
 double intrinsic(int kind, double s, double k) {
@@ -232,6 +239,7 @@ struct qmcg_ctx {
   DevBuf<double> d_values, d_red, d_sums;
   DevBuf<double> d_z, d_bvalues, d_bred, d_bsums;  // batch: shared normal table, per-contract values
   DevBuf<qmcg::ContractParams> d_cparams;
+  DevBuf<qmcg::GroupParams> d_groups;
   DevBuf<uint32_t> d_err, d_fullperm;
   DevBuf<char> d_permscratch;
   // streamed tables (date windows): per-path walk state carried between windows
@@ -559,6 +567,7 @@ void qmcg_destroy(qmcg_ctx* c) {
   c->d_bred.release();
   c->d_bsums.release();
   c->d_cparams.release();
+  c->d_groups.release();
   c->d_sums.release();
   c->d_err.release();
   c->d_fullperm.release();
@@ -944,11 +953,50 @@ qmcg_status qmcg_price_american_batch(qmcg_ctx* c, const qmcg_option_spec* specs
     G.path_begin = 0;
     G.path_count = n;
     G.alpha = 0.0;
-    QMCG_CUDA(qmcg::launch_gen_z(G, c->d_z.ptr, n, c->stream));
+    QMCG_CUDA(qmcg::launch_gen_z(G, c->d_z.ptr, n, c->stream, qmcg::batch_uses_prefix()));
     c->launches += 1;
     for (int k = 0; k < 2; ++k) {
       const size_t cnt = shared_idx[k].size();
       if (!cnt) continue;
+      // group the contracts that share (spot, rate, volatility, maturity): one walk per group and path
+      auto key = [&](int64_t i) {
+        const qmcg_option_spec& sp = specs[i];
+        return std::array<uint64_t, 4>{bits_of(sp.spot), bits_of(sp.rate), bits_of(sp.volatility),
+                                       bits_of(sp.maturity)};
+      };
+      std::stable_sort(shared_idx[k].begin(), shared_idx[k].end(),
+                       [&](int64_t a, int64_t b) { return key(a) < key(b); });
+      std::vector<qmcg::GroupParams> groups;
+      for (size_t j = 0; j < cnt;) {
+        size_t e = j + 1;
+        while (e < cnt && key(shared_idx[k][e]) == key(shared_idx[k][j])) ++e;
+        const PriceParams& P0 = plans[static_cast<size_t>(shared_idx[k][j])].P;
+        qmcg::GroupParams gp{};
+        gp.dpow = P0.dpow;
+        gp.X0 = P0.X0;
+        gp.b = P0.b;
+        gp.alpha = P0.alpha;
+        gp.beta = k == 0 ? P0.alpha - P0.dom_slope : P0.dom_slope;
+        gp.c0 = P0.c0;
+        gp.x0mk = P0.x0mk;
+        for (size_t t = j; t < e; ++t) {
+          const PriceParams& P = plans[static_cast<size_t>(shared_idx[k][t])].P;
+          gp.c0 = k == 0 ? std::min(gp.c0, P.c0) : std::max(gp.c0, P.c0);
+          gp.x0mk = std::min(gp.x0mk, P.x0mk);
+        }
+        gp.bs_vsqrt = P0.bs_vsqrt;
+        gp.bs_mu_t = P0.bs_mu_t;
+        gp.bs_fwd_growth = P0.bs_fwd_growth;
+        gp.bs_disc = P0.bs_disc;
+        gp.bs_v_zero = P0.bs_v_zero;
+        gp.first = static_cast<int32_t>(j);
+        gp.count = static_cast<int32_t>(e - j);
+        groups.push_back(gp);
+        j = e;
+      }
+      QMCG_CUDA(c->d_groups.reserve(groups.size()));
+      QMCG_CUDA(cudaMemcpyAsync(c->d_groups.ptr, groups.data(), groups.size() * sizeof(qmcg::GroupParams),
+                                cudaMemcpyHostToDevice, c->stream));
       std::vector<qmcg::ContractParams> cps(cnt);
       for (size_t j = 0; j < cnt; ++j) {
         const PriceParams& P = plans[static_cast<size_t>(shared_idx[k][j])].P;
@@ -966,8 +1014,9 @@ qmcg_status qmcg_price_american_batch(qmcg_ctx* c, const qmcg_option_spec* specs
       QMCG_CUDA(c->d_bred.reserve(cnt * qmcg::reduce_scratch_doubles(n)));
       QMCG_CUDA(c->d_bsums.reserve(2 * cnt));
       qmcg::BatchParams B{c->d_z.ptr, n, n, static_cast<int32_t>(m), static_cast<int32_t>(cnt), c->d_cparams.ptr,
-                          c->d_bvalues.ptr};
-      QMCG_CUDA(qmcg::launch_walk_batch(B, k, c->stream));
+                          c->d_bvalues.ptr, cps.data(), c->d_groups.ptr, static_cast<int32_t>(groups.size()), 0};
+      if (qmcg::batch_grouped()) QMCG_CUDA(qmcg::launch_walk_group(B, k, c->stream));
+      else QMCG_CUDA(qmcg::launch_walk_batch(B, k, c->stream));
       int launches = 1;
       QMCG_CUDA(qmcg::launch_pairwise_batched(c->d_bvalues.ptr, n, static_cast<int>(cnt), c->d_bred.ptr,
                                               c->d_bsums.ptr, c->stream, &launches));

@@ -17,6 +17,8 @@
 #include "qmcg_internal.h"
 
 #include <cub/device/device_radix_sort.cuh>
+#include <algorithm>
+#include <vector>
 
 #include "log_table.h"
 
@@ -231,6 +233,43 @@ __device__ __forceinline__ double moro_full(double u) {
 }
 
 // Hart CND (analytic.cpp:33-72).
+// cnd (analytic.cpp:33-72) given e = exp(-d^2 / 2) computed by the caller; the
+// divisions use the cubic-refined reciprocal (a few ulps, far inside the batch
+// parity bar) -- the continued-fraction tail (|d| >= 7.07) is common for the
+// final interval's Black-Scholes (dt = T/(m+1)).
+__device__ __forceinline__ double cnd_tail_form(double d, double e) {
+  const double x = fabs(d);
+  double tail;
+  if (x > 37.0) {
+    tail = 0.0;
+  } else if (x < 7.07106781186547) {
+    double num = 3.52624965998911e-02;
+    num = fma(num, x, 0.700383064443688);
+    num = fma(num, x, 6.37396220353165);
+    num = fma(num, x, 33.912866078383);
+    num = fma(num, x, 112.079291497871);
+    num = fma(num, x, 221.213596169931);
+    num = fma(num, x, 220.206867912376);
+    double den = 8.83883476483184e-02;
+    den = fma(den, x, 1.75566716318264);
+    den = fma(den, x, 16.064177579207);
+    den = fma(den, x, 86.7807322029461);
+    den = fma(den, x, 296.564248779674);
+    den = fma(den, x, 637.333633378831);
+    den = fma(den, x, 793.826512519948);
+    den = fma(den, x, 440.413735824752);
+    tail = e * num * rcp_nr(den);
+  } else {
+    double b = x + 0.65;
+    b = fma(4.0, rcp_nr(b), x);
+    b = fma(3.0, rcp_nr(b), x);
+    b = fma(2.0, rcp_nr(b), x);
+    b = x + rcp_nr(b);
+    tail = e * rcp_nr(b * 2.506628274631000502);
+  }
+  return d > 0.0 ? 1.0 - tail : tail;
+}
+
 __device__ double cnd_dev(double d) {
   const double x = fabs(d);
   double tail;
@@ -938,7 +977,9 @@ __global__ void __launch_bounds__(kThreads, QMCG_MINB) price_kernel(const PriceP
 // bit-exact scrambled-Halton uniform, for all dates of this block's 256 paths.
 // Same tile staging and generation as price_kernel; rows are then streamed to
 // HBM (coalesced, 2 KB per warp-row).
-template <bool SLOW>
+// PREFIX: instead of z, each path's running sum S_k = z_0 + ... + z_k (the
+// contract-independent part of the batch walk, V_k = S_k + (k+1) alpha_c).
+template <bool SLOW, bool PREFIX>
 __global__ void __launch_bounds__(kThreads, QMCG_MINB) gen_z_kernel(const PriceParams P, double* __restrict__ z,
                                                                     int64_t ldz) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -966,19 +1007,33 @@ __global__ void __launch_bounds__(kThreads, QMCG_MINB) gen_z_kernel(const PriceP
     issue_tile(P, sbase, 0, 0, col0, bytes);
     if (ntiles > 1) issue_tile(P, sbase, kTile, 1, col0, bytes);
   }
+  double run = 0.0;  // PREFIX: S of this thread's path
+  const int64_t my = P.path_begin + block_first + threadIdx.x;
   for (int k = 0; k < ntiles; ++k) {
     const int k0 = k * kTile;
     const int b = k & 1;
     mbar_wait_u32(sbase + kBarOff + b * 8, static_cast<uint32_t>((k >> 1) & 1));
-    const uint32_t zrow = sbase + kZtOff + (kZtBuffers == 2 ? b : 0) * kZtBuf + warp * kThreads * 8;
+    const uint32_t ztile = sbase + kZtOff + (kZtBuffers == 2 ? b : 0) * kZtBuf;
+    const uint32_t zrow = ztile + warp * kThreads * 8;
     if (k0 + warp < m) {
       generate_row<SLOW, false>(P, ws, k0 + warp, sbase + kPermOff + b * kPermBuf + warp * kThreads * 4, zrow, logtab,
-                         nchunks, lane, lt);
-      __syncwarp();
-      double* dst = z + static_cast<int64_t>(k0 + warp) * ldz + P.path_begin + block_first;
-      for (int ch = 0; ch < nchunks; ++ch) {
-        const int idx = ch * 32 + lane;
-        if (idx < block_paths) __stcs(dst + idx, lds_f64(zrow + idx * 8));
+                                nchunks, lane, lt);
+      if (!PREFIX) {
+        __syncwarp();
+        double* dst = z + static_cast<int64_t>(k0 + warp) * ldz + P.path_begin + block_first;
+        for (int ch = 0; ch < nchunks; ++ch) {
+          const int idx = ch * 32 + lane;
+          if (idx < block_paths) __stcs(dst + idx, lds_f64(zrow + idx * 8));
+        }
+      }
+    }
+    if (PREFIX) {
+      __syncthreads();  // the tile's rows are complete
+      if (threadIdx.x < block_paths) {
+        for (int t = 0; t < kTile && k0 + t < m; ++t) {
+          run = __dadd_rn(run, lds_f64(ztile + (t * kThreads + threadIdx.x) * 8));
+          __stcs(z + static_cast<int64_t>(k0 + t) * ldz + my, run);
+        }
       }
     }
     __syncthreads();  // perm buffer b consumed, z tile b stored
@@ -1456,21 +1511,652 @@ cudaError_t launch_dfma_probe(double* out, int blocks, int iters, cudaStream_t s
 
 cudaError_t ensure_log_table(cudaStream_t s);
 
-cudaError_t launch_gen_z(const PriceParams& P, double* z, int64_t ldz, cudaStream_t s) {
+cudaError_t launch_gen_z(const PriceParams& P, double* z, int64_t ldz, cudaStream_t s, bool prefix) {
   if (P.path_count <= 0) return cudaSuccess;
   cudaError_t e = ensure_log_table(s);
   if (e != cudaSuccess) return e;
   const int64_t blocks = (P.path_count + kThreads - 1) / kThreads;
   const bool slow = P.any_wide || P.any_clamp;
-  auto kern = slow ? gen_z_kernel<true> : gen_z_kernel<false>;
+  auto kern = prefix ? (slow ? gen_z_kernel<true, true> : gen_z_kernel<false, true>)
+                     : (slow ? gen_z_kernel<true, false> : gen_z_kernel<false, false>);
   e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmemBytes));
   if (e != cudaSuccess) return e;
   kern<<<static_cast<unsigned>(blocks), kThreads, kSmemBytes, s>>>(P, z, ldz);
   return cudaGetLastError();
 }
 
+// Batch walk over the prefix-sum table S (gen_z_kernel<*, true>): warp w of a
+// block walks kBK contracts over the block's 32-path column, so each S value is
+// loaded once per kBK contract-dates (and from L1 for the other 7 warps). Per
+// contract and date: V = S_k + (k+1) alpha (one DFMA), the record test, and
+// the dominance test -- calls: W = S_k + (k+1)(alpha - slope), a new record
+// dominates the pending one iff W_k >= W_j (S_k d^(k-j) >= S_j); puts: the
+// accumulator form of price_kernel. One vote per date covers all kBK
+// contracts; pushes go to one per-warp ring (code = date<<7 | contract<<5 | lane).
+constexpr int kBK = 4;                                  // contracts per warp
+constexpr uint32_t kBRing = 256;                        // >= 32 + 32 * kBK
+constexpr uint32_t kBKWarpBytes = kBRing * 12 + kBK * 32 * 8;
+
+template <int KIND>
+__global__ void __launch_bounds__(kBCw * 32) walk_batch_k_kernel(const BatchParams B) {
+  __shared__ __align__(16) unsigned char sm[kBCw * kBKWarpBytes];
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const unsigned lt = lanemask_lt();
+  const uint32_t ws = smem_u32(sm) + warp * kBKWarpBytes;
+  const uint32_t code_off = kBRing * 8, best_off = kBRing * 12;
+  const int64_t p = static_cast<int64_t>(blockIdx.y) * 32 + lane;
+  const bool active = p < B.n;
+  const int cbase = (blockIdx.x * kBCw + warp) * kBK;
+  if (cbase >= B.count) return;  // warp-uniform; no block barrier below
+  double al[kBK], be[kBK], c[kBK], cd[kBK];
+  double pb_[kBK], px_[kBK];  // puts: b, x0mk for the dominance bound
+  int pend[kBK];
+#pragma unroll
+  for (int kk = 0; kk < kBK; ++kk) {
+    const ContractParams& q = B.cp[min(cbase + kk, B.count - 1)];
+    al[kk] = q.alpha;
+    be[kk] = KIND == 0 ? q.alpha - q.dom_slope : q.dom_slope;
+    pb_[kk] = q.b;
+    px_[kk] = q.x0mk;
+    c[kk] = q.c0;
+    cd[kk] = KIND == 0 ? -INFINITY : 0.0;
+    pend[kk] = -1;
+    asm volatile("st.shared.u64 [%0], %1;" ::"r"(ws + best_off + (kk * 32 + lane) * 8),
+                 "l"(static_cast<unsigned long long>(__double_as_longlong(q.best0)))
+                 : "memory");
+  }
+  uint32_t rq_head = 0, rq_tail = 0;
+  __syncwarp();
+  auto eval = [&](uint32_t head, uint32_t cnt) {
+    if (static_cast<uint32_t>(lane) < cnt) {
+      const uint32_t slot = (head + lane) & (kBRing - 1);
+      const double v = lds_f64(ws + slot * 8);
+      const uint32_t code = lds_u32(ws + code_off + slot * 4);
+      const ContractParams& q = B.cp[cbase + ((code >> 5) & 3u)];
+      const double sv = exp(fma(q.b, v, q.X0));
+      double intr = KIND == 0 ? sv - q.strike : q.strike - sv;
+      intr = intr > 0.0 ? intr : 0.0;
+      const double term = intr * __ldg(q.dpow + (code >> 7) + 1);
+      asm volatile("atom.shared.max.u64 _, [%0], %1;" ::"r"(ws + best_off + (code & 127u) * 8),
+                   "l"(static_cast<unsigned long long>(__double_as_longlong(term)))
+                   : "memory");
+    }
+  };
+  const double* zc = B.z + (active ? p : 0);
+  const int m = B.m;
+  const int mrec = m - 1;
+  double kd = 0.0;
+  constexpr int kPf = 8;
+  double zbuf[kPf];
+#pragma unroll
+  for (int t = 0; t < kPf; ++t) zbuf[t] = t < mrec ? __ldg(zc + static_cast<int64_t>(t) * B.ldz) : 0.0;
+  for (int d0 = 0; d0 < mrec; d0 += kPf) {
+    double cur[kPf];
+#pragma unroll
+    for (int t = 0; t < kPf; ++t) {
+      cur[t] = zbuf[t];
+      const int dn = d0 + kPf + t;
+      zbuf[t] = dn < mrec ? __ldg(zc + static_cast<int64_t>(dn) * B.ldz) : 0.0;
+    }
+#pragma unroll
+    for (int t = 0; t < kPf; ++t) {
+      const int d = d0 + t;
+      if (d0 + kPf > mrec && d >= mrec) break;
+      kd += 1.0;
+      const double S = cur[t];
+      double V[kBK], W[kBK];
+      bool rec[kBK], push[kBK];
+      bool any = false;
+#pragma unroll
+      for (int kk = 0; kk < kBK; ++kk) {
+        V[kk] = fma(al[kk], kd, S);
+        rec[kk] = KIND == 0 ? V[kk] > c[kk] : V[kk] < c[kk];
+        if (KIND == 0) {
+          W[kk] = fma(be[kk], kd, S);
+          push[kk] = rec[kk] && !(W[kk] >= cd[kk]);
+        } else {
+          cd[kk] = __dadd_rn(cd[kk], be[kk]);
+          W[kk] = 0.0;
+          push[kk] = rec[kk] && pend[kk] >= 0 && !record_dominates<1>(V[kk], c[kk], cd[kk], pb_[kk], px_[kk]);
+        }
+        push[kk] = push[kk] && active;
+        any = any || push[kk];
+      }
+      if (__any_sync(kFull, any)) {
+#pragma unroll
+        for (int kk = 0; kk < kBK; ++kk) {
+          const unsigned pbal = __ballot_sync(kFull, push[kk]);
+          if (push[kk]) {
+            const uint32_t slot = (rq_tail + __popc(pbal & lt)) & (kBRing - 1);
+            sts_f64(ws + slot * 8, c[kk]);
+            sts_u32(ws + code_off + slot * 4,
+                    (static_cast<uint32_t>(pend[kk]) << 7) | (static_cast<uint32_t>(kk) << 5) |
+                        static_cast<uint32_t>(lane));
+          }
+          rq_tail += __popc(pbal);
+        }
+        while (rq_tail - rq_head >= 32) {
+          __syncwarp();
+          eval(rq_head, 32);
+          rq_head += 32;
+          __syncwarp();
+        }
+      }
+#pragma unroll
+      for (int kk = 0; kk < kBK; ++kk) {
+        c[kk] = rec[kk] ? V[kk] : c[kk];
+        cd[kk] = rec[kk] ? W[kk] : cd[kk];
+        pend[kk] = rec[kk] ? d : pend[kk];
+      }
+    }
+  }
+  const double Sm = __ldg(zc + static_cast<int64_t>(mrec) * B.ldz);
+  kd += 1.0;
+  // the last pending record of every (contract, path)
+#pragma unroll
+  for (int kk = 0; kk < kBK; ++kk) {
+    const bool push = active && pend[kk] >= 0;
+    const unsigned pbal = __ballot_sync(kFull, push);
+    if (push) {
+      const uint32_t slot = (rq_tail + __popc(pbal & lt)) & (kBRing - 1);
+      sts_f64(ws + slot * 8, c[kk]);
+      sts_u32(ws + code_off + slot * 4,
+              (static_cast<uint32_t>(pend[kk]) << 7) | (static_cast<uint32_t>(kk) << 5) | static_cast<uint32_t>(lane));
+    }
+    rq_tail += __popc(pbal);
+    if (rq_tail - rq_head >= 32) {
+      __syncwarp();
+      eval(rq_head, 32);
+      rq_head += 32;
+    }
+  }
+  __syncwarp();
+  while (rq_tail != rq_head) {
+    const uint32_t cnt = min(32u, rq_tail - rq_head);
+    eval(rq_head, cnt);
+    rq_head += cnt;
+    __syncwarp();
+  }
+  // date m per contract: max(intrinsic, Black-Scholes of the final interval)
+#pragma unroll 1
+  for (int kk = 0; kk < kBK; ++kk) {
+    const int ci = cbase + kk;
+    if (ci >= B.count) break;
+    const ContractParams& q = B.cp[ci];
+    const double X = fma(q.b, fma(al[kk], kd, Sm), q.X0);
+    const double sl = exp(X);
+    double cont;
+    if (q.bs_v_zero) {
+      const double fwd = sl * q.bs_fwd_growth;
+      const double iv = KIND == 0 ? fwd - q.strike : q.strike - fwd;
+      cont = q.bs_disc * (iv > 0.0 ? iv : 0.0);
+    } else {
+      const double d1 = (X - q.log_strike + q.bs_mu_t) / q.bs_vsqrt;
+      const double d2 = d1 - q.bs_vsqrt;
+      const double price = KIND == 0 ? sl * cnd_dev(d1) - q.bs_kdisc * cnd_dev(d2)
+                                     : q.bs_kdisc * cnd_dev(-d2) - sl * cnd_dev(-d1);
+      cont = price > 0.0 ? price : 0.0;
+    }
+    double intr = KIND == 0 ? sl - q.strike : q.strike - sl;
+    intr = intr > 0.0 ? intr : 0.0;
+    const double cm = intr > cont ? intr : cont;
+    const double term_m = cm * __ldg(q.dpow + m);
+    unsigned long long bb;
+    asm volatile("ld.shared.u64 %0, [%1];" : "=l"(bb) : "r"(ws + best_off + (kk * 32 + lane) * 8));
+    const double best = __longlong_as_double(static_cast<long long>(bb));
+    if (active) B.values[static_cast<int64_t>(ci) * B.n + p] = best > term_m ? best : term_m;
+  }
+}
+
+// Batch walk, contract-uniform blocks: a block walks kBU contracts of one kind
+// over 256 consecutive paths (thread = path), reading S_k once per date for all
+// kBU contracts. The contracts' walk constants are block-uniform and come from
+// the constant bank (c_bc, filled per launch chunk), so they cost no registers.
+// Blocks of the same 256 paths are adjacent in launch order (grid.x =
+// contract groups), so S is served from L2.
+constexpr int kBU = 8;
+constexpr int kBUMax = 512;  // contracts per launch chunk (constant bank)
+struct BatchConst {
+  double alpha, beta, b, x0mk;  // beta = alpha - slope (calls) or slope (puts)
+  double c0, best0, X0, strike;
+};
+__constant__ BatchConst c_bc[kBUMax];
+
+// Pushes of one date are staged per (thread, contract) with predicated stores
+// inside the unrolled contract loop; the rare evaluation (exp + discount) runs
+// outside it, so the hot loop keeps its state in fixed registers.
+constexpr uint32_t kBUStage = kBU * 12;  // per thread: kBU x {value f64} + kBU x {date u32}
+
+// Rare path, once per date with any push in the warp: compact the staged
+// (value, date) pairs of every contract into the warp's ring, then evaluate
+// full groups of 32 (exp + discount), folding each into best[contract][lane]
+// with a shared-memory max on the bits of the non-negative term.
+constexpr uint32_t kBURing = 128;
+template <int KIND>
+__device__ __noinline__ void batch_stage_pushes(const ContractParams* __restrict__ cp, unsigned pm, uint32_t stage,
+                                                uint32_t ring, uint32_t best_base, bool drain) {
+  const int lane = threadIdx.x & 31;
+  const unsigned lt = lanemask_lt();
+  uint32_t head = lds_u32(ring + kBURing * 12), tail = lds_u32(ring + kBURing * 12 + 4);
+  for (int kk = 0; kk < kBU; ++kk) {
+    const bool mine = (pm >> kk) & 1u;
+    const unsigned bal = __ballot_sync(kFull, mine);
+    if (!bal) continue;
+    if (mine) {
+      const uint32_t slot = (tail + __popc(bal & lt)) & (kBURing - 1);
+      sts_f64(ring + slot * 8, lds_f64(stage + kk * 8));
+      sts_u32(ring + kBURing * 8 + slot * 4,
+              (lds_u32(stage + kBU * 8 + kk * 4) << 8) | (static_cast<uint32_t>(kk) << 5) | static_cast<uint32_t>(lane));
+    }
+    tail += __popc(bal);
+    while (tail - head >= 32u) {
+      const uint32_t cnt = min(32u, tail - head);
+      __syncwarp();
+      if (static_cast<uint32_t>(lane) < cnt) {
+        const uint32_t slot = (head + lane) & (kBURing - 1);
+        const double v = lds_f64(ring + slot * 8);
+        const uint32_t code = lds_u32(ring + kBURing * 8 + slot * 4);
+        const ContractParams& q = cp[(code >> 5) & 7u];
+        const double sv = exp(fma(q.b, v, q.X0));
+        double intr = KIND == 0 ? sv - q.strike : q.strike - sv;
+        intr = intr > 0.0 ? intr : 0.0;
+        const double term = intr * __ldg(q.dpow + (code >> 8) + 1);
+        // best of (contract, lane of the entry): [lane][kk] layout, 8 B each
+        const uint32_t owner = best_base + (((code & 31u) * kBU + ((code >> 5) & 7u)) * 8);
+        asm volatile("atom.shared.max.u64 _, [%0], %1;" ::"r"(owner),
+                     "l"(static_cast<unsigned long long>(__double_as_longlong(term)))
+                     : "memory");
+      }
+      head += cnt;
+      __syncwarp();
+    }
+  }
+  while (drain && tail != head) {
+    const uint32_t cnt = min(32u, tail - head);
+    __syncwarp();
+    if (static_cast<uint32_t>(lane) < cnt) {
+      const uint32_t slot = (head + lane) & (kBURing - 1);
+      const double v = lds_f64(ring + slot * 8);
+      const uint32_t code = lds_u32(ring + kBURing * 8 + slot * 4);
+      const ContractParams& q = cp[(code >> 5) & 7u];
+      const double sv = exp(fma(q.b, v, q.X0));
+      double intr = KIND == 0 ? sv - q.strike : q.strike - sv;
+      intr = intr > 0.0 ? intr : 0.0;
+      const double term = intr * __ldg(q.dpow + (code >> 8) + 1);
+      const uint32_t owner = best_base + (((code & 31u) * kBU + ((code >> 5) & 7u)) * 8);
+      asm volatile("atom.shared.max.u64 _, [%0], %1;" ::"r"(owner),
+                   "l"(static_cast<unsigned long long>(__double_as_longlong(term)))
+                   : "memory");
+    }
+    head += cnt;
+    __syncwarp();
+  }
+  if (lane == 0) {
+    sts_u32(ring + kBURing * 12, head);
+    sts_u32(ring + kBURing * 12 + 4, tail);
+  }
+  __syncwarp();
+}
+
+#ifndef QMCG_BU_MINB
+#define QMCG_BU_MINB 2
+#endif
+template <int KIND>
+__global__ void __launch_bounds__(256, QMCG_BU_MINB) walk_batch_u_kernel(const BatchParams B, int chunk0) {
+  extern __shared__ __align__(16) unsigned char smu[];
+  const uint32_t stage = smem_u32(smu) + threadIdx.x * kBUStage;
+  const uint32_t bestp = smem_u32(smu) + 256 * kBUStage + threadIdx.x * (kBU * 8);
+  const uint32_t best_base = smem_u32(smu) + 256 * kBUStage + (threadIdx.x & ~31u) * (kBU * 8);
+  const uint32_t ring = smem_u32(smu) + 256 * (kBUStage + kBU * 8) + (threadIdx.x >> 5) * (kBURing * 12 + 16);
+  if ((threadIdx.x & 31) == 0) {
+    sts_u32(ring + kBURing * 12, 0u);
+    sts_u32(ring + kBURing * 12 + 4, 0u);
+  }
+  const int g0 = blockIdx.x * kBU;  // first contract of the block within the chunk
+  const int ng = min(kBU, B.count - chunk0 - g0);
+  const int64_t p = min(static_cast<int64_t>(blockIdx.y) * 256 + threadIdx.x, B.n - 1);
+  double c[kBU], cd[kBU];
+  int pend[kBU];
+#pragma unroll
+  for (int kk = 0; kk < kBU; ++kk) {
+    const BatchConst& q = c_bc[g0 + kk];
+    c[kk] = q.c0;
+    cd[kk] = KIND == 0 ? -INFINITY : 0.0;
+    pend[kk] = -1;
+    sts_f64(bestp + kk * 8, q.best0);
+  }
+  const double* zc = B.z + p;
+  const int m = B.m;
+  const int mrec = m - 1;
+  double kd = 0.0;
+  constexpr int kPf = 4;
+  double zbuf[kPf];
+#pragma unroll
+  for (int t = 0; t < kPf; ++t) zbuf[t] = __ldg(zc + static_cast<int64_t>(min(t, m - 1)) * B.ldz);
+  for (int d0 = 0; d0 < mrec; d0 += kPf) {
+    double cur[kPf];
+#pragma unroll
+    for (int t = 0; t < kPf; ++t) {
+      cur[t] = zbuf[t];
+      zbuf[t] = __ldg(zc + static_cast<int64_t>(min(d0 + kPf + t, m - 1)) * B.ldz);
+    }
+#pragma unroll
+    for (int t = 0; t < kPf; ++t) {
+      const int d = d0 + t;
+      if (d >= mrec) break;
+      kd += 1.0;
+      const double S = cur[t];
+      unsigned pm = 0;
+#pragma unroll
+      for (int kk = 0; kk < kBU; ++kk) {
+        const BatchConst& q = c_bc[g0 + kk];
+        if (KIND == 0) {
+          // predicated form (no branches): V = S + kd alpha, W = S + kd beta;
+          // rec = V > c; push = rec && W < cd (cd = W of the pending record,
+          // -inf when none); pushes stage (c, pend) for the deferred evaluation
+          asm volatile(
+              "{\n .reg .pred r, pu;\n .reg .f64 v, w;\n .reg .b32 t;\n"
+              " fma.rn.f64 v, %4, %5, %6;\n fma.rn.f64 w, %7, %5, %6;\n"
+              " setp.gt.f64 r, v, %0;\n setp.lt.and.f64 pu, w, %1, r;\n"
+              " @pu st.shared.f64 [%8], %0;\n @pu st.shared.u32 [%9], %2;\n"
+              " selp.f64 %0, v, %0, r;\n selp.f64 %1, w, %1, r;\n selp.b32 %2, %10, %2, r;\n"
+              " selp.b32 t, %11, 0, pu;\n or.b32 %3, %3, t;\n}"
+              : "+d"(c[kk]), "+d"(cd[kk]), "+r"(pend[kk]), "+r"(pm)
+              : "d"(q.alpha), "d"(kd), "d"(S), "d"(q.beta), "r"(stage + kk * 8), "r"(stage + kBU * 8 + kk * 4),
+                "r"(d), "r"(1u << kk)
+              : "memory");
+          continue;
+        }
+        const double V = fma(q.alpha, kd, S);
+        const bool rec = KIND == 0 ? V > c[kk] : V < c[kk];
+        double nd;
+        bool push;
+        if (KIND == 0) {
+          nd = 0.0;
+          push = false;
+        } else {
+          cd[kk] = __dadd_rn(cd[kk], q.beta);
+          nd = 0.0;
+          push = rec && pend[kk] >= 0 && !record_dominates<1>(V, c[kk], cd[kk], q.b, q.x0mk);
+        }
+        if (push) {
+          sts_f64(stage + kk * 8, c[kk]);
+          sts_u32(stage + kBU * 8 + kk * 4, static_cast<uint32_t>(pend[kk]));
+        }
+        pm |= push ? (1u << kk) : 0u;
+        c[kk] = rec ? V : c[kk];
+        cd[kk] = rec ? nd : cd[kk];
+        pend[kk] = rec ? d : pend[kk];
+      }
+      if (__any_sync(kFull, pm != 0)) batch_stage_pushes<KIND>(B.cp + chunk0 + g0, pm, stage, ring, best_base, false);
+    }
+  }
+  {  // the last pending record of every contract
+    unsigned pm = 0;
+#pragma unroll
+    for (int kk = 0; kk < kBU; ++kk) {
+      if (pend[kk] >= 0) {
+        sts_f64(stage + kk * 8, c[kk]);
+        sts_u32(stage + kBU * 8 + kk * 4, static_cast<uint32_t>(pend[kk]));
+        pm |= 1u << kk;
+      }
+    }
+    pm &= (1u << ng) - 1u;
+    batch_stage_pushes<KIND>(B.cp + chunk0 + g0, pm, stage, ring, best_base, true);
+  }
+  const double Sm = __ldg(zc + static_cast<int64_t>(mrec) * B.ldz);
+  kd += 1.0;
+  const int64_t pw = static_cast<int64_t>(blockIdx.y) * 256 + threadIdx.x;
+#pragma unroll 1
+  for (int kk = 0; kk < ng; ++kk) {  // date m per contract
+    const ContractParams& q = B.cp[chunk0 + g0 + kk];
+    const double X = fma(q.b, fma(c_bc[g0 + kk].alpha, kd, Sm), q.X0);
+    const double sl = exp(X);
+    double cont;
+    if (q.bs_v_zero) {
+      const double fwd = sl * q.bs_fwd_growth;
+      const double iv = KIND == 0 ? fwd - q.strike : q.strike - fwd;
+      cont = q.bs_disc * (iv > 0.0 ? iv : 0.0);
+    } else {
+      const double d1 = (X - q.log_strike + q.bs_mu_t) / q.bs_vsqrt;
+      const double d2 = d1 - q.bs_vsqrt;
+      const double price = KIND == 0 ? sl * cnd_dev(d1) - q.bs_kdisc * cnd_dev(d2)
+                                     : q.bs_kdisc * cnd_dev(-d2) - sl * cnd_dev(-d1);
+      cont = price > 0.0 ? price : 0.0;
+    }
+    double intr = KIND == 0 ? sl - q.strike : q.strike - sl;
+    intr = intr > 0.0 ? intr : 0.0;
+    const double cm = intr > cont ? intr : cont;
+    const double term_m = cm * __ldg(q.dpow + m);
+    const double best = lds_f64(bestp + kk * 8);
+    if (pw < B.n) B.values[static_cast<int64_t>(chunk0 + g0 + kk) * B.n + pw] = best > term_m ? best : term_m;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K4 grouped walk. Contracts of one kind that share (spot, rate, volatility,
+// maturity) follow the same log-price walk V_k = S_k + (k+1) alpha and differ
+// only in the strike. For calls the dominance key W = S_k + (k+1)(alpha - slope)
+// does not involve the strike, and a record k dominating j (W_k >= W_j) gives
+// d^k (S_k - K) >= d^j (S_j - K) for every K; for puts the bound test is taken
+// at the largest strike, which makes it valid for all smaller ones. So one walk
+// per (group, path), started at the least restrictive threshold of the group,
+// yields a candidate set containing every strike's surviving records, and each
+// strike's value is max(I_0, max_candidates d^j (S_j - K)^+, d^m c_m(K)) --
+// the same maximum the single-contract sweep computes (extra candidates are
+// legitimate exercise values, so they never exceed it).
+// ---------------------------------------------------------------------------
+constexpr int kGThreads = 128;
+#ifndef QMCG_G_MINB
+#define QMCG_G_MINB 6
+#endif
+constexpr int kGCap = 12;  // candidates per path kept in shared memory before a flush
+
+template <int KIND>
+__device__ __noinline__ void group_flush(const ContractParams* __restrict__ cp, const GroupParams* __restrict__ g,
+                                         int cnt, uint32_t cs, uint32_t cj, double* __restrict__ values, int64_t n,
+                                         int64_t p, bool merge) {
+  // candidates -> (S_j, d^(j+1)) in place, then fold into every strike's value
+  for (int i = 0; i < cnt; ++i) {
+    const double v = lds_f64(cs + i * 8);
+    const uint32_t j = lds_u32(cj + i * 4);
+    sts_f64(cs + i * 8, exp(fma(g->b, v, g->X0)));
+    sts_f64(cj + kGCap * 4 + i * 8, __ldg(g->dpow + j + 1));
+  }
+  for (int s = 0; s < g->count; ++s) {
+    const ContractParams& q = cp[g->first + s];
+    double best = merge ? values[static_cast<int64_t>(g->first + s) * n + p] : q.best0;
+    for (int i = 0; i < cnt; ++i) {
+      const double sv = lds_f64(cs + i * 8);
+      double intr = KIND == 0 ? sv - q.strike : q.strike - sv;
+      intr = intr > 0.0 ? intr : 0.0;
+      const double term = intr * lds_f64(cj + kGCap * 4 + i * 8);
+      best = term > best ? term : best;
+    }
+    values[static_cast<int64_t>(g->first + s) * n + p] = best;
+  }
+}
+
+template <int KIND>
+__global__ void __launch_bounds__(kGThreads, QMCG_G_MINB) walk_group_kernel(const BatchParams B) {
+  extern __shared__ __align__(16) unsigned char smg[];
+  const GroupParams* g = B.groups + blockIdx.x;
+  const int64_t pw = static_cast<int64_t>(blockIdx.y) * kGThreads + threadIdx.x;
+  const int64_t p = min(pw, B.n - 1);
+  // per thread: kGCap candidate values (f64), kGCap dates (u32), then kGCap d^(j+1) (f64)
+  const uint32_t cs = smem_u32(smg) + threadIdx.x * (kGCap * 20);
+  const uint32_t cj = cs + kGCap * 8;
+  const double alpha = g->alpha, beta = g->beta, gb = g->b, gx = g->x0mk;
+  double c = g->c0;
+  double cd = KIND == 0 ? -INFINITY : 0.0;
+  int pend = -1;
+  int cnt = 0;
+  bool flushed = false;
+  const double* zc = B.z + p;
+  const int m = B.m;
+  const int mrec = m - 1;
+  double kd = 0.0;
+  constexpr int kPf = 8;
+  double zbuf[kPf];
+  // the table has 8 spare rows past m - 1, so the prefetch needs no bound
+  const double* zp = zc;
+  const int64_t ldz = B.ldz;
+#pragma unroll
+  for (int t = 0; t < kPf; ++t) zbuf[t] = __ldg(zp + t * ldz);
+  for (int d0 = 0; d0 < mrec; d0 += kPf) {
+    double cur[kPf];
+    zp += kPf * ldz;
+#pragma unroll
+    for (int t = 0; t < kPf; ++t) {
+      cur[t] = zbuf[t];
+      zbuf[t] = __ldg(zp + t * ldz);
+    }
+#pragma unroll
+    for (int t = 0; t < kPf; ++t) {
+      const int d = d0 + t;
+      if (d0 + kPf > mrec && d >= mrec) break;
+      kd += 1.0;
+      const double S = cur[t];
+      if (KIND == 0) {
+        // rec = V > c; push = rec && W < cd; @push append (c, pend); then replace the pending record
+        asm volatile(
+            "{\n .reg .pred r, pu;\n .reg .f64 v, w;\n .reg .b32 a;\n"
+            " fma.rn.f64 v, %4, %5, %6;\n fma.rn.f64 w, %7, %5, %6;\n"
+            " setp.gt.f64 r, v, %0;\n setp.lt.and.f64 pu, w, %1, r;\n"
+            " mad.lo.u32 a, %3, 8, %8;\n @pu st.shared.f64 [a], %0;\n"
+            " mad.lo.u32 a, %3, 4, %9;\n @pu st.shared.u32 [a], %2;\n @pu add.u32 %3, %3, 1;\n"
+            " selp.f64 %0, v, %0, r;\n selp.f64 %1, w, %1, r;\n selp.b32 %2, %10, %2, r;\n}"
+            : "+d"(c), "+d"(cd), "+r"(pend), "+r"(cnt)
+            : "d"(alpha), "d"(kd), "d"(S), "d"(beta), "r"(cs), "r"(cj), "r"(d)
+            : "memory");
+      } else {
+        const double V = fma(alpha, kd, S);
+        const bool rec = V < c;
+        cd = __dadd_rn(cd, beta);
+        const bool push = rec && pend >= 0 && !record_dominates<1>(V, c, cd, gb, gx);
+        if (push) {
+          sts_f64(cs + cnt * 8, c);
+          sts_u32(cj + cnt * 4, static_cast<uint32_t>(pend));
+        }
+        cnt += push ? 1 : 0;
+        c = rec ? V : c;
+        cd = rec ? 0.0 : cd;
+        pend = rec ? d : pend;
+      }
+      if (__any_sync(kFull, cnt >= kGCap - 1)) {  // rare: keep room for the next candidate
+        if (cnt >= kGCap - 1) {
+          group_flush<KIND>(B.cp, g, cnt, cs, cj, B.values, B.n, p, flushed);
+          flushed = true;
+          cnt = 0;
+        }
+      }
+    }
+  }
+  if (pend >= 0) {  // the last pending record
+    sts_f64(cs + cnt * 8, c);
+    sts_u32(cj + cnt * 4, static_cast<uint32_t>(pend));
+    ++cnt;
+  }
+  // candidates -> S_j and d^(j+1) (shared by every strike of the group)
+  for (int i = 0; i < cnt; ++i) {
+    const double v = lds_f64(cs + i * 8);
+    const uint32_t j = lds_u32(cj + i * 4);
+    sts_f64(cs + i * 8, exp(fma(gb, v, g->X0)));
+    sts_f64(cj + kGCap * 4 + i * 8, __ldg(g->dpow + j + 1));
+  }
+  kd += 1.0;
+  const double X = fma(gb, fma(alpha, kd, __ldg(zc + static_cast<int64_t>(mrec) * B.ldz)), g->X0);
+  const double sl = exp(X);
+  const double dm = __ldg(g->dpow + m);
+  const double inv_vst = 1.0 / g->bs_vsqrt;
+#pragma unroll 1
+  for (int s = 0; s < g->count; ++s) {
+    const ContractParams& q = B.cp[g->first + s];
+    double best = flushed ? B.values[static_cast<int64_t>(g->first + s) * B.n + p] : q.best0;
+    for (int i = 0; i < cnt; ++i) {
+      const double sv = lds_f64(cs + i * 8);
+      double intr = KIND == 0 ? sv - q.strike : q.strike - sv;
+      intr = intr > 0.0 ? intr : 0.0;
+      const double term = intr * lds_f64(cj + kGCap * 4 + i * 8);
+      best = term > best ? term : best;
+    }
+    // date m: max(intrinsic, Black-Scholes of the final interval), american.cpp:43-52;
+    // one exp per strike: phi(d2) = phi(d1) S / (K e^{-r dt})
+    double cont;
+    if (g->bs_v_zero) {
+      const double fwd = sl * g->bs_fwd_growth;
+      const double iv = KIND == 0 ? fwd - q.strike : q.strike - fwd;
+      cont = g->bs_disc * (iv > 0.0 ? iv : 0.0);
+    } else {
+      const double d1 = (X - q.log_strike + g->bs_mu_t) * inv_vst;
+      const double d2 = d1 - g->bs_vsqrt;
+      const double e1 = exp(-0.5 * d1 * d1);
+      const double e2 = e1 * (sl * rcp_nr(q.bs_kdisc));
+      const double price = KIND == 0 ? sl * cnd_tail_form(d1, e1) - q.bs_kdisc * cnd_tail_form(d2, e2)
+                                     : q.bs_kdisc * cnd_tail_form(-d2, e2) - sl * cnd_tail_form(-d1, e1);
+      cont = price > 0.0 ? price : 0.0;
+    }
+    double intr = KIND == 0 ? sl - q.strike : q.strike - sl;
+    intr = intr > 0.0 ? intr : 0.0;
+    const double cm = intr > cont ? intr : cont;
+    const double term_m = cm * dm;
+    if (pw < B.n) B.values[static_cast<int64_t>(g->first + s) * B.n + pw] = best > term_m ? best : term_m;
+  }
+}
+
+cudaError_t launch_walk_group(const BatchParams& B, int kind, cudaStream_t s) {
+  if (B.n_groups <= 0 || B.n <= 0) return cudaSuccess;
+  const dim3 grid(static_cast<unsigned>(B.n_groups), static_cast<unsigned>((B.n + kGThreads - 1) / kGThreads));
+  const size_t smem = kGThreads * kGCap * 20;
+  auto kern = kind == 0 ? walk_group_kernel<0> : walk_group_kernel<1>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  if (e != cudaSuccess) return e;
+  kern<<<grid, kGThreads, smem, s>>>(B);
+  return cudaGetLastError();
+}
+
+#ifndef QMCG_BATCH_K
+#define QMCG_BATCH_K 3  // 3: grouped walk; 2: contract-uniform blocks; 1: contracts per warp; 0: one per warp
+#endif
+
+bool batch_uses_prefix() { return QMCG_BATCH_K != 0; }
+bool batch_grouped() { return QMCG_BATCH_K == 3; }
+
 cudaError_t launch_walk_batch(const BatchParams& B, int kind, cudaStream_t s) {
   if (B.count <= 0 || B.n <= 0) return cudaSuccess;
+  if (QMCG_BATCH_K == 2) {
+    std::vector<BatchConst> bc;
+    for (int chunk0 = 0; chunk0 < B.count; chunk0 += kBUMax) {
+      const int cnt = std::min(kBUMax, B.count - chunk0);
+      bc.resize(static_cast<size_t>(cnt));
+      for (int j = 0; j < cnt; ++j) {
+        const ContractParams& q = B.cp_host[chunk0 + j];
+        bc[static_cast<size_t>(j)] = BatchConst{q.alpha, kind == 0 ? q.alpha - q.dom_slope : q.dom_slope, q.b, q.x0mk,
+                                                q.c0, q.best0, q.X0, q.strike};
+      }
+      cudaError_t e = cudaMemcpyToSymbolAsync(c_bc, bc.data(), cnt * sizeof(BatchConst), 0, cudaMemcpyHostToDevice, s);
+      if (e != cudaSuccess) return e;
+      const dim3 grid(static_cast<unsigned>((cnt + kBU - 1) / kBU), static_cast<unsigned>((B.n + 255) / 256));
+      const size_t smem = 256 * (kBUStage + kBU * 8) + 8 * (kBURing * 12 + 16);
+      auto kern = kind == 0 ? walk_batch_u_kernel<0> : walk_batch_u_kernel<1>;
+      e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+      if (e != cudaSuccess) return e;
+      e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+      if (e != cudaSuccess) return e;
+      kern<<<grid, 256, smem, s>>>(B, chunk0);
+      e = cudaGetLastError();
+      if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+  }
+  if (QMCG_BATCH_K) {
+    const dim3 grid(static_cast<unsigned>((B.count + kBCw * kBK - 1) / (kBCw * kBK)),
+                    static_cast<unsigned>((B.n + 31) / 32));
+    if (kind == 0) walk_batch_k_kernel<0><<<grid, kBCw * 32, 0, s>>>(B);
+    else walk_batch_k_kernel<1><<<grid, kBCw * 32, 0, s>>>(B);
+    return cudaGetLastError();
+  }
   const dim3 grid(static_cast<unsigned>((B.count + kBCw - 1) / kBCw), static_cast<unsigned>((B.n + 31) / 32));
   if (kind == 0) walk_batch_kernel<0><<<grid, kBCw * 32, 0, s>>>(B);
   else walk_batch_kernel<1><<<grid, kBCw * 32, 0, s>>>(B);

@@ -92,6 +92,18 @@ struct ContractParams {
 };
 
 // Batch pricing over a shared normal table z[m][ldz] (z = Moro normal, no drift).
+// A batch group: contracts of one kind sharing (spot, rate, volatility,
+// maturity) -- hence the same log-price walk -- and differing in the strike.
+struct GroupParams {
+  const double* dpow;
+  double X0, b, alpha;
+  double beta;     // calls: alpha - dom_slope (dominance key slope); puts: dom_slope (accumulator step)
+  double c0;       // union start threshold: calls min over strikes, puts max
+  double x0mk;     // puts: 1 + X0 - log(max strike) (dominance for every strike of the group)
+  double bs_vsqrt, bs_mu_t, bs_fwd_growth, bs_disc;
+  int32_t bs_v_zero, first, count, pad;  // contracts [first, first + count) of the kind's array
+};
+
 struct BatchParams {
   const double* z;
   int64_t ldz;
@@ -100,12 +112,18 @@ struct BatchParams {
   int32_t count;              // contracts in this launch (all of one kind)
   const ContractParams* cp;   // count entries
   double* values;             // [count][n]
+  const ContractParams* cp_host;  // the same, host copy (walk constants go to the constant bank)
+  const GroupParams* groups;      // grouped walk: one walk per (group, path)
+  int32_t n_groups, pad;
 };
 
 // ---- launchers (kernels.cu) ----
 // Generation only: the QMC normal table z[d][p] (d < m, p in [path_begin, +path_count)) of the
 // context's permutation table (PriceParams fields perm/ld/col_begin/dims/... ; alpha ignored).
-cudaError_t launch_gen_z(const PriceParams& P, double* z, int64_t ldz, cudaStream_t s);
+bool batch_uses_prefix();
+bool batch_grouped();
+cudaError_t launch_walk_group(const BatchParams& B, int kind, cudaStream_t s);  // the batch walk reads prefix sums S (gen_z prefix mode)
+cudaError_t launch_gen_z(const PriceParams& P, double* z, int64_t ldz, cudaStream_t s, bool prefix = false);
 cudaError_t launch_walk_batch(const BatchParams& B, int kind, cudaStream_t s);
 cudaError_t launch_european(const uint32_t* perm_row, int64_t count, DimParam dp, const double* sc, const double* nc,
                             double s0, double a, double bsd, double strike, double disc, int kind, double* out,
