@@ -153,6 +153,23 @@ def test_batch_matches_single(ctx, qmcg):
         assert abs(one.std_error - r.std_error) <= 1e-9 * one.std_error + 1e-12
 
 
+@pytest.mark.parametrize("rate,vol", [(0.05, 0.2), (0.15, 0.05), (0.0, 0.3)])
+def test_batch_grouped_strikes(ctx, qmcg, rate, vol):
+    """The grouped batch walk: many strikes of both kinds sharing (spot, rate, vol, maturity), plus a
+    second spot, against single calls. (0.15, 0.05) makes records rarely dominate, so candidate
+    lists overflow the per-path buffer and exercise the flush."""
+    specs = [spec_of(qmcg, (spot, k, rate, vol, 1.5), kind=kind)
+             for spot in (100.0, 97.0) for kind in (0, 1) for k in (70.0, 85.0, 95.0, 100.0, 104.0, 120.0, 150.0)]
+    m, n = 128, 4096 + 96
+    batch = ctx.price_american_batch(specs, m, n, 7, allow_put=True)
+    for s, r in zip(specs, batch):
+        one = ctx.price_american(s, m, n, 7, allow_put=True)
+        # 1e-12 relative; deep-tail prices (~1e-200, carried by exp(-d^2/2) at |d| ~ 37) differ
+        # in the exponent's rounding, so an absolute floor of 1e-15 x spot applies
+        assert abs(one.price - r.price) <= 1e-12 * one.price + 1e-15 * s.spot, (s, one.price, r.price)
+        assert abs(one.std_error - r.std_error) <= 1e-9 * one.std_error + 1e-15 * s.spot
+
+
 def test_config4_grid_vs_oracle(ctx, qmcg, oracle_lib):
     """Config 4's contract grid (32 strikes x 32 vols, calls for even i+j) at a reduced size:
     every contract of an 8 x 8 sub-grid against the C restatement."""
