@@ -339,6 +339,16 @@ def main():
                             "frac": 4.0 * path_steps / (kernel_ms * 1e-3) / 1e9 / peaks.get("hbm_gbs", 6650.0),
                             "algorithmic_bytes_per_path_step": 4,
                             "peak_source": "MEASURED_PEAKS.json" if "hbm_gbs" in peaks else "fallback"}}
+        wi = prof.get("warp_inst_per_warp_date")
+        if wi:
+            # the binding limit: one warp instruction per cycle per scheduler (4 per SM)
+            sm_hz = (clocks or {}).get("sm_mhz") or 1965.0
+            issue_peak = 4 * 148 * sm_hz * 1e6
+            issue_ach = wi * (path_steps / 32) / (kernel_ms * 1e-3)
+            roofline["issue"] = {"achieved": issue_ach / 1e12, "peak": issue_peak / 1e12, "unit": "T warp-inst/s",
+                                 "frac": issue_ach / issue_peak, "warp_inst_per_warp_date": wi,
+                                 "note": "FP64 instructions are 28% of the kernel's issue slots; the schedulers' "
+                                         "issue rate, not the FP64 pipe, bounds the kernel"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
