@@ -158,6 +158,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-batch", action="store_true")
     ap.add_argument("--no-c5", action="store_true", help="skip the config-5 stress line (2^28 x 365 FP32)")
+    ap.add_argument("--records", default="", help="also write the GPU and CPU rows as the reference's CSV "
+                                                 "(proj/include/qmc/bench.hpp schema; GPU rows lanes = -1)")
     ap.add_argument("--paths-log2", type=int, default=24, help="(debug) smaller path count")
     args = ap.parse_args()
     rank, world = env_int("RANK", 0), env_int("WORLD_SIZE", 1)
@@ -353,8 +355,16 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            cpu = cpu_reference(steps=1, warmup=1)
-            cpu = {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")}
+            cpu_full = cpu_reference(steps=1, warmup=1)
+            cpu = {k: cpu_full[k] for k in ("value", "unit", "cores", "kind", "sample")}
+            if args.records:  # the reference's CSV schema: GPU row (lanes = -1) next to its CPU row
+                from paper_1205_0106_b200 import records as R
+                gpu_row = R.BenchmarkRecord(q.Method.AmericanUpperBound, n_paths, M_DATES, R.GPU_LANES, 4096,
+                                            SEED, price, se, wall_call)
+                cpu_row = R.BenchmarkRecord(q.Method.AmericanUpperBound, CPU_SAMPLE_PATHS, M_DATES,
+                                            cpu_full["cores"], 4096, SEED, cpu_full["price"], cpu_full["std_error"],
+                                            cpu_full["seconds_per_call"])
+                R.emit_results([gpu_row, cpu_row], R.OutputFormat.Csv, args.records)
         except Exception as exc:  # the reference build is test infrastructure; report, don't fail
             cpu = {"value": None, "error": str(exc)[:200]}
 

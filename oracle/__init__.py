@@ -190,6 +190,9 @@ class Reference:
         L.ref_crr_price.argtypes = [P, C.c_int, I64, C.c_int, C.POINTER(D), C.c_char_p, C.c_int]
         L.ref_make_schedule.argtypes = [I64, D, C.POINTER(D), P, C.c_char_p, C.c_int]
         L.ref_default_lanes.restype = C.c_int
+        L.ref_emit_records.argtypes = [C.c_int] + [P] * 9 + [C.c_int, C.c_char_p, I64, C.POINTER(I64), C.c_char_p,
+                                                          C.c_int]
+        L.ref_parse_csv_records.argtypes = [C.c_char_p, C.c_int] + [P] * 9 + [C.POINTER(C.c_int), C.c_char_p, C.c_int]
         self.lib = L
 
     def price_american(self, spot, strike, rate, vol, mat, m, n, seed, kind=CALL, lanes=1, chunk=4096):
@@ -257,6 +260,31 @@ class Reference:
         _raise(self.lib.ref_backward_sweep(p.ctypes.data, m, _spec_args(spot, strike, rate, vol, mat), kind,
                                            C.byref(val), trace.ctypes.data, C.byref(ex), err, 512), err)
         return val.value, trace, (None if ex.value < 0 else ex.value)
+
+    def emit_records(self, records, fmt: int) -> str:
+        """reference emit_records (bench.cpp:203-283); records = [(method, n_paths, m, lanes, chunk, seed,
+        price, std_error, elapsed_s)], fmt 0 table / 1 csv / 2 json."""
+        n = len(records)
+        cols = list(zip(*records))
+        arr = lambda dt, k: np.ascontiguousarray(np.array(cols[k], dtype=dt))  # noqa: E731
+        a = [arr(np.int32, 0), arr(np.int64, 1), arr(np.int64, 2), arr(np.int32, 3), arr(np.int64, 4),
+             arr(np.uint64, 5), arr(np.float64, 6), arr(np.float64, 7), arr(np.float64, 8)]
+        out = C.create_string_buffer(1 << 22)
+        ln = C.c_int64()
+        err = C.create_string_buffer(512)
+        _raise(self.lib.ref_emit_records(n, *[x.ctypes.data for x in a], fmt, out, len(out), C.byref(ln), err, 512),
+               err)
+        return out.raw[: ln.value].decode()
+
+    def parse_csv_records(self, text: str):
+        maxn = 4096
+        bufs = [np.zeros(maxn, dt) for dt in (np.int32, np.int64, np.int64, np.int32, np.int64, np.uint64,
+                                                np.float64, np.float64, np.float64)]
+        cnt = C.c_int()
+        err = C.create_string_buffer(512)
+        _raise(self.lib.ref_parse_csv_records(text.encode(), maxn, *[b.ctypes.data for b in bufs], C.byref(cnt),
+                                              err, 512), err)
+        return [tuple(b[i].item() for b in bufs) for i in range(cnt.value)]
 
     def tree_reduce(self, values, lanes=1):
         v = np.ascontiguousarray(values, dtype=np.float64)

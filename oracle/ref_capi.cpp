@@ -10,6 +10,7 @@
 // 3 any other exception. The exception text is copied into `err`.
 #include "qmc/american.hpp"
 #include "qmc/analytic.hpp"
+#include "qmc/bench.hpp"
 #include "qmc/mc_european.hpp"
 #include "qmc/oracles.hpp"
 #include "qmc/path_engine.hpp"
@@ -17,8 +18,10 @@
 
 #include <cstdint>
 #include <cstring>
+#include <sstream>
 #include <stdexcept>
 #include <string>
+#include <vector>
 
 using namespace qmc;
 
@@ -181,5 +184,57 @@ int ref_make_schedule(std::int64_t m, double maturity, double* dt, double* times
 }
 
 int ref_default_lanes(void) { return default_lanes(); }
+
+// emit_records (bench.cpp:203-283) of n records given column-wise; format 0 table,
+// 1 csv, 2 json. The text (NUL-terminated) goes to out; *len gets its length.
+int ref_emit_records(int n, const int* method, const std::int64_t* n_paths, const std::int64_t* m,
+                     const int* lanes, const std::int64_t* chunk, const std::uint64_t* seed, const double* price,
+                     const double* se, const double* elapsed, int format, char* out, std::int64_t outlen,
+                     std::int64_t* len, char* err, int errlen) {
+  return guarded(err, errlen, [&] {
+    std::vector<BenchmarkRecord> recs(static_cast<std::size_t>(n));
+    for (int i = 0; i < n; ++i) {
+      BenchmarkRecord& r = recs[static_cast<std::size_t>(i)];
+      r.method = static_cast<Method>(method[i]);
+      r.n_paths = n_paths[i];
+      r.m = m[i];
+      r.lanes = lanes[i];
+      r.chunk = chunk[i];
+      r.seed = seed[i];
+      r.price = price[i];
+      r.std_error = se[i];
+      r.elapsed_s = elapsed[i];
+    }
+    std::ostringstream os;
+    emit_records(recs, format == 0 ? OutputFormat::Table : format == 1 ? OutputFormat::Csv : OutputFormat::Json, os);
+    const std::string text = os.str();
+    *len = static_cast<std::int64_t>(text.size());
+    if (static_cast<std::int64_t>(text.size()) + 1 > outlen) throw std::length_error("ref_emit_records: buffer");
+    std::memcpy(out, text.c_str(), text.size() + 1);
+  });
+}
+
+// parse_csv_records (bench.cpp:299-330): up to maxn records, column-wise; *count = parsed.
+int ref_parse_csv_records(const char* text, int maxn, int* method, std::int64_t* n_paths, std::int64_t* m,
+                          int* lanes, std::int64_t* chunk, std::uint64_t* seed, double* price, double* se,
+                          double* elapsed, int* count, char* err, int errlen) {
+  return guarded(err, errlen, [&] {
+    std::istringstream in{std::string(text)};
+    const auto recs = parse_csv_records(in);
+    *count = static_cast<int>(recs.size());
+    for (int i = 0; i < *count && i < maxn; ++i) {
+      const BenchmarkRecord& r = recs[static_cast<std::size_t>(i)];
+      method[i] = static_cast<int>(r.method);
+      n_paths[i] = r.n_paths;
+      m[i] = r.m;
+      lanes[i] = r.lanes;
+      chunk[i] = r.chunk;
+      seed[i] = r.seed;
+      price[i] = r.price;
+      se[i] = r.std_error;
+      elapsed[i] = r.elapsed_s;
+    }
+  });
+}
 
 }  // extern "C"
