@@ -33,7 +33,7 @@ constexpr int kThreads = QMCG_THREADS;  // paths per block (one per thread)
 static_assert(kThreads % 32 == 0 && kThreads <= 256, "tail queue indices are 8-bit");
 constexpr int kWarps = kThreads / 32;
 #ifndef QMCG_WALK_V
-#define QMCG_WALK_V 0
+#define QMCG_WALK_V 2
 #endif
 #ifndef QMCG_MINB
 #define QMCG_MINB 4
@@ -127,6 +127,7 @@ __device__ __forceinline__ double moro_central_plus(double y, double alpha) {
 }
 
 __constant__ double2 c_log_table[128];
+__constant__ double c_tail_y = 0.42;  // Moro branch point |u - 1/2| > 0.42 (analytic.cpp:87)
 __constant__ double c_log_consts[2] = {0x1.0000000000400p+52 /* 2^52 + 1024 */, 0x1.62e42fefa39efp-1 /* ln 2 */};
 
 // Shared-memory accessors on 32-bit shared-window addresses (keeps the
@@ -563,22 +564,22 @@ __device__ __forceinline__ void park_point(uint32_t zslot, uint32_t qbase, uint3
   if constexpr (F32) {
     asm volatile(
         "{\n .reg .pred p;\n .reg .f64 ay;\n .reg .b32 m, a;\n"
-        " abs.f64 ay, %4;\n setp.gt.f64 p, ay, 0d3FDAE147AE147AE1;\n"
+        " abs.f64 ay, %4;\n setp.gt.f64 p, ay, %8;\n"
         " vote.sync.ballot.b32 %0, p, 0xffffffff;\n"
         " st.shared.f32 [%1], %2;\n @p st.shared.f32 [%1], %3;\n"
         " and.b32 m, %0, %5;\n popc.b32 m, m;\n add.u32 a, %6, m;\n @p st.shared.u8 [a], %7;\n}"
         : "=r"(b)
-        : "r"(zslot), "f"(z), "f"(park), "d"(y), "r"(lt), "r"(qbase + ntail), "r"(idx)
+        : "r"(zslot), "f"(z), "f"(park), "d"(y), "r"(lt), "r"(qbase + ntail), "r"(idx), "d"(c_tail_y)
         : "memory");
   } else {
     asm volatile(
         "{\n .reg .pred p;\n .reg .f64 ay;\n .reg .b32 m, a;\n"
-        " abs.f64 ay, %4;\n setp.gt.f64 p, ay, 0d3FDAE147AE147AE1;\n"
+        " abs.f64 ay, %4;\n setp.gt.f64 p, ay, %8;\n"
         " vote.sync.ballot.b32 %0, p, 0xffffffff;\n"
         " st.shared.f64 [%1], %2;\n @p st.shared.f64 [%1], %3;\n"
         " and.b32 m, %0, %5;\n popc.b32 m, m;\n add.u32 a, %6, m;\n @p st.shared.u8 [a], %7;\n}"
         : "=r"(b)
-        : "r"(zslot), "d"(z), "d"(park), "d"(y), "r"(lt), "r"(qbase + ntail), "r"(idx)
+        : "r"(zslot), "d"(z), "d"(park), "d"(y), "r"(lt), "r"(qbase + ntail), "r"(idx), "d"(c_tail_y)
         : "memory");
   }
   ntail += __popc(b);
@@ -851,6 +852,27 @@ __global__ void __launch_bounds__(kThreads, QMCG_MINB) price_kernel(const PriceP
         cd = add_rn(cd, slope);
         const bool rec = KIND == 0 ? V > c : V < c;
         const bool push = rec && (KIND == 0 || pl + k0 >= 0) && !record_dominates<KIND>(V, c, cd, bT, x0mkT);
+#if QMCG_WALK_V == 2
+        if constexpr (KIND == 0 && !F32) {
+          // calls, FP64: one predicated block per date (no branches, no select chains);
+          // push = new record that does not dominate the pending one (V < cd)
+          (void)rec;
+          (void)push;
+          double pv;
+          int pdl;
+          uint32_t pu32;
+          asm volatile(
+              "{\n .reg .pred r, pu;\n"
+              " setp.gt.f64 r, %0, %1;\n setp.lt.and.f64 pu, %0, %2, r;\n"
+              " mov.b64 %4, %1;\n mov.b32 %5, %3;\n"
+              " selp.f64 %1, %0, %1, r;\n selp.f64 %2, %0, %2, r;\n selp.b32 %3, %7, %3, r;\n"
+              " selp.u32 %6, 1, 0, pu;\n}"
+              : "+d"(V), "+d"(c), "+d"(cd), "+r"(pl), "=d"(pv), "=r"(pdl), "=r"(pu32)
+              : "r"(t));
+          push_record<KIND, RNEG>(ws, P, pu32 != 0, pv, k0 + pdl, lane, lt, rq_head, rq_tail);
+          continue;
+        }
+#endif
 #if QMCG_WALK_V == 1
         push_record<KIND, RNEG>(ws, P, push, c, k0 + pl, lane, lt, rq_head, rq_tail);
         c = rec ? V : c;
