@@ -176,11 +176,28 @@ def main():
     warmup = max(3, args.warmup)
     steps = max(1, args.steps)
     dist = None
+    # one GPU per rank; QMCG_DIST_BACKEND=gloo (functional tests of the multi-rank flow only, e.g.
+    # several ranks on one GPU, whose kernels never wait on each other) keeps the plumbing on the host
+    backend = os.environ.get("QMCG_DIST_BACKEND", "nccl")
+    device = local_rank % max(1, torch.cuda.device_count())
     if world > 1:
         import torch.distributed as dist
-        torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-    ctx = q.Context(local_rank)
+        torch.cuda.set_device(device)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", device))
+        else:
+            dist.init_process_group(backend)
+    red_dev = "cuda" if backend == "nccl" else "cpu"
+
+    def max_over_ranks(*vals):
+        if not dist:
+            return vals
+        t = torch.tensor(vals, dtype=torch.float64, device=red_dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return tuple(float(x) for x in t.tolist())
+
+    local_rank = device
+    ctx = q.Context(device)
     call = q.OptionSpec(*SPEC, kind=q.OptionKind.Call)
     put = q.OptionSpec(*SPEC, kind=q.OptionKind.Put)
     depth = distributed.tree_depth(n_paths, world)
@@ -228,9 +245,7 @@ def main():
             dist.barrier()
         dev_ms = e0.elapsed_time(e1)
         if dist:
-            t = torch.tensor([dev_ms, wall], dtype=torch.float64, device="cuda")
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            dev_ms, wall = float(t[0]), float(t[1])
+            dev_ms, wall = max_over_ranks(dev_ms, wall)
         return dev_ms / steps, wall / steps, res, launches, (sampler.summary() if sampler else None)
 
     ms_call, wall_call, (price, se), launches, clocks = timed(call, sample_clocks=True)
@@ -276,9 +291,7 @@ def main():
         bwall = (time.perf_counter() - t0) / breps
         bms = be0.elapsed_time(be1) / breps
         if dist:
-            t = torch.tensor([bms, bwall], dtype=torch.float64, device="cuda")
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            bms, bwall = float(t[0]), float(t[1])
+            bms, bwall = max_over_ranks(bms, bwall)
         batch = {"workload": "config 4: 1024 contracts (K = 80..120 x sigma = 0.10..0.50, calls for even i+j), "
                              "2^18 paths x 128 dates, seed 42, qmcg_price_american_batch"
                              + (f" on {world} ranks (contiguous contract blocks + all_gather)" if world > 1 else ""),
@@ -306,9 +319,7 @@ def main():
         ms5 = c0.elapsed_time(c1)
         windows = ctx.last_window_count()
         if dist:
-            t = torch.tensor([ms5, w5], dtype=torch.float64, device="cuda")
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            ms5, w5 = float(t[0]), float(t[1])
+            ms5, w5 = max_over_ranks(ms5, w5)
         c5 = {"workload": "config 5: 2^28 paths x 365 dates, FP32 normals + walk (bit-exact FP64 uniforms), call, "
                           "seed 42, cold (K1 rebuilds every table)",
               "value": n5 * m5 / (ms5 * 1e-3), "unit": "path-steps/s", "ms_per_option": ms5,
