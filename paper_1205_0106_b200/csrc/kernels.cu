@@ -2026,7 +2026,47 @@ __global__ void __launch_bounds__(kGThreads, QMCG_G_MINB) walk_group_kernel(cons
   const int64_t ldz = B.ldz;
 #pragma unroll
   for (int t = 0; t < kPf; ++t) zbuf[t] = __ldg(zp + t * ldz);
-  for (int d0 = 0; d0 < mrec; d0 += kPf) {
+  auto step = [&](int d, double S) {
+    kd += 1.0;
+    if (KIND == 0) {
+      // rec = V > c; push = rec && W < cd; @push append (c, pend); then replace the pending record
+      asm volatile(
+          "{\n .reg .pred r, pu;\n .reg .f64 v, w;\n .reg .b32 a;\n"
+          " fma.rn.f64 v, %4, %5, %6;\n fma.rn.f64 w, %7, %5, %6;\n"
+          " setp.gt.f64 r, v, %0;\n setp.lt.and.f64 pu, w, %1, r;\n"
+          " mad.lo.u32 a, %3, 8, %8;\n @pu st.shared.f64 [a], %0;\n"
+          " mad.lo.u32 a, %3, 4, %9;\n @pu st.shared.u32 [a], %2;\n @pu add.u32 %3, %3, 1;\n"
+          " selp.f64 %0, v, %0, r;\n selp.f64 %1, w, %1, r;\n selp.b32 %2, %10, %2, r;\n}"
+          : "+d"(c), "+d"(cd), "+r"(pend), "+r"(cnt)
+          : "d"(alpha), "d"(kd), "d"(S), "d"(beta), "r"(cs), "r"(cj), "r"(d)
+          : "memory");
+    } else {
+      const double V = fma(alpha, kd, S);
+      const bool rec = V < c;
+      cd = __dadd_rn(cd, beta);
+      const bool push = rec && pend >= 0 && !record_dominates<1>(V, c, cd, gb, gx);
+      if (push) {
+        sts_f64(cs + cnt * 8, c);
+        sts_u32(cj + cnt * 4, static_cast<uint32_t>(pend));
+      }
+      cnt += push ? 1 : 0;
+      c = rec ? V : c;
+      cd = rec ? 0.0 : cd;
+      pend = rec ? d : pend;
+    }
+  };
+  // rare: keep room for the next `room` candidates
+  auto make_room = [&](int room) {
+    if (__any_sync(kFull, cnt > kGCap - 1 - room)) {
+      if (cnt > kGCap - 1 - room) {
+        group_flush<KIND>(B.cp, g, cnt, cs, cj, B.values, B.n, p, flushed);
+        flushed = true;
+        cnt = 0;
+      }
+    }
+  };
+  int d0 = 0;
+  for (; d0 + kPf <= mrec; d0 += kPf) {
     double cur[kPf];
     zp += kPf * ldz;
 #pragma unroll
@@ -2036,44 +2076,17 @@ __global__ void __launch_bounds__(kGThreads, QMCG_G_MINB) walk_group_kernel(cons
     }
 #pragma unroll
     for (int t = 0; t < kPf; ++t) {
-      const int d = d0 + t;
-      if (d0 + kPf > mrec && d >= mrec) break;
-      kd += 1.0;
-      const double S = cur[t];
-      if (KIND == 0) {
-        // rec = V > c; push = rec && W < cd; @push append (c, pend); then replace the pending record
-        asm volatile(
-            "{\n .reg .pred r, pu;\n .reg .f64 v, w;\n .reg .b32 a;\n"
-            " fma.rn.f64 v, %4, %5, %6;\n fma.rn.f64 w, %7, %5, %6;\n"
-            " setp.gt.f64 r, v, %0;\n setp.lt.and.f64 pu, w, %1, r;\n"
-            " mad.lo.u32 a, %3, 8, %8;\n @pu st.shared.f64 [a], %0;\n"
-            " mad.lo.u32 a, %3, 4, %9;\n @pu st.shared.u32 [a], %2;\n @pu add.u32 %3, %3, 1;\n"
-            " selp.f64 %0, v, %0, r;\n selp.f64 %1, w, %1, r;\n selp.b32 %2, %10, %2, r;\n}"
-            : "+d"(c), "+d"(cd), "+r"(pend), "+r"(cnt)
-            : "d"(alpha), "d"(kd), "d"(S), "d"(beta), "r"(cs), "r"(cj), "r"(d)
-            : "memory");
-      } else {
-        const double V = fma(alpha, kd, S);
-        const bool rec = V < c;
-        cd = __dadd_rn(cd, beta);
-        const bool push = rec && pend >= 0 && !record_dominates<1>(V, c, cd, gb, gx);
-        if (push) {
-          sts_f64(cs + cnt * 8, c);
-          sts_u32(cj + cnt * 4, static_cast<uint32_t>(pend));
-        }
-        cnt += push ? 1 : 0;
-        c = rec ? V : c;
-        cd = rec ? 0.0 : cd;
-        pend = rec ? d : pend;
-      }
-      if (__any_sync(kFull, cnt >= kGCap - 1)) {  // rare: keep room for the next candidate
-        if (cnt >= kGCap - 1) {
-          group_flush<KIND>(B.cp, g, cnt, cs, cj, B.values, B.n, p, flushed);
-          flushed = true;
-          cnt = 0;
-        }
-      }
+      step(d0 + t, cur[t]);
+      if ((t & 3) == 3) make_room(4);
     }
+  }
+  for (int t = 0; d0 + t < mrec; ++t) {  // the last partial chunk (zbuf holds its values)
+    double S = zbuf[0];
+#pragma unroll
+    for (int u = 1; u < kPf; ++u)
+      if (u == t) S = zbuf[u];
+    step(d0 + t, S);
+    make_room(1);
   }
   if (pend >= 0) {  // the last pending record
     sts_f64(cs + cnt * 8, c);
