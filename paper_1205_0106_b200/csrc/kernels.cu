@@ -38,11 +38,7 @@ constexpr int kWarps = kThreads / 32;
 #ifndef QMCG_MINB
 #define QMCG_MINB 4
 #endif
-#ifndef QMCG_GEN_UNROLL
-#define QMCG_GEN_UNROLL 1
-#endif
 constexpr int kTile = kWarps;  // dates per tile = warps per block (one date row per warp)
-constexpr int kGenUnroll = QMCG_GEN_UNROLL;
 constexpr int kRecCap = 128;  // per-warp ring of pending record evaluations (mostly drained at path end)
 constexpr uint32_t kNone = 0xffffffffu;
 constexpr int kBins = 256;             // K1 binned scatter (== the bin kernel's block size)
@@ -157,9 +153,6 @@ __device__ __forceinline__ void sts_f64(uint32_t a, double v) {
 }
 __device__ __forceinline__ void sts_u32(uint32_t a, uint32_t v) {
   asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
-}
-__device__ __forceinline__ void sts_u8(uint32_t a, uint32_t v) {
-  asm volatile("st.shared.u8 [%0], %1;" ::"r"(a), "r"(v) : "memory");
 }
 __device__ __forceinline__ void sts_v2f64(uint32_t a, double2 v) {
   asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(a), "d"(v.x), "d"(v.y) : "memory");
@@ -372,36 +365,10 @@ __device__ __forceinline__ double clamp_endpoints(double v) {  // quasi_rng.cpp:
   return v;
 }
 
-// ---- bulk-copy staging (cp.async.bulk + mbarrier) ----
+// ---- shared-window addresses (the bulk copies and mbarriers use them) ----
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  asm volatile(
-      "{\n"
-      ".reg .pred P1;\n"
-      "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
-      "@!P1 bra WAIT_%=;\n"
-      "}\n" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-          smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar))
-      : "memory");
-}
-
 // Shared memory of one 256-path block (byte offsets from the dynamic base):
 //   perm[2][kTile][256] u32   permutation entries, bulk-copied, double-buffered
 //   zt[2][kTile][256]   f64   z_k + alpha per (date, path); reused for V_k in the walk
@@ -1414,16 +1381,69 @@ __device__ __forceinline__ void seq_sum(const double* __restrict__ v, int64_t of
   }
 }
 
-__global__ void pairwise_leaves_kernel(const double* __restrict__ v, int64_t len, int depth,
-                                       double* __restrict__ out, int64_t out_stride) {
+// Leaf sums, one node per lane. A warp's 32 consecutive leaves cover one
+// contiguous range of v: it is staged into shared memory with coalesced loads
+// (one pad slot per 64 values keeps the lanes' sequential reads off a single
+// bank), then each lane sums its leaf in order from 0.0 as the reference does.
+constexpr int kLeafWarps = 1, kLeafStage = 32 * 128;  // leaves are <= 128 values (split once above 64)
+__global__ void __launch_bounds__(kLeafWarps * 32) pairwise_leaves_kernel(const double* __restrict__ v, int64_t len,
+                                                                         int depth, double* __restrict__ out,
+                                                                         int64_t out_stride) {
+  __shared__ double stage[kLeafWarps][kLeafStage + kLeafStage / 64];
   v += static_cast<int64_t>(blockIdx.y) * len;
   out += static_cast<int64_t>(blockIdx.y) * out_stride;
-  const int64_t node = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (node >= (int64_t{1} << depth)) return;
-  int64_t off, size;
-  node_range(len, depth, node, off, size);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t nodes = int64_t{1} << depth;
+  const int64_t first = (static_cast<int64_t>(blockIdx.x) * kLeafWarps + warp) * 32;
+  if (first >= nodes) return;
+  const int64_t node = first + lane;
+  const bool live = node < nodes;
+  int64_t off = 0, size = 0;
+  if (live) node_range(len, depth, node, off, size);
+  const int64_t r0 = __shfl_sync(kFull, off, 0);
+  const int last = static_cast<int>(min(static_cast<int64_t>(31), nodes - 1 - first));
+  const int64_t r1 = __shfl_sync(kFull, off + size, last);
   double s, s2;
-  if (size <= 64) {
+  if (r1 - r0 <= kLeafStage) {
+    double* st = stage[warp];
+    for (int64_t k = lane; k < r1 - r0; k += 32) st[k + (k >> 6)] = v[r0 + k];
+    __syncwarp();
+    const int64_t b0 = off - r0;
+    auto sum = [&](int64_t a, int64_t n, double& x, double& x2) {
+      x = 0.0;
+      x2 = 0.0;
+      int64_t i = 0;
+      for (; i + 8 <= n; i += 8) {  // 8 loads in flight ahead of the ordered adds
+        double y[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const int64_t k = b0 + a + i + j;
+          y[j] = st[k + (k >> 6)];
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          x = __dadd_rn(x, y[j]);
+          x2 = __dadd_rn(x2, __dmul_rn(y[j], y[j]));
+        }
+      }
+      for (; i < n; ++i) {
+        const int64_t k = b0 + a + i;
+        const double y = st[k + (k >> 6)];
+        x = __dadd_rn(x, y);
+        x2 = __dadd_rn(x2, __dmul_rn(y, y));
+      }
+    };
+    if (size <= 64) {
+      sum(0, size, s, s2);
+    } else {
+      const int64_t half = size / 2;
+      double a, a2, b, b2;
+      sum(0, half, a, a2);
+      sum(half, size - half, b, b2);
+      s = __dadd_rn(a, b);
+      s2 = __dadd_rn(a2, b2);
+    }
+  } else if (size <= 64) {
     seq_sum(v, off, size, s, s2);
   } else {
     const int64_t half = size / 2;
@@ -1433,8 +1453,10 @@ __global__ void pairwise_leaves_kernel(const double* __restrict__ v, int64_t len
     s = __dadd_rn(a, b);
     s2 = __dadd_rn(a2, b2);
   }
-  out[2 * node] = s;
-  out[2 * node + 1] = s2;
+  if (live) {
+    out[2 * node] = s;
+    out[2 * node + 1] = s2;
+  }
 }
 
 // Reduces groups of `group` (power of two <= 1024) consecutive node pairs.
@@ -2444,8 +2466,9 @@ cudaError_t launch_pairwise_batched(const double* v, int64_t len, int count, dou
   double* b = scratch + strideA * count;
   int64_t sa = strideA, sb = strideB;
   {
-    const dim3 grid(static_cast<unsigned>((nodes + 255) / 256), static_cast<unsigned>(count));
-    pairwise_leaves_kernel<<<grid, 256, 0, s>>>(v, len, D, nodes == 1 ? out2 : a, nodes == 1 ? 2 : sa);
+    const dim3 grid(static_cast<unsigned>((nodes + kLeafWarps * 32 - 1) / (kLeafWarps * 32)),
+                    static_cast<unsigned>(count));
+    pairwise_leaves_kernel<<<grid, kLeafWarps * 32, 0, s>>>(v, len, D, nodes == 1 ? out2 : a, nodes == 1 ? 2 : sa);
     if (launches) ++*launches;
   }
   while (nodes > 1) {
