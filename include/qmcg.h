@@ -126,6 +126,16 @@ qmcg_status qmcg_combine_nodes(int64_t n_paths, int depth, const double* node_su
 qmcg_status qmcg_warm(qmcg_ctx* ctx, int64_t n_paths, uint64_t seed, int64_t dims);
 /* Drop every cached table. */
 qmcg_status qmcg_clear_cache(qmcg_ctx* ctx);
+/* Cold multi-GPU build: rank r builds the full tables of dims
+ * dim_begin + k * dim_stride (k < count) into its device buffer out_dev (row k at
+ * out_dev + k * ld; entries are perm + 1, the Halton index of uniform_at), the column
+ * slices are exchanged all-to-all, and each rank installs its slice of every dim
+ * with qmcg_import_tables. src_dev holds dims rows of col_end - col_begin entries
+ * (row stride src_ld); afterwards pricing over [col_begin, col_end) is warm. */
+qmcg_status qmcg_build_tables(qmcg_ctx* ctx, int64_t n_paths, uint64_t seed, int64_t dim_begin,
+                              int64_t dim_stride, int64_t count, uint32_t* out_dev, int64_t ld);
+qmcg_status qmcg_import_tables(qmcg_ctx* ctx, int64_t n_paths, uint64_t seed, int64_t col_begin,
+                               int64_t col_end, int64_t dims, const uint32_t* src_dev, int64_t src_ld);
 /* Cap the bytes the permutation tables may occupy (0 = whatever free device
  * memory allows). A pricing whose tables exceed it runs in date windows
  * ("streamed tables": each window's rows are built, walked, and replaced,

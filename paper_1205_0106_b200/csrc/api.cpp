@@ -630,6 +630,54 @@ qmcg_status qmcg_warm(qmcg_ctx* c, int64_t n, uint64_t seed, int64_t dims) {
   return QMCG_OK;
 }
 
+qmcg_status qmcg_build_tables(qmcg_ctx* c, int64_t n, uint64_t seed, int64_t dim_begin, int64_t dim_stride,
+                              int64_t count, uint32_t* out_dev, int64_t ld) {
+  if (!c || (!out_dev && count > 0)) return fail(QMCG_INVALID_ARGUMENT, "qmcg_build_tables: null argument");
+  if (n < 1 || static_cast<uint64_t>(n) > 0xffffffffULL || dim_begin < 0 || dim_stride < 1 || count < 0 || ld < n)
+    return fail(QMCG_INVALID_ARGUMENT, "qmcg_build_tables: bad size");
+  std::lock_guard<std::mutex> lock(c->mu);
+  DeviceGuard g(c->device);
+  c->launches = 0;
+  for (int64_t k = 0; k < count; ++k) {
+    qmcg_status st = build_perm(c, dimension_seed(seed, dim_begin + k * dim_stride), n,
+                                out_dev + static_cast<size_t>(k) * static_cast<size_t>(ld));
+    if (st) return st;
+  }
+  QMCG_CUDA(cudaStreamSynchronize(c->stream));
+  return QMCG_OK;
+}
+
+qmcg_status qmcg_import_tables(qmcg_ctx* c, int64_t n, uint64_t seed, int64_t col_begin, int64_t col_end,
+                               int64_t dims, const uint32_t* src_dev, int64_t src_ld) {
+  if (!c || !src_dev) return fail(QMCG_INVALID_ARGUMENT, "qmcg_import_tables: null argument");
+  const int64_t cols = col_end - col_begin;
+  if (n < 1 || static_cast<uint64_t>(n) > 0xffffffffULL || col_begin < 0 || cols < 1 || col_end > n || dims < 1 ||
+      src_ld < cols)
+    return fail(QMCG_INVALID_ARGUMENT, "qmcg_import_tables: bad size");
+  std::lock_guard<std::mutex> lock(c->mu);
+  DeviceGuard g(c->device);
+  drop_cache(c);
+  const int64_t ld = qmcg::table_ld(cols);
+  const size_t row_bytes = static_cast<size_t>(ld) * sizeof(uint32_t);
+  uint32_t* nt = nullptr;
+  if (cudaMalloc(&nt, row_bytes * static_cast<size_t>(dims) + qmcg::kTablePad * sizeof(uint32_t)) != cudaSuccess) {
+    cudaGetLastError();
+    return fail(QMCG_OUT_OF_MEMORY, "qmcg_import_tables: tables do not fit in device memory");
+  }
+  c->table = nt;
+  c->table_rows_cap = static_cast<size_t>(dims);
+  QMCG_CUDA(cudaMemcpy2DAsync(nt, row_bytes, src_dev, static_cast<size_t>(src_ld) * sizeof(uint32_t),
+                              static_cast<size_t>(cols) * sizeof(uint32_t), static_cast<size_t>(dims),
+                              cudaMemcpyDeviceToDevice, c->stream));
+  QMCG_CUDA(cudaStreamSynchronize(c->stream));
+  c->cache_n = n;
+  c->cache_seed = seed;
+  c->col_begin = col_begin;
+  c->col_end = col_end;
+  c->cache_dims = dims;
+  return QMCG_OK;
+}
+
 qmcg_status qmcg_set_table_budget(qmcg_ctx* c, uint64_t bytes) {
   if (!c) return fail(QMCG_INVALID_ARGUMENT, "qmcg_set_table_budget: null context");
   std::lock_guard<std::mutex> lock(c->mu);

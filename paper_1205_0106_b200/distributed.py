@@ -132,3 +132,64 @@ def price_american_batch_sharded(specs: Sequence["qmcg.OptionSpec"], m: int, n_p
         rb, re_ = contract_range(C, world, r)
         out[rb:re_] = rows[r][: re_ - rb]
     return out
+
+
+def rank_columns(n_paths: int, world: int, rank: int) -> Tuple[int, int]:
+    """The contiguous path (column) range of `rank`: the union of its pairwise-tree nodes."""
+    depth = tree_depth(n_paths, world)
+    mine = rank_nodes(depth, world, rank)
+    if not mine:
+        return 0, 0
+    b, _ = qmcg.tree_node_range(n_paths, depth, mine[0])
+    _, e = qmcg.tree_node_range(n_paths, depth, mine[-1])
+    return b, e
+
+
+def warm_tables_sharded(ctx: Optional["qmcg.Context"], n_paths: int, seed: int, dims: int, *, group=None,
+                        build_fn: Optional[Callable] = None, import_fn: Optional[Callable] = None,
+                        device=None) -> None:
+    """Cold table build over the ranks of `group`: the permutation table of dim d
+    is built (full n) by rank d mod G only, then an all-to-all sends each rank its column slice of
+    every table, which it installs in its context -- G times less K1 work than every rank
+    building every table. Afterwards price_american_sharded on the same (n_paths, seed) is warm.
+    build_fn(k_dims, dim_begin, stride, buf) / import_fn(b, e, table) replace the GPU calls (tests)."""
+    import torch
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    backend = dist.get_backend(group) if dist.is_initialized() else "nccl"
+    comm = torch.device("cuda", torch.cuda.current_device()) if backend == "nccl" else torch.device("cpu")
+    if device is None:  # where K1 writes: the GPU when the context builds, else the collective's device
+        device = torch.device("cuda", torch.cuda.current_device()) if build_fn is None else comm
+    cols = [rank_columns(n_paths, world, r) for r in range(world)]
+    my_dims = list(range(rank, dims, world))
+    k = len(my_dims)
+    buf = torch.empty((max(k, 1), n_paths), dtype=torch.int32, device=device)  # uint32 bit patterns
+    if k:
+        if build_fn is not None:
+            build_fn(k, rank, world, buf)
+        else:
+            ctx.build_tables(n_paths, seed, rank, world, k, buf.data_ptr(), n_paths)
+    b_me, e_me = cols[rank]
+    w_me = e_me - b_me
+    if world == 1:
+        table = buf[:dims]
+    else:
+        send = (torch.cat([buf[:k, b:e].reshape(-1) for (b, e) in cols]) if k else
+                torch.empty(0, dtype=torch.int32, device=device)).to(comm)
+        k_of = [len(range(r, dims, world)) for r in range(world)]
+        recv = torch.empty(sum(k_of) * w_me, dtype=torch.int32, device=comm)
+        dist.all_to_all_single(recv, send, output_split_sizes=[kk * w_me for kk in k_of],
+                               input_split_sizes=[k * (e - b) for (b, e) in cols], group=group)
+        table = torch.empty((dims, w_me), dtype=torch.int32, device=comm)
+        for r, piece in enumerate(recv.split([kk * w_me for kk in k_of])):
+            if k_of[r]:
+                table[r::world] = piece.view(k_of[r], w_me)
+    if import_fn is not None:
+        import_fn(b_me, e_me, table)
+    else:
+        if table.device.type != "cuda":
+            table = table.cuda()
+        table = table.contiguous()
+        ctx.import_tables(n_paths, seed, b_me, e_me, dims, table.data_ptr(), table.stride(0))

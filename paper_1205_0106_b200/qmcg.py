@@ -41,7 +41,7 @@ EXPORTS = (
     "qmcg_normals", "qmcg_normal_table", "qmcg_path_values", "qmcg_time_device", "qmcg_time_perm_build",
     "qmcg_last_launch_count", "qmcg_get_stream", "qmcg_fp64_peak", "qmcg_set_table_budget",
     "qmcg_last_window_count", "qmcg_price_american_nodes", "qmcg_simulate_batch", "qmcg_sweep_batch",
-    "qmcg_backward_sweep",
+    "qmcg_backward_sweep", "qmcg_build_tables", "qmcg_import_tables",
 )
 
 
@@ -126,6 +126,8 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
         L.qmcg_warm.argtypes = [P, I64, U64, I64]
         L.qmcg_clear_cache.argtypes = [P]
         L.qmcg_set_table_budget.argtypes = [P, U64]
+        L.qmcg_build_tables.argtypes = [P, I64, U64, I64, I64, I64, P, I64]
+        L.qmcg_import_tables.argtypes = [P, I64, U64, I64, I64, I64, P, I64]
         L.qmcg_simulate_batch.argtypes = [P, C.POINTER(_CSpec), I64, I64, U64, U32, C.c_int, P]
         L.qmcg_sweep_batch.argtypes = [P, C.POINTER(_CSpec), I64, I64, U64, U32, P, P]
         L.qmcg_backward_sweep.argtypes = [P, I64, C.POINTER(_CSpec), I64, U32, P, C.POINTER(I64)]
@@ -275,6 +277,18 @@ class Context:
 
     def clear_cache(self) -> None:
         _check(self._lib.qmcg_clear_cache(self._h))
+
+    def build_tables(self, n_paths: int, seed: int, dim_begin: int, dim_stride: int, count: int, out_ptr: int,
+                     ld: int) -> None:
+        """Full tables (perm + 1) of dims dim_begin + k * dim_stride into a caller device buffer."""
+        _check(self._lib.qmcg_build_tables(self._h, int(n_paths), int(seed), int(dim_begin), int(dim_stride),
+                                           int(count), C.c_void_p(out_ptr), int(ld)))
+
+    def import_tables(self, n_paths: int, seed: int, col_begin: int, col_end: int, dims: int, src_ptr: int,
+                      src_ld: int) -> None:
+        """Install the column slice [col_begin, col_end) of dims [0, dims) from a device buffer."""
+        _check(self._lib.qmcg_import_tables(self._h, int(n_paths), int(seed), int(col_begin), int(col_end), int(dims),
+                                            C.c_void_p(src_ptr), int(src_ld)))
 
     def set_table_budget(self, nbytes: int) -> None:
         """Cap the permutation-table bytes (0 = free device memory); larger pricings stream date windows."""

@@ -102,3 +102,53 @@ def test_batch_contract_sharding(world, oracle_lib):
     assert seen == sorted(specs)
     for r in range(world):
         assert np.array_equal(out[r][0], ref)
+
+
+def _tables_worker(rank, world, port, n, dims, out):
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import torch
+    import torch.distributed as dist
+    import oracle
+    from paper_1205_0106_b200 import distributed
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    O = oracle.Oracle()
+    built = []
+
+    def build(k, begin, stride, buf):
+        for j in range(k):
+            d = begin + j * stride
+            built.append(d)
+            perm = O.permutation_indices(n, O.dimension_seed(42, d))[:n].astype(np.int64) + 1
+            buf[j] = torch.from_numpy(perm.astype(np.uint32).view(np.int32))
+
+    got = {}
+
+    def imp(b, e, table):
+        got["range"] = (b, e)
+        got["table"] = table.numpy().view(np.uint32).copy()
+
+    distributed.warm_tables_sharded(None, n, 42, dims, build_fn=build, import_fn=imp)
+    out[rank] = (built, got["range"], got["table"])
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_table_build_all_to_all(world, oracle_lib):
+    """Cold multi-GPU build: dims round-robin over ranks (each built once), all-to-all of column
+    slices; every rank ends with exactly its columns of every dim's table (perm + 1)."""
+    n, dims = 5003, 7
+    manager = mp.Manager()
+    out = manager.dict()
+    mp.spawn(_tables_worker, args=(world, _free_port(), n, dims, out), nprocs=world, join=True)
+    assert sorted(d for r in range(world) for d in out[r][0]) == list(range(dims))
+    full = np.stack([oracle_lib.permutation_indices(n, oracle_lib.dimension_seed(42, d))[:n] for d in range(dims)])
+    cover = sorted(out[r][1] for r in range(world))
+    assert cover[0][0] == 0 and cover[-1][1] == n and all(a[1] == b[0] for a, b in zip(cover, cover[1:]))
+    for r in range(world):
+        b, e = out[r][1]
+        assert np.array_equal(out[r][2], (full[:, b:e] + 1).astype(np.uint32))

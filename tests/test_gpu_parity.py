@@ -271,3 +271,33 @@ def test_price_nodes_one_pass(ctx, qmcg):
         table = np.concatenate([lo, hi])
         assert np.array_equal(table, per)
         assert qmcg.combine_nodes(n, depth, table) == (single.price, single.std_error)
+
+
+def test_tables_build_import(ctx, qmcg):
+    """qmcg_build_tables + qmcg_import_tables (the cold multi-GPU path, here with one rank): the
+    imported tables price bit-identically to tables the context built itself."""
+    import torch
+    from paper_1205_0106_b200 import distributed
+    n, m = 40000, 24
+    s = spec_of(qmcg, REF)
+    ctx.clear_cache()
+    ref = ctx.price_american(s, m, n, 5)
+    ctx.clear_cache()
+    distributed.warm_tables_sharded(ctx, n, 5, m)
+    got = ctx.price_american(s, m, n, 5)
+    assert (got.price, got.std_error) == (ref.price, ref.std_error)
+    buf = torch.empty((2, n), dtype=torch.int32, device="cuda")
+    ctx.build_tables(n, 5, 3, 4, 2, buf.data_ptr(), n)  # dims 3 and 7
+    for j, d in enumerate((3, 7)):
+        perm = ctx.permutation(n, int(_dim_seed(5, d)))[:n]
+        assert np.array_equal(buf[j].cpu().numpy().view(np.uint32), perm + 1)
+    ctx.clear_cache()
+
+
+def _dim_seed(seed, d):
+    def sm(x):
+        x = (x + 0x9E3779B97F4A7C15) & (2**64 - 1)
+        x = ((x ^ (x >> 30)) * 0xBF58476D1CE4E5B9) & (2**64 - 1)
+        x = ((x ^ (x >> 27)) * 0x94D049BB133111EB) & (2**64 - 1)
+        return x ^ (x >> 31)
+    return sm(sm(seed) ^ ((d + 0x632BE59BD9B4E019) & (2**64 - 1)))
