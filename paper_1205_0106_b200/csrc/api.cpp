@@ -129,6 +129,7 @@ struct DimTables {
   std::vector<qmcg::DimPack> pack;
   std::vector<double> scnc;  // interleaved {sc, nc}
   std::vector<uint64_t> magic64;
+  std::vector<uint32_t> pairs;  // 4 per dimension (DIM_PAIR)
   bool any_wide = false, any_clamp = false;
 };
 
@@ -177,6 +178,38 @@ void build_dim_tables(int64_t n, int64_t m, DimTables& T) {
       dp.magic64 = static_cast<uint64_t>((two64 + p - 1) / p);
     }
     T.dims[static_cast<size_t>(d)] = dp;
+  }
+  // two-digit extraction for bases with >= 5 digits (p > 2: base 2 is a bit reversal)
+  T.pairs.assign(4 * T.dims.size(), 0u);
+  for (size_t d = 0; d < T.dims.size(); ++d) {
+    DimParam& dp = T.dims[d];
+    if (dp.ndig < 5 || dp.p == 2 || (dp.flags & qmcg::DIM_WIDE)) continue;
+    const uint64_t p2 = static_cast<uint64_t>(dp.p) * dp.p;
+    if (p2 >= (uint64_t{1} << 31)) continue;
+    uint32_t sh = 0;
+    while ((uint64_t{1} << (sh + 1)) < p2) ++sh;
+    const unsigned __int128 two = static_cast<unsigned __int128>(1) << (32 + sh);
+    const unsigned __int128 M = (two + p2 - 1) / p2;
+    const unsigned __int128 e = M * p2 - two;
+    if (!(M < (static_cast<unsigned __int128>(1) << 32) && static_cast<unsigned __int128>(max_index) * e < two))
+      continue;
+    // split r < p^2 by p: (r * sm) >> ss, verified for every r
+    uint32_t ss = 0, sm = 0;
+    for (uint32_t s2 = 1; s2 < 32 && !sm; ++s2) {
+      const uint64_t cand = ((uint64_t{1} << s2) + dp.p - 1) / dp.p;
+      bool ok = cand * (p2 - 1) < (uint64_t{1} << 32);
+      for (uint64_t r = 0; ok && r < p2; ++r) ok = ((r * cand) >> s2) == r / dp.p;
+      if (ok) {
+        ss = s2;
+        sm = static_cast<uint32_t>(cand);
+      }
+    }
+    if (!sm) continue;
+    dp.flags |= qmcg::DIM_PAIR;
+    T.pairs[4 * d] = static_cast<uint32_t>(p2);
+    T.pairs[4 * d + 1] = static_cast<uint32_t>(M);
+    T.pairs[4 * d + 2] = sh | (ss << 8);
+    T.pairs[4 * d + 3] = sm;
   }
   T.pack.resize(T.dims.size());
   T.magic64.resize(T.dims.size());
@@ -235,6 +268,7 @@ struct qmcg_ctx {
   DevBuf<double> d_path, d_path_t;   // path matrix [point][path] (+ path-major transpose)
   DevBuf<int32_t> d_ex;              // per-path exercise points
   DevBuf<uint64_t> d_m64;
+  DevBuf<uint32_t> d_pairs;
   DevBuf<double> d_sc, d_nc, d_scnc, d_dpow;
   DevBuf<double> d_values, d_red, d_sums;
   DevBuf<double> d_z, d_bvalues, d_bred, d_bsums;  // batch: shared normal table, per-contract values
@@ -270,6 +304,9 @@ qmcg_status ensure_dim_tables(qmcg_ctx* c, int64_t n, int64_t m) {
   QMCG_CUDA(cudaMemcpyAsync(c->d_dimp.ptr, c->dt.dims.data(), c->dt.dims.size() * sizeof(DimParam),
                             cudaMemcpyHostToDevice, c->stream));
   QMCG_CUDA(c->d_m64.reserve(c->dt.magic64.size()));
+  QMCG_CUDA(c->d_pairs.reserve(c->dt.pairs.size()));
+  QMCG_CUDA(cudaMemcpyAsync(c->d_pairs.ptr, c->dt.pairs.data(), c->dt.pairs.size() * sizeof(uint32_t),
+                            cudaMemcpyHostToDevice, c->stream));
   QMCG_CUDA(c->d_sc.reserve(c->dt.sc.size()));
   QMCG_CUDA(c->d_nc.reserve(c->dt.nc.size()));
   QMCG_CUDA(c->d_scnc.reserve(c->dt.scnc.size()));
@@ -426,6 +463,7 @@ void attach_dims(qmcg_ctx* c, PriceParams& P) {
   P.dims = c->d_pack.ptr;
   P.scnc = reinterpret_cast<const double2*>(c->d_scnc.ptr);
   P.magic64 = c->d_m64.ptr;
+  P.pairs = reinterpret_cast<const uint4*>(c->d_pairs.ptr);
   P.any_wide = c->dt.any_wide;
   P.any_clamp = c->dt.any_clamp;
 }
@@ -556,6 +594,7 @@ void qmcg_destroy(qmcg_ctx* c) {
   drop_cache(c);
   c->d_pack.release();
   c->d_m64.release();
+  c->d_pairs.release();
   c->d_scnc.release();
   c->d_sc.release();
   c->d_nc.release();

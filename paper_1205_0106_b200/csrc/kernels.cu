@@ -345,6 +345,9 @@ __device__ __forceinline__ double halton_digits(uint32_t x, uint32_t p, uint32_t
     const double2 s0 = sn[0];
     return digit_term(x, s0.x, s0.y);
   }
+  // base 2: the digit products d_j 2^-(j+1) and their running sums are exact, so
+  // radical_inverse(x, 2) is the bit reversal of x times 2^-32, exactly
+  if (p == 2u) return static_cast<double>(__brev(x)) * 0x1p-32;
   uint32_t q = divp<WIDE>(x, magic, shift, m64);
   double2 s = sn[0];
   double v = digit_term(x - q * p, s.x, s.y);
@@ -590,6 +593,62 @@ __device__ __forceinline__ void finish_point(uint32_t ws, uint32_t zslot, uint32
   park_point<F32>(zslot, ws + kWTailIdx, idx, central_z<F32>(y, alpha), tail_park<F32>(u, y), y, lt, ntail);
 }
 
+// radical_inverse with the digits taken two at a time (DIM_PAIR): q = x / p^2,
+// r = x - q p^2, high digit (r * sm) >> ss, low digit r - high * p. The products
+// and the running sum are formed digit by digit in the reference's order.
+__device__ __forceinline__ double halton_pairs(uint32_t x, uint32_t p, const uint4& pp, int D,
+                                               const double2* __restrict__ sn) {
+  const uint32_t p2 = pp.x, m2 = pp.y, sh2 = pp.z & 0xffu, ss = pp.z >> 8, sm = pp.w;
+  double v = 0.0;
+  int j = 0;
+#pragma unroll 1
+  for (; j + 2 < D; j += 2) {  // digits j, j+1, neither the last
+    const uint32_t q = __umulhi(x, m2) >> sh2;
+    const uint32_t r = x - q * p2;
+    const uint32_t hi = (r * sm) >> ss;
+    const uint32_t lo = r - hi * p;
+    const double2 s0 = sn[j], s1 = sn[j + 1];
+    v = __dadd_rn(v, digit_term(lo, s0.x, s0.y));
+    v = __dadd_rn(v, digit_term(hi, s1.x, s1.y));
+    x = q;
+  }
+  if (j == D - 2) {  // two digits left: x < p^2
+    const uint32_t hi = (x * sm) >> ss;
+    const double2 s0 = sn[j], s1 = sn[j + 1];
+    v = __dadd_rn(v, digit_term(x - hi * p, s0.x, s0.y));
+    return __dadd_rn(v, digit_term(hi, s1.x, s1.y));
+  }
+  const double2 s0 = sn[j];
+  return __dadd_rn(v, digit_term(x, s0.x, s0.y));
+}
+
+// The same with the digit count fixed at compile time (fully unrolled; the
+// scale loads are independent of the division chain and issue early).
+template <int D>
+__device__ __forceinline__ double halton_pairs_fixed(uint32_t x, uint32_t p, const uint4& pp,
+                                                     const double2* __restrict__ sn) {
+  const uint32_t p2 = pp.x, m2 = pp.y, sh2 = pp.z & 0xffu, ss = pp.z >> 8, sm = pp.w;
+  double2 s[D];
+#pragma unroll
+  for (int j = 0; j < D; ++j) s[j] = __ldg(sn + j);
+  double v = 0.0;
+#pragma unroll
+  for (int j = 0; j + 2 < D; j += 2) {
+    const uint32_t q = __umulhi(x, m2) >> sh2;
+    const uint32_t r = x - q * p2;
+    const uint32_t hi = (r * sm) >> ss;
+    v = __dadd_rn(v, digit_term(r - hi * p, s[j].x, s[j].y));
+    v = __dadd_rn(v, digit_term(hi, s[j + 1].x, s[j + 1].y));
+    x = q;
+  }
+  if (D % 2 == 0) {
+    const uint32_t hi = (x * sm) >> ss;
+    v = __dadd_rn(v, digit_term(x - hi * p, s[D - 2].x, s[D - 2].y));
+    return __dadd_rn(v, digit_term(hi, s[D - 1].x, s[D - 1].y));
+  }
+  return __dadd_rn(v, digit_term(x, s[D - 1].x, s[D - 1].y));
+}
+
 template <bool WIDE>
 __device__ __forceinline__ double halton_any(uint32_t x, const uint4& dp, uint64_t m64, const double2* sn) {
   return halton_digits<WIDE>(x, dp.x, dp.y, dp.z & 0xffu, m64, static_cast<int>((dp.z >> 8) & 0xffu), sn);
@@ -668,6 +727,16 @@ __device__ __forceinline__ void generate_row(const PriceParams& P, uint32_t ws, 
     ntail = generate_row_fixed<4, F32>(sn, magic, shift, negp, ws, pl, zl, nchunks, lane, lt, alpha);
   } else if (!SLOW && D == 2) {
     ntail = generate_row_fixed<2, F32>(sn, magic, shift, negp, ws, pl, zl, nchunks, lane, lt, alpha);
+  } else if (!SLOW && ((dp.z >> 16) & DIM_PAIR)) {
+    const uint4 pp = __ldg(P.pairs + d);
+    for (int ch = 0; ch < nchunks; ++ch) {
+      const uint32_t x = lds_u32(pl + ch * 128);
+      const double u = D == 5   ? halton_pairs_fixed<5>(x, dp.x, pp, sn)
+                       : D == 6 ? halton_pairs_fixed<6>(x, dp.x, pp, sn)
+                       : D == 7 ? halton_pairs_fixed<7>(x, dp.x, pp, sn)
+                                : halton_pairs(x, dp.x, pp, D, sn);
+      finish_point<false, F32>(ws, zl + ch * 32 * Z::kSize, ch * 32 + lane, u, false, alpha, lane, lt, ntail);
+    }
   } else {
     const bool clamp = SLOW && ((dp.z >> 16) & DIM_CLAMP);
     const bool wide = SLOW && ((dp.z >> 16) & DIM_WIDE);

@@ -26,7 +26,10 @@ struct DimParam {
 struct DimPack {
   uint32_t p, magic, meta, doff;
 };
-enum : uint32_t { DIM_CLAMP = 1u, DIM_WIDE = 2u };
+// DIM_PAIR: digits extracted two at a time (divide by p^2, then split the
+// remainder by p), which halves the dependent division chain of bases with
+// many digits; pairs[d] = {p^2, magic(p^2), shift(p^2) | split_shift << 8, split_magic}.
+enum : uint32_t { DIM_CLAMP = 1u, DIM_WIDE = 2u, DIM_PAIR = 4u };
 
 // Error bits raised by the pricing kernel (mapped to the reference's
 // exception text on the host).
@@ -43,6 +46,7 @@ struct PriceParams {
   const DimPack* dims;
   const double2* scnc;     // {sc[j], nc[j]} per digit, indexed by DimPack::doff
   const uint64_t* magic64; // per dimension, used when any dimension needs it
+  const uint4* pairs;      // per dimension, DIM_PAIR parameters
   int32_t any_wide;        // some dimension needs the 64-bit magic division
   int32_t any_clamp;       // some dimension can hit the endpoint clamp
   const double* dpow;    // dpow[k] = disc^k as the host's rounded chain, k = 0..m
