@@ -986,6 +986,8 @@ qmcg_status qmcg_price_american_nodes(qmcg_ctx* c, const qmcg_option_spec* spec,
 qmcg_status qmcg_price_american_batch(qmcg_ctx* c, const qmcg_option_spec* specs, int64_t n_specs, int64_t m,
                                       int64_t n, uint64_t seed, uint32_t flags, qmcg_pricing_result* out) {
   if (!c || !specs || !out || n_specs < 0) return fail(QMCG_INVALID_ARGUMENT, "qmcg_price_american_batch: bad argument");
+  if (flags & QMCG_FLAG_FP32)
+    return fail(QMCG_UNSUPPORTED, "qmcg_price_american_batch: QMCG_FLAG_FP32 is not supported (the batch walk is FP64)");
   const auto t0 = std::chrono::steady_clock::now();
   std::lock_guard<std::mutex> lock(c->mu);
   DeviceGuard g(c->device);

@@ -301,3 +301,12 @@ def _dim_seed(seed, d):
         x = ((x ^ (x >> 27)) * 0x94D049BB133111EB) & (2**64 - 1)
         return x ^ (x >> 31)
     return sm(sm(seed) ^ ((d + 0x632BE59BD9B4E019) & (2**64 - 1)))
+
+
+def test_batch_rejects_fp32(ctx, qmcg):
+    mod = qmcg.qmcg
+    arr = (mod._CSpec * 1)(mod._cspec(spec_of(qmcg, REF)))
+    res = (mod._CResult * 1)()
+    st = ctx._lib.qmcg_price_american_batch(ctx._h, arr, 1, 8, 1024, 42, mod.FLAG_FP32, res)
+    assert st == mod.UNSUPPORTED
+    assert b"FP32" in ctx._lib.qmcg_last_error()
