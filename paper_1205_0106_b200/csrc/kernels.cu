@@ -1333,18 +1333,20 @@ __global__ void fy_assign_kernel(const uint32_t* __restrict__ sk, const uint32_t
                                  uint2* __restrict__ pairs, uint32_t add) {
   const int64_t q = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (q >= n) return;
-  const uint32_t x = sk[q], i = sv[q];
+  // the sorted pairs stream through once (evict-first) so that F, read at random,
+  // keeps its place in L2
+  const uint32_t x = __ldcs(sk + q), i = __ldcs(sv + q);
   uint32_t out = x;
-  if (q + 1 < n && sk[q + 1] == x) {
-    uint32_t y = sv[q + 1];
-    for (uint32_t f = F[y]; f != kNone; f = F[y]) y = f;
+  if (q + 1 < n && __ldcs(sk + q + 1) == x) {
+    uint32_t y = __ldcs(sv + q + 1);
+    for (uint32_t f = __ldg(F + y); f != kNone; f = __ldg(F + y)) y = f;
     out = y;
   }
 #ifdef QMCG_K1_COALESCED_PROBE
   perm[q] = out + i;  // timing probe only: coalesced store (wrong result)
 #else
-  if (pairs) pairs[q] = make_uint2(i, out + add);
-  else perm[i] = out + add;
+  if (pairs) __stcs(pairs + q, make_uint2(i, out + add));
+  else __stcs(perm + i, out + add);
 #endif
 }
 
