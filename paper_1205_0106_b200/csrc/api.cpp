@@ -95,6 +95,26 @@ qmcg_status validate(const qmcg_option_spec& s) {
   return QMCG_OK;
 }
 
+// QMCG_TRACE=1: per-call host phase times on stderr (wall clock, microseconds).
+struct Trace {
+  const char* what;
+  bool on;
+  std::chrono::steady_clock::time_point t0, last;
+  explicit Trace(const char* w) : what(w) {
+    const char* e = std::getenv("QMCG_TRACE");
+    on = e && *e && *e != '0';
+    t0 = last = std::chrono::steady_clock::now();
+  }
+  void mark(const char* phase) {
+    if (!on) return;
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[qmcg trace] %s %-18s %9.1f us (total %9.1f)\n", what, phase,
+                 std::chrono::duration<double, std::micro>(now - last).count(),
+                 std::chrono::duration<double, std::micro>(now - t0).count());
+    last = now;
+  }
+};
+
 uint64_t bits_of(double x) {
   uint64_t u;
   std::memcpy(&u, &x, sizeof u);
@@ -993,11 +1013,13 @@ qmcg_status qmcg_price_american_batch(qmcg_ctx* c, const qmcg_option_spec* specs
   DeviceGuard g(c->device);
   c->launches = 0;
   if (n_specs == 0) return QMCG_OK;
+  Trace tr("batch");
   std::vector<CallPlan> plans(static_cast<size_t>(n_specs));
   for (int64_t i = 0; i < n_specs; ++i) {
     qmcg_status st = plan_call(specs[i], m, n, flags, plans[static_cast<size_t>(i)]);
     if (st) return st;
   }
+  tr.mark("plans");
   qmcg_status st = ensure_dim_tables(c, n, m);
   if (st) return st;
   st = ensure_perms(c, seed, n, 0, n, m, (flags & QMCG_FLAG_NO_CACHE) != 0);
@@ -1015,6 +1037,7 @@ qmcg_status qmcg_price_american_batch(qmcg_ctx* c, const qmcg_option_spec* specs
                               c->stream));
     QMCG_CUDA(cudaStreamSynchronize(c->stream));
   }
+  tr.mark("tables+dpow");
   // Contracts on the plain path share one normal table (generated once, inside
   // this call) and are walked kCpt per thread; the rest use the fused kernel.
   std::vector<int64_t> shared_idx[2], single_idx;
@@ -1044,6 +1067,7 @@ qmcg_status qmcg_price_american_batch(qmcg_ctx* c, const qmcg_option_spec* specs
     G.alpha = 0.0;
     QMCG_CUDA(qmcg::launch_gen_z(G, c->d_z.ptr, n, c->stream, qmcg::batch_uses_prefix()));
     c->launches += 1;
+    tr.mark("gen_z enqueued");
     for (int k = 0; k < 2; ++k) {
       const size_t cnt = shared_idx[k].size();
       if (!cnt) continue;
@@ -1123,6 +1147,7 @@ qmcg_status qmcg_price_american_batch(qmcg_ctx* c, const qmcg_option_spec* specs
       QMCG_CUDA(cudaMemcpyAsync(shared_sums[k].data(), c->d_bsums.ptr, 2 * cnt * sizeof(double),
                                 cudaMemcpyDeviceToHost, c->stream));
       QMCG_CUDA(cudaStreamSynchronize(c->stream));  // d_cparams / d_bsums are reused by the next kind
+      tr.mark(k == 0 ? "calls done" : "puts done");
     }
   }
   std::vector<double> sums;

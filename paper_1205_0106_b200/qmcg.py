@@ -95,6 +95,16 @@ class _CResult(C.Structure):
                 ("elapsed_s", C.c_double), ("method", C.c_int32), ("seed", C.c_uint64)]
 
 
+# numpy views of the C structs (qmcg_option_spec / qmcg_pricing_result), for column-wise batches
+_SPEC_DT = np.dtype({"names": [f[0] for f in _CSpec._fields_],
+                     "formats": [np.float64] * 5 + [np.int32],
+                     "offsets": [getattr(_CSpec, f[0]).offset for f in _CSpec._fields_],
+                     "itemsize": C.sizeof(_CSpec)})
+_RESULT_DT = np.dtype({"names": [f[0] for f in _CResult._fields_],
+                       "formats": [np.float64, np.float64, np.int64, np.float64, np.int32, np.uint64],
+                       "offsets": [getattr(_CResult, f[0]).offset for f in _CResult._fields_],
+                       "itemsize": C.sizeof(_CResult)})
+
 _lib = None
 _lib_lock = threading.Lock()
 
@@ -229,6 +239,24 @@ class Context:
         _check(self._lib.qmcg_price_american_batch(self._h, arr, len(specs), int(m), int(n_paths), int(seed),
                                                     flags, res))
         return [_result(r) for r in res]
+
+    def price_american_batch_arrays(self, spot, strike, rate, volatility, maturity, kind, m: int, n_paths: int,
+                                    seed: int, allow_put: bool = False) -> np.ndarray:
+        """Batch pricing from column arrays (one entry per contract; scalars broadcast), returning a
+        (C, 2) array of (price, std_error) -- the same call as price_american_batch without per-contract
+        Python objects, for large batches."""
+        cols = np.broadcast_arrays(*(np.asarray(x, dtype=np.float64) for x in (spot, strike, rate, volatility,
+                                                                                  maturity)),
+                                   np.asarray(kind, dtype=np.int32))
+        cnt = cols[0].size
+        specs = np.zeros(cnt, dtype=_SPEC_DT)
+        for name, col in zip(("spot", "strike", "rate", "volatility", "maturity", "kind"), cols):
+            specs[name] = col.reshape(-1)
+        res = np.zeros(cnt, dtype=_RESULT_DT)
+        _check(self._lib.qmcg_price_american_batch(self._h, specs.ctypes.data_as(C.POINTER(_CSpec)), cnt, int(m),
+                                                    int(n_paths), int(seed), FLAG_ALLOW_PUT if allow_put else 0,
+                                                    res.ctypes.data_as(C.POINTER(_CResult))))
+        return np.stack([res["price"], res["std_error"]], axis=1)
 
     def price_american_node(self, spec: OptionSpec, m: int, n_paths: int, seed: int, depth: int, node: int,
                             allow_put: bool = False, fp32: bool = False) -> np.ndarray:

@@ -310,3 +310,14 @@ def test_batch_rejects_fp32(ctx, qmcg):
     st = ctx._lib.qmcg_price_american_batch(ctx._h, arr, 1, 8, 1024, 42, mod.FLAG_FP32, res)
     assert st == mod.UNSUPPORTED
     assert b"FP32" in ctx._lib.qmcg_last_error()
+
+
+def test_batch_arrays_api(ctx, qmcg):
+    """Column-array batch entry == the list-of-specs entry, bit for bit."""
+    K = np.array([90.0, 100.0, 110.0, 95.0])
+    vol = np.array([0.2, 0.2, 0.3, 0.25])
+    kind = np.array([0, 1, 0, 1])
+    arr = ctx.price_american_batch_arrays(100.0, K, 0.05, vol, 1.0, kind, 16, 5000, 42, allow_put=True)
+    lst = ctx.price_american_batch([spec_of(qmcg, (100.0, k, 0.05, v, 1.0), int(t)) for k, v, t in zip(K, vol, kind)],
+                                   16, 5000, 42, allow_put=True)
+    assert np.array_equal(arr, np.array([(r.price, r.std_error) for r in lst]))
