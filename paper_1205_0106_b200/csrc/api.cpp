@@ -291,9 +291,10 @@ struct qmcg_ctx {
   DevBuf<uint32_t> d_pairs;
   DevBuf<double> d_sc, d_nc, d_scnc, d_dpow;
   DevBuf<double> d_values, d_red, d_sums;
-  DevBuf<double> d_z, d_bvalues, d_bred, d_bsums;  // batch: shared normal table, per-contract values
-  DevBuf<qmcg::ContractParams> d_cparams;
-  DevBuf<qmcg::GroupParams> d_groups;
+  DevBuf<double> d_z;                                // batch: shared normal (prefix-sum) table
+  DevBuf<double> d_bvalues[2], d_bred[2], d_bsums[2];  // per kind: per-contract values, scratch, sums
+  DevBuf<qmcg::ContractParams> d_cparams[2];
+  DevBuf<qmcg::GroupParams> d_groups[2];
   DevBuf<uint32_t> d_err, d_fullperm;
   DevBuf<char> d_permscratch;
   // streamed tables (date windows): per-path walk state carried between windows
@@ -622,11 +623,13 @@ void qmcg_destroy(qmcg_ctx* c) {
   c->d_values.release();
   c->d_red.release();
   c->d_z.release();
-  c->d_bvalues.release();
-  c->d_bred.release();
-  c->d_bsums.release();
-  c->d_cparams.release();
-  c->d_groups.release();
+  for (int k = 0; k < 2; ++k) {
+    c->d_bvalues[k].release();
+    c->d_bred[k].release();
+    c->d_bsums[k].release();
+    c->d_cparams[k].release();
+    c->d_groups[k].release();
+  }
   c->d_sums.release();
   c->d_err.release();
   c->d_fullperm.release();
@@ -846,11 +849,13 @@ static qmcg_status price_nodes(qmcg_ctx* c, const qmcg_option_spec* spec, int64_
   tree_node(n, depth, node0, b, size);
   tree_node(n, depth, node0 + count - 1, off, size);
   e = off + size;
+  Trace tr("price");
   CallPlan plan;
   qmcg_status st = plan_call(*spec, m, n, flags, plan);
   if (st) return st;
   st = upload_plan(c, plan, n);
   if (st) return st;
+  tr.mark("plan+upload");
   const bool rebuild = (flags & QMCG_FLAG_NO_CACHE) != 0;
   const bool cached = !rebuild && c->cache_n == n && c->cache_seed == seed && c->col_begin == b &&
                       c->col_end == e && c->cache_dims >= m;
@@ -880,9 +885,11 @@ static qmcg_status price_nodes(qmcg_ctx* c, const qmcg_option_spec* spec, int64_
                                     c->stream, &launches));
     c->launches += launches;
   }
+  tr.mark(streamed ? "streamed enqueued" : "enqueued");
   std::vector<double> out;
   st = sync_results(c, static_cast<size_t>(count), out);
   if (st) return st;
+  tr.mark("synced");
   std::copy(out.begin(), out.end(), sums);
   return QMCG_OK;
 }
@@ -1107,8 +1114,8 @@ qmcg_status qmcg_price_american_batch(qmcg_ctx* c, const qmcg_option_spec* specs
         groups.push_back(gp);
         j = e;
       }
-      QMCG_CUDA(c->d_groups.reserve(groups.size()));
-      QMCG_CUDA(cudaMemcpyAsync(c->d_groups.ptr, groups.data(), groups.size() * sizeof(qmcg::GroupParams),
+      QMCG_CUDA(c->d_groups[k].reserve(groups.size()));
+      QMCG_CUDA(cudaMemcpyAsync(c->d_groups[k].ptr, groups.data(), groups.size() * sizeof(qmcg::GroupParams),
                                 cudaMemcpyHostToDevice, c->stream));
       std::vector<qmcg::ContractParams> cps(cnt);
       for (size_t j = 0; j < cnt; ++j) {
@@ -1117,38 +1124,39 @@ qmcg_status qmcg_price_american_batch(qmcg_ctx* c, const qmcg_option_spec* specs
                                       P.dom_slope, P.bs_vsqrt, P.bs_mu_t, P.bs_kdisc, P.bs_fwd_growth, P.bs_disc,
                                       P.x0mk, P.bs_v_zero, 0};
       }
-      QMCG_CUDA(c->d_cparams.reserve(cnt));
-      QMCG_CUDA(cudaMemcpyAsync(c->d_cparams.ptr, cps.data(), cnt * sizeof(qmcg::ContractParams),
+      QMCG_CUDA(c->d_cparams[k].reserve(cnt));
+      QMCG_CUDA(cudaMemcpyAsync(c->d_cparams[k].ptr, cps.data(), cnt * sizeof(qmcg::ContractParams),
                                 cudaMemcpyHostToDevice, c->stream));
-      QMCG_CUDA(c->d_bvalues.reserve(cnt * static_cast<size_t>(n) + 16));
+      QMCG_CUDA(c->d_bvalues[k].reserve(cnt * static_cast<size_t>(n) + 16));
 #ifdef QMCG_COUNT_PUSHES
-      QMCG_CUDA(cudaMemsetAsync(c->d_bvalues.ptr + cnt * static_cast<size_t>(n), 0, 16, c->stream));
+      QMCG_CUDA(cudaMemsetAsync(c->d_bvalues[k].ptr + cnt * static_cast<size_t>(n), 0, 16, c->stream));
 #endif
-      QMCG_CUDA(c->d_bred.reserve(cnt * qmcg::reduce_scratch_doubles(n)));
-      QMCG_CUDA(c->d_bsums.reserve(2 * cnt));
-      qmcg::BatchParams B{c->d_z.ptr, n, n, static_cast<int32_t>(m), static_cast<int32_t>(cnt), c->d_cparams.ptr,
-                          c->d_bvalues.ptr, cps.data(), c->d_groups.ptr, static_cast<int32_t>(groups.size()), 0};
+      QMCG_CUDA(c->d_bred[k].reserve(cnt * qmcg::reduce_scratch_doubles(n)));
+      QMCG_CUDA(c->d_bsums[k].reserve(2 * cnt));
+      qmcg::BatchParams B{c->d_z.ptr, n, n, static_cast<int32_t>(m), static_cast<int32_t>(cnt), c->d_cparams[k].ptr,
+                          c->d_bvalues[k].ptr, cps.data(), c->d_groups[k].ptr, static_cast<int32_t>(groups.size()), 0};
       if (qmcg::batch_grouped()) QMCG_CUDA(qmcg::launch_walk_group(B, k, c->stream));
       else QMCG_CUDA(qmcg::launch_walk_batch(B, k, c->stream));
       int launches = 1;
-      QMCG_CUDA(qmcg::launch_pairwise_batched(c->d_bvalues.ptr, n, static_cast<int>(cnt), c->d_bred.ptr,
-                                              c->d_bsums.ptr, c->stream, &launches));
+      QMCG_CUDA(qmcg::launch_pairwise_batched(c->d_bvalues[k].ptr, n, static_cast<int>(cnt), c->d_bred[k].ptr,
+                                              c->d_bsums[k].ptr, c->stream, &launches));
       c->launches += launches;
 #ifdef QMCG_COUNT_PUSHES
       {
         unsigned long long cntr[2];
         cudaStreamSynchronize(c->stream);
-        cudaMemcpy(cntr, c->d_bvalues.ptr + cnt * static_cast<size_t>(n), 16, cudaMemcpyDeviceToHost);
+        cudaMemcpy(cntr, c->d_bvalues[k].ptr + cnt * static_cast<size_t>(n), 16, cudaMemcpyDeviceToHost);
         std::fprintf(stderr, "kind %d: pushes %llu records %llu (per path-contract %.3f / %.3f)\n", k, cntr[0], cntr[1],
                      cntr[0] / double(cnt * n), cntr[1] / double(cnt * n));
       }
 #endif
-      shared_sums[k].resize(2 * cnt);
-      QMCG_CUDA(cudaMemcpyAsync(shared_sums[k].data(), c->d_bsums.ptr, 2 * cnt * sizeof(double),
-                                cudaMemcpyDeviceToHost, c->stream));
-      QMCG_CUDA(cudaStreamSynchronize(c->stream));  // d_cparams / d_bsums are reused by the next kind
-      tr.mark(k == 0 ? "calls done" : "puts done");
+      shared_sums[k].resize(2 * cnt);  // read back with the other results (no sync between the kinds)
+      tr.mark(k == 0 ? "calls enqueued" : "puts enqueued");
     }
+    for (int k = 0; k < 2; ++k)
+      if (!shared_sums[k].empty())
+        QMCG_CUDA(cudaMemcpyAsync(shared_sums[k].data(), c->d_bsums[k].ptr, shared_sums[k].size() * sizeof(double),
+                                  cudaMemcpyDeviceToHost, c->stream));
   }
   std::vector<double> sums;
   st = sync_results(c, static_cast<size_t>(n_specs), sums);
