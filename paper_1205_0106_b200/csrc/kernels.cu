@@ -2134,18 +2134,24 @@ __global__ void __launch_bounds__(kGThreads, QMCG_G_MINB) walk_group_kernel(cons
           : "d"(alpha), "d"(kd), "d"(S), "d"(beta), "r"(cs), "r"(cj), "r"(d)
           : "memory");
     } else {
-      const double V = fma(alpha, kd, S);
-      const bool rec = V < c;
-      cd = __dadd_rn(cd, beta);
-      const bool push = rec && pend >= 0 && !record_dominates<1>(V, c, cd, gb, gx);
-      if (push) {
-        sts_f64(cs + cnt * 8, c);
-        sts_u32(cj + cnt * 4, static_cast<uint32_t>(pend));
-      }
-      cnt += push ? 1 : 0;
-      c = rec ? V : c;
-      cd = rec ? 0.0 : cd;
-      pend = rec ? d : pend;
+      // puts, predicated: rec = V < c; acc += slope; dominated iff u1 > 0 && s < 2 &&
+      // u1 s (1 - s/2) >= acc (1 + 1e-12) (record_dominates<1>); push = rec && pending && !dominated
+      asm volatile(
+          "{\n .reg .pred r, pe, a, b, e, dm, pu;\n .reg .f64 v, u1, dv, s, t, pr, th;\n .reg .b32 ad;\n"
+          " fma.rn.f64 v, %4, %5, %6;\n add.rn.f64 %1, %1, %7;\n"
+          " setp.lt.f64 r, v, %0;\n setp.ge.s32 pe, %2, 0;\n"
+          " fma.rn.f64 u1, %8, %0, %9;\n sub.rn.f64 dv, %0, v;\n fma.rn.f64 s, %8, dv, %1;\n"
+          " fma.rn.f64 t, 0dBFE0000000000000, s, 0d3FF0000000000000;\n mul.rn.f64 pr, u1, s;\n mul.rn.f64 pr, pr, t;\n"
+          " mul.rn.f64 th, %1, 0d3FF0000000001198;\n"
+          " setp.gt.f64 a, u1, 0d0000000000000000;\n setp.lt.and.f64 b, s, 0d4000000000000000, a;\n"
+          " setp.ge.and.f64 dm, pr, th, b;\n"
+          " and.pred pu, r, pe;\n not.pred e, dm;\n and.pred pu, pu, e;\n"
+          " mad.lo.u32 ad, %3, 8, %10;\n @pu st.shared.f64 [ad], %0;\n"
+          " mad.lo.u32 ad, %3, 4, %11;\n @pu st.shared.u32 [ad], %2;\n @pu add.u32 %3, %3, 1;\n"
+          " selp.f64 %0, v, %0, r;\n selp.f64 %1, 0d0000000000000000, %1, r;\n selp.b32 %2, %12, %2, r;\n}"
+          : "+d"(c), "+d"(cd), "+r"(pend), "+r"(cnt)
+          : "d"(alpha), "d"(kd), "d"(S), "d"(beta), "d"(gb), "d"(gx), "r"(cs), "r"(cj), "r"(d)
+          : "memory");
     }
   };
   // rare: keep room for the next `room` candidates
