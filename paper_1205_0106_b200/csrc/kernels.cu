@@ -908,6 +908,30 @@ __global__ void __launch_bounds__(kThreads, QMCG_MINB) price_kernel(const PriceP
           push_record<KIND, RNEG>(ws, P, pu32 != 0, pv, k0 + pdl, lane, lt, rq_head, rq_tail);
           continue;
         }
+        if constexpr (KIND == 1 && !F32) {
+          // puts, FP64, predicated: the accumulator bound of record_dominates<1> (V and cd
+          // already advanced above); a pending record exists iff pl + k0 >= 0
+          (void)rec;
+          (void)push;
+          double pv;
+          int pdl;
+          uint32_t pu32;
+          asm volatile(
+              "{\n .reg .pred r, pe, a, b, e, dm, pu;\n .reg .f64 u1, dv, s, t, pr, th;\n .reg .s32 pk;\n"
+              " setp.lt.f64 r, %0, %1;\n add.s32 pk, %3, %8;\n setp.ge.s32 pe, pk, 0;\n"
+              " fma.rn.f64 u1, %9, %1, %10;\n sub.rn.f64 dv, %1, %0;\n fma.rn.f64 s, %9, dv, %2;\n"
+              " fma.rn.f64 t, 0dBFE0000000000000, s, 0d3FF0000000000000;\n mul.rn.f64 pr, u1, s;\n"
+              " mul.rn.f64 pr, pr, t;\n mul.rn.f64 th, %2, 0d3FF0000000001198;\n"
+              " setp.gt.f64 a, u1, 0d0000000000000000;\n setp.lt.and.f64 b, s, 0d4000000000000000, a;\n"
+              " setp.ge.and.f64 dm, pr, th, b;\n and.pred pu, r, pe;\n not.pred e, dm;\n and.pred pu, pu, e;\n"
+              " mov.b64 %4, %1;\n mov.b32 %5, %3;\n"
+              " selp.f64 %1, %0, %1, r;\n selp.f64 %2, 0d0000000000000000, %2, r;\n selp.b32 %3, %7, %3, r;\n"
+              " selp.u32 %6, 1, 0, pu;\n}"
+              : "+d"(V), "+d"(c), "+d"(cd), "+r"(pl), "=d"(pv), "=r"(pdl), "=r"(pu32)
+              : "r"(t), "r"(k0), "d"(P.b), "d"(P.x0mk));
+          push_record<KIND, RNEG>(ws, P, pu32 != 0, pv, k0 + pdl, lane, lt, rq_head, rq_tail);
+          continue;
+        }
 #endif
 #if QMCG_WALK_V == 1
         push_record<KIND, RNEG>(ws, P, push, c, k0 + pl, lane, lt, rq_head, rq_tail);
