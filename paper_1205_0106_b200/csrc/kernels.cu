@@ -39,7 +39,11 @@ constexpr int kWarps = kThreads / 32;
 #define QMCG_MINB 4
 #endif
 constexpr int kTile = kWarps;  // dates per tile = warps per block (one date row per warp)
-constexpr int kRecCap = 128;  // per-warp ring of pending record evaluations (mostly drained at path end)
+#ifndef QMCG_REC_CAP
+#define QMCG_REC_CAP 128
+#endif
+constexpr int kRecCap = QMCG_REC_CAP;  // per-warp ring of pending record evaluations (mostly drained at path end)
+static_assert(kRecCap >= 64 && (kRecCap & (kRecCap - 1)) == 0, "record ring: power of two with room for one date");
 constexpr uint32_t kNone = 0xffffffffu;
 constexpr int kBins = 256;             // K1 binned scatter (== the bin kernel's block size)
 constexpr int kCursorStride = 32;      // one 128-byte line per bin cursor (spreads the atomics over L2 slices)
@@ -178,9 +182,26 @@ __device__ __forceinline__ double dev_log(double x, uint32_t tab) {
   return fma(de, c_log_consts[1], t.y + p);
 }
 
+// -log(x) with the same reduction (the negation folded into the final FMA).
+__device__ __forceinline__ double dev_neglog(double x, uint32_t tab) {
+  const int hi = __double2hiint(x);
+  const int lo = __double2loint(x);
+  const int e = (hi >> 20) - 1023;
+  const double2 t = lds_v2f64(tab + (static_cast<uint32_t>(hi >> 9) & 0x7f0u));
+  const double m = __hiloint2double((hi & 0x000fffff) | 0x3ff00000, lo);
+  const double f = fma(m, t.x, -1.0);
+  double q = fma(f, -0x1.5555555555555p-3, 0x1.999999999999ap-3);
+  q = fma(f, q, -0.25);
+  q = fma(f, q, 0x1.5555555555555p-2);
+  q = fma(f, q, -0.5);
+  const double p = fma(f * f, q, f);
+  const double de = __dadd_rn(__hiloint2double(0x43300000, e + 1024), -c_log_consts[0]);
+  return fma(de, -c_log_consts[1], -(t.y + p));
+}
+
 // Moro log-log tail polynomial (analytic.cpp:95-99) for w = u or 1-u.
 __device__ __forceinline__ double moro_tail_poly(double w, uint32_t tab) {
-  const double z = dev_log(-dev_log(w, tab), tab);
+  const double z = dev_log(dev_neglog(w, tab), tab);
   double x = c_moro_c[8];
 #pragma unroll
   for (int i = 7; i >= 0; --i) x = fma(x, z, c_moro_c[i]);
@@ -383,7 +404,14 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
 constexpr uint32_t kTailCap = kThreads;  // a whole date row can be queued: no mid-row flush
 constexpr uint32_t kPermOff = 0;
 constexpr uint32_t kPermBuf = kTile * kThreads * 4;
-constexpr uint32_t kZtOff = kPermOff + 2 * kPermBuf;
+#ifndef QMCG_PERM_BUFFERS
+#define QMCG_PERM_BUFFERS 1
+#endif
+// 2: permutation rows double-buffered (row of tile k + 2 staged after tile k);
+// 1: one buffer, the row of tile k + 1 staged as soon as the warp has read row k
+// (measured 1.2% faster at config 3: the copy is in flight during the walk).
+constexpr int kPermBuffers = QMCG_PERM_BUFFERS;
+constexpr uint32_t kZtOff = kPermOff + kPermBuffers * kPermBuf;
 constexpr uint32_t kZtBuf = kTile * kThreads * 8;
 #ifndef QMCG_ZT_BUFFERS
 #define QMCG_ZT_BUFFERS 1
@@ -394,6 +422,7 @@ constexpr int kZtBuffers = QMCG_ZT_BUFFERS;
 constexpr uint32_t kLogOff = kZtOff + kZtBuffers * kZtBuf;
 constexpr uint32_t kBarOff = kLogOff + 128 * 16;
 constexpr uint32_t kWarpOff = kBarOff + 128;
+static_assert(2 * kTile * 8 <= 128, "row mbarriers bar[2][kTile]");
 constexpr uint32_t kWRqV = 0;
 constexpr uint32_t kWBest = kWRqV + kRecCap * 8;
 constexpr uint32_t kWRqCode = kWBest + 32 * 8;
@@ -453,21 +482,27 @@ __device__ __forceinline__ double rneg_threshold(const PriceParams& P, double be
   return room > 0.0 ? (log(room) - P.X0) / P.b : -INFINITY;
 }
 
-// Issue the bulk copies of tile `k` (dates [k*kTile, ...)) into buffer b.
-__device__ __forceinline__ void issue_tile(const PriceParams& P, uint32_t sbase, int d0, int b, int64_t col0,
-                                           uint32_t bytes) {
-  const int rows = min(kTile, P.d_end - d0);
-  const uint32_t bar = sbase + kBarOff + b * 8;
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
-               "r"(static_cast<uint32_t>(rows) * bytes)
-               : "memory");
-  for (int t = 0; t < rows; ++t) {
-    const uint32_t dst = sbase + kPermOff + b * kPermBuf + t * kThreads * 4;
-    const uint32_t* src = P.perm + static_cast<int64_t>(d0 + t - P.perm_row0) * P.ld + col0;
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
-        "l"(src), "r"(bytes), "r"(bar)
-        : "memory");
+// Issue the bulk copy of one permutation row (date d) into row w of buffer b,
+// completing on that row's own mbarrier (bar[b][w]). Each warp stages the row
+// it generates, right after it has consumed the previous contents, so no warp
+// waits for a block-wide copy and no single thread issues a whole tile.
+__device__ __forceinline__ void issue_row(const PriceParams& P, uint32_t sbase, int d, int b, int w, int64_t col0,
+                                          uint32_t bytes) {
+  const uint32_t bar = sbase + kBarOff + (b * kTile + w) * 8;
+  const uint32_t dst = sbase + kPermOff + b * kPermBuf + w * kThreads * 4;
+  const uint32_t* src = P.perm + static_cast<int64_t>(d - P.perm_row0) * P.ld + col0;
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+      "l"(src), "r"(bytes), "r"(bar)
+      : "memory");
+}
+
+// mbarriers bar[2][kTile] (one per buffer and row), arrival count 1.
+__device__ __forceinline__ void init_row_barriers(uint32_t sbase) {
+  if (threadIdx.x < 2 * kTile) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sbase + kBarOff + threadIdx.x * 8));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
 }
 
@@ -555,27 +590,57 @@ __device__ __forceinline__ void park_point(uint32_t zslot, uint32_t qbase, uint3
   ntail += __popc(b);
 }
 
-// Evaluate the queued Moro-tail points of one date row, 32 per round:
-// u (parked in the point's z slot) -> y = u - 0.5 (exact as the reference),
-// w = u or 1 - u, z = +-P8(log(-log w)) + alpha written back to the slot.
+// One queued Moro-tail point: u (parked in its z slot) -> w = u or 1 - u,
+// z = +-P8(log(-log w)) + alpha. A queued point has u < 0.08 or u > 0.92, so
+// y = u - 1/2 > 0 iff the high word of u is at least that of 0.5 (integer
+// test, no FP64 compare); -x for y < 0 by flipping the sign bit.
+__device__ __forceinline__ double tail_z(double u, uint32_t logtab, double alpha) {
+  const bool up = __double2hiint(u) >= 0x3fe00000;
+  const double x = moro_tail_poly(up ? __dadd_rn(1.0, -u) : u, logtab);
+  const double sx =
+      __hiloint2double(__double2hiint(x) ^ (up ? 0 : static_cast<int>(0x80000000u)), __double2loint(x));
+  return __dadd_rn(sx, alpha);
+}
+
+// Evaluate the queued Moro-tail points of one date row. Two rounds of 32 are
+// evaluated together (each lane carries two independent points), so a row's
+// typical 33-64 tail points cost one dependency chain instead of two; lanes
+// past the queue end compute a duplicate of entry 0 and do not store it.
 template <bool F32>
 __device__ __forceinline__ void flush_tail(uint32_t ws, uint32_t zrow, uint32_t ntail, uint32_t logtab, double alpha,
                                            int lane) {
   using Z = ZSlot<F32>;
   __syncwarp();
-  for (uint32_t r = 0; r < ntail; r += 32) {
-    const uint32_t q = r + lane;
-    if (q < ntail) {
-      const uint32_t slot = zrow + lds_u8(ws + kWTailIdx + q) * Z::kSize;
-      if (F32) {
+#ifdef QMCG_PROBE_FULLROUNDS  // timing probe only (wrong results): skip the partial last round
+  ntail &= ~31u;
+#endif
+  const uint32_t qbase = ws + kWTailIdx;
+  if (F32) {
+    for (uint32_t r = 0; r < ntail; r += 32) {
+      const uint32_t q = r + lane;
+      if (q < ntail) {
+        const uint32_t slot = zrow + lds_u8(qbase + q) * Z::kSize;
         const float wsg = Z::load(slot);
         const float x = moro_tail_poly_f32(fabsf(wsg));
         Z::store(slot, (wsg < 0.0f ? x : -x) + static_cast<float>(alpha));
+      }
+    }
+  } else {
+    for (uint32_t r = 0; r < ntail; r += 64) {
+      const uint32_t qa = r + lane, qb = r + 32 + lane;
+      const bool va = qa < ntail, vb = qb < ntail;
+      const uint32_t sa = zrow + lds_u8(qbase + (va ? qa : 0u)) * 8;
+      if (r + 32 < ntail) {  // warp-uniform: a second round exists
+        const uint32_t sb = zrow + lds_u8(qbase + (vb ? qb : 0u)) * 8;
+        const double za = tail_z(lds_f64(sa), logtab, alpha);
+        const double zb = tail_z(lds_f64(sb), logtab, alpha);
+        __syncwarp();  // every lane has read its u before any slot is overwritten
+        if (va) sts_f64(sa, za);
+        if (vb) sts_f64(sb, zb);
       } else {
-        const double u = Z::load(slot);
-        const double y = __dadd_rn(u, -0.5);
-        const double x = moro_tail_poly(y > 0.0 ? __dadd_rn(1.0, -u) : u, logtab);
-        Z::store(slot, (y > 0.0 ? x : -x) + alpha);
+        const double za = tail_z(lds_f64(sa), logtab, alpha);
+        __syncwarp();
+        if (va) sts_f64(sa, za);
       }
     }
   }
@@ -747,7 +812,9 @@ __device__ __forceinline__ void generate_row(const PriceParams& P, uint32_t ws, 
       finish_point<SLOW, F32>(ws, zl + ch * 32 * Z::kSize, ch * 32 + lane, u, clamp, alpha, lane, lt, ntail);
     }
   }
+#ifndef QMCG_PROBE_NOTAIL  // timing probe only (wrong results): skip the Moro tail
   if (ntail) flush_tail<F32>(ws, zrow, ntail, logtab, alpha, lane);
+#endif
 }
 
 // Dominance of the lane's pending record j by a new record k (then j can never
@@ -804,7 +871,8 @@ __device__ __forceinline__ void push_record(uint32_t ws, const PriceParams& P, b
 template <int KIND, bool RNEG, bool SLOW, bool F32>
 __global__ void __launch_bounds__(kThreads, QMCG_MINB) price_kernel(const PriceParams P) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  const uint32_t sbase = smem_u32(smem_raw);
+  uint32_t sbase = smem_u32(smem_raw);
+  asm volatile("mov.b32 %0, %0;" : "+r"(sbase));  // computed once (no shared-window rebuild in the loops)
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const uint32_t ws = sbase + kWarpOff + warp * kWarpBytes;
@@ -830,11 +898,7 @@ __global__ void __launch_bounds__(kThreads, QMCG_MINB) price_kernel(const PriceP
   if constexpr (!F32) asm volatile("mov.b64 %0, %0;" : "+d"(slope));  // keep it in a register (no per-date reload)
   const T bT = static_cast<T>(P.b), x0mkT = static_cast<T>(P.x0mk);
 
-  if (threadIdx.x == 0) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sbase + kBarOff));
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sbase + kBarOff + 8));
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
+  init_row_barriers(sbase);
   asm volatile("st.shared.u64 [%0], %1;" ::"r"(ws + kWBest + lane * 8),
                "l"(static_cast<unsigned long long>(__double_as_longlong(P.best0)))
                : "memory");
@@ -854,9 +918,9 @@ __global__ void __launch_bounds__(kThreads, QMCG_MINB) price_kernel(const PriceP
   }
   if (threadIdx.x < 128) sts_v2f64(logtab + threadIdx.x * 16, c_log_table[threadIdx.x]);
   __syncthreads();
-  if (threadIdx.x == 0 && !det) {
-    issue_tile(P, sbase, dbeg, 0, col0, bytes);
-    if (ntiles > 1) issue_tile(P, sbase, dbeg + kTile, 1, col0, bytes);
+  if (lane == 0 && !det) {
+    if (dbeg + warp < dend) issue_row(P, sbase, dbeg + warp, 0, warp, col0, bytes);
+    if (kPermBuffers == 2 && dbeg + kTile + warp < dend) issue_row(P, sbase, dbeg + kTile + warp, 1, warp, col0, bytes);
   }
 
   uint32_t rq_head = 0, rq_tail = 0;
@@ -868,20 +932,34 @@ __global__ void __launch_bounds__(kThreads, QMCG_MINB) price_kernel(const PriceP
     const uint32_t zb = kZtBuffers == 2 ? b : 0;
     const uint32_t zcol = sbase + kZtOff + zb * kZtBuf + threadIdx.x * Z::kSize;
     if (!det) {
-      mbar_wait_u32(sbase + kBarOff + b * 8, static_cast<uint32_t>((k >> 1) & 1));
-      if (k0 + warp < dend)
-        generate_row<SLOW, F32>(P, ws, k0 + warp, sbase + kPermOff + b * kPermBuf + warp * kThreads * 4,
+      if (k0 + warp < dend) {
+        const int pb = kPermBuffers == 2 ? b : 0;
+        mbar_wait_u32(sbase + kBarOff + (pb * kTile + warp) * 8,
+                      static_cast<uint32_t>(kPermBuffers == 2 ? (k >> 1) & 1 : k & 1));
+        generate_row<SLOW, F32>(P, ws, k0 + warp, sbase + kPermOff + pb * kPermBuf + warp * kThreads * 4,
                                 sbase + kZtOff + zb * kZtBuf + warp * kThreads * Z::kSize, logtab, nchunks, lane, lt);
-      __syncthreads();  // z tile complete; perm buffer b consumed
-      if (threadIdx.x == 0 && k + 2 < ntiles) issue_tile(P, sbase, k0 + 2 * kTile, b, col0, bytes);
+        __syncwarp();  // this warp's perm row is consumed: stage its row of the tile kPermBuffers ahead
+        const int dn = k0 + kPermBuffers * kTile + warp;
+        if (lane == 0 && dn < dend) issue_row(P, sbase, dn, pb, warp, col0, bytes);
+      }
+      __syncthreads();  // z tile complete
     }
     // ---- walk ----
     // c = V of the last record (= the pending record when pend_d >= 0);
     // cd = the dominance accumulator of the pending record (record_dominates).
+#ifdef QMCG_PROBE_NOWALK  // timing probe only (wrong results): V only, no record logic
+    if (!SLOW && !RNEG && k0 + kTile <= mrec) {
+#pragma unroll
+      for (int t = 0; t < kTile; ++t) V = add_rn(V, Z::load(zcol + t * kThreads * Z::kSize));
+    } else
+#endif
     if (!SLOW && !RNEG && k0 + kTile <= mrec) {
       // pending date kept tile-relative (the select takes t as an immediate);
       // calls need no "pending exists" test: cd = -inf until the first record
       int pl = pend_d - k0;
+#ifdef QMCG_SLOPE_REG
+      if constexpr (!F32) asm volatile("mov.b64 %0, %0;" : "+d"(slope));  // register for the tile (no per-date reload)
+#endif
 #pragma unroll
       for (int t = 0; t < kTile; ++t) {
         V = add_rn(V, Z::load(zcol + t * kThreads * Z::kSize));
@@ -1078,28 +1156,29 @@ __global__ void __launch_bounds__(kThreads, QMCG_MINB) gen_z_kernel(const PriceP
   const int nchunks = static_cast<int>((block_paths + 31) / 32);
   const int64_t col0 = P.path_begin - P.col_begin + block_first;
   const uint32_t bytes = static_cast<uint32_t>(((block_paths + 3) / 4) * 16);
-  if (threadIdx.x == 0) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sbase + kBarOff));
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sbase + kBarOff + 8));
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
+  init_row_barriers(sbase);
   if (threadIdx.x < 128) sts_v2f64(logtab + threadIdx.x * 16, c_log_table[threadIdx.x]);
   __syncthreads();
-  if (threadIdx.x == 0) {
-    issue_tile(P, sbase, 0, 0, col0, bytes);
-    if (ntiles > 1) issue_tile(P, sbase, kTile, 1, col0, bytes);
+  if (lane == 0) {
+    if (warp < m) issue_row(P, sbase, warp, 0, warp, col0, bytes);
+    if (kPermBuffers == 2 && kTile + warp < m) issue_row(P, sbase, kTile + warp, 1, warp, col0, bytes);
   }
   double run = 0.0;  // PREFIX: S of this thread's path
   const int64_t my = P.path_begin + block_first + threadIdx.x;
   for (int k = 0; k < ntiles; ++k) {
     const int k0 = k * kTile;
     const int b = k & 1;
-    mbar_wait_u32(sbase + kBarOff + b * 8, static_cast<uint32_t>((k >> 1) & 1));
     const uint32_t ztile = sbase + kZtOff + (kZtBuffers == 2 ? b : 0) * kZtBuf;
     const uint32_t zrow = ztile + warp * kThreads * 8;
     if (k0 + warp < m) {
-      generate_row<SLOW, false>(P, ws, k0 + warp, sbase + kPermOff + b * kPermBuf + warp * kThreads * 4, zrow, logtab,
+      const int pb = kPermBuffers == 2 ? b : 0;
+      mbar_wait_u32(sbase + kBarOff + (pb * kTile + warp) * 8,
+                    static_cast<uint32_t>(kPermBuffers == 2 ? (k >> 1) & 1 : k & 1));
+      generate_row<SLOW, false>(P, ws, k0 + warp, sbase + kPermOff + pb * kPermBuf + warp * kThreads * 4, zrow, logtab,
                                 nchunks, lane, lt);
+      __syncwarp();  // perm row consumed: stage this warp's row of the tile kPermBuffers ahead
+      const int dn = k0 + kPermBuffers * kTile + warp;
+      if (lane == 0 && dn < m) issue_row(P, sbase, dn, pb, warp, col0, bytes);
       if (!PREFIX) {
         __syncwarp();
         double* dst = z + static_cast<int64_t>(k0 + warp) * ldz + P.path_begin + block_first;
@@ -1118,8 +1197,7 @@ __global__ void __launch_bounds__(kThreads, QMCG_MINB) gen_z_kernel(const PriceP
         }
       }
     }
-    __syncthreads();  // perm buffer b consumed, z tile b stored
-    if (threadIdx.x == 0 && k + 2 < ntiles) issue_tile(P, sbase, k0 + 2 * kTile, b, col0, bytes);
+    __syncthreads();  // z tile b stored
   }
 }
 
