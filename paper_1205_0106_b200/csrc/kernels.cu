@@ -856,6 +856,52 @@ __device__ __forceinline__ void push_record(uint32_t ws, const PriceParams& P, b
   }
 }
 
+// One walk date of the FP64 fast path (predicated, no branches): advances the
+// record state (c = V of the last record, cd = dominance accumulator of the
+// pending record, pl = its tile-relative date) and returns 1 when the pending
+// record must be queued for exact evaluation (pv, pdl = its V and date).
+//   calls: record = V > c; push = record and V < cd (the new record does not
+//          dominate the pending one; cd = -inf until the first record);
+//   puts:  record = V < c; push = record, a pending record exists
+//          (pl + k0 >= 0) and the accumulator bound of record_dominates<1> fails
+//          (V and cd already advanced by the caller).
+template <int KIND>
+__device__ __forceinline__ uint32_t walk_date(double V, double& c, double& cd, int& pl, int t, int k0, double& pv,
+                                              int& pdl, double b, double x0mk) {
+  uint32_t pu32;
+  if constexpr (KIND == 0) {
+    asm("{\n .reg .pred r, pu;\n"
+        " setp.gt.f64 r, %7, %0;\n setp.lt.and.f64 pu, %7, %1, r;\n"
+        " mov.b64 %3, %0;\n mov.b32 %4, %2;\n"
+        " selp.f64 %0, %7, %0, r;\n selp.f64 %1, %7, %1, r;\n selp.b32 %2, %6, %2, r;\n"
+        " selp.u32 %5, 1, 0, pu;\n}"
+        : "+d"(c), "+d"(cd), "+r"(pl), "=d"(pv), "=r"(pdl), "=r"(pu32)
+        : "r"(t), "d"(V));
+  } else {
+    asm("{\n .reg .pred r, pe, a, b, e, dm, pu;\n .reg .f64 u1, dv, s, t, pr, th;\n .reg .s32 pk;\n"
+        " setp.lt.f64 r, %7, %0;\n add.s32 pk, %2, %8;\n setp.ge.s32 pe, pk, 0;\n"
+        " fma.rn.f64 u1, %9, %0, %10;\n sub.rn.f64 dv, %0, %7;\n fma.rn.f64 s, %9, dv, %1;\n"
+        " fma.rn.f64 t, 0dBFE0000000000000, s, 0d3FF0000000000000;\n mul.rn.f64 pr, u1, s;\n"
+        " mul.rn.f64 pr, pr, t;\n mul.rn.f64 th, %1, 0d3FF0000000001198;\n"
+        " setp.gt.f64 a, u1, 0d0000000000000000;\n setp.lt.and.f64 b, s, 0d4000000000000000, a;\n"
+        " setp.ge.and.f64 dm, pr, th, b;\n and.pred pu, r, pe;\n not.pred e, dm;\n and.pred pu, pu, e;\n"
+        " mov.b64 %3, %0;\n mov.b32 %4, %2;\n"
+        " selp.f64 %0, %7, %0, r;\n selp.f64 %1, 0d0000000000000000, %1, r;\n selp.b32 %2, %6, %2, r;\n"
+        " selp.u32 %5, 1, 0, pu;\n}"
+        : "+d"(c), "+d"(cd), "+r"(pl), "=d"(pv), "=r"(pdl), "=r"(pu32)
+        : "r"(t), "d"(V), "r"(k0), "d"(b), "d"(x0mk));
+  }
+  return pu32;
+}
+
+#ifndef QMCG_PUSH_GROUP
+#define QMCG_PUSH_GROUP 4
+#endif
+// dates per push check in the walk: one warp vote + (rarely taken) branch per
+// group instead of per date, so the dates of a group issue back to back
+constexpr int kPushGroup = QMCG_PUSH_GROUP;
+static_assert(kTile % kPushGroup == 0, "push groups tile the dates");
+
 // One block = 256 consecutive paths; thread i walks path i. Per tile of
 // kTile dates: (1) the permutation rows arrive by cp.async.bulk; (2) warp w
 // generates date row w of the tile (uniform -> normal, bit-exact uniforms);
@@ -960,57 +1006,40 @@ __global__ void __launch_bounds__(kThreads, QMCG_MINB) price_kernel(const PriceP
 #ifdef QMCG_SLOPE_REG
       if constexpr (!F32) asm volatile("mov.b64 %0, %0;" : "+d"(slope));  // register for the tile (no per-date reload)
 #endif
+#if QMCG_WALK_V == 2
+      if constexpr (!F32) {
+        const double bd = P.b, x0mkd = P.x0mk;
+#pragma unroll
+        for (int g = 0; g < kTile; g += kPushGroup) {
+          double pv[kPushGroup];
+          int pdl[kPushGroup];
+          uint32_t pu[kPushGroup];
+          uint32_t anyp = 0;
+#pragma unroll
+          for (int u = 0; u < kPushGroup; ++u) {
+            V = add_rn(V, Z::load(zcol + (g + u) * kThreads * Z::kSize));
+            cd = add_rn(cd, slope);
+            pu[u] = walk_date<KIND>(V, c, cd, pl, g + u, k0, pv[u], pdl[u], bd, x0mkd);
+            anyp |= pu[u];
+          }
+#ifndef QMCG_PROBE_NOPUSH
+          if (__any_sync(kFull, anyp)) {
+#pragma unroll
+            for (int u = 0; u < kPushGroup; ++u)
+              push_record<KIND, RNEG>(ws, P, pu[u] != 0, pv[u], k0 + pdl[u], lane, lt, rq_head, rq_tail);
+          }
+#else
+          (void)anyp;
+#endif
+        }
+      } else
+#endif
 #pragma unroll
       for (int t = 0; t < kTile; ++t) {
         V = add_rn(V, Z::load(zcol + t * kThreads * Z::kSize));
         cd = add_rn(cd, slope);
         const bool rec = KIND == 0 ? V > c : V < c;
         const bool push = rec && (KIND == 0 || pl + k0 >= 0) && !record_dominates<KIND>(V, c, cd, bT, x0mkT);
-#if QMCG_WALK_V == 2
-        if constexpr (KIND == 0 && !F32) {
-          // calls, FP64: one predicated block per date (no branches, no select chains);
-          // push = new record that does not dominate the pending one (V < cd)
-          (void)rec;
-          (void)push;
-          double pv;
-          int pdl;
-          uint32_t pu32;
-          asm volatile(
-              "{\n .reg .pred r, pu;\n"
-              " setp.gt.f64 r, %0, %1;\n setp.lt.and.f64 pu, %0, %2, r;\n"
-              " mov.b64 %4, %1;\n mov.b32 %5, %3;\n"
-              " selp.f64 %1, %0, %1, r;\n selp.f64 %2, %0, %2, r;\n selp.b32 %3, %7, %3, r;\n"
-              " selp.u32 %6, 1, 0, pu;\n}"
-              : "+d"(V), "+d"(c), "+d"(cd), "+r"(pl), "=d"(pv), "=r"(pdl), "=r"(pu32)
-              : "r"(t));
-          push_record<KIND, RNEG>(ws, P, pu32 != 0, pv, k0 + pdl, lane, lt, rq_head, rq_tail);
-          continue;
-        }
-        if constexpr (KIND == 1 && !F32) {
-          // puts, FP64, predicated: the accumulator bound of record_dominates<1> (V and cd
-          // already advanced above); a pending record exists iff pl + k0 >= 0
-          (void)rec;
-          (void)push;
-          double pv;
-          int pdl;
-          uint32_t pu32;
-          asm volatile(
-              "{\n .reg .pred r, pe, a, b, e, dm, pu;\n .reg .f64 u1, dv, s, t, pr, th;\n .reg .s32 pk;\n"
-              " setp.lt.f64 r, %0, %1;\n add.s32 pk, %3, %8;\n setp.ge.s32 pe, pk, 0;\n"
-              " fma.rn.f64 u1, %9, %1, %10;\n sub.rn.f64 dv, %1, %0;\n fma.rn.f64 s, %9, dv, %2;\n"
-              " fma.rn.f64 t, 0dBFE0000000000000, s, 0d3FF0000000000000;\n mul.rn.f64 pr, u1, s;\n"
-              " mul.rn.f64 pr, pr, t;\n mul.rn.f64 th, %2, 0d3FF0000000001198;\n"
-              " setp.gt.f64 a, u1, 0d0000000000000000;\n setp.lt.and.f64 b, s, 0d4000000000000000, a;\n"
-              " setp.ge.and.f64 dm, pr, th, b;\n and.pred pu, r, pe;\n not.pred e, dm;\n and.pred pu, pu, e;\n"
-              " mov.b64 %4, %1;\n mov.b32 %5, %3;\n"
-              " selp.f64 %1, %0, %1, r;\n selp.f64 %2, 0d0000000000000000, %2, r;\n selp.b32 %3, %7, %3, r;\n"
-              " selp.u32 %6, 1, 0, pu;\n}"
-              : "+d"(V), "+d"(c), "+d"(cd), "+r"(pl), "=d"(pv), "=r"(pdl), "=r"(pu32)
-              : "r"(t), "r"(k0), "d"(P.b), "d"(P.x0mk));
-          push_record<KIND, RNEG>(ws, P, pu32 != 0, pv, k0 + pdl, lane, lt, rq_head, rq_tail);
-          continue;
-        }
-#endif
 #if QMCG_WALK_V == 1
         push_record<KIND, RNEG>(ws, P, push, c, k0 + pl, lane, lt, rq_head, rq_tail);
         c = rec ? V : c;
@@ -1057,15 +1086,6 @@ __global__ void __launch_bounds__(kThreads, QMCG_MINB) price_kernel(const PriceP
       }
     }
     if (kZtBuffers == 1) __syncthreads();  // the z tile is rewritten by the next generation
-#ifndef QMCG_DRAIN_AT_END
-#define QMCG_DRAIN_AT_END 1
-#endif
-    if (!RNEG && !QMCG_DRAIN_AT_END && rq_tail - rq_head >= 32) {
-      __syncwarp();
-      process_records_inline<KIND, RNEG>(P, ws, rq_head, 32, lane);
-      rq_head += 32;
-      __syncwarp();
-    }
     if (RNEG && rq_tail - rq_head >= 32) {  // r < 0: the threshold follows the evaluated best
       __syncwarp();
       process_records_inline<KIND, RNEG>(P, ws, rq_head, 32, lane);
