@@ -1072,7 +1072,7 @@ qmcg_status qmcg_price_american_batch(qmcg_ctx* c, const qmcg_option_spec* specs
     G.path_begin = 0;
     G.path_count = n;
     G.alpha = 0.0;
-    QMCG_CUDA(qmcg::launch_gen_z(G, c->d_z.ptr, n, c->stream, qmcg::batch_uses_prefix()));
+    QMCG_CUDA(qmcg::launch_gen_z(G, c->d_z.ptr, n, c->stream, /*prefix=*/true));
     c->launches += 1;
     tr.mark("gen_z enqueued");
     for (int k = 0; k < 2; ++k) {
@@ -1127,29 +1127,16 @@ qmcg_status qmcg_price_american_batch(qmcg_ctx* c, const qmcg_option_spec* specs
       QMCG_CUDA(c->d_cparams[k].reserve(cnt));
       QMCG_CUDA(cudaMemcpyAsync(c->d_cparams[k].ptr, cps.data(), cnt * sizeof(qmcg::ContractParams),
                                 cudaMemcpyHostToDevice, c->stream));
-      QMCG_CUDA(c->d_bvalues[k].reserve(cnt * static_cast<size_t>(n) + 16));
-#ifdef QMCG_COUNT_PUSHES
-      QMCG_CUDA(cudaMemsetAsync(c->d_bvalues[k].ptr + cnt * static_cast<size_t>(n), 0, 16, c->stream));
-#endif
+      QMCG_CUDA(c->d_bvalues[k].reserve(cnt * static_cast<size_t>(n)));
       QMCG_CUDA(c->d_bred[k].reserve(cnt * qmcg::reduce_scratch_doubles(n)));
       QMCG_CUDA(c->d_bsums[k].reserve(2 * cnt));
       qmcg::BatchParams B{c->d_z.ptr, n, n, static_cast<int32_t>(m), static_cast<int32_t>(cnt), c->d_cparams[k].ptr,
-                          c->d_bvalues[k].ptr, cps.data(), c->d_groups[k].ptr, static_cast<int32_t>(groups.size()), 0};
-      if (qmcg::batch_grouped()) QMCG_CUDA(qmcg::launch_walk_group(B, k, c->stream));
-      else QMCG_CUDA(qmcg::launch_walk_batch(B, k, c->stream));
+                          c->d_bvalues[k].ptr, c->d_groups[k].ptr, static_cast<int32_t>(groups.size()), 0};
+      QMCG_CUDA(qmcg::launch_walk_group(B, k, c->stream));
       int launches = 1;
       QMCG_CUDA(qmcg::launch_pairwise_batched(c->d_bvalues[k].ptr, n, static_cast<int>(cnt), c->d_bred[k].ptr,
                                               c->d_bsums[k].ptr, c->stream, &launches));
       c->launches += launches;
-#ifdef QMCG_COUNT_PUSHES
-      {
-        unsigned long long cntr[2];
-        cudaStreamSynchronize(c->stream);
-        cudaMemcpy(cntr, c->d_bvalues[k].ptr + cnt * static_cast<size_t>(n), 16, cudaMemcpyDeviceToHost);
-        std::fprintf(stderr, "kind %d: pushes %llu records %llu (per path-contract %.3f / %.3f)\n", k, cntr[0], cntr[1],
-                     cntr[0] / double(cnt * n), cntr[1] / double(cnt * n));
-      }
-#endif
       shared_sums[k].resize(2 * cnt);  // read back with the other results (no sync between the kinds)
       tr.mark(k == 0 ? "calls enqueued" : "puts enqueued");
     }

@@ -1215,151 +1215,6 @@ __global__ void __launch_bounds__(kThreads, QMCG_MINB) gen_z_kernel(const PriceP
   }
 }
 
-// Batch walk over a shared normal table. Block = 8 warps = 8 contracts of one
-// kind x the same 32 paths (lane = path): every warp walks its contract over
-// the block's 32-path column of z (read once from HBM/L2, then L1 hits for the
-// other 7 warps). Per contract the same foresight walk as price_kernel:
-// V_k = sum (z_j + alpha_c), records filtered by the running extreme and the
-// pending-record dominance test, survivors evaluated 32 per warp.
-constexpr int kBCw = 8;  // contracts (warps) per block
-constexpr uint32_t kBWarpBytes = kRecCap * 12 + 32 * 8;
-
-template <int KIND>
-__global__ void __launch_bounds__(kBCw * 32) walk_batch_kernel(const BatchParams B) {
-  __shared__ __align__(16) unsigned char sm[kBCw * kBWarpBytes];
-  const int warp = threadIdx.x >> 5;
-  const int lane = threadIdx.x & 31;
-  const unsigned lt = lanemask_lt();
-  const uint32_t ws = smem_u32(sm) + warp * kBWarpBytes;
-  const uint32_t rq_code_off = kRecCap * 8, best_off = kRecCap * 12;
-  const int64_t p = static_cast<int64_t>(blockIdx.y) * 32 + lane;
-  const bool active = p < B.n;
-  const int ci = blockIdx.x * kBCw + warp;
-  if (ci >= B.count) return;  // warp-uniform; no block barrier below
-  const ContractParams& q = B.cp[ci];
-  const double alpha = q.alpha, slope = q.dom_slope;
-  double c = q.c0, cd = 0.0, V = 0.0;
-  int pend_d = -1;
-  uint32_t rq_head = 0, rq_tail = 0;
-  asm volatile("st.shared.u64 [%0], %1;" ::"r"(ws + best_off + lane * 8),
-               "l"(static_cast<unsigned long long>(__double_as_longlong(q.best0)))
-               : "memory");
-  __syncwarp();
-  const double* zc = B.z + (active ? p : 0);
-  const int m = B.m;
-  const int mrec = m - 1;
-  auto eval = [&](uint32_t head, uint32_t cnt) {
-    if (static_cast<uint32_t>(lane) < cnt) {
-      const uint32_t slot = (head + lane) & (kRecCap - 1);
-      const double v = lds_f64(ws + slot * 8);
-      const uint32_t code = lds_u32(ws + rq_code_off + slot * 4);
-      const double sv = exp(fma(q.b, v, q.X0));
-      double intr = KIND == 0 ? sv - q.strike : q.strike - sv;
-      intr = intr > 0.0 ? intr : 0.0;
-      const double term = intr * __ldg(q.dpow + (code >> 5) + 1);
-      asm volatile("atom.shared.max.u64 _, [%0], %1;" ::"r"(ws + best_off + (code & 31u) * 8),
-                   "l"(static_cast<unsigned long long>(__double_as_longlong(term)))
-                   : "memory");
-    }
-  };
-#ifdef QMCG_COUNT_PUSHES
-  unsigned long long* dbg_counter = reinterpret_cast<unsigned long long*>(B.values + static_cast<int64_t>(B.count) * B.n);
-#endif
-  auto step = [&](int d, double zv) {
-    V = __dadd_rn(V, __dadd_rn(zv, alpha));
-    cd = __dadd_rn(cd, slope);
-    const bool rec = KIND == 0 ? V > c : V < c;
-    const bool push = active && rec && pend_d >= 0 && !record_dominates<KIND>(V, c, cd, q.b, q.x0mk);
-#ifdef QMCG_COUNT_PUSHES
-    if (push) atomicAdd(dbg_counter, 1ull);
-    if (rec && active) atomicAdd(dbg_counter + 1, 1ull);
-#endif
-    const double pv = c;
-    const int pd = pend_d;
-    c = rec ? V : c;
-    cd = rec ? (KIND == 0 ? V : 0.0) : cd;
-    pend_d = rec ? d : pend_d;
-    const unsigned pb = __ballot_sync(kFull, push);
-    if (pb) {
-      if (push) {
-        const uint32_t slot = (rq_tail + __popc(pb & lt)) & (kRecCap - 1);
-        sts_f64(ws + slot * 8, pv);
-        sts_u32(ws + rq_code_off + slot * 4, (static_cast<uint32_t>(pd) << 5) | static_cast<uint32_t>(lane));
-      }
-      rq_tail += __popc(pb);
-      if (rq_tail - rq_head >= 32) {
-        __syncwarp();
-        eval(rq_head, 32);
-        rq_head += 32;
-        __syncwarp();
-      }
-    }
-  };
-  // z is read 8 dates ahead of use (the walk itself is a serial chain per path)
-  constexpr int kPf = 8;
-  double zbuf[kPf];
-#pragma unroll
-  for (int t = 0; t < kPf; ++t) zbuf[t] = t < mrec ? __ldg(zc + static_cast<int64_t>(t) * B.ldz) : 0.0;
-  for (int d0 = 0; d0 < mrec; d0 += kPf) {
-    double cur[kPf];
-#pragma unroll
-    for (int t = 0; t < kPf; ++t) {
-      cur[t] = zbuf[t];
-      const int dn = d0 + kPf + t;
-      zbuf[t] = dn < mrec ? __ldg(zc + static_cast<int64_t>(dn) * B.ldz) : 0.0;
-    }
-    if (d0 + kPf <= mrec) {
-#pragma unroll
-      for (int t = 0; t < kPf; ++t) step(d0 + t, cur[t]);
-    } else {
-#pragma unroll
-      for (int t = 0; t < kPf; ++t)
-        if (d0 + t < mrec) step(d0 + t, cur[t]);
-    }
-  }
-  V = __dadd_rn(V, __dadd_rn(__ldg(zc + static_cast<int64_t>(mrec) * B.ldz), alpha));
-  {
-    const bool push = active && pend_d >= 0;
-    const unsigned pb = __ballot_sync(kFull, push);
-    if (push) {
-      const uint32_t slot = (rq_tail + __popc(pb & lt)) & (kRecCap - 1);
-      sts_f64(ws + slot * 8, c);
-      sts_u32(ws + rq_code_off + slot * 4, (static_cast<uint32_t>(pend_d) << 5) | static_cast<uint32_t>(lane));
-    }
-    rq_tail += __popc(pb);
-    __syncwarp();
-    while (rq_tail != rq_head) {
-      const uint32_t cnt = min(32u, rq_tail - rq_head);
-      eval(rq_head, cnt);
-      rq_head += cnt;
-      __syncwarp();
-    }
-  }
-  // date m
-  const double X = fma(q.b, V, q.X0);
-  const double sl = exp(X);
-  double cont;
-  if (q.bs_v_zero) {
-    const double fwd = sl * q.bs_fwd_growth;
-    const double iv = KIND == 0 ? fwd - q.strike : q.strike - fwd;
-    cont = q.bs_disc * (iv > 0.0 ? iv : 0.0);
-  } else {
-    const double d1 = (X - q.log_strike + q.bs_mu_t) / q.bs_vsqrt;
-    const double d2 = d1 - q.bs_vsqrt;
-    const double price = KIND == 0 ? sl * cnd_dev(d1) - q.bs_kdisc * cnd_dev(d2)
-                                   : q.bs_kdisc * cnd_dev(-d2) - sl * cnd_dev(-d1);
-    cont = price > 0.0 ? price : 0.0;
-  }
-  double intr = KIND == 0 ? sl - q.strike : q.strike - sl;
-  intr = intr > 0.0 ? intr : 0.0;
-  const double cm = intr > cont ? intr : cont;
-  const double term_m = cm * __ldg(q.dpow + m);
-  unsigned long long bb;
-  asm volatile("ld.shared.u64 %0, [%1];" : "=l"(bb) : "r"(ws + best_off + lane * 8));
-  const double best = __longlong_as_double(static_cast<long long>(bb));
-  if (active) B.values[static_cast<int64_t>(ci) * B.n + p] = best > term_m ? best : term_m;
-}
-
 // European pricing (reference mc_european_price, mc_european.cpp:11-46, with
 // simulate_terminal, path_engine.cpp:154-172): one GBM step of width T from the
 // dimension-0 scrambled-Halton normal, discounted intrinsic per path.
@@ -1756,415 +1611,6 @@ cudaError_t launch_gen_z(const PriceParams& P, double* z, int64_t ldz, cudaStrea
   return cudaGetLastError();
 }
 
-// Batch walk over the prefix-sum table S (gen_z_kernel<*, true>): warp w of a
-// block walks kBK contracts over the block's 32-path column, so each S value is
-// loaded once per kBK contract-dates (and from L1 for the other 7 warps). Per
-// contract and date: V = S_k + (k+1) alpha (one DFMA), the record test, and
-// the dominance test -- calls: W = S_k + (k+1)(alpha - slope), a new record
-// dominates the pending one iff W_k >= W_j (S_k d^(k-j) >= S_j); puts: the
-// accumulator form of price_kernel. One vote per date covers all kBK
-// contracts; pushes go to one per-warp ring (code = date<<7 | contract<<5 | lane).
-constexpr int kBK = 4;                                  // contracts per warp
-constexpr uint32_t kBRing = 256;                        // >= 32 + 32 * kBK
-constexpr uint32_t kBKWarpBytes = kBRing * 12 + kBK * 32 * 8;
-
-template <int KIND>
-__global__ void __launch_bounds__(kBCw * 32) walk_batch_k_kernel(const BatchParams B) {
-  __shared__ __align__(16) unsigned char sm[kBCw * kBKWarpBytes];
-  const int warp = threadIdx.x >> 5;
-  const int lane = threadIdx.x & 31;
-  const unsigned lt = lanemask_lt();
-  const uint32_t ws = smem_u32(sm) + warp * kBKWarpBytes;
-  const uint32_t code_off = kBRing * 8, best_off = kBRing * 12;
-  const int64_t p = static_cast<int64_t>(blockIdx.y) * 32 + lane;
-  const bool active = p < B.n;
-  const int cbase = (blockIdx.x * kBCw + warp) * kBK;
-  if (cbase >= B.count) return;  // warp-uniform; no block barrier below
-  double al[kBK], be[kBK], c[kBK], cd[kBK];
-  double pb_[kBK], px_[kBK];  // puts: b, x0mk for the dominance bound
-  int pend[kBK];
-#pragma unroll
-  for (int kk = 0; kk < kBK; ++kk) {
-    const ContractParams& q = B.cp[min(cbase + kk, B.count - 1)];
-    al[kk] = q.alpha;
-    be[kk] = KIND == 0 ? q.alpha - q.dom_slope : q.dom_slope;
-    pb_[kk] = q.b;
-    px_[kk] = q.x0mk;
-    c[kk] = q.c0;
-    cd[kk] = KIND == 0 ? -INFINITY : 0.0;
-    pend[kk] = -1;
-    asm volatile("st.shared.u64 [%0], %1;" ::"r"(ws + best_off + (kk * 32 + lane) * 8),
-                 "l"(static_cast<unsigned long long>(__double_as_longlong(q.best0)))
-                 : "memory");
-  }
-  uint32_t rq_head = 0, rq_tail = 0;
-  __syncwarp();
-  auto eval = [&](uint32_t head, uint32_t cnt) {
-    if (static_cast<uint32_t>(lane) < cnt) {
-      const uint32_t slot = (head + lane) & (kBRing - 1);
-      const double v = lds_f64(ws + slot * 8);
-      const uint32_t code = lds_u32(ws + code_off + slot * 4);
-      const ContractParams& q = B.cp[cbase + ((code >> 5) & 3u)];
-      const double sv = exp(fma(q.b, v, q.X0));
-      double intr = KIND == 0 ? sv - q.strike : q.strike - sv;
-      intr = intr > 0.0 ? intr : 0.0;
-      const double term = intr * __ldg(q.dpow + (code >> 7) + 1);
-      asm volatile("atom.shared.max.u64 _, [%0], %1;" ::"r"(ws + best_off + (code & 127u) * 8),
-                   "l"(static_cast<unsigned long long>(__double_as_longlong(term)))
-                   : "memory");
-    }
-  };
-  const double* zc = B.z + (active ? p : 0);
-  const int m = B.m;
-  const int mrec = m - 1;
-  double kd = 0.0;
-  constexpr int kPf = 8;
-  double zbuf[kPf];
-#pragma unroll
-  for (int t = 0; t < kPf; ++t) zbuf[t] = t < mrec ? __ldg(zc + static_cast<int64_t>(t) * B.ldz) : 0.0;
-  for (int d0 = 0; d0 < mrec; d0 += kPf) {
-    double cur[kPf];
-#pragma unroll
-    for (int t = 0; t < kPf; ++t) {
-      cur[t] = zbuf[t];
-      const int dn = d0 + kPf + t;
-      zbuf[t] = dn < mrec ? __ldg(zc + static_cast<int64_t>(dn) * B.ldz) : 0.0;
-    }
-#pragma unroll
-    for (int t = 0; t < kPf; ++t) {
-      const int d = d0 + t;
-      if (d0 + kPf > mrec && d >= mrec) break;
-      kd += 1.0;
-      const double S = cur[t];
-      double V[kBK], W[kBK];
-      bool rec[kBK], push[kBK];
-      bool any = false;
-#pragma unroll
-      for (int kk = 0; kk < kBK; ++kk) {
-        V[kk] = fma(al[kk], kd, S);
-        rec[kk] = KIND == 0 ? V[kk] > c[kk] : V[kk] < c[kk];
-        if (KIND == 0) {
-          W[kk] = fma(be[kk], kd, S);
-          push[kk] = rec[kk] && !(W[kk] >= cd[kk]);
-        } else {
-          cd[kk] = __dadd_rn(cd[kk], be[kk]);
-          W[kk] = 0.0;
-          push[kk] = rec[kk] && pend[kk] >= 0 && !record_dominates<1>(V[kk], c[kk], cd[kk], pb_[kk], px_[kk]);
-        }
-        push[kk] = push[kk] && active;
-        any = any || push[kk];
-      }
-      if (__any_sync(kFull, any)) {
-#pragma unroll
-        for (int kk = 0; kk < kBK; ++kk) {
-          const unsigned pbal = __ballot_sync(kFull, push[kk]);
-          if (push[kk]) {
-            const uint32_t slot = (rq_tail + __popc(pbal & lt)) & (kBRing - 1);
-            sts_f64(ws + slot * 8, c[kk]);
-            sts_u32(ws + code_off + slot * 4,
-                    (static_cast<uint32_t>(pend[kk]) << 7) | (static_cast<uint32_t>(kk) << 5) |
-                        static_cast<uint32_t>(lane));
-          }
-          rq_tail += __popc(pbal);
-        }
-        while (rq_tail - rq_head >= 32) {
-          __syncwarp();
-          eval(rq_head, 32);
-          rq_head += 32;
-          __syncwarp();
-        }
-      }
-#pragma unroll
-      for (int kk = 0; kk < kBK; ++kk) {
-        c[kk] = rec[kk] ? V[kk] : c[kk];
-        cd[kk] = rec[kk] ? W[kk] : cd[kk];
-        pend[kk] = rec[kk] ? d : pend[kk];
-      }
-    }
-  }
-  const double Sm = __ldg(zc + static_cast<int64_t>(mrec) * B.ldz);
-  kd += 1.0;
-  // the last pending record of every (contract, path)
-#pragma unroll
-  for (int kk = 0; kk < kBK; ++kk) {
-    const bool push = active && pend[kk] >= 0;
-    const unsigned pbal = __ballot_sync(kFull, push);
-    if (push) {
-      const uint32_t slot = (rq_tail + __popc(pbal & lt)) & (kBRing - 1);
-      sts_f64(ws + slot * 8, c[kk]);
-      sts_u32(ws + code_off + slot * 4,
-              (static_cast<uint32_t>(pend[kk]) << 7) | (static_cast<uint32_t>(kk) << 5) | static_cast<uint32_t>(lane));
-    }
-    rq_tail += __popc(pbal);
-    if (rq_tail - rq_head >= 32) {
-      __syncwarp();
-      eval(rq_head, 32);
-      rq_head += 32;
-    }
-  }
-  __syncwarp();
-  while (rq_tail != rq_head) {
-    const uint32_t cnt = min(32u, rq_tail - rq_head);
-    eval(rq_head, cnt);
-    rq_head += cnt;
-    __syncwarp();
-  }
-  // date m per contract: max(intrinsic, Black-Scholes of the final interval)
-#pragma unroll 1
-  for (int kk = 0; kk < kBK; ++kk) {
-    const int ci = cbase + kk;
-    if (ci >= B.count) break;
-    const ContractParams& q = B.cp[ci];
-    const double X = fma(q.b, fma(al[kk], kd, Sm), q.X0);
-    const double sl = exp(X);
-    double cont;
-    if (q.bs_v_zero) {
-      const double fwd = sl * q.bs_fwd_growth;
-      const double iv = KIND == 0 ? fwd - q.strike : q.strike - fwd;
-      cont = q.bs_disc * (iv > 0.0 ? iv : 0.0);
-    } else {
-      const double d1 = (X - q.log_strike + q.bs_mu_t) / q.bs_vsqrt;
-      const double d2 = d1 - q.bs_vsqrt;
-      const double price = KIND == 0 ? sl * cnd_dev(d1) - q.bs_kdisc * cnd_dev(d2)
-                                     : q.bs_kdisc * cnd_dev(-d2) - sl * cnd_dev(-d1);
-      cont = price > 0.0 ? price : 0.0;
-    }
-    double intr = KIND == 0 ? sl - q.strike : q.strike - sl;
-    intr = intr > 0.0 ? intr : 0.0;
-    const double cm = intr > cont ? intr : cont;
-    const double term_m = cm * __ldg(q.dpow + m);
-    unsigned long long bb;
-    asm volatile("ld.shared.u64 %0, [%1];" : "=l"(bb) : "r"(ws + best_off + (kk * 32 + lane) * 8));
-    const double best = __longlong_as_double(static_cast<long long>(bb));
-    if (active) B.values[static_cast<int64_t>(ci) * B.n + p] = best > term_m ? best : term_m;
-  }
-}
-
-// Batch walk, contract-uniform blocks: a block walks kBU contracts of one kind
-// over 256 consecutive paths (thread = path), reading S_k once per date for all
-// kBU contracts. The contracts' walk constants are block-uniform and come from
-// the constant bank (c_bc, filled per launch chunk), so they cost no registers.
-// Blocks of the same 256 paths are adjacent in launch order (grid.x =
-// contract groups), so S is served from L2.
-constexpr int kBU = 8;
-constexpr int kBUMax = 512;  // contracts per launch chunk (constant bank)
-struct BatchConst {
-  double alpha, beta, b, x0mk;  // beta = alpha - slope (calls) or slope (puts)
-  double c0, best0, X0, strike;
-};
-__constant__ BatchConst c_bc[kBUMax];
-
-// Pushes of one date are staged per (thread, contract) with predicated stores
-// inside the unrolled contract loop; the rare evaluation (exp + discount) runs
-// outside it, so the hot loop keeps its state in fixed registers.
-constexpr uint32_t kBUStage = kBU * 12;  // per thread: kBU x {value f64} + kBU x {date u32}
-
-// Rare path, once per date with any push in the warp: compact the staged
-// (value, date) pairs of every contract into the warp's ring, then evaluate
-// full groups of 32 (exp + discount), folding each into best[contract][lane]
-// with a shared-memory max on the bits of the non-negative term.
-constexpr uint32_t kBURing = 128;
-template <int KIND>
-__device__ __noinline__ void batch_stage_pushes(const ContractParams* __restrict__ cp, unsigned pm, uint32_t stage,
-                                                uint32_t ring, uint32_t best_base, bool drain) {
-  const int lane = threadIdx.x & 31;
-  const unsigned lt = lanemask_lt();
-  uint32_t head = lds_u32(ring + kBURing * 12), tail = lds_u32(ring + kBURing * 12 + 4);
-  for (int kk = 0; kk < kBU; ++kk) {
-    const bool mine = (pm >> kk) & 1u;
-    const unsigned bal = __ballot_sync(kFull, mine);
-    if (!bal) continue;
-    if (mine) {
-      const uint32_t slot = (tail + __popc(bal & lt)) & (kBURing - 1);
-      sts_f64(ring + slot * 8, lds_f64(stage + kk * 8));
-      sts_u32(ring + kBURing * 8 + slot * 4,
-              (lds_u32(stage + kBU * 8 + kk * 4) << 8) | (static_cast<uint32_t>(kk) << 5) | static_cast<uint32_t>(lane));
-    }
-    tail += __popc(bal);
-    while (tail - head >= 32u) {
-      const uint32_t cnt = min(32u, tail - head);
-      __syncwarp();
-      if (static_cast<uint32_t>(lane) < cnt) {
-        const uint32_t slot = (head + lane) & (kBURing - 1);
-        const double v = lds_f64(ring + slot * 8);
-        const uint32_t code = lds_u32(ring + kBURing * 8 + slot * 4);
-        const ContractParams& q = cp[(code >> 5) & 7u];
-        const double sv = exp(fma(q.b, v, q.X0));
-        double intr = KIND == 0 ? sv - q.strike : q.strike - sv;
-        intr = intr > 0.0 ? intr : 0.0;
-        const double term = intr * __ldg(q.dpow + (code >> 8) + 1);
-        // best of (contract, lane of the entry): [lane][kk] layout, 8 B each
-        const uint32_t owner = best_base + (((code & 31u) * kBU + ((code >> 5) & 7u)) * 8);
-        asm volatile("atom.shared.max.u64 _, [%0], %1;" ::"r"(owner),
-                     "l"(static_cast<unsigned long long>(__double_as_longlong(term)))
-                     : "memory");
-      }
-      head += cnt;
-      __syncwarp();
-    }
-  }
-  while (drain && tail != head) {
-    const uint32_t cnt = min(32u, tail - head);
-    __syncwarp();
-    if (static_cast<uint32_t>(lane) < cnt) {
-      const uint32_t slot = (head + lane) & (kBURing - 1);
-      const double v = lds_f64(ring + slot * 8);
-      const uint32_t code = lds_u32(ring + kBURing * 8 + slot * 4);
-      const ContractParams& q = cp[(code >> 5) & 7u];
-      const double sv = exp(fma(q.b, v, q.X0));
-      double intr = KIND == 0 ? sv - q.strike : q.strike - sv;
-      intr = intr > 0.0 ? intr : 0.0;
-      const double term = intr * __ldg(q.dpow + (code >> 8) + 1);
-      const uint32_t owner = best_base + (((code & 31u) * kBU + ((code >> 5) & 7u)) * 8);
-      asm volatile("atom.shared.max.u64 _, [%0], %1;" ::"r"(owner),
-                   "l"(static_cast<unsigned long long>(__double_as_longlong(term)))
-                   : "memory");
-    }
-    head += cnt;
-    __syncwarp();
-  }
-  if (lane == 0) {
-    sts_u32(ring + kBURing * 12, head);
-    sts_u32(ring + kBURing * 12 + 4, tail);
-  }
-  __syncwarp();
-}
-
-#ifndef QMCG_BU_MINB
-#define QMCG_BU_MINB 2
-#endif
-template <int KIND>
-__global__ void __launch_bounds__(256, QMCG_BU_MINB) walk_batch_u_kernel(const BatchParams B, int chunk0) {
-  extern __shared__ __align__(16) unsigned char smu[];
-  const uint32_t stage = smem_u32(smu) + threadIdx.x * kBUStage;
-  const uint32_t bestp = smem_u32(smu) + 256 * kBUStage + threadIdx.x * (kBU * 8);
-  const uint32_t best_base = smem_u32(smu) + 256 * kBUStage + (threadIdx.x & ~31u) * (kBU * 8);
-  const uint32_t ring = smem_u32(smu) + 256 * (kBUStage + kBU * 8) + (threadIdx.x >> 5) * (kBURing * 12 + 16);
-  if ((threadIdx.x & 31) == 0) {
-    sts_u32(ring + kBURing * 12, 0u);
-    sts_u32(ring + kBURing * 12 + 4, 0u);
-  }
-  const int g0 = blockIdx.x * kBU;  // first contract of the block within the chunk
-  const int ng = min(kBU, B.count - chunk0 - g0);
-  const int64_t p = min(static_cast<int64_t>(blockIdx.y) * 256 + threadIdx.x, B.n - 1);
-  double c[kBU], cd[kBU];
-  int pend[kBU];
-#pragma unroll
-  for (int kk = 0; kk < kBU; ++kk) {
-    const BatchConst& q = c_bc[g0 + kk];
-    c[kk] = q.c0;
-    cd[kk] = KIND == 0 ? -INFINITY : 0.0;
-    pend[kk] = -1;
-    sts_f64(bestp + kk * 8, q.best0);
-  }
-  const double* zc = B.z + p;
-  const int m = B.m;
-  const int mrec = m - 1;
-  double kd = 0.0;
-  constexpr int kPf = 4;
-  double zbuf[kPf];
-#pragma unroll
-  for (int t = 0; t < kPf; ++t) zbuf[t] = __ldg(zc + static_cast<int64_t>(min(t, m - 1)) * B.ldz);
-  for (int d0 = 0; d0 < mrec; d0 += kPf) {
-    double cur[kPf];
-#pragma unroll
-    for (int t = 0; t < kPf; ++t) {
-      cur[t] = zbuf[t];
-      zbuf[t] = __ldg(zc + static_cast<int64_t>(min(d0 + kPf + t, m - 1)) * B.ldz);
-    }
-#pragma unroll
-    for (int t = 0; t < kPf; ++t) {
-      const int d = d0 + t;
-      if (d >= mrec) break;
-      kd += 1.0;
-      const double S = cur[t];
-      unsigned pm = 0;
-#pragma unroll
-      for (int kk = 0; kk < kBU; ++kk) {
-        const BatchConst& q = c_bc[g0 + kk];
-        if (KIND == 0) {
-          // predicated form (no branches): V = S + kd alpha, W = S + kd beta;
-          // rec = V > c; push = rec && W < cd (cd = W of the pending record,
-          // -inf when none); pushes stage (c, pend) for the deferred evaluation
-          asm volatile(
-              "{\n .reg .pred r, pu;\n .reg .f64 v, w;\n .reg .b32 t;\n"
-              " fma.rn.f64 v, %4, %5, %6;\n fma.rn.f64 w, %7, %5, %6;\n"
-              " setp.gt.f64 r, v, %0;\n setp.lt.and.f64 pu, w, %1, r;\n"
-              " @pu st.shared.f64 [%8], %0;\n @pu st.shared.u32 [%9], %2;\n"
-              " selp.f64 %0, v, %0, r;\n selp.f64 %1, w, %1, r;\n selp.b32 %2, %10, %2, r;\n"
-              " selp.b32 t, %11, 0, pu;\n or.b32 %3, %3, t;\n}"
-              : "+d"(c[kk]), "+d"(cd[kk]), "+r"(pend[kk]), "+r"(pm)
-              : "d"(q.alpha), "d"(kd), "d"(S), "d"(q.beta), "r"(stage + kk * 8), "r"(stage + kBU * 8 + kk * 4),
-                "r"(d), "r"(1u << kk)
-              : "memory");
-          continue;
-        }
-        const double V = fma(q.alpha, kd, S);
-        const bool rec = KIND == 0 ? V > c[kk] : V < c[kk];
-        double nd;
-        bool push;
-        if (KIND == 0) {
-          nd = 0.0;
-          push = false;
-        } else {
-          cd[kk] = __dadd_rn(cd[kk], q.beta);
-          nd = 0.0;
-          push = rec && pend[kk] >= 0 && !record_dominates<1>(V, c[kk], cd[kk], q.b, q.x0mk);
-        }
-        if (push) {
-          sts_f64(stage + kk * 8, c[kk]);
-          sts_u32(stage + kBU * 8 + kk * 4, static_cast<uint32_t>(pend[kk]));
-        }
-        pm |= push ? (1u << kk) : 0u;
-        c[kk] = rec ? V : c[kk];
-        cd[kk] = rec ? nd : cd[kk];
-        pend[kk] = rec ? d : pend[kk];
-      }
-      if (__any_sync(kFull, pm != 0)) batch_stage_pushes<KIND>(B.cp + chunk0 + g0, pm, stage, ring, best_base, false);
-    }
-  }
-  {  // the last pending record of every contract
-    unsigned pm = 0;
-#pragma unroll
-    for (int kk = 0; kk < kBU; ++kk) {
-      if (pend[kk] >= 0) {
-        sts_f64(stage + kk * 8, c[kk]);
-        sts_u32(stage + kBU * 8 + kk * 4, static_cast<uint32_t>(pend[kk]));
-        pm |= 1u << kk;
-      }
-    }
-    pm &= (1u << ng) - 1u;
-    batch_stage_pushes<KIND>(B.cp + chunk0 + g0, pm, stage, ring, best_base, true);
-  }
-  const double Sm = __ldg(zc + static_cast<int64_t>(mrec) * B.ldz);
-  kd += 1.0;
-  const int64_t pw = static_cast<int64_t>(blockIdx.y) * 256 + threadIdx.x;
-#pragma unroll 1
-  for (int kk = 0; kk < ng; ++kk) {  // date m per contract
-    const ContractParams& q = B.cp[chunk0 + g0 + kk];
-    const double X = fma(q.b, fma(c_bc[g0 + kk].alpha, kd, Sm), q.X0);
-    const double sl = exp(X);
-    double cont;
-    if (q.bs_v_zero) {
-      const double fwd = sl * q.bs_fwd_growth;
-      const double iv = KIND == 0 ? fwd - q.strike : q.strike - fwd;
-      cont = q.bs_disc * (iv > 0.0 ? iv : 0.0);
-    } else {
-      const double d1 = (X - q.log_strike + q.bs_mu_t) / q.bs_vsqrt;
-      const double d2 = d1 - q.bs_vsqrt;
-      const double price = KIND == 0 ? sl * cnd_dev(d1) - q.bs_kdisc * cnd_dev(d2)
-                                     : q.bs_kdisc * cnd_dev(-d2) - sl * cnd_dev(-d1);
-      cont = price > 0.0 ? price : 0.0;
-    }
-    double intr = KIND == 0 ? sl - q.strike : q.strike - sl;
-    intr = intr > 0.0 ? intr : 0.0;
-    const double cm = intr > cont ? intr : cont;
-    const double term_m = cm * __ldg(q.dpow + m);
-    const double best = lds_f64(bestp + kk * 8);
-    if (pw < B.n) B.values[static_cast<int64_t>(chunk0 + g0 + kk) * B.n + pw] = best > term_m ? best : term_m;
-  }
-}
-
 // ---------------------------------------------------------------------------
 // K4 grouped walk. Contracts of one kind that share (spot, rate, volatility,
 // maturity) follow the same log-price walk V_k = S_k + (k+1) alpha and differ
@@ -2363,53 +1809,6 @@ cudaError_t launch_walk_group(const BatchParams& B, int kind, cudaStream_t s) {
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   if (e != cudaSuccess) return e;
   kern<<<grid, kGThreads, smem, s>>>(B);
-  return cudaGetLastError();
-}
-
-#ifndef QMCG_BATCH_K
-#define QMCG_BATCH_K 3  // 3: grouped walk; 2: contract-uniform blocks; 1: contracts per warp; 0: one per warp
-#endif
-
-bool batch_uses_prefix() { return QMCG_BATCH_K != 0; }
-bool batch_grouped() { return QMCG_BATCH_K == 3; }
-
-cudaError_t launch_walk_batch(const BatchParams& B, int kind, cudaStream_t s) {
-  if (B.count <= 0 || B.n <= 0) return cudaSuccess;
-  if (QMCG_BATCH_K == 2) {
-    std::vector<BatchConst> bc;
-    for (int chunk0 = 0; chunk0 < B.count; chunk0 += kBUMax) {
-      const int cnt = std::min(kBUMax, B.count - chunk0);
-      bc.resize(static_cast<size_t>(cnt));
-      for (int j = 0; j < cnt; ++j) {
-        const ContractParams& q = B.cp_host[chunk0 + j];
-        bc[static_cast<size_t>(j)] = BatchConst{q.alpha, kind == 0 ? q.alpha - q.dom_slope : q.dom_slope, q.b, q.x0mk,
-                                                q.c0, q.best0, q.X0, q.strike};
-      }
-      cudaError_t e = cudaMemcpyToSymbolAsync(c_bc, bc.data(), cnt * sizeof(BatchConst), 0, cudaMemcpyHostToDevice, s);
-      if (e != cudaSuccess) return e;
-      const dim3 grid(static_cast<unsigned>((cnt + kBU - 1) / kBU), static_cast<unsigned>((B.n + 255) / 256));
-      const size_t smem = 256 * (kBUStage + kBU * 8) + 8 * (kBURing * 12 + 16);
-      auto kern = kind == 0 ? walk_batch_u_kernel<0> : walk_batch_u_kernel<1>;
-      e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-      if (e != cudaSuccess) return e;
-      e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-      if (e != cudaSuccess) return e;
-      kern<<<grid, 256, smem, s>>>(B, chunk0);
-      e = cudaGetLastError();
-      if (e != cudaSuccess) return e;
-    }
-    return cudaSuccess;
-  }
-  if (QMCG_BATCH_K) {
-    const dim3 grid(static_cast<unsigned>((B.count + kBCw * kBK - 1) / (kBCw * kBK)),
-                    static_cast<unsigned>((B.n + 31) / 32));
-    if (kind == 0) walk_batch_k_kernel<0><<<grid, kBCw * 32, 0, s>>>(B);
-    else walk_batch_k_kernel<1><<<grid, kBCw * 32, 0, s>>>(B);
-    return cudaGetLastError();
-  }
-  const dim3 grid(static_cast<unsigned>((B.count + kBCw - 1) / kBCw), static_cast<unsigned>((B.n + 31) / 32));
-  if (kind == 0) walk_batch_kernel<0><<<grid, kBCw * 32, 0, s>>>(B);
-  else walk_batch_kernel<1><<<grid, kBCw * 32, 0, s>>>(B);
   return cudaGetLastError();
 }
 

@@ -116,7 +116,6 @@ struct BatchParams {
   int32_t count;              // contracts in this launch (all of one kind)
   const ContractParams* cp;   // count entries
   double* values;             // [count][n]
-  const ContractParams* cp_host;  // the same, host copy (walk constants go to the constant bank)
   const GroupParams* groups;      // grouped walk: one walk per (group, path)
   int32_t n_groups, pad;
 };
@@ -124,11 +123,8 @@ struct BatchParams {
 // ---- launchers (kernels.cu) ----
 // Generation only: the QMC normal table z[d][p] (d < m, p in [path_begin, +path_count)) of the
 // context's permutation table (PriceParams fields perm/ld/col_begin/dims/... ; alpha ignored).
-bool batch_uses_prefix();
-bool batch_grouped();
 cudaError_t launch_walk_group(const BatchParams& B, int kind, cudaStream_t s);  // the batch walk reads prefix sums S (gen_z prefix mode)
 cudaError_t launch_gen_z(const PriceParams& P, double* z, int64_t ldz, cudaStream_t s, bool prefix = false);
-cudaError_t launch_walk_batch(const BatchParams& B, int kind, cudaStream_t s);
 cudaError_t launch_european(const uint32_t* perm_row, int64_t count, DimParam dp, const double* sc, const double* nc,
                             double s0, double a, double bsd, double strike, double disc, int kind, double* out,
                             cudaStream_t s);
