@@ -32,9 +32,6 @@ constexpr unsigned kFull = 0xffffffffu;
 constexpr int kThreads = QMCG_THREADS;  // paths per block (one per thread)
 static_assert(kThreads % 32 == 0 && kThreads <= 256, "tail queue indices are 8-bit");
 constexpr int kWarps = kThreads / 32;
-#ifndef QMCG_WALK_V
-#define QMCG_WALK_V 2
-#endif
 #ifndef QMCG_MINB
 #define QMCG_MINB 4
 #endif
@@ -997,11 +994,7 @@ __global__ void __launch_bounds__(kThreads, QMCG_MINB) price_kernel(const PriceP
       // pending date kept tile-relative (the select takes t as an immediate);
       // calls need no "pending exists" test: cd = -inf until the first record
       int pl = pend_d - k0;
-#ifdef QMCG_SLOPE_REG
-      if constexpr (!F32) asm volatile("mov.b64 %0, %0;" : "+d"(slope));  // register for the tile (no per-date reload)
-#endif
-#if QMCG_WALK_V == 2
-      if constexpr (!F32) {
+      if constexpr (!F32) {  // FP64: grouped predicated walk; FP32 takes the generic loop below
         const double bd = P.b, x0mkd = P.x0mk;
 #pragma unroll
         for (int g = 0; g < kTile; g += kPushGroup) {
@@ -1027,26 +1020,18 @@ __global__ void __launch_bounds__(kThreads, QMCG_MINB) price_kernel(const PriceP
 #endif
         }
       } else
-#endif
 #pragma unroll
       for (int t = 0; t < kTile; ++t) {
         V = add_rn(V, Z::load(zcol + t * kThreads * Z::kSize));
         cd = add_rn(cd, slope);
         const bool rec = KIND == 0 ? V > c : V < c;
         const bool push = rec && (KIND == 0 || pl + k0 >= 0) && !record_dominates<KIND>(V, c, cd, bT, x0mkT);
-#if QMCG_WALK_V == 1
-        push_record<KIND, RNEG>(ws, P, push, c, k0 + pl, lane, lt, rq_head, rq_tail);
-        c = rec ? V : c;
-        cd = rec ? (KIND == 0 ? V : T(0)) : cd;
-        pl = rec ? t : pl;
-#else
         const double pv = c;
         const int pdl = pl;
         c = rec ? V : c;
         cd = rec ? (KIND == 0 ? V : T(0)) : cd;
         pl = rec ? t : pl;
         push_record<KIND, RNEG>(ws, P, push, pv, k0 + pdl, lane, lt, rq_head, rq_tail);
-#endif
       }
       pend_d = k0 + pl;
     } else {
