@@ -1755,12 +1755,21 @@ __global__ void __launch_bounds__(kGThreads, QMCG_G_MINB) walk_group_kernel(cons
   for (int s = 0; s < g->count; ++s) {
     const ContractParams& q = B.cp[g->first + s];
     double best = flushed ? B.values[static_cast<int64_t>(g->first + s) * B.n + p] : q.best0;
-    for (int i = 0; i < cnt; ++i) {
-      const double sv = lds_f64(cs + i * 8);
-      double intr = KIND == 0 ? sv - q.strike : q.strike - sv;
-      intr = intr > 0.0 ? intr : 0.0;
-      const double term = intr * lds_f64(cj + kGCap * 4 + i * 8);
-      best = term > best ? term : best;
+    // best >= 0 (the date-0 intrinsic or a flushed value) and d^(j+1) > 0, so a
+    // negative (S_j - K) d^(j+1) never wins the running max: the (.)^+ is implied
+    const double K = q.strike;
+    int i = 0;
+    for (; i + 1 < cnt; i += 2) {
+      const double s0 = lds_f64(cs + i * 8), s1 = lds_f64(cs + i * 8 + 8);
+      const double t0 = (KIND == 0 ? s0 - K : K - s0) * lds_f64(cj + kGCap * 4 + i * 8);
+      const double t1 = (KIND == 0 ? s1 - K : K - s1) * lds_f64(cj + kGCap * 4 + i * 8 + 8);
+      best = t0 > best ? t0 : best;
+      best = t1 > best ? t1 : best;
+    }
+    if (i < cnt) {
+      const double s0 = lds_f64(cs + i * 8);
+      const double t0 = (KIND == 0 ? s0 - K : K - s0) * lds_f64(cj + kGCap * 4 + i * 8);
+      best = t0 > best ? t0 : best;
     }
     // date m: max(intrinsic, Black-Scholes of the final interval), american.cpp:43-52;
     // one exp per strike: phi(d2) = phi(d1) S / (K e^{-r dt})

@@ -34,6 +34,11 @@ src = list(csv.reader(io.StringIO(subprocess.run(
 h = src[1]
 ix = {k: i for i, k in enumerate(h)}
 rows = src[2:]
+# a report with several kernels repeats the header: keep the first kernel's rows
+for k, r in enumerate(rows):
+    if r and r[0] == "Kernel Name":
+        rows = rows[:k]
+        break
 base = int(rows[0][ix["Address"]], 16)
 agg = collections.Counter()
 samp = collections.Counter()
