@@ -500,6 +500,17 @@ __device__ __forceinline__ void issue_row(const PriceParams& P, uint32_t sbase, 
       : "memory");
 }
 
+// The same with the source row given as a pointer (advanced per tile by the caller).
+__device__ __forceinline__ void issue_row_src(const uint32_t* src, uint32_t sbase, int b, int w, uint32_t bytes) {
+  const uint32_t bar = sbase + kBarOff + (b * kTile + w) * 8;
+  const uint32_t dst = sbase + kPermOff + b * kPermBuf + w * kThreads * 4;
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+      "l"(src), "r"(bytes), "r"(bar)
+      : "memory");
+}
+
 // mbarriers bar[2][kTile] (one per buffer and row), arrival count 1.
 __device__ __forceinline__ void init_row_barriers(uint32_t sbase) {
   if (threadIdx.x < 2 * kTile) {
@@ -921,8 +932,11 @@ __global__ void __launch_bounds__(kThreads, QMCG_MINB) price_kernel(const PriceP
   extern __shared__ __align__(128) unsigned char smem_raw[];
   uint32_t sbase = smem_u32(smem_raw);
   asm volatile("mov.b32 %0, %0;" : "+r"(sbase));  // computed once (no shared-window rebuild in the loops)
-  const int warp = threadIdx.x >> 5;
-  const int lane = threadIdx.x & 31;
+  int warp = threadIdx.x >> 5;
+  int lane = threadIdx.x & 31;
+  // held in registers: rebuilding them from %tid inside the loops cost ~3 instructions per warp-date
+  asm volatile("mov.b32 %0, %0;" : "+r"(warp));
+  asm volatile("mov.b32 %0, %0;" : "+r"(lane));
   const uint32_t ws = sbase + kWarpOff + warp * kWarpBytes;
   const uint32_t logtab = sbase + kLogOff;
   const unsigned lt = lanemask_lt();
@@ -973,6 +987,9 @@ __global__ void __launch_bounds__(kThreads, QMCG_MINB) price_kernel(const PriceP
 
   uint32_t rq_head = 0, rq_tail = 0;
   uint32_t err = 0;
+  // this warp's last staged row (date dbeg + warp + (kPermBuffers - 1) kTile), advanced one tile
+  // per pass: a pointer add instead of the row address arithmetic per copy
+  const uint32_t* nsrc = P.perm + static_cast<int64_t>(dbeg + warp + (kPermBuffers - 1) * kTile - P.perm_row0) * P.ld + col0;
 
   for (int k = 0; k < ntiles; ++k) {
     const int k0 = dbeg + k * kTile;
@@ -988,7 +1005,8 @@ __global__ void __launch_bounds__(kThreads, QMCG_MINB) price_kernel(const PriceP
                                 sbase + kZtOff + zb * kZtBuf + warp * kThreads * Z::kSize, logtab, nchunks, lane, lt);
         __syncwarp();  // this warp's perm row is consumed: stage its row of the tile kPermBuffers ahead
         const int dn = k0 + kPermBuffers * kTile + warp;
-        if (lane == 0 && dn < dend) issue_row(P, sbase, dn, pb, warp, col0, bytes);
+        nsrc += kTile * P.ld;  // row dn of this warp's column slice
+        if (lane == 0 && dn < dend) issue_row_src(nsrc, sbase, pb, warp, bytes);
       }
       __syncthreads();  // z tile complete
     }
