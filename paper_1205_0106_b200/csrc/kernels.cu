@@ -17,7 +17,10 @@
 #include "qmcg_internal.h"
 
 #include <cub/device/device_radix_sort.cuh>
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <algorithm>
+#include <mutex>
 #include <vector>
 
 #include "log_table.h"
@@ -412,7 +415,12 @@ constexpr uint32_t kPermBuf = kTile * kThreads * 4;
 // 2: permutation rows double-buffered (row of tile k + 2 staged after tile k);
 // 1: one buffer, the row of tile k + 1 staged as soon as the warp has read row k
 // (measured 1.2% faster at config 3: the copy is in flight during the walk).
-constexpr int kPermBuffers = QMCG_PERM_BUFFERS;
+#ifndef QMCG_TMA
+#define QMCG_TMA 1
+#endif
+// QMCG_TMA: price_kernel stages each tile with one 2-D TMA copy (double-buffered)
+constexpr bool kTma = QMCG_TMA != 0;
+constexpr int kPermBuffers = kTma ? 2 : QMCG_PERM_BUFFERS;
 constexpr uint32_t kZtOff = kPermOff + kPermBuffers * kPermBuf;
 constexpr uint32_t kZtBuf = kTile * kThreads * 8;
 #ifndef QMCG_ZT_BUFFERS
@@ -508,6 +516,20 @@ __device__ __forceinline__ void issue_row_src(const uint32_t* src, uint32_t sbas
   asm volatile(
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
       "l"(src), "r"(bytes), "r"(bar)
+      : "memory");
+}
+
+// One 2-D TMA copy of a whole tile (kTile dates x 256 paths of the [date][path]
+// table) into perm buffer b, completing on the buffer's mbarrier bar[b][0].
+// Out-of-range rows/columns (last tile, last block) arrive zero-filled.
+__device__ __forceinline__ void issue_tile_tma(const CUtensorMap* tmap, uint32_t sbase, int b, int col, int row) {
+  const uint32_t bar = sbase + kBarOff + b * kTile * 8;
+  const uint32_t dst = sbase + kPermOff + b * kPermBuf;
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(kPermBuf) : "memory");
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::
+          "r"(dst),
+      "l"(reinterpret_cast<uint64_t>(tmap)), "r"(col), "r"(row), "r"(bar)
       : "memory");
 }
 
@@ -928,7 +950,8 @@ static_assert(kTile % kPushGroup == 0, "push groups tile the dates");
 // for exact evaluation (exp + discount) in warp-wide batches of 32.
 // SLOW = any of: volatility 0, range checks, 64-bit magic, endpoint clamp.
 template <int KIND, bool RNEG, bool SLOW, bool F32>
-__global__ void __launch_bounds__(kThreads, QMCG_MINB) price_kernel(const PriceParams P) {
+__global__ void __launch_bounds__(kThreads, QMCG_MINB)
+    price_kernel(const PriceParams P, const __grid_constant__ CUtensorMap tmap) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   uint32_t sbase = smem_u32(smem_raw);
   asm volatile("mov.b32 %0, %0;" : "+r"(sbase));  // computed once (no shared-window rebuild in the loops)
@@ -980,7 +1003,12 @@ __global__ void __launch_bounds__(kThreads, QMCG_MINB) price_kernel(const PriceP
   }
   if (threadIdx.x < 128) sts_v2f64(logtab + threadIdx.x * 16, c_log_table[threadIdx.x]);
   __syncthreads();
-  if (lane == 0 && !det) {
+  if (kTma) {
+    if (threadIdx.x == 0 && !det) {
+      issue_tile_tma(&tmap, sbase, 0, static_cast<int>(col0), dbeg - P.perm_row0);
+      if (ntiles > 1) issue_tile_tma(&tmap, sbase, 1, static_cast<int>(col0), dbeg + kTile - P.perm_row0);
+    }
+  } else if (lane == 0 && !det) {
     if (dbeg + warp < dend) issue_row(P, sbase, dbeg + warp, 0, warp, col0, bytes);
     if (kPermBuffers == 2 && dbeg + kTile + warp < dend) issue_row(P, sbase, dbeg + kTile + warp, 1, warp, col0, bytes);
   }
@@ -996,7 +1024,16 @@ __global__ void __launch_bounds__(kThreads, QMCG_MINB) price_kernel(const PriceP
     const int b = k & 1;
     const uint32_t zb = kZtBuffers == 2 ? b : 0;
     const uint32_t zcol = sbase + kZtOff + zb * kZtBuf + threadIdx.x * Z::kSize;
-    if (!det) {
+    if (kTma && !det) {
+      if (k0 + warp < dend) {
+        mbar_wait_u32(sbase + kBarOff + b * kTile * 8, static_cast<uint32_t>((k >> 1) & 1));
+        generate_row<SLOW, F32>(P, ws, k0 + warp, sbase + kPermOff + b * kPermBuf + warp * kThreads * 4,
+                                sbase + kZtOff + zb * kZtBuf + warp * kThreads * Z::kSize, logtab, nchunks, lane, lt);
+      }
+      __syncthreads();  // z tile complete; perm buffer b consumed by every warp
+      if (threadIdx.x == 0 && k + 2 < ntiles)
+        issue_tile_tma(&tmap, sbase, b, static_cast<int>(col0), k0 + 2 * kTile - P.perm_row0);
+    } else if (!det) {
       if (k0 + warp < dend) {
         const int pb = kPermBuffers == 2 ? b : 0;
         mbar_wait_u32(sbase + kBarOff + (pb * kTile + warp) * 8,
@@ -1566,6 +1603,31 @@ int leaf_depth(int64_t len) {
 
 }  // namespace
 
+// Tensor map of the permutation table slice for the pricing kernel's tile copies:
+// dim 0 = columns (ld entries per row), dim 1 = the rows [0, d_end - perm_row0),
+// box = kTile rows x kThreads columns (one tile of one block).
+cudaError_t encode_perm_tmap(const PriceParams& P, CUtensorMap* map) {
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  static std::once_flag once;
+  static cudaError_t init_err = cudaSuccess;
+  std::call_once(once, [] {
+    cudaDriverEntryPointQueryResult q{};
+    void* fn = nullptr;
+    init_err = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q);
+    if (init_err == cudaSuccess && q != cudaDriverEntryPointSuccess) init_err = cudaErrorNotSupported;
+    encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  });
+  if (init_err != cudaSuccess) return init_err;
+  const cuuint64_t dims[2] = {static_cast<cuuint64_t>(P.ld), static_cast<cuuint64_t>(P.d_end - P.perm_row0)};
+  const cuuint64_t strides[1] = {static_cast<cuuint64_t>(P.ld) * sizeof(uint32_t)};
+  const cuuint32_t box[2] = {static_cast<cuuint32_t>(kThreads), static_cast<cuuint32_t>(kTile)};
+  const cuuint32_t estr[2] = {1, 1};
+  const CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, const_cast<uint32_t*>(P.perm), dims, strides, box,
+                            estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+
 template <int KIND, bool RNEG, bool SLOW, bool F32>
 cudaError_t launch_price_t(const PriceParams& P, cudaStream_t s) {
   const int64_t blocks = (P.path_count + kThreads - 1) / kThreads;
@@ -1573,7 +1635,12 @@ cudaError_t launch_price_t(const PriceParams& P, cudaStream_t s) {
   auto kern = price_kernel<KIND, RNEG, SLOW, F32>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   if (e != cudaSuccess) return e;
-  kern<<<static_cast<unsigned>(blocks), kThreads, smem, s>>>(P);
+  alignas(64) CUtensorMap tmap{};
+  if (kTma && !(SLOW && P.deterministic)) {
+    e = encode_perm_tmap(P, &tmap);
+    if (e != cudaSuccess) return e;
+  }
+  kern<<<static_cast<unsigned>(blocks), kThreads, smem, s>>>(P, tmap);
   return cudaGetLastError();
 }
 
