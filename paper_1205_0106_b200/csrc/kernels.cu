@@ -175,8 +175,12 @@ __device__ __forceinline__ void sts_v2f64(uint32_t a, double2 v) {
 
 // Natural log for positive normal x: x = 2^e * m, m = c_i (1 + f) with the
 // 128-entry table {1/c_i, -log(1/c_i)} (log_table.h) in shared memory at
-// `tab`, |f| <= 2^-8, log1p(f) by a degree-6 polynomial. ~11 FP64 operations,
-// error about 1 ulp of the result (CUDA's log() costs ~3x the issue slots).
+// `tab`, |f| <= 2^-8, log1p(f) by a degree-5 polynomial: the Taylor series
+// with its f^6/6 term folded into the f^4 and f^2 coefficients by Chebyshev
+// economization on [-2^-8, 2^-8] (f^4: -1/4 - 2^-18, f^2: -1/2 + 3*2^-37),
+// truncation error < 4e-17 absolute (Taylor degree 5 would leave 6e-16).
+// ~10 FP64 operations, error about 1 ulp of the result (CUDA's log() costs ~3x
+// the issue slots); only used on the Moro tail where |result| > 0.9.
 __device__ __forceinline__ double dev_log(double x, uint32_t tab) {
   const int hi = __double2hiint(x);
   const int lo = __double2loint(x);
@@ -184,10 +188,9 @@ __device__ __forceinline__ double dev_log(double x, uint32_t tab) {
   const double2 t = lds_v2f64(tab + (static_cast<uint32_t>(hi >> 9) & 0x7f0u));
   const double m = __hiloint2double((hi & 0x000fffff) | 0x3ff00000, lo);
   const double f = fma(m, t.x, -1.0);
-  double q = fma(f, -0x1.5555555555555p-3, 0x1.999999999999ap-3);
-  q = fma(f, q, -0.25);
+  double q = fma(f, 0x1.999999999999ap-3, -0x1.0001p-2);
   q = fma(f, q, 0x1.5555555555555p-2);
-  q = fma(f, q, -0.5);
+  q = fma(f, q, -0x1.ffffffffap-2);
   const double p = fma(f * f, q, f);
   const double de = __dadd_rn(__hiloint2double(0x43300000, e + 1024), -c_log_consts[0]);
   return fma(de, c_log_consts[1], t.y + p);
@@ -201,10 +204,9 @@ __device__ __forceinline__ double dev_neglog(double x, uint32_t tab) {
   const double2 t = lds_v2f64(tab + (static_cast<uint32_t>(hi >> 9) & 0x7f0u));
   const double m = __hiloint2double((hi & 0x000fffff) | 0x3ff00000, lo);
   const double f = fma(m, t.x, -1.0);
-  double q = fma(f, -0x1.5555555555555p-3, 0x1.999999999999ap-3);
-  q = fma(f, q, -0.25);
+  double q = fma(f, 0x1.999999999999ap-3, -0x1.0001p-2);
   q = fma(f, q, 0x1.5555555555555p-2);
-  q = fma(f, q, -0.5);
+  q = fma(f, q, -0x1.ffffffffap-2);
   const double p = fma(f * f, q, f);
   const double de = __dadd_rn(__hiloint2double(0x43300000, e + 1024), -c_log_consts[0]);
   return fma(de, -c_log_consts[1], -(t.y + p));
