@@ -627,6 +627,32 @@ __device__ __forceinline__ void park_point(uint32_t zslot, uint32_t qbase, uint3
   ntail += __popc(b);
 }
 
+// Two chunks' points at once (FP64): the queue base is formed once, the second
+// chunk's rank adds the first chunk's count in one 3-input add, and ntail
+// advances by both counts in another.
+__device__ __forceinline__ void park_pair(uint32_t zslot_a, uint32_t zslot_b, uint32_t qbase, uint32_t idx_a,
+                                          double za, double ua, double ya, double zb, double ub, double yb,
+                                          unsigned lt, uint32_t& ntail) {
+  asm volatile(
+      "{\n .reg .pred pa, pb;\n .reg .f64 ay;\n .reg .b32 ba, bb, ca, ra, rb, q, a;\n"
+      " abs.f64 ay, %4;\n setp.gt.f64 pa, ay, %11;\n"
+      " abs.f64 ay, %7;\n setp.gt.f64 pb, ay, %11;\n"
+      " vote.sync.ballot.b32 ba, pa, 0xffffffff;\n"
+      " vote.sync.ballot.b32 bb, pb, 0xffffffff;\n"
+      " st.shared.f64 [%1], %2;\n @pa st.shared.f64 [%1], %3;\n"
+      " st.shared.f64 [%5], %6;\n @pb st.shared.f64 [%5], %8;\n"
+      " add.u32 q, %9, %0;\n"
+      " and.b32 ra, ba, %10;\n popc.b32 ra, ra;\n popc.b32 ca, ba;\n"
+      " and.b32 rb, bb, %10;\n popc.b32 rb, rb;\n"
+      " add.u32 a, q, ra;\n @pa st.shared.u8 [a], %12;\n"
+      " add.u32 a, q, ca;\n add.u32 a, a, rb;\n @pb st.shared.u8 [a], %13;\n"
+      " popc.b32 bb, bb;\n add.u32 %0, %0, ca;\n add.u32 %0, %0, bb;\n}"
+      : "+r"(ntail)
+      : "r"(zslot_a), "d"(za), "d"(ua), "d"(ya), "r"(zslot_b), "d"(zb), "d"(yb), "d"(ub), "r"(qbase), "r"(lt),
+        "d"(c_tail_y), "r"(idx_a), "r"(idx_a + 32)
+      : "memory");
+}
+
 // One queued Moro-tail point: u (parked in its z slot) -> w = u or 1 - u,
 // z = +-P8(log(-log w)) + alpha. A queued point has u < 0.08 or u > 0.92, so
 // y = u - 1/2 > 0 iff the high word of u is at least that of 0.5 (integer
@@ -778,31 +804,45 @@ __device__ __forceinline__ double halton_fixed(uint32_t x, uint32_t magic, uint3
   return u;
 }
 
+// Two independent 32-path chunks (ch, ch + 1) of one fixed-digit row.
+template <int D, bool F32>
+__device__ __forceinline__ void generate_chunk_pair(const double2 (&sc)[4], uint32_t magic, uint32_t shift,
+                                                    uint32_t negp, uint32_t ws, uint32_t prow, uint32_t zrow, int ch,
+                                                    int lane, unsigned lt, double alpha, uint32_t& ntail) {
+  using Z = ZSlot<F32>;
+  constexpr uint32_t kCh = 32 * Z::kSize;  // bytes per 32-path chunk of a row
+  const uint32_t xa = lds_u32(prow + ch * 128);  // tables hold perm + 1 (the Halton index)
+  const uint32_t xb = lds_u32(prow + ch * 128 + 128);
+  const double ua = halton_fixed<D>(xa, magic, shift, negp, sc);
+  const double ub = halton_fixed<D>(xb, magic, shift, negp, sc);
+  const double ya = __dadd_rn(ua, -0.5);
+  const double yb = __dadd_rn(ub, -0.5);
+  const auto za = central_z<F32>(ya, alpha);
+  const auto zb = central_z<F32>(yb, alpha);
+  if constexpr (!F32) {
+    park_pair(zrow + ch * kCh, zrow + ch * kCh + kCh, ws + kWTailIdx, ch * 32 + lane, za, ua, ya, zb, ub, yb, lt,
+              ntail);
+  } else {
+    park_point<F32>(zrow + ch * kCh, ws + kWTailIdx, ch * 32 + lane, za, tail_park<F32>(ua, ya), ya, lt, ntail);
+    park_point<F32>(zrow + ch * kCh + kCh, ws + kWTailIdx, ch * 32 + 32 + lane, zb, tail_park<F32>(ub, yb), yb, lt,
+                    ntail);
+  }
+}
+
 template <int D, bool F32>
 __device__ __forceinline__ uint32_t generate_row_fixed(const double2* sn, uint32_t magic, uint32_t shift,
                                                        uint32_t negp, uint32_t ws, uint32_t prow, uint32_t zrow,
                                                        int nchunks, int lane, unsigned lt, double alpha) {
   using Z = ZSlot<F32>;
-  constexpr uint32_t kCh = 32 * Z::kSize;  // bytes per 32-path chunk of a row
+  constexpr uint32_t kCh = 32 * Z::kSize;
   double2 sc[4];
 #pragma unroll
   for (int j = 0; j < 4; ++j) sc[j] = j < D ? __ldg(sn + j) : make_double2(0.0, 0.0);
   uint32_t ntail = 0;
   int ch = 0;
 #pragma unroll 1
-  for (; ch + 1 < nchunks; ch += 2) {  // two independent chunks in flight
-    const uint32_t xa = lds_u32(prow + ch * 128);  // tables hold perm + 1 (the Halton index)
-    const uint32_t xb = lds_u32(prow + ch * 128 + 128);
-    const double ua = halton_fixed<D>(xa, magic, shift, negp, sc);
-    const double ub = halton_fixed<D>(xb, magic, shift, negp, sc);
-    const double ya = __dadd_rn(ua, -0.5);
-    const double yb = __dadd_rn(ub, -0.5);
-    const auto za = central_z<F32>(ya, alpha);
-    const auto zb = central_z<F32>(yb, alpha);
-    park_point<F32>(zrow + ch * kCh, ws + kWTailIdx, ch * 32 + lane, za, tail_park<F32>(ua, ya), ya, lt, ntail);
-    park_point<F32>(zrow + ch * kCh + kCh, ws + kWTailIdx, ch * 32 + 32 + lane, zb, tail_park<F32>(ub, yb), yb, lt,
-                    ntail);
-  }
+  for (; ch + 1 < nchunks; ch += 2)  // two independent chunks in flight
+    generate_chunk_pair<D, F32>(sc, magic, shift, negp, ws, prow, zrow, ch, lane, lt, alpha, ntail);
   if (ch < nchunks) {
     const uint32_t x = lds_u32(prow + ch * 128);
     const double u = halton_fixed<D>(x, magic, shift, negp, sc);
