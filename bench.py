@@ -131,16 +131,20 @@ def cpu_reference(steps, warmup, n_paths=CPU_SAMPLE_PATHS, lanes=None):
 def run_reference_arm(args, rank, world):
     if rank != 0:
         return 0
-    steps = max(1, min(args.steps, 5))
-    warmup = max(1, min(args.warmup, 1))
-    base = cpu_reference(steps, warmup)
+    # every requested step and warm-up is run; the per-call sample shrinks (2^20 -> 2^18 paths of the
+    # 2^24 x 256 workload) as K + W grows, so the whole run stays within a few minutes of host time
+    steps, warmup = max(1, args.steps), max(1, args.warmup)
+    sample = CPU_SAMPLE_PATHS
+    while sample > (1 << 18) and (steps + warmup) * sample > 24 * CPU_SAMPLE_PATHS:
+        sample //= 2
+    base = cpu_reference(steps, warmup, n_paths=sample)
     line = {"impl": "reference", "metric": METRIC, "value": base["value"], "unit": "path-steps/s",
             "n_gpus": args.gpus, "steps": steps, "warmup": warmup,
-            "ms_per_step": 1e3 * base["seconds_per_call"] * (N_PATHS / CPU_SAMPLE_PATHS),
+            "ms_per_step": 1e3 * base["seconds_per_call"] * (N_PATHS / sample),
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (QMC paths from the reference's scrambled Halton stream)",
             "config": {"workload": WORKLOAD, "n_paths": N_PATHS, "m_dates": M_DATES, "seed": SEED,
-                       "sample_paths": CPU_SAMPLE_PATHS, "parallelism": "host threads (reference lanes)"},
+                       "sample_paths": sample, "parallelism": "host threads (reference lanes)"},
             "cpu_baseline": {k: base[k] for k in ("value", "unit", "cores", "kind", "sample")},
             "e2e": {"value": base["value"], "unit": "path-steps/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0},
