@@ -297,6 +297,11 @@ struct qmcg_ctx {
   DevBuf<qmcg::GroupParams> d_groups[2];
   DevBuf<uint32_t> d_err, d_fullperm;
   DevBuf<char> d_permscratch;
+  // second K1 lane: tables built alternately on `stream` and `side` so one table's latency-bound
+  // assign pass overlaps the next table's sort (n <= kOverlapMaxN)
+  cudaStream_t side[2] = {nullptr, nullptr};
+  DevBuf<char> d_permscratch_side[2];
+  cudaEvent_t ev_fork = nullptr, ev_join[2] = {nullptr, nullptr};
   // streamed tables (date windows): per-path walk state carried between windows
   DevBuf<double> d_stV, d_stc, d_stcd, d_stbest;
   DevBuf<int32_t> d_stpend;
@@ -358,6 +363,49 @@ qmcg_status build_perm(qmcg_ctx* c, uint64_t seed64, int64_t n, uint32_t* dst, u
   return QMCG_OK;
 }
 
+#ifndef QMCG_K1_LANES
+#define QMCG_K1_LANES 2
+#endif
+constexpr int kK1Lanes = QMCG_K1_LANES;             // K1 builds in flight (main stream + side lanes)
+static_assert(kK1Lanes >= 2 && kK1Lanes <= 3, "one or two side lanes");
+constexpr int64_t kOverlapMaxN = int64_t{1} << 25;  // the extra K1 scratch stays below ~0.6 GB per lane
+
+// Rows [d0, d1) of full tables (n columns, leading dimension ld) with kK1Lanes K1 builds in
+// flight: row d on lane (d - d0) mod kK1Lanes (lane 0 = `stream`), each lane with its own
+// scratch, so one table's latency-bound assign pass overlaps the next table's sort; `stream`
+// then waits for the side lanes, so everything after sees all rows.
+// Row k holds dimension dim_begin + k * dim_stride.
+qmcg_status build_rows_overlapped(qmcg_ctx* c, uint64_t seed, int64_t n, uint32_t* table, int64_t ld,
+                                  int64_t d0, int64_t d1, int64_t dim_begin = 0, int64_t dim_stride = 1) {
+  const size_t need = qmcg::perm_scratch_bytes(n);
+  QMCG_CUDA(c->d_permscratch.reserve(need));
+  if (!c->ev_fork) QMCG_CUDA(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
+  QMCG_CUDA(cudaEventRecord(c->ev_fork, c->stream));
+  for (int l = 0; l + 1 < kK1Lanes; ++l) {
+    if (!c->side[l]) {
+      QMCG_CUDA(cudaStreamCreateWithFlags(&c->side[l], cudaStreamNonBlocking));
+      QMCG_CUDA(cudaEventCreateWithFlags(&c->ev_join[l], cudaEventDisableTiming));
+    }
+    QMCG_CUDA(c->d_permscratch_side[l].reserve(need));
+    QMCG_CUDA(cudaStreamWaitEvent(c->side[l], c->ev_fork, 0));
+  }
+  for (int64_t d = d0; d < d1; ++d) {
+    const int lane = static_cast<int>((d - d0) % kK1Lanes);
+    DevBuf<char>& scratch = lane == 0 ? c->d_permscratch : c->d_permscratch_side[lane - 1];
+    cudaStream_t s = lane == 0 ? c->stream : c->side[lane - 1];
+    uint32_t* row = table + static_cast<size_t>(d) * static_cast<size_t>(ld);
+    int launches = 0;
+    QMCG_CUDA(qmcg::launch_perm_build(dimension_seed(seed, dim_begin + d * dim_stride), n, row, scratch.ptr,
+                                      scratch.cap, s, &launches, 1));
+    c->launches += launches;
+  }
+  for (int l = 0; l + 1 < kK1Lanes; ++l) {
+    QMCG_CUDA(cudaEventRecord(c->ev_join[l], c->side[l]));
+    QMCG_CUDA(cudaStreamWaitEvent(c->stream, c->ev_join[l], 0));
+  }
+  return QMCG_OK;
+}
+
 // Make rows [0, m) of the table for (seed, n) over columns [b, e) resident.
 qmcg_status ensure_perms(qmcg_ctx* c, uint64_t seed, int64_t n, int64_t b, int64_t e, int64_t m, bool rebuild) {
   if (c->cache_n != n || c->cache_seed != seed || c->col_begin != b || c->col_end != e || rebuild) drop_cache(c);
@@ -393,6 +441,14 @@ qmcg_status ensure_perms(qmcg_ctx* c, uint64_t seed, int64_t n, int64_t b, int64
   c->col_end = e;
   const bool full = (b == 0 && e == n);
   if (!full) QMCG_CUDA(c->d_fullperm.reserve(static_cast<size_t>(n)));
+#ifndef QMCG_NO_K1_OVERLAP
+  if (full && n <= kOverlapMaxN && m - c->cache_dims >= 2) {
+    qmcg_status st = build_rows_overlapped(c, seed, n, c->table, ld, c->cache_dims, m);
+    if (st) return st;
+    c->cache_dims = m;
+    return QMCG_OK;
+  }
+#endif
   for (int64_t d = c->cache_dims; d < m; ++d) {
     uint32_t* row = c->table + static_cast<size_t>(d) * static_cast<size_t>(ld);
     qmcg_status st = build_perm(c, dimension_seed(seed, d), n, full ? row : c->d_fullperm.ptr);
@@ -634,6 +690,13 @@ void qmcg_destroy(qmcg_ctx* c) {
   c->d_err.release();
   c->d_fullperm.release();
   c->d_permscratch.release();
+  for (int l = 0; l < 2; ++l) {
+    if (c->side[l]) cudaStreamSynchronize(c->side[l]);
+    c->d_permscratch_side[l].release();
+    if (c->side[l]) cudaStreamDestroy(c->side[l]);
+    if (c->ev_join[l]) cudaEventDestroy(c->ev_join[l]);
+  }
+  if (c->ev_fork) cudaEventDestroy(c->ev_fork);
   c->d_dimp.release();
   c->d_path.release();
   c->d_path_t.release();
@@ -700,10 +763,15 @@ qmcg_status qmcg_build_tables(qmcg_ctx* c, int64_t n, uint64_t seed, int64_t dim
   std::lock_guard<std::mutex> lock(c->mu);
   DeviceGuard g(c->device);
   c->launches = 0;
-  for (int64_t k = 0; k < count; ++k) {
-    qmcg_status st = build_perm(c, dimension_seed(seed, dim_begin + k * dim_stride), n,
-                                out_dev + static_cast<size_t>(k) * static_cast<size_t>(ld));
+  if (n <= kOverlapMaxN && count >= 2) {
+    qmcg_status st = build_rows_overlapped(c, seed, n, out_dev, ld, 0, count, dim_begin, dim_stride);
     if (st) return st;
+  } else {
+    for (int64_t k = 0; k < count; ++k) {
+      qmcg_status st = build_perm(c, dimension_seed(seed, dim_begin + k * dim_stride), n,
+                                  out_dev + static_cast<size_t>(k) * static_cast<size_t>(ld));
+      if (st) return st;
+    }
   }
   QMCG_CUDA(cudaStreamSynchronize(c->stream));
   return QMCG_OK;
