@@ -321,3 +321,24 @@ def test_batch_arrays_api(ctx, qmcg):
     lst = ctx.price_american_batch([spec_of(qmcg, (100.0, k, 0.05, v, 1.0), int(t)) for k, v, t in zip(K, vol, kind)],
                                    16, 5000, 42, allow_put=True)
     assert np.array_equal(arr, np.array([(r.price, r.std_error) for r in lst]))
+
+
+def test_random_specs_vs_oracle(ctx, qmcg, oracle_lib):
+    """Seeded random contracts (spot, strike, rate incl. r <= 0, vol, maturity, m, n not a multiple
+    of the block) through every K2 instantiation the drop-in reaches: calls (pinned to the
+    reference algorithm) and opt-in puts (the oracle's mirrored rule), per-path values and price."""
+    rng = np.random.default_rng(20261018)
+    for t in range(24):
+        s = (float(rng.uniform(50, 150)), float(rng.uniform(60, 140)), float(rng.uniform(-0.03, 0.12)),
+             float(rng.uniform(0.05, 0.6)), float(rng.uniform(0.1, 3.0)))
+        m = int(rng.integers(1, 70))
+        n = int(rng.integers(2, 5000))
+        seed = int(rng.integers(0, 2**63))
+        kind = t % 2
+        kw = dict(kind=O.PUT, allow_put=True) if kind else {}
+        p, se, vals = oracle_lib.price_american(*s, m, n, seed, want_values=True, **kw)
+        v = ctx.path_values(spec_of(qmcg, s, kind), m, n, seed, **({"allow_put": True} if kind else {}))
+        assert np.max(np.abs(v - vals) / np.maximum(np.abs(vals), 1e-300)) < 1e-9, (t, s, m, n)
+        r = ctx.price_american(spec_of(qmcg, s, kind), m, n, seed, allow_put=bool(kind))
+        assert abs(r.price - p) <= PRICE_RTOL * max(p, 1e-12), (t, s, m, n, r.price, p)
+        assert abs(r.std_error - se) <= 1e-8 * max(se, 1e-12), (t, s, m, n, r.std_error, se)
