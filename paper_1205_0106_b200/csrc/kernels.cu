@@ -139,7 +139,7 @@ __device__ __forceinline__ double moro_central_plus(double y, double alpha) {
 
 __constant__ double2 c_log_table[128];
 __constant__ double c_tail_y = 0.42;  // Moro branch point |u - 1/2| > 0.42 (analytic.cpp:87)
-__constant__ double c_log_consts[2] = {0x1.0000000000400p+52 /* 2^52 + 1024 */, 0x1.62e42fefa39efp-1 /* ln 2 */};
+__constant__ double c_log_consts[2] = {0.0 /* unused */, 0x1.62e42fefa39efp-1 /* ln 2 */};
 
 // Shared-memory accessors on 32-bit shared-window addresses (keeps the
 // compiler from rebuilding generic->shared windows inside the hot loops).
@@ -192,7 +192,7 @@ __device__ __forceinline__ double dev_log(double x, uint32_t tab) {
   q = fma(f, q, 0x1.5555555555555p-2);
   q = fma(f, q, -0x1.ffffffffap-2);
   const double p = fma(f * f, q, f);
-  const double de = __dadd_rn(__hiloint2double(0x43300000, e + 1024), -c_log_consts[0]);
+  const double de = static_cast<double>(e);  // exact: one I2F.F64 (the 2^52 magic took 3 issue slots)
   return fma(de, c_log_consts[1], t.y + p);
 }
 
@@ -208,7 +208,7 @@ __device__ __forceinline__ double dev_neglog(double x, uint32_t tab) {
   q = fma(f, q, 0x1.5555555555555p-2);
   q = fma(f, q, -0x1.ffffffffap-2);
   const double p = fma(f * f, q, f);
-  const double de = __dadd_rn(__hiloint2double(0x43300000, e + 1024), -c_log_consts[0]);
+  const double de = static_cast<double>(e);  // exact: one I2F.F64 (the 2^52 magic took 3 issue slots)
   return fma(de, -c_log_consts[1], -(t.y + p));
 }
 
