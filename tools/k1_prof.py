@@ -1,5 +1,6 @@
 """K1 at n = 2^LOG (default 28): build 2 tables (for an ncu launch list)."""
 import sys
+sys.path.insert(0, ".")
 import paper_1205_0106_b200 as q
 
 lg = int(sys.argv[1]) if len(sys.argv) > 1 else 28
