@@ -157,6 +157,11 @@ qmcg_status qmcg_normals(qmcg_ctx* ctx, int64_t n, uint64_t seed, int64_t dim, d
 /* The normal table z[d][p] = moro_inv_cnd(uniform_at(p, d)) for d < dims, as the batch
  * path generates it (row-major [dims][n_paths]). */
 qmcg_status qmcg_normal_table(qmcg_ctx* ctx, int64_t n_paths, uint64_t seed, int64_t dims, double* out_host);
+/* uniform_at(p, d) (quasi_rng.cpp:96-101) for d in [dim_begin, dim_begin + dim_count) and all p,
+ * produced by the pricing kernels' own generator code (generate_row: per-date fixed digit counts,
+ * digit pairs, the base-2 bit reversal) rather than the D1 export: row-major [dim_count][n_paths]. */
+qmcg_status qmcg_uniform_rows(qmcg_ctx* ctx, int64_t n_paths, uint64_t seed, int64_t dim_begin,
+                              int64_t dim_count, double* out_host);
 /* Per-path t0 values of the foresight sweep (american.cpp:119-124). */
 qmcg_status qmcg_path_values(qmcg_ctx* ctx, const qmcg_option_spec* spec, int64_t m,
                              int64_t n_paths, uint64_t seed, uint32_t flags, double* out_host);

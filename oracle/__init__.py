@@ -178,6 +178,7 @@ class Reference:
         L.ref_radical_inverse.restype = D
         L.ref_radical_inverse.argtypes = [U64, C.c_uint32]
         L.ref_uniform_matrix.argtypes = [I64, I64, U64, P, C.c_char_p, C.c_int]
+        L.ref_uniform_column.argtypes = [I64, U64, I64, C.c_uint32, P, C.c_char_p, C.c_int]
         L.ref_moro_inv_cnd.argtypes = [D, C.POINTER(D), C.c_char_p, C.c_int]
         L.ref_cnd.argtypes = [D, C.POINTER(D), C.c_char_p, C.c_int]
         L.ref_bs_price.argtypes = [P, C.c_int, C.POINTER(D), C.c_char_p, C.c_int]
@@ -225,6 +226,13 @@ class Reference:
         out = np.zeros((length, dims), dtype=np.float64)
         err = C.create_string_buffer(512)
         _raise(self.lib.ref_uniform_matrix(dims, length, seed, out.ctypes.data, err, 512), err)
+        return out
+
+    def uniform_column(self, length, seed, dim, base):
+        """uniform_at(p, dim) for all p (the composition inside QuasiStream::uniform_at)."""
+        out = np.zeros(length, dtype=np.float64)
+        err = C.create_string_buffer(512)
+        _raise(self.lib.ref_uniform_column(length, seed, dim, base, out.ctypes.data, err, 512), err)
         return out
 
     def moro_inv_cnd(self, u):

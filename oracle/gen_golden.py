@@ -5,7 +5,8 @@ oracle/Makefile) and writes small JSON fixtures: full-precision prices and
 standard errors, permutation / uniform hashes, analytic function values.
 The GPU box has no /root/reference, so the parity tests read these fixtures.
 
-usage: python oracle/gen_golden.py [--big | --only-big | --only-c5]
+usage: python oracle/gen_golden.py [--big | --only-big | --only-c5 | --only-columns | --only-c4 |
+                                   --only-put-bounds]
   --big additionally prices 2^24 x 256 (config 3; ~52 GB RAM, minutes); --only-big / --only-c5
   price just config 3 / the config-5 ladder rung 2^20 x 365 and merge them into prices.json.
 """
@@ -74,7 +75,62 @@ def only_big(m: int = 256, n: int = 1 << 24) -> None:
     print(f"m={m} n={n}: price={p!r} se={se!r} ({el:.1f}s, {lanes} lanes)")
 
 
+def uniform_columns() -> None:
+    """FNV-1a-64 of every uniform column the pricing path reads at config 2 (2^20 x 100) and
+    config 3 (2^24 x 256): uniform_at(p, d) for all p, from the reference's own functions
+    (ref_uniform_column), one dimension per host thread."""
+    from concurrent.futures import ThreadPoolExecutor
+    R = oracle.Reference()
+    primes = oracle.Oracle().first_primes(256)
+    out = {"source": "oracle/_ref uniform_at composition (quasi_rng.cpp:96-101)", "seed": SEED, "sets": []}
+    for n, dims in ((1 << 20, 100), (1 << 24, 256)):
+        def col(d, n=n):
+            return fnv1a64_c(R.uniform_column(n, SEED, d, int(primes[d])))
+        with ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1)) as ex:
+            hashes = list(ex.map(col, range(dims)))
+        out["sets"].append({"n": n, "dims": dims, "fnv1a64": hashes})
+        print(f"n={n}: {dims} columns hashed")
+    write("uniform_columns.json", out)
+
+
+# config 4 grid (SURVEY 8d): K = 80 + 40 i / 31, sigma = 0.10 + 0.40 j / 31, call for even i + j
+C4_CALLS = ((0, 0), (0, 30), (10, 10), (10, 20), (21, 1), (21, 31), (31, 3), (31, 31))
+
+
+def config4_goldens() -> None:
+    """The reference's price_american for 8 calls of the config-4 grid at the full 2^18 x 128
+    (the reference rejects puts), looped as the reference would (american.cpp:103-131)."""
+    R = oracle.Reference()
+    lanes = os.cpu_count() or 1
+    cases = []
+    for i, j in C4_CALLS:
+        sp = (100.0, 80 + 40 * i / 31, 0.05, 0.10 + 0.40 * j / 31, 1.0)
+        p, se, el = R.price_american(*sp, 128, 1 << 18, SEED, lanes=lanes)
+        cases.append({"i": i, "j": j, "spec": list(sp), "m": 128, "n": 1 << 18, "seed": SEED, "price": hexf(p),
+                      "std_error": hexf(se), "price_dec": repr(p), "elapsed_s_ref": el})
+        print(f"  ({i},{j}) {sp}: {p!r} / {se!r} ({el:.2f}s)")
+    write("config4.json", {"source": "oracle/_ref price_american, one call per contract", "cases": cases})
+
+
+def put_bounds() -> None:
+    """Lower bounds the reference's own tests apply to American prices (acceptance.cpp:118-154),
+    for the put extension at the headline config: bs_price(Put) and crr_price(2048 steps,
+    American put) from the reference's analytic.cpp / oracles.cpp."""
+    R = oracle.Reference()
+    rows = []
+    for sp in [REF_SPEC, (90.0, 100.0, 0.03, 0.3, 0.5), (110.0, 100.0, 0.08, 0.15, 2.0)]:
+        rows.append({"spec": list(sp), "steps": 2048, "american_put": R.crr_price(*sp, 2048, True, kind=1),
+                     "european_put": R.crr_price(*sp, 2048, False, kind=1), "bs_put": R.bs_price(*sp, kind=1)})
+    write("put_bounds.json", {"source": "oracle/_ref crr_price / bs_price (puts)", "cases": rows})
+
+
 def main() -> None:
+    if "--only-columns" in sys.argv:
+        return uniform_columns()
+    if "--only-c4" in sys.argv:
+        return config4_goldens()
+    if "--only-put-bounds" in sys.argv:
+        return put_bounds()
     if "--only-big" in sys.argv:
         return only_big()
     if "--only-c5" in sys.argv:

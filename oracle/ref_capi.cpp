@@ -96,6 +96,19 @@ double ref_radical_inverse(std::uint64_t index, std::uint32_t base) {
   return radical_inverse(index, base);
 }
 
+// One column of QuasiStream(dims > dim, length, seed): uniform_at(p, dim) for every p, i.e.
+// radical_inverse(perm_dim[p] + 1, base) with perm_dim = permutation_indices(length,
+// dimension_seed(seed, dim)) -- the body of uniform_at (quasi_rng.cpp:96-101, pinned to that
+// composition by proj/tests/test_quasi_rng.cpp:154-169) without building every other dimension.
+int ref_uniform_column(std::int64_t length, std::uint64_t seed, std::int64_t dim, std::uint32_t base, double* out,
+                       char* err, int errlen) {
+  return guarded(err, errlen, [&] {
+    const auto perm = permutation_indices(length, dimension_seed(seed, dim));
+    for (std::int64_t p = 0; p < length; ++p)
+      out[p] = radical_inverse(static_cast<std::uint64_t>(perm[static_cast<std::size_t>(p)]) + 1, base);
+  });
+}
+
 // Row-major [length][dims] uniforms, as uniform_matrix returns them.
 int ref_uniform_matrix(std::int64_t dims, std::int64_t length, std::uint64_t seed, double* out,
                        char* err, int errlen) {

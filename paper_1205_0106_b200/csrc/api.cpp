@@ -308,6 +308,8 @@ struct qmcg_ctx {
   size_t table_budget = 0;  // bytes the permutation table may take; 0 = what free memory allows
   int64_t last_windows = 0;  // date windows of the last pricing (1 = resident tables)
   double* h_pinned = nullptr;  // [0..1] sums, [2] err as double bits
+  double* h_res = nullptr;     // pinned: node sums + the error word (enqueue_results)
+  size_t h_res_cap = 0;
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
   int64_t launches = 0;
 };
@@ -406,14 +408,15 @@ qmcg_status build_rows_overlapped(qmcg_ctx* c, uint64_t seed, int64_t n, uint32_
   return QMCG_OK;
 }
 
-// Make rows [0, m) of the table for (seed, n) over columns [b, e) resident.
-qmcg_status ensure_perms(qmcg_ctx* c, uint64_t seed, int64_t n, int64_t b, int64_t e, int64_t m, bool rebuild) {
+// Table storage for rows [0, m) of (seed, n) over columns [b, e): a cache for another key is
+// dropped; rows [0, cache_dims) already built for this key are kept. Rows [cache_dims, m)
+// are left for the caller to build.
+qmcg_status reserve_table(qmcg_ctx* c, uint64_t seed, int64_t n, int64_t b, int64_t e, int64_t m, bool rebuild) {
   if (c->cache_n != n || c->cache_seed != seed || c->col_begin != b || c->col_end != e || rebuild) drop_cache(c);
   if (c->cache_n == n && c->cache_dims >= m) return QMCG_OK;
   const int64_t cols = e - b;
   const int64_t ld = qmcg::table_ld(cols);
   const size_t row_bytes = static_cast<size_t>(ld) * sizeof(uint32_t);
-  const size_t copy_bytes = static_cast<size_t>(cols) * sizeof(uint32_t);
   if (static_cast<size_t>(m) > c->table_rows_cap) {
     uint32_t* nt = nullptr;
     cudaError_t err = cudaMalloc(&nt, row_bytes * static_cast<size_t>(m) + qmcg::kTablePad * sizeof(uint32_t));
@@ -439,6 +442,16 @@ qmcg_status ensure_perms(qmcg_ctx* c, uint64_t seed, int64_t n, int64_t b, int64
   c->cache_seed = seed;
   c->col_begin = b;
   c->col_end = e;
+  return QMCG_OK;
+}
+
+// Make rows [0, m) of the table for (seed, n) over columns [b, e) resident.
+qmcg_status ensure_perms(qmcg_ctx* c, uint64_t seed, int64_t n, int64_t b, int64_t e, int64_t m, bool rebuild) {
+  qmcg_status rs = reserve_table(c, seed, n, b, e, m, rebuild);
+  if (rs) return rs;
+  if (c->cache_dims >= m) return QMCG_OK;
+  const int64_t ld = qmcg::table_ld(e - b);
+  const size_t copy_bytes = static_cast<size_t>(e - b) * sizeof(uint32_t);
   const bool full = (b == 0 && e == n);
   if (!full) QMCG_CUDA(c->d_fullperm.reserve(static_cast<size_t>(n)));
 #ifndef QMCG_NO_K1_OVERLAP
@@ -614,14 +627,36 @@ void finish_stats(int64_t n, double sum, double sum_sq, double& mean, double& se
   }
 }
 
+// Results in two phases, so a device group can enqueue every member before waiting on any:
+// enqueue_results queues the D2H copy of the node sums and the error word into pinned memory,
+// finish_results waits for it and maps the error word to the reference's exceptions.
+qmcg_status enqueue_results(qmcg_ctx* c, size_t slots) {
+  if (2 * slots + 1 > c->h_res_cap) {
+    if (c->h_res) cudaFreeHost(c->h_res);
+    c->h_res = nullptr;
+    c->h_res_cap = 0;
+    QMCG_CUDA(cudaMallocHost(&c->h_res, (2 * slots + 1) * sizeof(double)));
+    c->h_res_cap = 2 * slots + 1;
+  }
+  QMCG_CUDA(cudaMemcpyAsync(c->h_res, c->d_sums.ptr, 2 * slots * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  QMCG_CUDA(cudaMemcpyAsync(c->h_res + 2 * slots, c->d_err.ptr, sizeof(uint32_t), cudaMemcpyDeviceToHost,
+                            c->stream));
+  return QMCG_OK;
+}
+
+qmcg_status finish_results(qmcg_ctx* c, size_t slots, double* sums) {
+  QMCG_CUDA(cudaStreamSynchronize(c->stream));
+  uint32_t err = 0;
+  std::memcpy(&err, c->h_res + 2 * slots, sizeof err);
+  std::copy(c->h_res, c->h_res + 2 * slots, sums);
+  return map_err(err);
+}
+
 qmcg_status sync_results(qmcg_ctx* c, size_t slots, std::vector<double>& sums) {
   sums.resize(2 * slots);
-  uint32_t err = 0;
-  QMCG_CUDA(cudaMemcpyAsync(sums.data(), c->d_sums.ptr, 2 * slots * sizeof(double), cudaMemcpyDeviceToHost,
-                            c->stream));
-  QMCG_CUDA(cudaMemcpyAsync(&err, c->d_err.ptr, sizeof(uint32_t), cudaMemcpyDeviceToHost, c->stream));
-  QMCG_CUDA(cudaStreamSynchronize(c->stream));
-  return map_err(err);
+  qmcg_status st = enqueue_results(c, slots);
+  if (st) return st;
+  return finish_results(c, slots, sums.data());
 }
 
 struct DeviceGuard {
@@ -707,6 +742,7 @@ void qmcg_destroy(qmcg_ctx* c) {
   c->d_stbest.release();
   c->d_stpend.release();
   if (c->h_pinned) cudaFreeHost(c->h_pinned);
+  if (c->h_res) cudaFreeHost(c->h_res);
   for (auto& ev : c->ev)
     if (ev) cudaEventDestroy(ev);
   cudaStreamDestroy(c->stream);
@@ -826,6 +862,11 @@ qmcg_status qmcg_clear_cache(qmcg_ctx* c) {
   return QMCG_OK;
 }
 
+}  // extern "C"
+
+// ---- pricing of a path range (resident or streamed tables) ----
+namespace {
+
 // Bytes the permutation table of `cols` columns may occupy: the caller's
 // budget, capped by free device memory (+ the table already held) minus the
 // K1 scratch, the carried walk state, the per-path values and a margin.
@@ -838,6 +879,20 @@ size_t table_bytes_allowed(qmcg_ctx* c, int64_t n, int64_t cols, bool full) {
                          static_cast<size_t>(cols) * (4 * 8 + 4 + 8 + 8) + (size_t{1} << 30);
   const size_t avail = free_b + held > reserve ? free_b + held - reserve : 0;
   return c->table_budget ? std::min(c->table_budget, avail) : avail;
+}
+
+// The pairwise sums of the `count` consecutive tree nodes [node0, node0 + count) at `depth`
+// from the per-path values of paths [b, ...) in d_values, into d_sums[2k, 2k + 1].
+qmcg_status enqueue_node_sums(qmcg_ctx* c, int64_t n, int depth, int64_t node0, int64_t count, int64_t b) {
+  for (int64_t k = 0; k < count; ++k) {
+    int64_t off, size;
+    tree_node(n, depth, node0 + k, off, size);
+    int launches = 0;
+    QMCG_CUDA(qmcg::launch_pairwise(c->d_values.ptr + (off - b), size, c->d_red.ptr, c->d_sums.ptr + 2 * k, c->stream,
+                                    &launches));
+    c->launches += launches;
+  }
+  return QMCG_OK;
 }
 
 // Tables larger than device memory (config 5: 2^28 paths x 365 dates = 392 GB):
@@ -910,9 +965,10 @@ qmcg_status enqueue_streamed(qmcg_ctx* c, CallPlan& plan, uint64_t seed, int64_t
 // Per-path values of paths [b, e) into d_values (resident tables from the
 // cache, or streamed date windows when the tables exceed the budget), then
 // the pairwise sums of each of the `count` consecutive tree nodes
-// [node0, node0 + count) at `depth` (which must tile [b, e)) into d_sums.
-static qmcg_status price_nodes(qmcg_ctx* c, const qmcg_option_spec* spec, int64_t m, int64_t n, uint64_t seed,
-                               uint32_t flags, int depth, int64_t node0, int64_t count, double* sums) {
+// [node0, node0 + count) at `depth` (which must tile [b, e)) into d_sums, and
+// their copy to pinned host memory (price_nodes_finish waits for it).
+static qmcg_status price_nodes_enqueue(qmcg_ctx* c, const qmcg_option_spec* spec, int64_t m, int64_t n,
+                                       uint64_t seed, uint32_t flags, int depth, int64_t node0, int64_t count) {
   int64_t b, e, off, size;
   tree_node(n, depth, node0, b, size);
   tree_node(n, depth, node0 + count - 1, off, size);
@@ -946,26 +1002,32 @@ static qmcg_status price_nodes(qmcg_ctx* c, const qmcg_option_spec* spec, int64_
     st = enqueue_values(c, plan, b, e);
     if (st) return st;
   }
-  for (int64_t k = 0; k < count; ++k) {
-    tree_node(n, depth, node0 + k, off, size);
-    int launches = 0;
-    QMCG_CUDA(qmcg::launch_pairwise(c->d_values.ptr + (off - b), size, c->d_red.ptr, c->d_sums.ptr + 2 * k,
-                                    c->stream, &launches));
-    c->launches += launches;
-  }
-  tr.mark(streamed ? "streamed enqueued" : "enqueued");
-  std::vector<double> out;
-  st = sync_results(c, static_cast<size_t>(count), out);
+  st = enqueue_node_sums(c, n, depth, node0, count, b);
   if (st) return st;
-  tr.mark("synced");
-  std::copy(out.begin(), out.end(), sums);
-  return QMCG_OK;
+  tr.mark(streamed ? "streamed enqueued" : "enqueued");
+  return enqueue_results(c, static_cast<size_t>(count));
+}
+
+static qmcg_status price_nodes_finish(qmcg_ctx* c, int64_t count, double* sums) {
+  return finish_results(c, static_cast<size_t>(count), sums);
+}
+
+static qmcg_status price_nodes(qmcg_ctx* c, const qmcg_option_spec* spec, int64_t m, int64_t n, uint64_t seed,
+                               uint32_t flags, int depth, int64_t node0, int64_t count, double* sums) {
+  qmcg_status st = price_nodes_enqueue(c, spec, m, n, seed, flags, depth, node0, count);
+  if (st) return st;
+  return price_nodes_finish(c, count, sums);
 }
 
 static qmcg_status price_range(qmcg_ctx* c, const qmcg_option_spec* spec, int64_t m, int64_t n, uint64_t seed,
                                uint32_t flags, double sums[2]) {
   return price_nodes(c, spec, m, n, seed, flags, 0, 0, 1, sums);
 }
+
+//@@GROUP@@
+}  // namespace
+
+extern "C" {
 
 qmcg_status qmcg_price_american(qmcg_ctx* c, const qmcg_option_spec* spec, int64_t m, int64_t n, uint64_t seed,
                                 uint32_t flags, qmcg_pricing_result* out) {
@@ -1140,7 +1202,7 @@ qmcg_status qmcg_price_american_batch(qmcg_ctx* c, const qmcg_option_spec* specs
     G.path_begin = 0;
     G.path_count = n;
     G.alpha = 0.0;
-    QMCG_CUDA(qmcg::launch_gen_z(G, c->d_z.ptr, n, c->stream, /*prefix=*/true));
+    QMCG_CUDA(qmcg::launch_gen_z(G, c->d_z.ptr, n, c->stream, qmcg::kGenPrefix));
     c->launches += 1;
     tr.mark("gen_z enqueued");
     for (int k = 0; k < 2; ++k) {
@@ -1304,6 +1366,40 @@ qmcg_status qmcg_normal_table(qmcg_ctx* c, int64_t n, uint64_t seed, int64_t dim
   G.alpha = 0.0;
   QMCG_CUDA(qmcg::launch_gen_z(G, c->d_z.ptr, n, c->stream));
   QMCG_CUDA(cudaMemcpyAsync(out_host, c->d_z.ptr, static_cast<size_t>(dims) * static_cast<size_t>(n) * sizeof(double),
+                            cudaMemcpyDeviceToHost, c->stream));
+  QMCG_CUDA(cudaStreamSynchronize(c->stream));
+  return QMCG_OK;
+}
+
+qmcg_status qmcg_uniform_rows(qmcg_ctx* c, int64_t n, uint64_t seed, int64_t dim_begin, int64_t dim_count,
+                              double* out_host) {
+  if (!c || !out_host || n < 2 || dim_begin < 0 || dim_count < 1)
+    return fail(QMCG_INVALID_ARGUMENT, "qmcg_uniform_rows: bad argument");
+  if (static_cast<uint64_t>(n) > 0xffffffffULL)
+    return fail(QMCG_LENGTH_ERROR, "permutation_indices: n exceeds the 2^32-1 supported maximum");
+  std::lock_guard<std::mutex> lock(c->mu);
+  DeviceGuard g(c->device);
+  const int64_t dims = dim_begin + dim_count;
+  qmcg_option_spec s{100.0, 100.0, 0.05, 0.2, 1.0, QMCG_CALL};
+  CallPlan plan;
+  qmcg_status st = plan_call(s, dims, n, 0, plan);
+  if (st) return st;
+  st = upload_plan(c, plan, n);
+  if (st) return st;
+  st = ensure_perms(c, seed, n, 0, n, dims, false);
+  if (st) return st;
+  QMCG_CUDA(c->d_z.reserve(static_cast<size_t>(dim_count) * static_cast<size_t>(n)));
+  PriceParams G = plan.P;
+  G.perm = c->table;
+  G.ld = qmcg::table_ld(c->col_end - c->col_begin);
+  G.col_begin = c->col_begin;
+  G.path_begin = 0;
+  G.path_count = n;
+  G.d_begin = static_cast<int32_t>(dim_begin);
+  G.d_end = static_cast<int32_t>(dims);
+  QMCG_CUDA(qmcg::launch_gen_z(G, c->d_z.ptr, n, c->stream, qmcg::kGenUniform));
+  QMCG_CUDA(cudaMemcpyAsync(out_host, c->d_z.ptr,
+                            static_cast<size_t>(dim_count) * static_cast<size_t>(n) * sizeof(double),
                             cudaMemcpyDeviceToHost, c->stream));
   QMCG_CUDA(cudaStreamSynchronize(c->stream));
   return QMCG_OK;

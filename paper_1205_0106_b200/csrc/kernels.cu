@@ -594,6 +594,15 @@ __device__ __forceinline__ typename ZSlot<F32>::T central_z(double y, double alp
   return moro_central_plus(y, alpha);
 }
 
+// UEXP: the generator's uniform u goes to the slot instead of the normal (parity
+// export of exactly the digits the pricing kernel computes; FP64 slots only).
+template <bool F32, bool UEXP>
+__device__ __forceinline__ typename ZSlot<F32>::T central_or_u(double u, double y, double alpha) {
+  static_assert(!(F32 && UEXP), "uniform export uses FP64 slots");
+  if constexpr (UEXP) return u;
+  else return central_z<F32>(y, alpha);
+}
+
 // Store one generated point: z in its slot; a tail point (|u - 1/2| > 0.42, the
 // reference's branch on the bit-exact uniform) then overwrites the slot with its
 // parked value and queues its index at ntail + rank. One predicate feeds the
@@ -713,12 +722,13 @@ __device__ __forceinline__ void flush_tail(uint32_t ws, uint32_t zrow, uint32_t 
 // One point of a date row: tail test; a tail point parks u in its z slot and
 // queues its index (branch-free: other lanes write a dummy slot); otherwise
 // the central normal + alpha goes to the slot.
-template <bool CLAMP, bool F32>
+template <bool CLAMP, bool F32, bool UEXP>
 __device__ __forceinline__ void finish_point(uint32_t ws, uint32_t zslot, uint32_t idx, double u, bool clamp,
                                              double alpha, int lane, unsigned lt, uint32_t& ntail) {
   if (CLAMP && clamp) u = clamp_endpoints(u);
   const double y = __dadd_rn(u, -0.5);
-  park_point<F32>(zslot, ws + kWTailIdx, idx, central_z<F32>(y, alpha), tail_park<F32>(u, y), y, lt, ntail);
+  park_point<F32>(zslot, ws + kWTailIdx, idx, central_or_u<F32, UEXP>(u, y, alpha), tail_park<F32>(u, y), y, lt,
+                  ntail);
 }
 
 // radical_inverse with the digits taken two at a time (DIM_PAIR): q = x / p^2,
@@ -805,7 +815,7 @@ __device__ __forceinline__ double halton_fixed(uint32_t x, uint32_t magic, uint3
 }
 
 // Two independent 32-path chunks (ch, ch + 1) of one fixed-digit row.
-template <int D, bool F32>
+template <int D, bool F32, bool UEXP>
 __device__ __forceinline__ void generate_chunk_pair(const double2 (&sc)[4], uint32_t magic, uint32_t shift,
                                                     uint32_t negp, uint32_t ws, uint32_t prow, uint32_t zrow, int ch,
                                                     int lane, unsigned lt, double alpha, uint32_t& ntail) {
@@ -817,8 +827,9 @@ __device__ __forceinline__ void generate_chunk_pair(const double2 (&sc)[4], uint
   const double ub = halton_fixed<D>(xb, magic, shift, negp, sc);
   const double ya = __dadd_rn(ua, -0.5);
   const double yb = __dadd_rn(ub, -0.5);
-  const auto za = central_z<F32>(ya, alpha);
-  const auto zb = central_z<F32>(yb, alpha);
+  // UEXP (parity export): the slot receives the uniform itself, through the same digit code
+  const auto za = central_or_u<F32, UEXP>(ua, ya, alpha);
+  const auto zb = central_or_u<F32, UEXP>(ub, yb, alpha);
   if constexpr (!F32) {
     park_pair(zrow + ch * kCh, zrow + ch * kCh + kCh, ws + kWTailIdx, ch * 32 + lane, za, ua, ya, zb, ub, yb, lt,
               ntail);
@@ -829,7 +840,7 @@ __device__ __forceinline__ void generate_chunk_pair(const double2 (&sc)[4], uint
   }
 }
 
-template <int D, bool F32>
+template <int D, bool F32, bool UEXP>
 __device__ __forceinline__ uint32_t generate_row_fixed(const double2* sn, uint32_t magic, uint32_t shift,
                                                        uint32_t negp, uint32_t ws, uint32_t prow, uint32_t zrow,
                                                        int nchunks, int lane, unsigned lt, double alpha) {
@@ -842,16 +853,16 @@ __device__ __forceinline__ uint32_t generate_row_fixed(const double2* sn, uint32
   int ch = 0;
 #pragma unroll 1
   for (; ch + 1 < nchunks; ch += 2)  // two independent chunks in flight
-    generate_chunk_pair<D, F32>(sc, magic, shift, negp, ws, prow, zrow, ch, lane, lt, alpha, ntail);
+    generate_chunk_pair<D, F32, UEXP>(sc, magic, shift, negp, ws, prow, zrow, ch, lane, lt, alpha, ntail);
   if (ch < nchunks) {
     const uint32_t x = lds_u32(prow + ch * 128);
     const double u = halton_fixed<D>(x, magic, shift, negp, sc);
-    finish_point<false, F32>(ws, zrow + ch * kCh, ch * 32 + lane, u, false, alpha, lane, lt, ntail);
+    finish_point<false, F32, UEXP>(ws, zrow + ch * kCh, ch * 32 + lane, u, false, alpha, lane, lt, ntail);
   }
   return ntail;
 }
 
-template <bool SLOW, bool F32>
+template <bool SLOW, bool F32, bool UEXP = false>
 __device__ __forceinline__ void generate_row(const PriceParams& P, uint32_t ws, int d, uint32_t prow, uint32_t zrow,
                                              uint32_t logtab, int nchunks, int lane, unsigned lt) {
   using Z = ZSlot<F32>;
@@ -864,11 +875,11 @@ __device__ __forceinline__ void generate_row(const PriceParams& P, uint32_t ws, 
   const uint32_t zl = zrow + lane * Z::kSize;
   uint32_t ntail = 0;
   if (!SLOW && D == 3) {
-    ntail = generate_row_fixed<3, F32>(sn, magic, shift, negp, ws, pl, zl, nchunks, lane, lt, alpha);
+    ntail = generate_row_fixed<3, F32, UEXP>(sn, magic, shift, negp, ws, pl, zl, nchunks, lane, lt, alpha);
   } else if (!SLOW && D == 4) {
-    ntail = generate_row_fixed<4, F32>(sn, magic, shift, negp, ws, pl, zl, nchunks, lane, lt, alpha);
+    ntail = generate_row_fixed<4, F32, UEXP>(sn, magic, shift, negp, ws, pl, zl, nchunks, lane, lt, alpha);
   } else if (!SLOW && D == 2) {
-    ntail = generate_row_fixed<2, F32>(sn, magic, shift, negp, ws, pl, zl, nchunks, lane, lt, alpha);
+    ntail = generate_row_fixed<2, F32, UEXP>(sn, magic, shift, negp, ws, pl, zl, nchunks, lane, lt, alpha);
   } else if (!SLOW && ((dp.z >> 16) & DIM_PAIR)) {
     const uint4 pp = __ldg(P.pairs + d);
     for (int ch = 0; ch < nchunks; ++ch) {
@@ -877,7 +888,7 @@ __device__ __forceinline__ void generate_row(const PriceParams& P, uint32_t ws, 
                        : D == 6 ? halton_pairs_fixed<6>(x, dp.x, pp, sn)
                        : D == 7 ? halton_pairs_fixed<7>(x, dp.x, pp, sn)
                                 : halton_pairs(x, dp.x, pp, D, sn);
-      finish_point<false, F32>(ws, zl + ch * 32 * Z::kSize, ch * 32 + lane, u, false, alpha, lane, lt, ntail);
+      finish_point<false, F32, UEXP>(ws, zl + ch * 32 * Z::kSize, ch * 32 + lane, u, false, alpha, lane, lt, ntail);
     }
   } else {
     const bool clamp = SLOW && ((dp.z >> 16) & DIM_CLAMP);
@@ -886,11 +897,11 @@ __device__ __forceinline__ void generate_row(const PriceParams& P, uint32_t ws, 
     for (int ch = 0; ch < nchunks; ++ch) {
       const uint32_t x = lds_u32(pl + ch * 128);
       const double u = wide ? halton_any<true>(x, dp, m64, sn) : halton_any<false>(x, dp, m64, sn);
-      finish_point<SLOW, F32>(ws, zl + ch * 32 * Z::kSize, ch * 32 + lane, u, clamp, alpha, lane, lt, ntail);
+      finish_point<SLOW, F32, UEXP>(ws, zl + ch * 32 * Z::kSize, ch * 32 + lane, u, clamp, alpha, lane, lt, ntail);
     }
   }
 #ifndef QMCG_PROBE_NOTAIL  // timing probe only (wrong results): skip the Moro tail
-  if (ntail) flush_tail<F32>(ws, zrow, ntail, logtab, alpha, lane);
+  if (!UEXP && ntail) flush_tail<F32>(ws, zrow, ntail, logtab, alpha, lane);
 #endif
 }
 
@@ -1244,11 +1255,14 @@ __global__ void __launch_bounds__(kThreads, QMCG_MINB)
 // bit-exact scrambled-Halton uniform, for all dates of this block's 256 paths.
 // Same tile staging and generation as price_kernel; rows are then streamed to
 // HBM (coalesced, 2 KB per warp-row).
-// PREFIX: instead of z, each path's running sum S_k = z_0 + ... + z_k (the
+// MODE kGenPrefix: instead of z, each path's running sum S_k = z_0 + ... + z_k (the
 // contract-independent part of the batch walk, V_k = S_k + (k+1) alpha_c).
-template <bool SLOW, bool PREFIX>
+// MODE kGenUniform: the scrambled-Halton uniforms the generator computes (parity
+// export of the pricing kernel's own digit code, generate_row<..., UEXP>).
+template <bool SLOW, int MODE>
 __global__ void __launch_bounds__(kThreads, QMCG_MINB) gen_z_kernel(const PriceParams P, double* __restrict__ z,
                                                                     int64_t ldz) {
+  constexpr bool PREFIX = MODE == kGenPrefix;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const uint32_t sbase = smem_u32(smem_raw);
   const int warp = threadIdx.x >> 5;
@@ -1257,8 +1271,10 @@ __global__ void __launch_bounds__(kThreads, QMCG_MINB) gen_z_kernel(const PriceP
   const uint32_t logtab = sbase + kLogOff;
   const unsigned lt = lanemask_lt();
   const int64_t block_first = static_cast<int64_t>(blockIdx.x) * kThreads;
-  const int m = P.m;
-  const int ntiles = (m + kTile - 1) / kTile;
+  // date window [d_begin, d_end) (the whole [0, m) except for windowed exports); row d of the
+  // output is d - d_begin (PREFIX needs d_begin = 0)
+  const int dbeg = P.d_begin, dend = P.d_end;
+  const int ntiles = (dend - dbeg + kTile - 1) / kTile;
   const int64_t block_paths = min(static_cast<int64_t>(kThreads), P.path_count - block_first);
   const int nchunks = static_cast<int>((block_paths + 31) / 32);
   const int64_t col0 = P.path_begin - P.col_begin + block_first;
@@ -1267,28 +1283,28 @@ __global__ void __launch_bounds__(kThreads, QMCG_MINB) gen_z_kernel(const PriceP
   if (threadIdx.x < 128) sts_v2f64(logtab + threadIdx.x * 16, c_log_table[threadIdx.x]);
   __syncthreads();
   if (lane == 0) {
-    if (warp < m) issue_row(P, sbase, warp, 0, warp, col0, bytes);
-    if (kPermBuffers == 2 && kTile + warp < m) issue_row(P, sbase, kTile + warp, 1, warp, col0, bytes);
+    if (dbeg + warp < dend) issue_row(P, sbase, dbeg + warp, 0, warp, col0, bytes);
+    if (kPermBuffers == 2 && dbeg + kTile + warp < dend) issue_row(P, sbase, dbeg + kTile + warp, 1, warp, col0, bytes);
   }
   double run = 0.0;  // PREFIX: S of this thread's path
   const int64_t my = P.path_begin + block_first + threadIdx.x;
   for (int k = 0; k < ntiles; ++k) {
-    const int k0 = k * kTile;
+    const int k0 = dbeg + k * kTile;
     const int b = k & 1;
     const uint32_t ztile = sbase + kZtOff + (kZtBuffers == 2 ? b : 0) * kZtBuf;
     const uint32_t zrow = ztile + warp * kThreads * 8;
-    if (k0 + warp < m) {
+    if (k0 + warp < dend) {
       const int pb = kPermBuffers == 2 ? b : 0;
       mbar_wait_u32(sbase + kBarOff + (pb * kTile + warp) * 8,
                     static_cast<uint32_t>(kPermBuffers == 2 ? (k >> 1) & 1 : k & 1));
-      generate_row<SLOW, false>(P, ws, k0 + warp, sbase + kPermOff + pb * kPermBuf + warp * kThreads * 4, zrow, logtab,
-                                nchunks, lane, lt);
+      generate_row<SLOW, false, MODE == kGenUniform>(P, ws, k0 + warp, sbase + kPermOff + pb * kPermBuf + warp * kThreads * 4,
+                                                     zrow, logtab, nchunks, lane, lt);
       __syncwarp();  // perm row consumed: stage this warp's row of the tile kPermBuffers ahead
       const int dn = k0 + kPermBuffers * kTile + warp;
-      if (lane == 0 && dn < m) issue_row(P, sbase, dn, pb, warp, col0, bytes);
+      if (lane == 0 && dn < dend) issue_row(P, sbase, dn, pb, warp, col0, bytes);
       if (!PREFIX) {
         __syncwarp();
-        double* dst = z + static_cast<int64_t>(k0 + warp) * ldz + P.path_begin + block_first;
+        double* dst = z + static_cast<int64_t>(k0 + warp - dbeg) * ldz + P.path_begin + block_first;
         for (int ch = 0; ch < nchunks; ++ch) {
           const int idx = ch * 32 + lane;
           if (idx < block_paths) __stcs(dst + idx, lds_f64(zrow + idx * 8));
@@ -1298,7 +1314,7 @@ __global__ void __launch_bounds__(kThreads, QMCG_MINB) gen_z_kernel(const PriceP
     if (PREFIX) {
       __syncthreads();  // the tile's rows are complete
       if (threadIdx.x < block_paths) {
-        for (int t = 0; t < kTile && k0 + t < m; ++t) {
+        for (int t = 0; t < kTile && k0 + t < dend; ++t) {
           run = __dadd_rn(run, lds_f64(ztile + (t * kThreads + threadIdx.x) * 8));
           __stcs(z + static_cast<int64_t>(k0 + t) * ldz + my, run);
         }
@@ -1724,14 +1740,15 @@ cudaError_t launch_dfma_probe(double* out, int blocks, int iters, cudaStream_t s
 
 cudaError_t ensure_log_table(cudaStream_t s);
 
-cudaError_t launch_gen_z(const PriceParams& P, double* z, int64_t ldz, cudaStream_t s, bool prefix) {
+cudaError_t launch_gen_z(const PriceParams& P, double* z, int64_t ldz, cudaStream_t s, int mode) {
   if (P.path_count <= 0) return cudaSuccess;
   cudaError_t e = ensure_log_table(s);
   if (e != cudaSuccess) return e;
   const int64_t blocks = (P.path_count + kThreads - 1) / kThreads;
   const bool slow = P.any_wide || P.any_clamp;
-  auto kern = prefix ? (slow ? gen_z_kernel<true, true> : gen_z_kernel<false, true>)
-                     : (slow ? gen_z_kernel<true, false> : gen_z_kernel<false, false>);
+  auto kern = mode == kGenPrefix    ? (slow ? gen_z_kernel<true, kGenPrefix> : gen_z_kernel<false, kGenPrefix>)
+              : mode == kGenUniform ? (slow ? gen_z_kernel<true, kGenUniform> : gen_z_kernel<false, kGenUniform>)
+                                    : (slow ? gen_z_kernel<true, kGenZ> : gen_z_kernel<false, kGenZ>);
   e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmemBytes));
   if (e != cudaSuccess) return e;
   kern<<<static_cast<unsigned>(blocks), kThreads, kSmemBytes, s>>>(P, z, ldz);

@@ -124,7 +124,10 @@ struct BatchParams {
 // Generation only: the QMC normal table z[d][p] (d < m, p in [path_begin, +path_count)) of the
 // context's permutation table (PriceParams fields perm/ld/col_begin/dims/... ; alpha ignored).
 cudaError_t launch_walk_group(const BatchParams& B, int kind, cudaStream_t s);  // the batch walk reads prefix sums S (gen_z prefix mode)
-cudaError_t launch_gen_z(const PriceParams& P, double* z, int64_t ldz, cudaStream_t s, bool prefix = false);
+// mode: kGenZ (normals), kGenPrefix (per-path running sums of the normals, the batch walk's input),
+// kGenUniform (the uniforms themselves: parity export of the pricing kernel's generator).
+enum : int { kGenZ = 0, kGenPrefix = 1, kGenUniform = 2 };
+cudaError_t launch_gen_z(const PriceParams& P, double* z, int64_t ldz, cudaStream_t s, int mode = kGenZ);
 cudaError_t launch_european(const uint32_t* perm_row, int64_t count, DimParam dp, const double* sc, const double* nc,
                             double s0, double a, double bsd, double strike, double disc, int kind, double* out,
                             cudaStream_t s);

@@ -170,6 +170,10 @@ def warm_tables_sharded(ctx: Optional["qmcg.Context"], n_paths: int, seed: int, 
         if build_fn is not None:
             build_fn(k, rank, world, buf)
         else:
+            # the context writes `buf` on its own (non-blocking) stream: torch's stream must be idle
+            # first (the allocator may hand out memory still in use by queued torch work); the
+            # call returns after its stream has synchronised, so later torch work sees the rows
+            _sync_torch_stream(buf)
             ctx.build_tables(n_paths, seed, rank, world, k, buf.data_ptr(), n_paths)
     b_me, e_me = cols[rank]
     w_me = e_me - b_me
@@ -192,4 +196,15 @@ def warm_tables_sharded(ctx: Optional["qmcg.Context"], n_paths: int, seed: int, 
         if table.device.type != "cuda":
             table = table.cuda()
         table = table.contiguous()
+        # the all-to-all and the slice copies above are queued on torch's stream; the context
+        # copies from `table` on its own non-blocking stream, so wait for them to finish
+        _sync_torch_stream(table)
         ctx.import_tables(n_paths, seed, b_me, e_me, dims, table.data_ptr(), table.stride(0))
+
+
+def _sync_torch_stream(t) -> None:
+    """Block until torch's current stream on t's device has drained (orders torch-side work
+    before a qmcg context call that runs on the context's own stream)."""
+    import torch
+    if t.device.type == "cuda":
+        torch.cuda.current_stream(t.device).synchronize()

@@ -41,7 +41,7 @@ EXPORTS = (
     "qmcg_normals", "qmcg_normal_table", "qmcg_path_values", "qmcg_time_device", "qmcg_time_perm_build",
     "qmcg_last_launch_count", "qmcg_get_stream", "qmcg_fp64_peak", "qmcg_set_table_budget",
     "qmcg_last_window_count", "qmcg_price_american_nodes", "qmcg_simulate_batch", "qmcg_sweep_batch",
-    "qmcg_backward_sweep", "qmcg_build_tables", "qmcg_import_tables",
+    "qmcg_backward_sweep", "qmcg_build_tables", "qmcg_import_tables", "qmcg_uniform_rows",
 )
 
 
@@ -148,6 +148,7 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
         L.qmcg_normals.argtypes = [P, I64, U64, I64, P]
         L.qmcg_path_values.argtypes = [P, C.POINTER(_CSpec), I64, I64, U64, U32, P]
         L.qmcg_normal_table.argtypes = [P, I64, U64, I64, P]
+        L.qmcg_uniform_rows.argtypes = [P, I64, U64, I64, I64, P]
         L.qmcg_time_device.argtypes = [P, C.POINTER(_CSpec), I64, I64, U64, U32, C.c_int, PD, PD, PD]
         L.qmcg_time_perm_build.argtypes = [P, I64, U64, I64, PD]
         L.qmcg_last_launch_count.argtypes = [P]
@@ -344,6 +345,13 @@ class Context:
     def normal_table(self, n: int, seed: int, dims: int) -> np.ndarray:
         out = np.zeros((int(dims), int(n)), dtype=np.float64)
         _check(self._lib.qmcg_normal_table(self._h, int(n), int(seed), int(dims), out.ctypes.data))
+        return out
+
+    def uniform_rows(self, n: int, seed: int, dim_begin: int, dim_count: int) -> np.ndarray:
+        """(dim_count, n) uniforms of dims [dim_begin, +dim_count) from the pricing kernels' generator."""
+        out = np.zeros((int(dim_count), int(n)), dtype=np.float64)
+        _check(self._lib.qmcg_uniform_rows(self._h, int(n), int(seed), int(dim_begin), int(dim_count),
+                                           out.ctypes.data))
         return out
 
     def path_values(self, spec: OptionSpec, m: int, n_paths: int, seed: int, allow_put: bool = False,
