@@ -108,6 +108,25 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
+def cpu_model():
+    """The host CPU model (lscpu 'Model name', else /proc/cpuinfo)."""
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for ln in out.splitlines():
+            if ln.lower().startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except (OSError, subprocess.SubprocessError):
+        pass
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
 def cpu_reference(steps, warmup, n_paths=CPU_SAMPLE_PATHS, lanes=None):
     """The reference's own price_american (oracle/_ref, compiled from proj/src) on the host cores."""
     import oracle
@@ -138,19 +157,32 @@ def run_reference_arm(args, rank, world):
     while sample > (1 << 18) and (steps + warmup) * sample > 24 * CPU_SAMPLE_PATHS:
         sample //= 2
     base = cpu_reference(steps, warmup, n_paths=sample)
+    model = cpu_model()
     line = {"impl": "reference", "metric": METRIC, "value": base["value"], "unit": "path-steps/s",
             "n_gpus": args.gpus, "steps": steps, "warmup": warmup,
-            "ms_per_step": 1e3 * base["seconds_per_call"] * (N_PATHS / sample),
+            # measured: the median per-call time of the sample this arm actually ran (no extrapolation)
+            "ms_per_step": 1e3 * base["seconds_per_call"],
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (QMC paths from the reference's scrambled Halton stream)",
-            "config": {"workload": WORKLOAD, "n_paths": N_PATHS, "m_dates": M_DATES, "seed": SEED,
-                       "sample_paths": sample, "parallelism": "host threads (reference lanes)"},
-            "cpu_baseline": {k: base[k] for k in ("value", "unit", "cores", "kind", "sample")},
+            "config": {"workload": f"reference CPU sample of config 3: {sample} paths x {M_DATES} dates per step "
+                                   f"(1/{N_PATHS // sample} of the 2^24-path workload; the metric is per path-step), "
+                                   "S0=K=100 r=0.05 sigma=0.2 T=1 call, seed 42, cold (each call builds its "
+                                   "permutation tables, as the reference always does)",
+                       "n_paths": sample, "m_dates": M_DATES, "seed": SEED, "full_workload": WORKLOAD,
+                       "parallelism": f"host threads (reference lanes = {base['cores']})"},
+            "cpu_baseline": {k: base[k] for k in ("value", "unit", "cores", "kind", "sample")} | {"cpu_model": model},
             "e2e": {"value": base["value"], "unit": "path-steps/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0},
-            "reference_price": base["price"], "reference_std_error": base["std_error"]}
+            "reference_price": base["price"], "reference_std_error": base["std_error"],
+            "times_s": base["times_s"]}
     print(json.dumps(line), flush=True)
     return 0
+
+
+def fail_loudly(msg):
+    print(json.dumps({"error": msg}), flush=True)
+    print(f"bench.py: {msg}", file=sys.stderr, flush=True)
+    return 2
 
 
 def main():
@@ -165,6 +197,8 @@ def main():
     ap.add_argument("--records", default="", help="also write the GPU and CPU rows as the reference's CSV "
                                                  "(proj/include/qmc/bench.hpp schema; GPU rows lanes = -1)")
     ap.add_argument("--paths-log2", type=int, default=24, help="(debug) smaller path count")
+    ap.add_argument("--devices", default="", help="(testing) comma-separated device list of the single-process "
+                                                  "group, e.g. 0,0 (one GPU listed twice); default 0..gpus-1")
     args = ap.parse_args()
     rank, world = env_int("RANK", 0), env_int("WORLD_SIZE", 1)
     local_rank = env_int("LOCAL_RANK", 0)
@@ -180,11 +214,33 @@ def main():
     warmup = max(3, args.warmup)
     steps = max(1, args.steps)
     dist = None
+    visible = torch.cuda.device_count()
+    # Two multi-GPU layouts: torchrun (one process per GPU, torch.distributed for the 16-byte node
+    # all-gather) or, without torchrun, ONE process driving a device group through the C ABI
+    # (qmcg_create_multi: node sharding, peer-copied table slices, host fold). Both must cover
+    # exactly --gpus devices; anything else is an error, never a silent single-GPU run.
+    if world > 1:
+        if args.gpus != world:
+            return fail_loudly(f"--gpus {args.gpus} but torchrun started {world} ranks")
+        mode = "ranks"
+    elif args.gpus > 1 or args.devices:
+        mode = "group"
+    else:
+        mode = "single"
+    if mode == "group":
+        devices = [int(x) for x in args.devices.split(",")] if args.devices else list(range(args.gpus))
+        if len(devices) != args.gpus:
+            return fail_loudly(f"--devices lists {len(devices)} devices for --gpus {args.gpus}")
+        if max(devices) >= visible:
+            return fail_loudly(f"--gpus {args.gpus} needs devices {sorted(set(devices))}, {visible} visible")
+    if mode == "single" and visible < 1:
+        return fail_loudly("no CUDA device visible")
+    n_gpus = world if mode == "ranks" else args.gpus
     # one GPU per rank; QMCG_DIST_BACKEND=gloo (functional tests of the multi-rank flow only, e.g.
     # several ranks on one GPU, whose kernels never wait on each other) keeps the plumbing on the host
     backend = os.environ.get("QMCG_DIST_BACKEND", "nccl")
-    device = local_rank % max(1, torch.cuda.device_count())
-    if world > 1:
+    device = local_rank % max(1, visible)
+    if mode == "ranks":
         import torch.distributed as dist
         torch.cuda.set_device(device)
         if backend == "nccl":
@@ -200,19 +256,55 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return tuple(float(x) for x in t.tolist())
 
-    local_rank = device
-    ctx = q.Context(device)
+    if mode == "group":
+        ctx = q.Context(devices=devices)
+    else:
+        ctx = q.Context(device)
+    assert ctx.device_count() == (len(devices) if mode == "group" else 1)
     call = q.OptionSpec(*SPEC, kind=q.OptionKind.Call)
     put = q.OptionSpec(*SPEC, kind=q.OptionKind.Put)
     depth = distributed.tree_depth(n_paths, world)
     my_nodes = distributed.rank_nodes(depth, world, rank)
+    # device streams of this process (one per group member): CUDA events on each, max over them
+    members = ctx.member_streams()
+    ext = [(torch.cuda.ExternalStream(sp, device=torch.device("cuda", dv)), dv) for dv, sp in members]
 
-    stream = torch.cuda.ExternalStream(ctx.stream_ptr(), device=torch.device("cuda", local_rank))
+    class DeviceTimer:
+        """Elapsed device time of the work queued between start() and stop() on every member stream
+        of this process (max over members; then max over ranks by the caller)."""
 
-    # ---- config 5 (stress): 2^28 paths x 365 dates, FP32 walk, tables rebuilt by K1 in date
-    # windows when they exceed HBM (392 GB on one GPU; 49 GB per GPU at 8); one cold call,
-    # run first (on a fresh device: after the other lines' allocations its K1 scatter ran
-    # ~15% slower) ----
+        def start(self):
+            self.ev = []
+            for st, dv in ext:
+                e0 = torch.cuda.Event(enable_timing=True)
+                with torch.cuda.device(dv):
+                    e0.record(st)
+                self.ev.append([e0, None, st, dv])
+
+        def stop(self):
+            for rec in self.ev:
+                e1 = torch.cuda.Event(enable_timing=True)
+                with torch.cuda.device(rec[3]):
+                    e1.record(rec[2])
+                rec[1] = e1
+            for rec in self.ev:
+                rec[1].synchronize()
+            return max(e0.elapsed_time(e1) for e0, e1, _, _ in self.ev)
+
+    def sync_all():
+        for dv in sorted({dv for _, dv in members}):
+            torch.cuda.synchronize(dv)
+
+    def price(spec, m, n, **kw):
+        if mode == "ranks":
+            p, se, _ = distributed.price_american_sharded(spec, m, n, SEED, ctx=ctx, **kw)
+            return p, se
+        r = ctx.price_american(spec, m, n, SEED, **kw)
+        return r.price, r.std_error
+
+    # ---- config 5 (stress): 2^28 paths x 365 dates, FP32 walk, one cold call, run first (on a fresh
+    # device). One GPU: tables rebuilt by K1 in date windows (392 GB > HBM). A group: dims built
+    # sharded over the members, each member's 2^28/G-column slice resident or windowed ----
     c5 = None
     if not args.no_c5 and args.paths_log2 == 24:
         ctx.price_american(call, 16, 1 << 12, SEED, fp32=True)  # module and launch setup outside the timing
@@ -220,27 +312,28 @@ def main():
         n5, m5 = 1 << 28, 365
         if dist:
             dist.barrier()
-        torch.cuda.synchronize()
-        c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        sync_all()
+        tm = DeviceTimer()
         t0 = time.perf_counter()
-        c0.record(stream)
-        p5, se5, _ = distributed.price_american_sharded(call, m5, n5, SEED, ctx=ctx, fp32=True)
-        c1.record(stream)
-        torch.cuda.synchronize()
+        tm.start()
+        p5, se5 = price(call, m5, n5, fp32=True)
+        ms5 = tm.stop()
         w5 = time.perf_counter() - t0
-        ms5 = c0.elapsed_time(c1)
         windows = ctx.last_window_count()
         if dist:
             ms5, w5 = max_over_ranks(ms5, w5)
         c5 = {"workload": "config 5: 2^28 paths x 365 dates, FP32 normals + walk (bit-exact FP64 uniforms), call, "
-                          "seed 42, cold (K1 rebuilds every table)",
+                          "seed 42, cold (K1 rebuilds every table)"
+                          + (f", dims built sharded over {n_gpus} devices" if n_gpus > 1 else ""),
               "value": n5 * m5 / (ms5 * 1e-3), "unit": "path-steps/s", "ms_per_option": ms5,
-              "e2e_ms_per_option": 1e3 * w5, "date_windows_rank0": windows,
+              "e2e_ms_per_option": 1e3 * w5, "date_windows_member0": windows,
               "tables": "streamed date windows" if windows > 1 else "resident", "price": p5, "std_error": se5}
         ctx.clear_cache()
 
-    # ---- cold: rebuild every permutation table of this rank's slice (K1), device-timed ----
-    if world == 1:
+    # ---- cold: (a) K1 alone for every table this process needs; (b) one measured cold pricing call
+    # through the C ABI (QMCG_FLAG_NO_CACHE: table allocation + K1 + pricing, like the reference's
+    # elapsed_s, which includes its QuasiStream construction, american.cpp:113-116) ----
+    if mode != "ranks":
         cold_perm_ms = ctx.time_perm_build(n_paths, SEED, M_DATES)
     else:
         # dimension-sharded K1 (dim d on rank d mod N) + all-to-all of column slices
@@ -249,57 +342,64 @@ def main():
         distributed.warm_tables_sharded(ctx, n_paths, SEED, M_DATES)
         dist.barrier()
         cold_perm_ms = max_over_ranks(1e3 * (time.perf_counter() - t0))[0]
-
-    def one_step(spec, allow_put=False):
-        if world == 1:
-            r = ctx.price_american(spec, M_DATES, n_paths, SEED, allow_put=allow_put)
-            return r.price, r.std_error
-        p, se, _ = distributed.price_american_sharded(spec, M_DATES, n_paths, SEED, ctx=ctx, allow_put=allow_put)
-        return p, se
+    cold_e2e = []
+    for _ in range(3):
+        if dist:
+            dist.barrier()
+        sync_all()
+        t0 = time.perf_counter()
+        if mode == "ranks":
+            ctx.clear_cache()
+            distributed.warm_tables_sharded(ctx, n_paths, SEED, M_DATES)
+            cp, cse = price(call, M_DATES, n_paths)
+        else:
+            cp, cse = price(call, M_DATES, n_paths, no_cache=True)
+        w = time.perf_counter() - t0
+        if dist:
+            w = max_over_ranks(w)[0]
+        cold_e2e.append(w)
 
     def timed(spec, allow_put=False, sample_clocks=False):
         for _ in range(warmup):
-            one_step(spec, allow_put)
+            price(spec, M_DATES, n_paths, allow_put=allow_put)
         if dist:
             dist.barrier()
-        torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        sampler = ClockSampler(local_rank) if sample_clocks else None
+        sync_all()
+        sampler = ClockSampler(sorted({dv for _, dv in members})[0]) if sample_clocks else None
         if sampler:
             sampler.__enter__()
         launches = 0
+        tm = DeviceTimer()
         t0 = time.perf_counter()
-        e0.record(stream)
+        tm.start()
         for _ in range(steps):
-            res = one_step(spec, allow_put)
+            res = price(spec, M_DATES, n_paths, allow_put=allow_put)
             launches += ctx.last_launch_count()
-        e1.record(stream)
-        torch.cuda.synchronize()
+        dev_ms = tm.stop()
         wall = time.perf_counter() - t0
         if sampler:
             sampler.__exit__(None, None, None)
         if dist:
             dist.barrier()
-        dev_ms = e0.elapsed_time(e1)
-        if dist:
             dev_ms, wall = max_over_ranks(dev_ms, wall)
         return dev_ms / steps, wall / steps, res, launches, (sampler.summary() if sampler else None)
 
-    ms_call, wall_call, (price, se), launches, clocks = timed(call, sample_clocks=True)
+    ms_call, wall_call, (price_c, se), launches, clocks = timed(call, sample_clocks=True)
     ms_put, wall_put, (price_put, se_put), _, _ = timed(put, allow_put=True)
 
-    # ---- dominant kernel alone (CUDA events around price_kernel on the pricer's stream) ----
-    kernel_ms = step_ms = None
-    if world == 1:
-        kernel_ms, step_ms, _, _ = ctx.time_device(call, M_DATES, n_paths, SEED, 10)
+    # ---- dominant kernel alone (CUDA events around price_kernel on each pricing stream), every N:
+    # one GPU / a group: qmcg_time_device (max over members); ranks: this rank's nodes, max over ranks ----
+    if mode == "ranks":
+        kernel_ms, step_ms, _ = ctx.time_device_nodes(call, M_DATES, n_paths, SEED, depth, my_nodes[0],
+                                                      len(my_nodes), 10)
+        kernel_ms, step_ms = max_over_ranks(kernel_ms, step_ms)
     else:
-        b, e = q.tree_node_range(n_paths, depth, my_nodes[0])
-        kernel_ms = None
+        kernel_ms, step_ms, _, _ = ctx.time_device(call, M_DATES, n_paths, SEED, 10)
     fp64_peak = ctx.fp64_peak(100.0)
 
     # ---- config 4: 1024 contracts, 32 strikes x 32 vols, calls/puts alternating, 2^18 paths x
-    # 128 dates, one shared permutation set; contracts sharded over the ranks (N > 1) with an
-    # all-gather of the (price, se) rows; contract-path-steps/s, max over ranks ----
+    # 128 dates, one shared permutation set; contracts sharded over the devices (N > 1);
+    # contract-path-steps/s, max over devices ----
     batch = None
     if not args.no_batch:
         bspecs = [q.OptionSpec(100.0, 80 + 40 * i / 31, 0.05, 0.10 + 0.40 * j / 31, 1.0, q.OptionKind((i + j) % 2))
@@ -310,36 +410,34 @@ def main():
         b_strike, b_vol, b_kind = 80 + 40 * gi.ravel() / 31, 0.10 + 0.40 * gj.ravel() / 31, (gi + gj).ravel() % 2
 
         def batch_step():
-            if world == 1:  # column arrays: no per-contract Python objects in the timed call
+            if mode != "ranks":  # column arrays: no per-contract Python objects in the timed call
                 return ctx.price_american_batch_arrays(100.0, b_strike, 0.05, b_vol, 1.0, b_kind, bm, bn, SEED,
                                                        allow_put=True)
             return distributed.price_american_batch_sharded(bspecs, bm, bn, SEED, ctx=ctx, allow_put=True)
 
-        ctx.warm(bn, SEED, bm)
+        if mode == "single":
+            ctx.warm(bn, SEED, bm)
         batch_step()
         if dist:
             dist.barrier()
-        torch.cuda.synchronize()
-        be0, be1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        sync_all()
         breps = 3
+        tm = DeviceTimer()
         t0 = time.perf_counter()
-        be0.record(stream)
+        tm.start()
         for _ in range(breps):
             bres = batch_step()
-        be1.record(stream)
-        torch.cuda.synchronize()
+        bms = tm.stop() / breps
         bwall = (time.perf_counter() - t0) / breps
-        bms = be0.elapsed_time(be1) / breps
         if dist:
             bms, bwall = max_over_ranks(bms, bwall)
         batch = {"workload": "config 4: 1024 contracts (K = 80..120 x sigma = 0.10..0.50, calls for even i+j), "
                              "2^18 paths x 128 dates, seed 42, qmcg_price_american_batch"
-                             + (f" on {world} ranks (contiguous contract blocks + all_gather)" if world > 1 else ""),
+                             + (f" on {n_gpus} devices (contiguous contract blocks)" if n_gpus > 1 else ""),
                  "value": len(bspecs) * bn * bm / (bms * 1e-3), "unit": "contract-path-steps/s",
                  "ms_per_batch": bms, "e2e_ms_per_batch": 1e3 * bwall, "us_per_contract": 1e3 * bms / len(bspecs),
                  "price_first": float(bres[0][0]), "price_last": float(bres[-1][0])}
         ctx.clear_cache()
-
 
     path_steps = n_paths * M_DATES
     value = path_steps / (ms_call * 1e-3)
@@ -353,39 +451,49 @@ def main():
         pass
     fp64_per_step = prof.get("fp64_inst_per_path_step")
     roofline = None
+    # per-device work: each device prices n_paths / n_gpus paths in kernel_ms
+    dev_path_steps = path_steps / n_gpus
     if kernel_ms and fp64_per_step:
-        achieved = fp64_per_step * path_steps / (kernel_ms * 1e-3) / 1e12
+        achieved = fp64_per_step * dev_path_steps / (kernel_ms * 1e-3) / 1e12
         roofline = {"bound": "fp64", "achieved": achieved, "peak": fp64_peak / 1e12,
                     "unit": "T FP64-inst/s", "frac": achieved * 1e12 / fp64_peak,
                     "traffic": prof.get("dram_bytes_per_launch"),
                     "algorithmic_per_path_step": fp64_per_step,
                     "peak_source": "measured live: DFMA issue-rate probe (qmcg_fp64_peak) on this GPU",
-                    "kernel_ms": kernel_ms,
-                    "hbm": {"achieved": 4.0 * path_steps / (kernel_ms * 1e-3) / 1e9,
+                    "kernel_ms": kernel_ms, "per_device": n_gpus > 1,
+                    "hbm": {"achieved": 4.0 * dev_path_steps / (kernel_ms * 1e-3) / 1e9,
                             "peak": peaks.get("hbm_gbs", 6650.0), "unit": "GB/s",
-                            "frac": 4.0 * path_steps / (kernel_ms * 1e-3) / 1e9 / peaks.get("hbm_gbs", 6650.0),
+                            "frac": 4.0 * dev_path_steps / (kernel_ms * 1e-3) / 1e9 / peaks.get("hbm_gbs", 6650.0),
                             "algorithmic_bytes_per_path_step": 4,
                             "peak_source": "MEASURED_PEAKS.json" if "hbm_gbs" in peaks else "fallback"}}
+        if n_gpus > 1:
+            roofline["note"] = ("per device: the slowest device's pricing kernel over its n/N paths; traffic is the "
+                                "1-GPU ncu capture")
         wi = prof.get("warp_inst_per_warp_date")
         if wi:
             # the binding limit: one warp instruction per cycle per scheduler (4 per SM)
             sm_hz = (clocks or {}).get("sm_mhz") or 1965.0
             issue_peak = 4 * 148 * sm_hz * 1e6
-            issue_ach = wi * (path_steps / 32) / (kernel_ms * 1e-3)
+            issue_ach = wi * (dev_path_steps / 32) / (kernel_ms * 1e-3)
             roofline["issue"] = {"achieved": issue_ach / 1e12, "peak": issue_peak / 1e12, "unit": "T warp-inst/s",
                                  "frac": issue_ach / issue_peak, "warp_inst_per_warp_date": wi,
-                                 "note": "FP64 instructions are 28% of the kernel's issue slots; the schedulers' "
+                                 "note": "FP64 instructions are 30% of the kernel's issue slots; the schedulers' "
                                          "issue rate, not the FP64 pipe, bounds the kernel"}
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and n_gpus == 1 and not args.no_cpu_baseline:
         try:
             cpu_full = cpu_reference(steps=1, warmup=1)
             cpu = {k: cpu_full[k] for k in ("value", "unit", "cores", "kind", "sample")}
+            cpu["cpu_model"] = cpu_model()
+            one = cpu_reference(steps=1, warmup=0, n_paths=1 << 18, lanes=1)
+            cpu["lanes1"] = {"value": one["value"], "unit": "path-steps/s", "cores": 1,
+                             "sample": f"{1 << 18} paths x {M_DATES} dates, one call, ExecPolicy lanes = 1",
+                             "seconds_per_call": one["seconds_per_call"]}
             if args.records:  # the reference's CSV schema: GPU row (lanes = -1) next to its CPU row
                 from paper_1205_0106_b200 import records as R
                 gpu_row = R.BenchmarkRecord(q.Method.AmericanUpperBound, n_paths, M_DATES, R.GPU_LANES, 4096,
-                                            SEED, price, se, wall_call)
+                                            SEED, price_c, se, wall_call)
                 cpu_row = R.BenchmarkRecord(q.Method.AmericanUpperBound, CPU_SAMPLE_PATHS, M_DATES,
                                             cpu_full["cores"], 4096, SEED, cpu_full["price"], cpu_full["std_error"],
                                             cpu_full["seconds_per_call"])
@@ -394,26 +502,37 @@ def main():
             cpu = {"value": None, "error": str(exc)[:200]}
 
     if rank == 0:
-        line = {"metric": METRIC, "value": value, "unit": "path-steps/s", "n_gpus": world, "steps": steps,
-                "warmup": warmup, "ms_per_step": ms_call, "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        cold_med = statistics.median(cold_e2e)
+        line = {"metric": METRIC, "value": value, "unit": "path-steps/s", "n_gpus": n_gpus, "steps": steps,
+                "warmup": warmup, "ms_per_step": ms_call, "higher_is_better": True, "scaling": "strong",
+                "vs_baseline": None, "dtype": "f64",
                 "data": "synthetic (QMC paths from the reference's scrambled Halton stream, seed 42)",
                 "config": {"workload": WORKLOAD, "n_paths": n_paths, "m_dates": M_DATES, "seed": SEED,
-                           "parallelism": f"paths sharded over {world} GPU(s) (pairwise-tree nodes)",
-                           "tables": "warm: permutation tables resident in HBM (cold rebuild timed separately)",
+                           "parallelism": (f"paths sharded over {n_gpus} GPU(s) (pairwise-tree nodes); "
+                                           + {"single": "one process, one device",
+                                              "group": f"one process, device group {devices} (qmcg_create_multi)",
+                                              "ranks": "one process per GPU (torchrun, NCCL all-gather of node "
+                                                       "sums)"}[mode]),
+                           "tables": "warm: permutation tables resident in HBM (cold call measured separately)",
                            "l2": "inputs larger than L2 (4 B x 2^24 x 256 = 17.2 GB of tables per step)"},
                 "e2e": {"value": e2e_value, "unit": "path-steps/s", "h2d_bytes_per_step": 8 * (M_DATES + 1),
                         "d2h_bytes_per_step": 20, "ms_per_option": 1e3 * wall_call,
-                        "api": "qmcg_price_american (C ABI) per step"},
+                        "api": "qmcg_price_american (C ABI) per step" + (
+                            " per rank + all-gather" if mode == "ranks" else "")},
                 "roofline": roofline, "cpu_baseline": cpu, "gpu_launches": launches, "clocks": clocks,
-                "price": price, "std_error": se,
+                "price": price_c, "std_error": se,
                 "put": {"value": path_steps / (ms_put * 1e-3), "ms_per_step": ms_put, "price": price_put,
                         "std_error": se_put, "e2e_value": path_steps / wall_put},
                 "cold": {"perm_build_ms": cold_perm_ms,
-                         "ms_per_option_cold": cold_perm_ms + ms_call,
-                         "note": "K1 rebuilds all 256 Fisher-Yates tables (the reference's QuasiStream "
-                                 "construction, included in its elapsed_s)" + (
-                                     "" if world == 1 else "; dimension-sharded over the ranks (dim d on rank "
-                                     "d mod N) + all-to-all of column slices, wall time max over ranks")},
+                         "e2e_ms_per_option_cold": 1e3 * cold_med,
+                         "e2e_value_cold": path_steps / cold_med,
+                         "e2e_cold_s_all": cold_e2e,
+                         "note": "one real cold call per sample through the C ABI (QMCG_FLAG_NO_CACHE: table "
+                                 "allocation + K1 for all 256 tables + pricing), median of 3, host wall clock -- "
+                                 "the counterpart of the reference's elapsed_s, which includes its QuasiStream "
+                                 "construction; perm_build_ms is K1 alone" + (
+                                     "" if mode == "single" else "; tables built dimension-sharded over the "
+                                     "devices with column slices exchanged")},
                 "kernel_ms": kernel_ms, "device_step_ms": step_ms, "batch_config4": batch,
                 "stress_config5": c5}
         print(json.dumps(line), flush=True)

@@ -74,6 +74,19 @@ typedef struct qmcg_ctx qmcg_ctx;
 /* Context on one CUDA device: owns the stream, scratch and the permutation-table
  * cache keyed by (seed, n_paths). */
 qmcg_status qmcg_create(int device, qmcg_ctx** out);
+/* Context over a device group (one process, n_dev listed CUDA devices; a device may be listed
+ * more than once). It replaces the reference's host thread pool (ExecPolicy lanes,
+ * proj/src/path_engine.cpp:83-122, and the fork-join reduction :51-59) at the GPU level:
+ * qmcg_price_american shards the paths as whole pairwise-tree nodes over the members (member r
+ * owns a contiguous column slice of the permutation tables), each member reduces its nodes and
+ * the host folds the 16-byte node sums with the reference's tree, so results are bit-identical
+ * to one device for any member count. Cold tables are built dimension-sharded (dim d on member
+ * d mod n_dev) and column slices copied peer to peer; tables larger than memory are streamed in
+ * date windows the same way. qmcg_price_american_batch shards contracts. Every other call runs on
+ * the first member; the per-device node / table-exchange calls return QMCG_UNSUPPORTED. */
+qmcg_status qmcg_create_multi(const int* dev_ids, int n_dev, qmcg_ctx** out);
+/* Number of devices a context drives (1 for qmcg_create). */
+int qmcg_device_count(qmcg_ctx* ctx);
 void qmcg_destroy(qmcg_ctx* ctx);
 const char* qmcg_last_error(void);
 const char* qmcg_version(void);
@@ -198,6 +211,12 @@ qmcg_status qmcg_backward_sweep(const double* path, int64_t path_len, const qmcg
 qmcg_status qmcg_time_device(qmcg_ctx* ctx, const qmcg_option_spec* spec, int64_t m,
                              int64_t n_paths, uint64_t seed, uint32_t flags, int reps,
                              double* kernel_ms, double* step_ms, double* out_price_se);
+/* The same for the tree nodes [node_begin, node_begin + node_count) at `depth` (the range a rank of
+ * a multi-GPU job prices with qmcg_price_american_nodes); out_sums as there. */
+qmcg_status qmcg_time_device_nodes(qmcg_ctx* ctx, const qmcg_option_spec* spec, int64_t m, int64_t n_paths,
+                                   uint64_t seed, uint32_t flags, int depth, int64_t node_begin,
+                                   int64_t node_count, int reps, double* kernel_ms, double* step_ms,
+                                   double* out_sums);
 /* Device time (ms) of rebuilding the permutation tables for dims [0, dims). */
 qmcg_status qmcg_time_perm_build(qmcg_ctx* ctx, int64_t n_paths, uint64_t seed, int64_t dims,
                                  double* ms);
@@ -206,6 +225,10 @@ int64_t qmcg_last_launch_count(qmcg_ctx* ctx);
 /* The context's CUDA stream (a cudaStream_t) so a caller can record its own
  * events around a sequence of calls. */
 void* qmcg_get_stream(qmcg_ctx* ctx);
+/* The CUDA stream and device of member `member` of a device group (member 0 of a single-device
+ * context), for events around a sequence of group calls; NULL / -1 if out of range. */
+void* qmcg_get_member_stream(qmcg_ctx* ctx, int member);
+int qmcg_member_device(qmcg_ctx* ctx, int member);
 /* Measured FP64 FMA issue rate of this device (instructions/s), from a
  * dependent-chain-free DFMA kernel run for about `ms` milliseconds. */
 qmcg_status qmcg_fp64_peak(qmcg_ctx* ctx, double ms, double* inst_per_s);

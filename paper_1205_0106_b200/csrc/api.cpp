@@ -18,6 +18,7 @@
 #include <limits>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 using qmcg::DimParam;
@@ -306,6 +307,11 @@ struct qmcg_ctx {
   DevBuf<double> d_stV, d_stc, d_stcd, d_stbest;
   DevBuf<int32_t> d_stpend;
   size_t table_budget = 0;  // bytes the permutation table may take; 0 = what free memory allows
+  // device group (qmcg_create_multi): members[r] is the context of the r-th listed device; the
+  // group handle owns them and dispatches (its own stream, cache and scratch stay unused)
+  std::vector<qmcg_ctx*> members;
+  DevBuf<uint32_t> d_gtmp;                                  // builder rows of a group table build
+  cudaEvent_t ev_built = nullptr, ev_priced = nullptr;      // cross-member ordering of group builds
   int64_t last_windows = 0;  // date windows of the last pricing (1 = resident tables)
   double* h_pinned = nullptr;  // [0..1] sums, [2] err as double bits
   double* h_res = nullptr;     // pinned: node sums + the error word (enqueue_results)
@@ -672,6 +678,16 @@ struct DeviceGuard {
   }
 };
 
+// device-group forms (defined with the group code below)
+qmcg_status group_warm(qmcg_ctx* g, int64_t n, uint64_t seed, int64_t dims);
+qmcg_status group_batch(qmcg_ctx* g, const qmcg_option_spec* specs, int64_t n_specs, int64_t m, int64_t n,
+                        uint64_t seed, uint32_t flags, qmcg_pricing_result* out);
+qmcg_status group_path_values(qmcg_ctx* g, const qmcg_option_spec& spec, int64_t m, int64_t n, uint64_t seed,
+                              uint32_t flags, double* out_host);
+qmcg_status group_time_device(qmcg_ctx* g, const qmcg_option_spec& spec, int64_t m, int64_t n, uint64_t seed,
+                              uint32_t flags, int reps, double* kernel_ms, double* step_ms, double* price_se);
+qmcg_status group_time_perm_build(qmcg_ctx* g, int64_t n, uint64_t seed, int64_t dims, double* ms);
+
 }  // namespace
 
 extern "C" {
@@ -699,8 +715,43 @@ qmcg_status qmcg_create(int device, qmcg_ctx** out) {
   return QMCG_OK;
 }
 
+qmcg_status qmcg_create_multi(const int* dev_ids, int n_dev, qmcg_ctx** out) {
+  if (!out || !dev_ids || n_dev < 1) return fail(QMCG_INVALID_ARGUMENT, "qmcg_create_multi: bad device list");
+  auto* g = new qmcg_ctx();
+  g->device = dev_ids[0];
+  for (int r = 0; r < n_dev; ++r) {
+    qmcg_ctx* c = nullptr;
+    const qmcg_status st = qmcg_create(dev_ids[r], &c);
+    if (st) {
+      qmcg_destroy(g);
+      return st;
+    }
+    g->members.push_back(c);
+  }
+  // peer access between distinct listed devices (NVLink / NVSwitch); the slice copies also work
+  // without it (staged by the driver), so failures here are not errors
+  for (int a = 0; a < n_dev; ++a)
+    for (int b = 0; b < n_dev; ++b) {
+      if (dev_ids[a] == dev_ids[b]) continue;
+      int can = 0;
+      if (cudaDeviceCanAccessPeer(&can, dev_ids[a], dev_ids[b]) == cudaSuccess && can) {
+        DeviceGuard dg(dev_ids[a]);
+        if (cudaDeviceEnablePeerAccess(dev_ids[b], 0) != cudaSuccess) cudaGetLastError();
+      }
+    }
+  *out = g;
+  return QMCG_OK;
+}
+
+int qmcg_device_count(qmcg_ctx* c) { return !c ? 0 : c->members.empty() ? 1 : static_cast<int>(c->members.size()); }
+
 void qmcg_destroy(qmcg_ctx* c) {
   if (!c) return;
+  if (!c->members.empty() || !c->stream) {  // a group handle owns only its members
+    for (qmcg_ctx* m : c->members) qmcg_destroy(m);
+    delete c;
+    return;
+  }
   DeviceGuard g(c->device);
   cudaStreamSynchronize(c->stream);
   drop_cache(c);
@@ -732,6 +783,9 @@ void qmcg_destroy(qmcg_ctx* c) {
     if (c->ev_join[l]) cudaEventDestroy(c->ev_join[l]);
   }
   if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+  if (c->ev_built) cudaEventDestroy(c->ev_built);
+  if (c->ev_priced) cudaEventDestroy(c->ev_priced);
+  c->d_gtmp.release();
   c->d_dimp.release();
   c->d_path.release();
   c->d_path_t.release();
@@ -785,6 +839,7 @@ qmcg_status qmcg_warm(qmcg_ctx* c, int64_t n, uint64_t seed, int64_t dims) {
   DeviceGuard g(c->device);
   if (n < 1 || static_cast<uint64_t>(n) > 0xffffffffULL || dims < 1)
     return fail(QMCG_INVALID_ARGUMENT, "qmcg_warm: bad size");
+  if (!c->members.empty()) return group_warm(c, n, seed, dims);  // the slices group pricing reads
   qmcg_status st = ensure_perms(c, seed, n, 0, n, dims, false);
   if (st) return st;
   QMCG_CUDA(cudaStreamSynchronize(c->stream));
@@ -793,6 +848,8 @@ qmcg_status qmcg_warm(qmcg_ctx* c, int64_t n, uint64_t seed, int64_t dims) {
 
 qmcg_status qmcg_build_tables(qmcg_ctx* c, int64_t n, uint64_t seed, int64_t dim_begin, int64_t dim_stride,
                               int64_t count, uint32_t* out_dev, int64_t ld) {
+  if (c && !c->members.empty())
+    return fail(QMCG_UNSUPPORTED, "qmcg_build_tables: a per-device call (use a single-device context per rank)");
   if (!c || (!out_dev && count > 0)) return fail(QMCG_INVALID_ARGUMENT, "qmcg_build_tables: null argument");
   if (n < 1 || static_cast<uint64_t>(n) > 0xffffffffULL || dim_begin < 0 || dim_stride < 1 || count < 0 || ld < n)
     return fail(QMCG_INVALID_ARGUMENT, "qmcg_build_tables: bad size");
@@ -815,6 +872,8 @@ qmcg_status qmcg_build_tables(qmcg_ctx* c, int64_t n, uint64_t seed, int64_t dim
 
 qmcg_status qmcg_import_tables(qmcg_ctx* c, int64_t n, uint64_t seed, int64_t col_begin, int64_t col_end,
                                int64_t dims, const uint32_t* src_dev, int64_t src_ld) {
+  if (c && !c->members.empty())
+    return fail(QMCG_UNSUPPORTED, "qmcg_import_tables: a per-device call (use a single-device context per rank)");
   if (!c || !src_dev) return fail(QMCG_INVALID_ARGUMENT, "qmcg_import_tables: null argument");
   const int64_t cols = col_end - col_begin;
   if (n < 1 || static_cast<uint64_t>(n) > 0xffffffffULL || col_begin < 0 || cols < 1 || col_end > n || dims < 1 ||
@@ -848,14 +907,20 @@ qmcg_status qmcg_set_table_budget(qmcg_ctx* c, uint64_t bytes) {
   if (!c) return fail(QMCG_INVALID_ARGUMENT, "qmcg_set_table_budget: null context");
   std::lock_guard<std::mutex> lock(c->mu);
   c->table_budget = static_cast<size_t>(bytes);
+  for (qmcg_ctx* m : c->members) qmcg_set_table_budget(m, bytes);
   return QMCG_OK;
 }
 
-int64_t qmcg_last_window_count(qmcg_ctx* c) { return c ? c->last_windows : -1; }
+int64_t qmcg_last_window_count(qmcg_ctx* c) {
+  if (c && !c->members.empty()) return c->members[0]->last_windows;
+  return c ? c->last_windows : -1;
+}
 
 qmcg_status qmcg_clear_cache(qmcg_ctx* c) {
   if (!c) return fail(QMCG_INVALID_ARGUMENT, "qmcg_clear_cache: null context");
   std::lock_guard<std::mutex> lock(c->mu);
+  for (qmcg_ctx* m : c->members) qmcg_clear_cache(m);
+  if (!c->members.empty()) return QMCG_OK;
   DeviceGuard g(c->device);
   cudaStreamSynchronize(c->stream);
   drop_cache(c);
@@ -1024,7 +1089,499 @@ static qmcg_status price_range(qmcg_ctx* c, const qmcg_option_spec* spec, int64_
   return price_nodes(c, spec, m, n, seed, flags, 0, 0, 1, sums);
 }
 
-//@@GROUP@@
+// ---------------------------------------------------------------------------
+// Device groups (qmcg_create_multi): one host handle over several CUDA devices.
+// The reference's only parallel axis is the path range (parallel_for_chunks,
+// proj/src/path_engine.cpp:83-122) plus a fixed pairwise tree (:39-59); a group
+// gives member r the contiguous tree nodes node_owner(i) = min(G-1, i G / 2^D) at
+// depth D = ceil(log2 G), so every member prices its own column
+// slice of the permutation tables, 16 bytes per node come back, and the host
+// folds them up the same tree: bit-identical to one device for every G.
+// Cold tables are built dimension-sharded (dim d by member d mod G, full n) and
+// each member's column slice is copied to it with one cudaMemcpyPeerAsync per
+// (dim, member) over NVLink; tables that exceed device memory are streamed in
+// date windows with the same sharded build per window.
+// ---------------------------------------------------------------------------
+struct MemberRange {
+  int64_t node0 = 0, count = 0;  // tree nodes [node0, node0 + count) at the group depth
+  int64_t b = 0, e = 0;          // their path (column) range
+};
+
+int group_depth(int64_t n, int G) {
+  int want = 0;
+  while ((int64_t{1} << want) < G) ++want;
+  int depth = 0;
+  while (depth < want && (n >> depth) > 64) ++depth;  // nodes at depth+1 need parents above a leaf
+  return depth;
+}
+
+std::vector<MemberRange> member_ranges(int64_t n, int G, int depth) {
+  std::vector<MemberRange> R(static_cast<size_t>(G));
+  const int64_t nodes = int64_t{1} << depth;
+  for (int64_t i = 0; i < nodes; ++i) {
+    const int r = static_cast<int>(std::min<int64_t>(G - 1, (i * G) / nodes));
+    MemberRange& m = R[static_cast<size_t>(r)];
+    if (m.count == 0) m.node0 = i;
+    ++m.count;
+  }
+  for (auto& m : R) {
+    if (!m.count) continue;
+    int64_t off, size;
+    tree_node(n, depth, m.node0, off, size);
+    m.b = off;
+    tree_node(n, depth, m.node0 + m.count - 1, off, size);
+    m.e = off + size;
+  }
+  return R;
+}
+
+// Fold 2^depth interleaved node sums up the reference tree (pairwise_sum's splits).
+void fold_nodes(std::vector<double>& s, int depth) {
+  for (int d = depth; d > 0; --d) {
+    const size_t cnt = size_t{1} << (d - 1);
+    for (size_t i = 0; i < cnt; ++i) {
+      s[2 * i] = s[4 * i] + s[4 * i + 2];
+      s[2 * i + 1] = s[4 * i + 1] + s[4 * i + 3];
+    }
+  }
+}
+
+qmcg_status ensure_events(qmcg_ctx* c) {
+  DeviceGuard g(c->device);
+  if (!c->ev_built) QMCG_CUDA(cudaEventCreateWithFlags(&c->ev_built, cudaEventDisableTiming));
+  if (!c->ev_priced) QMCG_CUDA(cudaEventCreateWithFlags(&c->ev_priced, cudaEventDisableTiming));
+  return QMCG_OK;
+}
+
+// Every stream in `to` waits for the work queued so far on every stream of `from`.
+qmcg_status cross_wait(const std::vector<qmcg_ctx*>& from, const std::vector<qmcg_ctx*>& to, bool built) {
+  for (qmcg_ctx* f : from) {
+    DeviceGuard g(f->device);
+    QMCG_CUDA(cudaEventRecord(built ? f->ev_built : f->ev_priced, f->stream));
+  }
+  for (qmcg_ctx* t : to) {
+    DeviceGuard g(t->device);
+    for (qmcg_ctx* f : from) QMCG_CUDA(cudaStreamWaitEvent(t->stream, built ? f->ev_built : f->ev_priced, 0));
+  }
+  return QMCG_OK;
+}
+
+// Rows of dims `dims` (full n) built by member `bc` into its scratch `tmp` (rows of n entries),
+// then row k's slice [R[s].b, R[s].e) copied into row dst_row[k] of member s's table.
+qmcg_status build_and_scatter(qmcg_ctx* bc, uint64_t seed, int64_t n, const std::vector<int64_t>& dims,
+                              const std::vector<int64_t>& dst_row, const std::vector<qmcg_ctx*>& M,
+                              const std::vector<MemberRange>& R, uint32_t* tmp, int64_t tmp_rows) {
+  DeviceGuard g(bc->device);
+  for (size_t k0 = 0; k0 < dims.size(); k0 += static_cast<size_t>(tmp_rows)) {
+    const size_t cnt = std::min(dims.size() - k0, static_cast<size_t>(tmp_rows));
+    // dims of a member are an arithmetic progression with stride G
+    const int64_t stride = cnt > 1 ? dims[k0 + 1] - dims[k0] : 1;
+    if (n <= kOverlapMaxN && cnt >= 2) {
+      qmcg_status st = build_rows_overlapped(bc, seed, n, tmp, n, 0, static_cast<int64_t>(cnt), dims[k0], stride);
+      if (st) return st;
+    } else {
+      for (size_t k = 0; k < cnt; ++k) {
+        qmcg_status st = build_perm(bc, dimension_seed(seed, dims[k0 + k]), n, tmp + k * static_cast<size_t>(n));
+        if (st) return st;
+      }
+    }
+    for (size_t s = 0; s < M.size(); ++s) {
+      const MemberRange& r = R[s];
+      if (r.e <= r.b) continue;
+      const size_t ld = static_cast<size_t>(qmcg::table_ld(r.e - r.b));
+      for (size_t k = 0; k < cnt; ++k)
+        QMCG_CUDA(cudaMemcpyPeerAsync(M[s]->table + static_cast<size_t>(dst_row[k0 + k]) * ld, M[s]->device,
+                                      tmp + k * static_cast<size_t>(n) + r.b, bc->device,
+                                      static_cast<size_t>(r.e - r.b) * sizeof(uint32_t), bc->stream));
+    }
+  }
+  return QMCG_OK;
+}
+
+// Scratch rows a builder holds for the sharded build (~512 MB, at least one row).
+int64_t group_tmp_rows(int64_t n) {
+  return std::max<int64_t>(1, std::min<int64_t>(8, (int64_t{1} << 29) / (4 * n)));
+}
+
+// Resident tables for (seed, n) rows [0, m) on every member, each over its range R[s]:
+// the missing dims are built dimension-sharded and scattered to the members.
+qmcg_status group_ensure_tables(qmcg_ctx* g, uint64_t seed, int64_t n, int64_t m, const std::vector<MemberRange>& R,
+                                bool rebuild) {
+  const auto& M = g->members;
+  int64_t d0 = m;
+  for (size_t s = 0; s < M.size(); ++s) {
+    qmcg_ctx* c = M[s];
+    const bool same = !rebuild && c->cache_n == n && c->cache_seed == seed && c->col_begin == R[s].b &&
+                      c->col_end == R[s].e;
+    d0 = std::min(d0, R[s].e > R[s].b ? (same ? c->cache_dims : 0) : m);
+  }
+  if (d0 >= m) return QMCG_OK;
+  for (size_t s = 0; s < M.size(); ++s) {
+    if (R[s].e <= R[s].b) continue;
+    DeviceGuard dg(M[s]->device);
+    qmcg_status st = ensure_dim_tables(M[s], n, m);
+    if (st) return st;
+    st = reserve_table(M[s], seed, n, R[s].b, R[s].e, m, rebuild);
+    if (st) return st;
+    M[s]->cache_dims = std::min(M[s]->cache_dims, d0);
+  }
+  for (qmcg_ctx* c : M) {
+    qmcg_status st = ensure_events(c);
+    if (st) return st;
+  }
+  // member tables may still be read by queued pricing: the builders start after it
+  qmcg_status st = cross_wait(M, M, false);
+  if (st) return st;
+  const int G = static_cast<int>(M.size());
+  const int64_t tmp_rows = group_tmp_rows(n);
+  for (int r = 0; r < G; ++r) {
+    std::vector<int64_t> dims;
+    for (int64_t d = d0; d < m; ++d)
+      if (d % G == r) dims.push_back(d);
+    if (dims.empty()) continue;
+    qmcg_ctx* bc = M[static_cast<size_t>(r)];
+    DeviceGuard dg(bc->device);
+    QMCG_CUDA(bc->d_gtmp.reserve(static_cast<size_t>(tmp_rows) * static_cast<size_t>(n)));
+    st = build_and_scatter(bc, seed, n, dims, dims, M, R, bc->d_gtmp.ptr, tmp_rows);
+    if (st) return st;
+  }
+  st = cross_wait(M, M, true);  // every member prices only after every builder's copies
+  if (st) return st;
+  for (size_t s = 0; s < M.size(); ++s)
+    if (R[s].e > R[s].b) M[s]->cache_dims = m;
+  return QMCG_OK;
+}
+
+// Tables of a group pricing that exceed a member's memory: date windows of W rows (the same W
+// on every member); each window's dims are built dimension-sharded and scattered into the
+// members' window buffers, then every member walks its paths through the window (K2 with the
+// walk state carried in HBM, as enqueue_streamed). Returns the node sums via enqueue_results.
+qmcg_status group_enqueue_streamed(qmcg_ctx* g, std::vector<CallPlan>& plans, uint64_t seed, int64_t n, int64_t m,
+                                   int depth, const std::vector<MemberRange>& R) {
+  const auto& M = g->members;
+  const int G = static_cast<int>(M.size());
+  int64_t W = (m + 7) / 8 * 8;
+  for (size_t s = 0; s < M.size(); ++s) {
+    if (R[s].e <= R[s].b) continue;
+    DeviceGuard dg(M[s]->device);
+    drop_cache(M[s]);
+    const int64_t cols = R[s].e - R[s].b;
+    const size_t row_bytes = static_cast<size_t>(qmcg::table_ld(cols)) * sizeof(uint32_t);
+    // the builder scratch (one full row) lives on every member as well
+    size_t budget = table_bytes_allowed(M[s], n, cols, false);
+    budget = budget > static_cast<size_t>(n) * 4 ? budget - static_cast<size_t>(n) * 4 : 0;
+    W = std::min<int64_t>(W, static_cast<int64_t>(budget / row_bytes) / 8 * 8);
+  }
+  if (W < 8) return fail(QMCG_OUT_OF_MEMORY, "price_american: not enough device memory for 8 permutation rows");
+  std::vector<PriceParams> P(M.size());
+  for (size_t s = 0; s < M.size(); ++s) {
+    qmcg_ctx* c = M[s];
+    DeviceGuard dg(c->device);
+    qmcg_status st = ensure_events(c);
+    if (st) return st;
+    QMCG_CUDA(c->d_gtmp.reserve(static_cast<size_t>(n)));
+    if (R[s].e <= R[s].b) continue;
+    const int64_t cols = R[s].e - R[s].b;
+    const int64_t ld = qmcg::table_ld(cols);
+    uint32_t* nt = nullptr;
+    if (cudaMalloc(&nt, static_cast<size_t>(ld) * 4 * static_cast<size_t>(W) + qmcg::kTablePad * 4) != cudaSuccess) {
+      cudaGetLastError();
+      return fail(QMCG_OUT_OF_MEMORY, "price_american: permutation window does not fit in device memory");
+    }
+    c->table = nt;
+    c->table_rows_cap = static_cast<size_t>(W);
+    c->col_begin = R[s].b;  // a window buffer, never a cache (cache_n stays -1)
+    c->col_end = R[s].e;
+    QMCG_CUDA(c->d_values.reserve(static_cast<size_t>(cols)));
+    QMCG_CUDA(c->d_red.reserve(qmcg::reduce_scratch_doubles(cols)));
+    for (auto* buf : {&c->d_stV, &c->d_stc, &c->d_stcd, &c->d_stbest}) QMCG_CUDA(buf->reserve(static_cast<size_t>(cols)));
+    QMCG_CUDA(c->d_stpend.reserve(static_cast<size_t>(cols)));
+    PriceParams& p = P[s];
+    p = plans[s].P;
+    p.perm = c->table;
+    p.ld = ld;
+    p.col_begin = R[s].b;
+    p.path_begin = R[s].b;
+    p.path_count = cols;
+    p.values = c->d_values.ptr;
+    p.err = c->d_err.ptr;
+    p.st_V = c->d_stV.ptr;
+    p.st_c = c->d_stc.ptr;
+    p.st_cd = c->d_stcd.ptr;
+    p.st_best = c->d_stbest.ptr;
+    p.st_pend = c->d_stpend.ptr;
+    c->last_windows = 0;
+  }
+  qmcg_status st = cross_wait(M, M, false);
+  if (st) return st;
+  for (int64_t d0 = 0; d0 < m; d0 += W) {
+    const int64_t d1 = std::min(m, d0 + W);
+    for (int r = 0; r < G; ++r) {
+      std::vector<int64_t> dims, rows;
+      for (int64_t d = d0; d < d1; ++d)
+        if (d % G == r) {
+          dims.push_back(d);
+          rows.push_back(d - d0);
+        }
+      if (dims.empty()) continue;
+      qmcg_ctx* bc = M[static_cast<size_t>(r)];
+      st = build_and_scatter(bc, seed, n, dims, rows, M, R, bc->d_gtmp.ptr, 1);
+      if (st) return st;
+    }
+    st = cross_wait(M, M, true);  // the window's rows are in place on every member
+    if (st) return st;
+    for (size_t s = 0; s < M.size(); ++s) {
+      if (R[s].e <= R[s].b) continue;
+      qmcg_ctx* c = M[s];
+      DeviceGuard dg(c->device);
+      PriceParams& p = P[s];
+      p.d_begin = static_cast<int32_t>(d0);
+      p.d_end = static_cast<int32_t>(d1);
+      p.perm_row0 = static_cast<int32_t>(d0);
+      p.stream_load = d0 > 0;
+      p.stream_store = d1 < m;
+      QMCG_CUDA(qmcg::launch_price(p, c->stream));
+      c->launches += 1;
+      c->last_windows += 1;
+    }
+    if (d1 < m) {
+      st = cross_wait(M, M, false);  // the next window's copies overwrite rows the walk reads
+      if (st) return st;
+    }
+  }
+  for (size_t s = 0; s < M.size(); ++s) {
+    if (R[s].e <= R[s].b) continue;
+    DeviceGuard dg(M[s]->device);
+    st = enqueue_node_sums(M[s], n, depth, R[s].node0, R[s].count, R[s].b);
+    if (st) return st;
+    st = enqueue_results(M[s], static_cast<size_t>(R[s].count));
+    if (st) return st;
+  }
+  return QMCG_OK;
+}
+
+// price_american over a device group: (sum v, sum v^2) of every node at the group depth into
+// `sums` (2 per node), folded by the caller.
+qmcg_status group_price_nodes(qmcg_ctx* g, const qmcg_option_spec& spec, int64_t m, int64_t n, uint64_t seed,
+                              uint32_t flags, int& depth, std::vector<double>& sums) {
+  const auto& M = g->members;
+  const int G = static_cast<int>(M.size());
+  CallPlan probe;
+  qmcg_status st = plan_call(spec, m, n, flags, probe);  // the reference's checks, before any device work
+  if (st) return st;
+  depth = group_depth(n, G);
+  const std::vector<MemberRange> R = member_ranges(n, G, depth);
+  sums.assign(2 * (size_t{1} << depth), 0.0);
+  for (qmcg_ctx* c : M) c->launches = 0;
+  const bool rebuild = (flags & QMCG_FLAG_NO_CACHE) != 0;
+  // tables: resident (the cached slices, or a sharded build) unless a slice exceeds its member's memory
+  bool streamed = false;
+  if (!probe.P.deterministic) {
+    for (size_t s = 0; s < M.size(); ++s) {
+      const MemberRange& r = R[s];
+      if (r.e <= r.b) continue;
+      qmcg_ctx* c = M[s];
+      const bool cached = !rebuild && c->cache_n == n && c->cache_seed == seed && c->col_begin == r.b &&
+                          c->col_end == r.e && c->cache_dims >= m;
+      if (cached) continue;
+      DeviceGuard dg(c->device);
+      const size_t need = static_cast<size_t>(qmcg::table_ld(r.e - r.b)) * 4 * static_cast<size_t>(m) +
+                          static_cast<size_t>(group_tmp_rows(n)) * static_cast<size_t>(n) * 4;
+      if (need > table_bytes_allowed(c, n, r.e - r.b, false)) streamed = true;
+    }
+  }
+  if (streamed) {
+    std::vector<CallPlan> plans(M.size());
+    for (size_t s = 0; s < M.size(); ++s) {
+      DeviceGuard dg(M[s]->device);
+      plans[s] = probe;
+      st = upload_plan(M[s], plans[s], n);
+      if (st) return st;
+      st = prepare_scratch(M[s], static_cast<size_t>(std::max<int64_t>(R[s].count, 1)));
+      if (st) return st;
+    }
+    st = group_enqueue_streamed(g, plans, seed, n, m, depth, R);
+    if (st) return st;
+  } else {
+    if (!probe.P.deterministic) {
+      st = group_ensure_tables(g, seed, n, m, R, rebuild);
+      if (st) return st;
+    }
+    for (size_t s = 0; s < M.size(); ++s) {
+      if (!R[s].count) continue;
+      DeviceGuard dg(M[s]->device);
+      // flags without NO_CACHE: the slices are in place (a cold call rebuilt them above)
+      st = price_nodes_enqueue(M[s], &spec, m, n, seed, flags & ~static_cast<uint32_t>(QMCG_FLAG_NO_CACHE), depth,
+                               R[s].node0, R[s].count);
+      if (st) return st;
+    }
+  }
+  for (size_t s = 0; s < M.size(); ++s) {
+    if (!R[s].count) continue;
+    DeviceGuard dg(M[s]->device);
+    st = finish_results(M[s], static_cast<size_t>(R[s].count), sums.data() + 2 * R[s].node0);
+    if (st) return st;
+  }
+  return QMCG_OK;
+}
+
+// ---- group forms of the remaining context calls ----
+qmcg_status group_warm(qmcg_ctx* g, int64_t n, uint64_t seed, int64_t dims) {
+  const int G = static_cast<int>(g->members.size());
+  const int depth = group_depth(n, G);
+  qmcg_status st = group_ensure_tables(g, seed, n, dims, member_ranges(n, G, depth), false);
+  if (st) return st;
+  for (qmcg_ctx* c : g->members) {
+    DeviceGuard dg(c->device);
+    QMCG_CUDA(cudaStreamSynchronize(c->stream));
+  }
+  return QMCG_OK;
+}
+
+// Config 4 on a group: contract blocks [C r / G, C (r + 1) / G) per member, every member with
+// the full tables (built dimension-sharded once), the member batches run concurrently (one
+// host thread each; a batch call is synchronous).
+qmcg_status group_batch(qmcg_ctx* g, const qmcg_option_spec* specs, int64_t n_specs, int64_t m, int64_t n,
+                        uint64_t seed, uint32_t flags, qmcg_pricing_result* out) {
+  const auto& M = g->members;
+  const int G = static_cast<int>(M.size());
+  for (int64_t i = 0; i < n_specs; ++i) {  // the reference's checks before any device work
+    CallPlan probe;
+    qmcg_status st = plan_call(specs[i], m, n, flags, probe);
+    if (st) return st;
+  }
+  if (n_specs == 0) return QMCG_OK;
+  std::vector<MemberRange> full(M.size());
+  for (auto& r : full) {
+    r.b = 0;
+    r.e = n;
+  }
+  qmcg_status st = group_ensure_tables(g, seed, n, m, full, (flags & QMCG_FLAG_NO_CACHE) != 0);
+  if (st) return st;
+  const uint32_t mflags = flags & ~static_cast<uint32_t>(QMCG_FLAG_NO_CACHE);
+  std::vector<qmcg_status> res(M.size(), QMCG_OK);
+  std::vector<std::string> msg(M.size());
+  std::vector<std::thread> th;
+  for (int r = 0; r < G; ++r) {
+    const int64_t b = n_specs * r / G, e = n_specs * (r + 1) / G;
+    if (e <= b) continue;
+    th.emplace_back([&, r, b, e] {
+      res[r] = qmcg_price_american_batch(M[r], specs + b, e - b, m, n, seed, mflags, out + b);
+      if (res[r]) msg[r] = g_last_error;  // thread-local: carry the text to the caller's thread
+    });
+  }
+  for (auto& t : th) t.join();
+  for (int r = 0; r < G; ++r)
+    if (res[r]) return fail(res[r], msg[r]);
+  return QMCG_OK;
+}
+
+qmcg_status group_path_values(qmcg_ctx* g, const qmcg_option_spec& spec, int64_t m, int64_t n, uint64_t seed,
+                              uint32_t flags, double* out_host) {
+  int depth = 0;
+  std::vector<double> sums;
+  qmcg_status st = group_price_nodes(g, spec, m, n, seed, flags, depth, sums);
+  if (st) return st;
+  const auto R = member_ranges(n, static_cast<int>(g->members.size()), depth);
+  for (size_t s = 0; s < g->members.size(); ++s) {
+    if (R[s].e <= R[s].b) continue;
+    qmcg_ctx* c = g->members[s];
+    DeviceGuard dg(c->device);
+    QMCG_CUDA(cudaMemcpyAsync(out_host + R[s].b, c->d_values.ptr, static_cast<size_t>(R[s].e - R[s].b) * sizeof(double),
+                              cudaMemcpyDeviceToHost, c->stream));
+    QMCG_CUDA(cudaStreamSynchronize(c->stream));
+  }
+  return QMCG_OK;
+}
+
+// Every member prices its node range `reps` times (launched round-robin so the devices run
+// concurrently); the pricing-kernel and whole-step device times are the max over members.
+qmcg_status group_time_device(qmcg_ctx* g, const qmcg_option_spec& spec, int64_t m, int64_t n, uint64_t seed,
+                              uint32_t flags, int reps, double* kernel_ms, double* step_ms, double* price_se) {
+  const auto& M = g->members;
+  int depth = 0;
+  std::vector<double> sums;
+  qmcg_status st = group_price_nodes(g, spec, m, n, seed, flags, depth, sums);  // tables + module warm-up
+  if (st) return st;
+  const auto R = member_ranges(n, static_cast<int>(M.size()), depth);
+  std::vector<CallPlan> plans(M.size());
+  std::vector<double> kms(M.size(), 0.0);
+  for (size_t s = 0; s < M.size(); ++s) {
+    if (!R[s].count) continue;
+    DeviceGuard dg(M[s]->device);
+    st = plan_call(spec, m, n, flags, plans[s]);
+    if (st) return st;
+    st = upload_plan(M[s], plans[s], n);
+    if (st) return st;
+    st = prepare_scratch(M[s], static_cast<size_t>(R[s].count));
+    if (st) return st;
+    QMCG_CUDA(cudaEventRecord(M[s]->ev[2], M[s]->stream));
+  }
+  for (int rep = 0; rep < reps; ++rep) {
+    for (size_t s = 0; s < M.size(); ++s) {
+      if (!R[s].count) continue;
+      qmcg_ctx* c = M[s];
+      DeviceGuard dg(c->device);
+      QMCG_CUDA(cudaEventRecord(c->ev[0], c->stream));
+      st = enqueue_values(c, plans[s], R[s].b, R[s].e, c->ev[1]);
+      if (st) return st;
+      st = enqueue_node_sums(c, n, depth, R[s].node0, R[s].count, R[s].b);
+      if (st) return st;
+    }
+    for (size_t s = 0; s < M.size(); ++s) {
+      if (!R[s].count) continue;
+      DeviceGuard dg(M[s]->device);
+      QMCG_CUDA(cudaEventSynchronize(M[s]->ev[1]));
+      float ms = 0.f;
+      QMCG_CUDA(cudaEventElapsedTime(&ms, M[s]->ev[0], M[s]->ev[1]));
+      kms[s] += ms;
+    }
+  }
+  double kmax = 0.0, smax = 0.0;
+  for (size_t s = 0; s < M.size(); ++s) {
+    if (!R[s].count) continue;
+    qmcg_ctx* c = M[s];
+    DeviceGuard dg(c->device);
+    QMCG_CUDA(cudaEventRecord(c->ev[3], c->stream));
+    st = enqueue_results(c, static_cast<size_t>(R[s].count));
+    if (st) return st;
+    st = finish_results(c, static_cast<size_t>(R[s].count), sums.data() + 2 * R[s].node0);
+    if (st) return st;
+    float total = 0.f;
+    QMCG_CUDA(cudaEventElapsedTime(&total, c->ev[2], c->ev[3]));
+    kmax = std::max(kmax, kms[s] / reps);
+    smax = std::max(smax, static_cast<double>(total) / reps);
+  }
+  fold_nodes(sums, depth);
+  if (kernel_ms) *kernel_ms = kmax;
+  if (step_ms) *step_ms = smax;
+  if (price_se) finish_stats(n, sums[0], sums[1], price_se[0], price_se[1]);
+  return QMCG_OK;
+}
+
+// Cold sharded build of the pricing slices for dims [0, dims), host wall clock around the
+// group (ms): every member is idle before, and all of them have finished after.
+qmcg_status group_time_perm_build(qmcg_ctx* g, int64_t n, uint64_t seed, int64_t dims, double* ms) {
+  const int G = static_cast<int>(g->members.size());
+  const auto R = member_ranges(n, G, group_depth(n, G));
+  qmcg_status st = group_ensure_tables(g, seed, n, dims, R, false);  // allocation outside the timing
+  if (st) return st;
+  for (qmcg_ctx* c : g->members) {
+    DeviceGuard dg(c->device);
+    QMCG_CUDA(cudaStreamSynchronize(c->stream));
+    c->cache_dims = 0;
+  }
+  const auto t0 = std::chrono::steady_clock::now();
+  st = group_ensure_tables(g, seed, n, dims, R, false);
+  if (st) return st;
+  for (qmcg_ctx* c : g->members) {
+    DeviceGuard dg(c->device);
+    QMCG_CUDA(cudaStreamSynchronize(c->stream));
+  }
+  *ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  return QMCG_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -1037,8 +1594,19 @@ qmcg_status qmcg_price_american(qmcg_ctx* c, const qmcg_option_spec* spec, int64
   DeviceGuard g(c->device);
   c->launches = 0;
   double sums[2];
-  qmcg_status st = price_range(c, spec, m, n, seed, flags, sums);
-  if (st) return st;
+  qmcg_status st;
+  if (!c->members.empty()) {  // device group: nodes sharded over the members, folded here
+    int depth = 0;
+    std::vector<double> t;
+    st = group_price_nodes(c, *spec, m, n, seed, flags, depth, t);
+    if (st) return st;
+    fold_nodes(t, depth);
+    sums[0] = t[0];
+    sums[1] = t[1];
+  } else {
+    st = price_range(c, spec, m, n, seed, flags, sums);
+    if (st) return st;
+  }
   double mean, se;
   finish_stats(n, sums[0], sums[1], mean, se);
   out->price = mean;
@@ -1052,6 +1620,7 @@ qmcg_status qmcg_price_american(qmcg_ctx* c, const qmcg_option_spec* spec, int64
 
 qmcg_status qmcg_mc_european_price(qmcg_ctx* c, const qmcg_option_spec* spec, int64_t n, uint64_t seed,
                                    uint32_t flags, qmcg_pricing_result* out) {
+  if (c && !c->members.empty()) c = c->members[0];  // single-device call on a group: its first member
   if (!c || !spec || !out) return fail(QMCG_INVALID_ARGUMENT, "qmcg_mc_european_price: null argument");
   const auto t0 = std::chrono::steady_clock::now();
   std::lock_guard<std::mutex> lock(c->mu);
@@ -1101,6 +1670,8 @@ qmcg_status qmcg_mc_european_price(qmcg_ctx* c, const qmcg_option_spec* spec, in
 
 qmcg_status qmcg_price_american_node(qmcg_ctx* c, const qmcg_option_spec* spec, int64_t m, int64_t n,
                                      uint64_t seed, uint32_t flags, int depth, int64_t node, double out_sums[2]) {
+  if (c && !c->members.empty())
+    return fail(QMCG_UNSUPPORTED, "qmcg_price_american_node: a per-device call (use a single-device context per rank)");
   if (!c || !spec || !out_sums) return fail(QMCG_INVALID_ARGUMENT, "qmcg_price_american_node: null argument");
   std::lock_guard<std::mutex> lock(c->mu);
   DeviceGuard g(c->device);
@@ -1123,6 +1694,8 @@ qmcg_status qmcg_price_american_node(qmcg_ctx* c, const qmcg_option_spec* spec, 
 qmcg_status qmcg_price_american_nodes(qmcg_ctx* c, const qmcg_option_spec* spec, int64_t m, int64_t n,
                                       uint64_t seed, uint32_t flags, int depth, int64_t node_begin,
                                       int64_t node_count, double* out_sums) {
+  if (c && !c->members.empty())
+    return fail(QMCG_UNSUPPORTED, "qmcg_price_american_nodes: a per-device call (use a single-device context per rank)");
   if (!c || !spec || !out_sums) return fail(QMCG_INVALID_ARGUMENT, "qmcg_price_american_nodes: null argument");
   std::lock_guard<std::mutex> lock(c->mu);
   DeviceGuard g(c->device);
@@ -1149,6 +1722,12 @@ qmcg_status qmcg_price_american_batch(qmcg_ctx* c, const qmcg_option_spec* specs
   std::lock_guard<std::mutex> lock(c->mu);
   DeviceGuard g(c->device);
   c->launches = 0;
+  if (!c->members.empty()) {  // contracts sharded over the group's members
+    qmcg_status st = group_batch(c, specs, n_specs, m, n, seed, flags, out);
+    const double el = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    for (int64_t i = 0; i < n_specs && st == QMCG_OK; ++i) out[i].elapsed_s = el;
+    return st;
+  }
   if (n_specs == 0) return QMCG_OK;
   Trace tr("batch");
   std::vector<CallPlan> plans(static_cast<size_t>(n_specs));
@@ -1299,6 +1878,7 @@ qmcg_status qmcg_price_american_batch(qmcg_ctx* c, const qmcg_option_spec* specs
 }
 
 qmcg_status qmcg_permutation(qmcg_ctx* c, int64_t n, uint64_t seed64, uint32_t* out_host) {
+  if (c && !c->members.empty()) c = c->members[0];  // single-device call on a group: its first member
   if (!c || !out_host) return fail(QMCG_INVALID_ARGUMENT, "qmcg_permutation: null argument");
   if (n < 1) return fail(QMCG_INVALID_ARGUMENT, "permutation_indices: n must be >= 1");
   if (static_cast<uint64_t>(n) > 0xffffffffULL)
@@ -1315,6 +1895,7 @@ qmcg_status qmcg_permutation(qmcg_ctx* c, int64_t n, uint64_t seed64, uint32_t* 
 }
 
 static qmcg_status export_dim(qmcg_ctx* c, int64_t n, uint64_t seed, int64_t dim, int normals, double* out_host) {
+  if (c && !c->members.empty()) c = c->members[0];  // single-device call on a group: its first member
   if (!c || !out_host) return fail(QMCG_INVALID_ARGUMENT, "qmcg_uniforms: null argument");
   if (n < 1) return fail(QMCG_INVALID_ARGUMENT, "QuasiStream: length must be >= 1");
   if (dim < 0) return fail(QMCG_INVALID_ARGUMENT, "QuasiStream: dimensions must be >= 1");
@@ -1345,6 +1926,7 @@ qmcg_status qmcg_normals(qmcg_ctx* c, int64_t n, uint64_t seed, int64_t dim, dou
 }
 
 qmcg_status qmcg_normal_table(qmcg_ctx* c, int64_t n, uint64_t seed, int64_t dims, double* out_host) {
+  if (c && !c->members.empty()) c = c->members[0];  // single-device call on a group: its first member
   if (!c || !out_host || n < 1 || dims < 1) return fail(QMCG_INVALID_ARGUMENT, "qmcg_normal_table: bad argument");
   std::lock_guard<std::mutex> lock(c->mu);
   DeviceGuard g(c->device);
@@ -1373,6 +1955,7 @@ qmcg_status qmcg_normal_table(qmcg_ctx* c, int64_t n, uint64_t seed, int64_t dim
 
 qmcg_status qmcg_uniform_rows(qmcg_ctx* c, int64_t n, uint64_t seed, int64_t dim_begin, int64_t dim_count,
                               double* out_host) {
+  if (c && !c->members.empty()) c = c->members[0];  // single-device call on a group: its first member
   if (!c || !out_host || n < 2 || dim_begin < 0 || dim_count < 1)
     return fail(QMCG_INVALID_ARGUMENT, "qmcg_uniform_rows: bad argument");
   if (static_cast<uint64_t>(n) > 0xffffffffULL)
@@ -1410,6 +1993,7 @@ qmcg_status qmcg_path_values(qmcg_ctx* c, const qmcg_option_spec* spec, int64_t 
   if (!c || !spec || !out_host) return fail(QMCG_INVALID_ARGUMENT, "qmcg_path_values: null argument");
   std::lock_guard<std::mutex> lock(c->mu);
   DeviceGuard g(c->device);
+  if (!c->members.empty()) return group_path_values(c, *spec, m, n, seed, flags, out_host);
   double sums[2];
   qmcg_status st = price_range(c, spec, m, n, seed, flags, sums);
   if (st) return st;
@@ -1419,22 +2003,27 @@ qmcg_status qmcg_path_values(qmcg_ctx* c, const qmcg_option_spec* spec, int64_t 
   return QMCG_OK;
 }
 
-qmcg_status qmcg_time_device(qmcg_ctx* c, const qmcg_option_spec* spec, int64_t m, int64_t n, uint64_t seed,
-                             uint32_t flags, int reps, double* kernel_ms, double* step_ms, double* out_price_se) {
-  if (!c || !spec || reps < 1) return fail(QMCG_INVALID_ARGUMENT, "qmcg_time_device: bad argument");
-  std::lock_guard<std::mutex> lock(c->mu);
-  DeviceGuard g(c->device);
+// Device time of pricing the tree nodes [node0, node0 + count) at `depth` (their contiguous path
+// range; the whole option for depth 0): `reps` launches of the pricing kernel (CUDA events on the
+// context stream around the kernel alone) and of the whole device step (kernel + node sums),
+// after one untimed launch. sums: 2 per node.
+static qmcg_status time_nodes(qmcg_ctx* c, const qmcg_option_spec& spec, int64_t m, int64_t n, uint64_t seed,
+                              uint32_t flags, int depth, int64_t node0, int64_t count, int reps, double* kernel_ms,
+                              double* step_ms, std::vector<double>& sums) {
+  int64_t b, e, off, size;
+  tree_node(n, depth, node0, b, size);
+  tree_node(n, depth, node0 + count - 1, off, size);
+  e = off + size;
   CallPlan plan;
-  qmcg_status st = plan_call(*spec, m, n, flags, plan);
+  qmcg_status st = plan_call(spec, m, n, flags, plan);
   if (st) return st;
   st = upload_plan(c, plan, n);
   if (st) return st;
-  st = ensure_perms(c, seed, n, 0, n, m, false);
+  st = ensure_perms(c, seed, n, b, e, m, false);
   if (st) return st;
-  st = prepare_scratch(c, 1);
+  st = prepare_scratch(c, static_cast<size_t>(count));
   if (st) return st;
-  // one untimed launch (module load, caches)
-  st = enqueue_price(c, plan, 0, n, 0, nullptr);
+  st = enqueue_values(c, plan, b, e);  // one untimed launch (module load, caches)
   if (st) return st;
   QMCG_CUDA(cudaStreamSynchronize(c->stream));
   c->launches = 0;
@@ -1442,7 +2031,9 @@ qmcg_status qmcg_time_device(qmcg_ctx* c, const qmcg_option_spec* spec, int64_t 
   QMCG_CUDA(cudaEventRecord(c->ev[2], c->stream));
   for (int r = 0; r < reps; ++r) {
     QMCG_CUDA(cudaEventRecord(c->ev[0], c->stream));
-    st = enqueue_price(c, plan, 0, n, 0, c->ev[1]);
+    st = enqueue_values(c, plan, b, e, c->ev[1]);
+    if (st) return st;
+    st = enqueue_node_sums(c, n, depth, node0, count, b);
     if (st) return st;
     QMCG_CUDA(cudaEventSynchronize(c->ev[1]));
     float ms = 0.f;
@@ -1450,21 +2041,66 @@ qmcg_status qmcg_time_device(qmcg_ctx* c, const qmcg_option_spec* spec, int64_t 
     kms += ms;
   }
   QMCG_CUDA(cudaEventRecord(c->ev[3], c->stream));
-  std::vector<double> sums;
-  st = sync_results(c, 1, sums);
+  st = sync_results(c, static_cast<size_t>(count), sums);
   if (st) return st;
   float total = 0.f;
   QMCG_CUDA(cudaEventElapsedTime(&total, c->ev[2], c->ev[3]));
   if (kernel_ms) *kernel_ms = kms / reps;
   if (step_ms) *step_ms = static_cast<double>(total) / reps;
+  return QMCG_OK;
+}
+
+qmcg_status qmcg_time_device(qmcg_ctx* c, const qmcg_option_spec* spec, int64_t m, int64_t n, uint64_t seed,
+                             uint32_t flags, int reps, double* kernel_ms, double* step_ms, double* out_price_se) {
+  if (!c || !spec || reps < 1) return fail(QMCG_INVALID_ARGUMENT, "qmcg_time_device: bad argument");
+  std::lock_guard<std::mutex> lock(c->mu);
+  DeviceGuard g(c->device);
+  if (!c->members.empty())
+    return group_time_device(c, *spec, m, n, seed, flags, reps, kernel_ms, step_ms, out_price_se);
+  std::vector<double> sums;
+  qmcg_status st = time_nodes(c, *spec, m, n, seed, flags, 0, 0, 1, reps, kernel_ms, step_ms, sums);
+  if (st) return st;
   if (out_price_se) finish_stats(n, sums[0], sums[1], out_price_se[0], out_price_se[1]);
   return QMCG_OK;
+}
+
+qmcg_status qmcg_time_device_nodes(qmcg_ctx* c, const qmcg_option_spec* spec, int64_t m, int64_t n, uint64_t seed,
+                                   uint32_t flags, int depth, int64_t node_begin, int64_t node_count, int reps,
+                                   double* kernel_ms, double* step_ms, double* out_sums) {
+  if (!c || !spec || reps < 1 || depth < 0 || depth > 30 || node_count < 1 || node_begin < 0 ||
+      node_begin + node_count > (int64_t{1} << depth))
+    return fail(QMCG_INVALID_ARGUMENT, "qmcg_time_device_nodes: bad argument");
+  if (!c->members.empty())
+    return fail(QMCG_UNSUPPORTED, "qmcg_time_device_nodes: a per-device call (use a single-device context per rank)");
+  std::lock_guard<std::mutex> lock(c->mu);
+  DeviceGuard g(c->device);
+  std::vector<double> sums;
+  qmcg_status st = time_nodes(c, *spec, m, n, seed, flags, depth, node_begin, node_count, reps, kernel_ms, step_ms,
+                              sums);
+  if (st) return st;
+  if (out_sums) std::copy(sums.begin(), sums.end(), out_sums);
+  return QMCG_OK;
+}
+
+void* qmcg_get_member_stream(qmcg_ctx* c, int member) {
+  if (!c) return nullptr;
+  if (c->members.empty()) return member == 0 ? static_cast<void*>(c->stream) : nullptr;
+  if (member < 0 || member >= static_cast<int>(c->members.size())) return nullptr;
+  return static_cast<void*>(c->members[static_cast<size_t>(member)]->stream);
+}
+
+int qmcg_member_device(qmcg_ctx* c, int member) {
+  if (!c) return -1;
+  if (c->members.empty()) return member == 0 ? c->device : -1;
+  if (member < 0 || member >= static_cast<int>(c->members.size())) return -1;
+  return c->members[static_cast<size_t>(member)]->device;
 }
 
 qmcg_status qmcg_time_perm_build(qmcg_ctx* c, int64_t n, uint64_t seed, int64_t dims, double* ms) {
   if (!c || !ms) return fail(QMCG_INVALID_ARGUMENT, "qmcg_time_perm_build: bad argument");
   std::lock_guard<std::mutex> lock(c->mu);
   DeviceGuard g(c->device);
+  if (!c->members.empty()) return group_time_perm_build(c, n, seed, dims, ms);
   // make the table resident and allocated, then invalidate its rows so only
   // the rebuild (K1 for every dimension) is timed
   qmcg_status st = ensure_perms(c, seed, n, 0, n, dims, false);
@@ -1482,11 +2118,20 @@ qmcg_status qmcg_time_perm_build(qmcg_ctx* c, int64_t n, uint64_t seed, int64_t 
   return QMCG_OK;
 }
 
-int64_t qmcg_last_launch_count(qmcg_ctx* c) { return c ? c->launches : 0; }
+int64_t qmcg_last_launch_count(qmcg_ctx* c) {
+  if (!c) return 0;
+  int64_t n = c->launches;
+  for (qmcg_ctx* m : c->members) n += m->launches;
+  return n;
+}
 
-void* qmcg_get_stream(qmcg_ctx* c) { return c ? static_cast<void*>(c->stream) : nullptr; }
+void* qmcg_get_stream(qmcg_ctx* c) {
+  if (c && !c->members.empty()) c = c->members[0];
+  return c ? static_cast<void*>(c->stream) : nullptr;
+}
 
 qmcg_status qmcg_fp64_peak(qmcg_ctx* c, double ms, double* inst_per_s) {
+  if (c && !c->members.empty()) c = c->members[0];  // single-device call on a group: its first member
   if (!c || !inst_per_s || !(ms > 0.0)) return fail(QMCG_INVALID_ARGUMENT, "qmcg_fp64_peak: bad argument");
   std::lock_guard<std::mutex> lock(c->mu);
   DeviceGuard g(c->device);
@@ -1619,6 +2264,7 @@ double bs_price_host(double s, double x, double r, double v, double t, int kind)
 
 qmcg_status qmcg_simulate_batch(qmcg_ctx* c, const qmcg_option_spec* spec, int64_t m, int64_t n, uint64_t seed,
                                 uint32_t flags, int layout, double* out_host) {
+  if (c && !c->members.empty()) c = c->members[0];  // single-device call on a group: its first member
   if (!spec) return fail(QMCG_INVALID_ARGUMENT, "qmcg_simulate_batch: null argument");
   if (layout != QMCG_LAYOUT_PATH_MAJOR && layout != QMCG_LAYOUT_POINT_MAJOR)
     return fail(QMCG_INVALID_ARGUMENT, "qmcg_simulate_batch: bad layout");
@@ -1648,6 +2294,7 @@ qmcg_status qmcg_simulate_batch(qmcg_ctx* c, const qmcg_option_spec* spec, int64
 
 qmcg_status qmcg_sweep_batch(qmcg_ctx* c, const qmcg_option_spec* spec, int64_t m, int64_t n, uint64_t seed,
                              uint32_t flags, double* values_host, int32_t* exercise_host) {
+  if (c && !c->members.empty()) c = c->members[0];  // single-device call on a group: its first member
   if (!c || !spec || !values_host || !exercise_host)
     return fail(QMCG_INVALID_ARGUMENT, "qmcg_sweep_batch: null argument");
   if (spec->kind != QMCG_CALL && !(flags & QMCG_FLAG_ALLOW_PUT))

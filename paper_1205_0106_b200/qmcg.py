@@ -42,6 +42,8 @@ EXPORTS = (
     "qmcg_last_launch_count", "qmcg_get_stream", "qmcg_fp64_peak", "qmcg_set_table_budget",
     "qmcg_last_window_count", "qmcg_price_american_nodes", "qmcg_simulate_batch", "qmcg_sweep_batch",
     "qmcg_backward_sweep", "qmcg_build_tables", "qmcg_import_tables", "qmcg_uniform_rows",
+    "qmcg_create_multi", "qmcg_device_count", "qmcg_time_device_nodes", "qmcg_get_member_stream",
+    "qmcg_member_device",
 )
 
 
@@ -122,6 +124,9 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
         P, I64, U64, U32, D = C.c_void_p, C.c_int64, C.c_uint64, C.c_uint32, C.c_double
         PD = C.POINTER(C.c_double)
         L.qmcg_create.argtypes = [C.c_int, C.POINTER(P)]
+        L.qmcg_create_multi.argtypes = [C.POINTER(C.c_int), C.c_int, C.POINTER(P)]
+        L.qmcg_device_count.argtypes = [P]
+        L.qmcg_device_count.restype = C.c_int
         L.qmcg_destroy.argtypes = [P]
         L.qmcg_destroy.restype = None
         L.qmcg_last_error.restype = C.c_char_p
@@ -151,6 +156,12 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
         L.qmcg_uniform_rows.argtypes = [P, I64, U64, I64, I64, P]
         L.qmcg_time_device.argtypes = [P, C.POINTER(_CSpec), I64, I64, U64, U32, C.c_int, PD, PD, PD]
         L.qmcg_time_perm_build.argtypes = [P, I64, U64, I64, PD]
+        L.qmcg_time_device_nodes.argtypes = [P, C.POINTER(_CSpec), I64, I64, U64, U32, C.c_int, I64, I64, C.c_int,
+                                             PD, PD, PD]
+        L.qmcg_get_member_stream.argtypes = [P, C.c_int]
+        L.qmcg_get_member_stream.restype = P
+        L.qmcg_member_device.argtypes = [P, C.c_int]
+        L.qmcg_member_device.restype = C.c_int
         L.qmcg_last_launch_count.argtypes = [P]
         L.qmcg_last_launch_count.restype = I64
         L.qmcg_get_stream.argtypes = [P]
@@ -183,13 +194,24 @@ def _result(r: _CResult) -> PricingResult:
 
 
 class Context:
-    """One CUDA device: stream, scratch and the permutation-table cache."""
+    """One CUDA device (stream, scratch, permutation-table cache), or with `devices` a device
+    group: pricing sharded over the listed devices as pairwise-tree nodes (qmcg_create_multi)."""
 
-    def __init__(self, device: int = 0):
+    def __init__(self, device: int = 0, devices: Optional[Sequence[int]] = None):
         self._lib = load_library()
         self._h = C.c_void_p()
-        _check(self._lib.qmcg_create(int(device), C.byref(self._h)))
-        self.device = device
+        if devices is not None:
+            ids = (C.c_int * len(devices))(*[int(d) for d in devices])
+            _check(self._lib.qmcg_create_multi(ids, len(devices), C.byref(self._h)))
+            self.device = int(devices[0])
+            self.devices = [int(d) for d in devices]
+        else:
+            _check(self._lib.qmcg_create(int(device), C.byref(self._h)))
+            self.device = device
+            self.devices = [int(device)]
+
+    def device_count(self) -> int:
+        return int(self._lib.qmcg_device_count(self._h))
 
     def close(self) -> None:
         if self._h:
@@ -372,6 +394,23 @@ class Context:
                                           _flags(allow_put, fp32=fp32), int(reps), C.byref(k), C.byref(st),
                                           ps.ctypes.data_as(C.POINTER(C.c_double))))
         return k.value, st.value, float(ps[0]), float(ps[1])
+
+    def time_device_nodes(self, spec: OptionSpec, m: int, n_paths: int, seed: int, depth: int, node_begin: int,
+                          node_count: int, reps: int, allow_put: bool = False, fp32: bool = False):
+        """(kernel ms, step ms, (node_count, 2) sums) of pricing one rank's tree nodes."""
+        k, st = C.c_double(), C.c_double()
+        out = np.zeros((int(node_count), 2), dtype=np.float64)
+        s = _cspec(spec)
+        _check(self._lib.qmcg_time_device_nodes(self._h, C.byref(s), int(m), int(n_paths), int(seed),
+                                                _flags(allow_put, fp32=fp32), int(depth), int(node_begin),
+                                                int(node_count), int(reps), C.byref(k), C.byref(st),
+                                                out.ctypes.data_as(C.POINTER(C.c_double))))
+        return k.value, st.value, out
+
+    def member_streams(self):
+        """[(device, cudaStream_t)] of every member (one entry for a single-device context)."""
+        return [(int(self._lib.qmcg_member_device(self._h, r)), int(self._lib.qmcg_get_member_stream(self._h, r) or 0))
+                for r in range(self.device_count())]
 
     def time_perm_build(self, n_paths: int, seed: int, dims: int) -> float:
         ms = C.c_double()
