@@ -292,7 +292,7 @@ def main():
             return max(e0.elapsed_time(e1) for e0, e1, _, _ in self.ev)
 
     def sync_all():
-        for dv in sorted({dv for _, dv in members}):
+        for dv in sorted({dv for dv, _ in members}):
             torch.cuda.synchronize(dv)
 
     def price(spec, m, n, **kw):
@@ -365,7 +365,7 @@ def main():
         if dist:
             dist.barrier()
         sync_all()
-        sampler = ClockSampler(sorted({dv for _, dv in members})[0]) if sample_clocks else None
+        sampler = ClockSampler(sorted({dv for dv, _ in members})[0]) if sample_clocks else None
         if sampler:
             sampler.__enter__()
         launches = 0
@@ -503,16 +503,15 @@ def main():
 
     if rank == 0:
         cold_med = statistics.median(cold_e2e)
+        layout = ("one process, one device" if mode == "single" else
+                  f"one process, device group {devices} (qmcg_create_multi)" if mode == "group" else
+                  "one process per GPU (torchrun, NCCL all-gather of node sums)")
         line = {"metric": METRIC, "value": value, "unit": "path-steps/s", "n_gpus": n_gpus, "steps": steps,
                 "warmup": warmup, "ms_per_step": ms_call, "higher_is_better": True, "scaling": "strong",
                 "vs_baseline": None, "dtype": "f64",
                 "data": "synthetic (QMC paths from the reference's scrambled Halton stream, seed 42)",
                 "config": {"workload": WORKLOAD, "n_paths": n_paths, "m_dates": M_DATES, "seed": SEED,
-                           "parallelism": (f"paths sharded over {n_gpus} GPU(s) (pairwise-tree nodes); "
-                                           + {"single": "one process, one device",
-                                              "group": f"one process, device group {devices} (qmcg_create_multi)",
-                                              "ranks": "one process per GPU (torchrun, NCCL all-gather of node "
-                                                       "sums)"}[mode]),
+                           "parallelism": f"paths sharded over {n_gpus} GPU(s) (pairwise-tree nodes); {layout}",
                            "tables": "warm: permutation tables resident in HBM (cold call measured separately)",
                            "l2": "inputs larger than L2 (4 B x 2^24 x 256 = 17.2 GB of tables per step)"},
                 "e2e": {"value": e2e_value, "unit": "path-steps/s", "h2d_bytes_per_step": 8 * (M_DATES + 1),

@@ -112,6 +112,13 @@ qmcg_status qmcg_price_american_batch(qmcg_ctx* ctx, const qmcg_option_spec* spe
                                       int64_t n_specs, int64_t m, int64_t n_paths, uint64_t seed,
                                       uint32_t flags, qmcg_pricing_result* out);
 
+/* The same batch, also returning every contract's per-path t0 values (values_host[i * n_paths + p],
+ * contract i in the caller's order) from the same launches (parity export: the batch's fused
+ * tree must equal the reference's reduce_stats of these values). */
+qmcg_status qmcg_price_american_batch_values(qmcg_ctx* ctx, const qmcg_option_spec* specs,
+                                             int64_t n_specs, int64_t m, int64_t n_paths, uint64_t seed,
+                                             uint32_t flags, qmcg_pricing_result* out, double* values_host);
+
 /* Sharded pricing for multi-GPU: computes (sum v, sum v^2) of the pairwise
  * tree node `node` at depth `depth` (reference pairwise_sum,
  * proj/src/path_engine.cpp:39-47), over the paths of that node only. Nodes at

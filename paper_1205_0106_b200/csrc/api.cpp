@@ -294,6 +294,7 @@ struct qmcg_ctx {
   DevBuf<double> d_values, d_red, d_sums;
   DevBuf<double> d_z;                                // batch: shared normal (prefix-sum) table
   DevBuf<double> d_bvalues[2], d_bred[2], d_bsums[2];  // per kind: per-contract values, scratch, sums
+  DevBuf<double> d_bnodes[2];                        // per kind: fused leaf-node sums of the batch walk
   DevBuf<qmcg::ContractParams> d_cparams[2];
   DevBuf<qmcg::GroupParams> d_groups[2];
   DevBuf<uint32_t> d_err, d_fullperm;
@@ -769,6 +770,7 @@ void qmcg_destroy(qmcg_ctx* c) {
     c->d_bvalues[k].release();
     c->d_bred[k].release();
     c->d_bsums[k].release();
+    c->d_bnodes[k].release();
     c->d_cparams[k].release();
     c->d_groups[k].release();
   }
@@ -1713,8 +1715,25 @@ qmcg_status qmcg_price_american_nodes(qmcg_ctx* c, const qmcg_option_spec* spec,
   return price_nodes(c, spec, m, n, seed, flags, depth, node_begin, node_count, out_sums);
 }
 
+static qmcg_status batch_impl(qmcg_ctx* c, const qmcg_option_spec* specs, int64_t n_specs, int64_t m, int64_t n,
+                              uint64_t seed, uint32_t flags, qmcg_pricing_result* out, double* values_host);
+
 qmcg_status qmcg_price_american_batch(qmcg_ctx* c, const qmcg_option_spec* specs, int64_t n_specs, int64_t m,
                                       int64_t n, uint64_t seed, uint32_t flags, qmcg_pricing_result* out) {
+  return batch_impl(c, specs, n_specs, m, n, seed, flags, out, nullptr);
+}
+
+qmcg_status qmcg_price_american_batch_values(qmcg_ctx* c, const qmcg_option_spec* specs, int64_t n_specs, int64_t m,
+                                             int64_t n, uint64_t seed, uint32_t flags, qmcg_pricing_result* out,
+                                             double* values_host) {
+  if (!values_host) return fail(QMCG_INVALID_ARGUMENT, "qmcg_price_american_batch_values: null argument");
+  if (c && !c->members.empty())
+    return fail(QMCG_UNSUPPORTED, "qmcg_price_american_batch_values: a per-device call (single-device context)");
+  return batch_impl(c, specs, n_specs, m, n, seed, flags, out, values_host);
+}
+
+static qmcg_status batch_impl(qmcg_ctx* c, const qmcg_option_spec* specs, int64_t n_specs, int64_t m, int64_t n,
+                              uint64_t seed, uint32_t flags, qmcg_pricing_result* out, double* values_host) {
   if (!c || !specs || !out || n_specs < 0) return fail(QMCG_INVALID_ARGUMENT, "qmcg_price_american_batch: bad argument");
   if (flags & QMCG_FLAG_FP32)
     return fail(QMCG_UNSUPPORTED, "qmcg_price_american_batch: QMCG_FLAG_FP32 is not supported (the batch walk is FP64)");
@@ -1770,6 +1789,9 @@ qmcg_status qmcg_price_american_batch(qmcg_ctx* c, const qmcg_option_spec* specs
   for (int64_t i : single_idx) {
     st = enqueue_price(c, plans[static_cast<size_t>(i)], 0, n, static_cast<int>(i), nullptr);
     if (st) return st;
+    if (values_host)
+      QMCG_CUDA(cudaMemcpyAsync(values_host + static_cast<size_t>(i) * static_cast<size_t>(n), c->d_values.ptr,
+                                static_cast<size_t>(n) * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
   }
   std::vector<double> shared_sums[2];
   if (use_shared) {
@@ -1839,13 +1861,28 @@ qmcg_status qmcg_price_american_batch(qmcg_ctx* c, const qmcg_option_spec* specs
       QMCG_CUDA(c->d_bvalues[k].reserve(cnt * static_cast<size_t>(n)));
       QMCG_CUDA(c->d_bred[k].reserve(cnt * qmcg::reduce_scratch_doubles(n)));
       QMCG_CUDA(c->d_bsums[k].reserve(2 * cnt));
+      // n a power of two >= 128: every leaf-depth node of the reference tree is one 128-path block
+      // of the walk, which then writes the node sums itself (no per-path values round trip)
+      const bool fused = n >= 128 && (n & (n - 1)) == 0;
+      const int64_t nodes = n / 128;
+      if (fused) QMCG_CUDA(c->d_bnodes[k].reserve(cnt * static_cast<size_t>(2 * nodes)));
       qmcg::BatchParams B{c->d_z.ptr, n, n, static_cast<int32_t>(m), static_cast<int32_t>(cnt), c->d_cparams[k].ptr,
-                          c->d_bvalues[k].ptr, c->d_groups[k].ptr, static_cast<int32_t>(groups.size()), 0};
+                          c->d_bvalues[k].ptr, c->d_groups[k].ptr, static_cast<int32_t>(groups.size()),
+                          (values_host || !fused) ? 1 : 0, fused ? c->d_bnodes[k].ptr : nullptr};
       QMCG_CUDA(qmcg::launch_walk_group(B, k, c->stream));
       int launches = 1;
-      QMCG_CUDA(qmcg::launch_pairwise_batched(c->d_bvalues[k].ptr, n, static_cast<int>(cnt), c->d_bred[k].ptr,
-                                              c->d_bsums[k].ptr, c->stream, &launches));
+      if (fused)
+        QMCG_CUDA(qmcg::launch_pairwise_from_nodes(c->d_bnodes[k].ptr, nodes, static_cast<int>(cnt), c->d_bred[k].ptr,
+                                                   c->d_bsums[k].ptr, c->stream, &launches));
+      else
+        QMCG_CUDA(qmcg::launch_pairwise_batched(c->d_bvalues[k].ptr, n, static_cast<int>(cnt), c->d_bred[k].ptr,
+                                                c->d_bsums[k].ptr, c->stream, &launches));
       c->launches += launches;
+      if (values_host)  // parity export: contract shared_idx[k][j] is row j of the kind's value table
+        for (size_t j = 0; j < cnt; ++j)
+          QMCG_CUDA(cudaMemcpyAsync(values_host + static_cast<size_t>(shared_idx[k][j]) * static_cast<size_t>(n),
+                                    c->d_bvalues[k].ptr + j * static_cast<size_t>(n),
+                                    static_cast<size_t>(n) * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
       shared_sums[k].resize(2 * cnt);  // read back with the other results (no sync between the kinds)
       tr.mark(k == 0 ? "calls enqueued" : "puts enqueued");
     }

@@ -1371,6 +1371,30 @@ __host__ __device__ __forceinline__ void lcg_jump(uint64_t delta, uint64_t& mult
   plus = acc_plus;
 }
 
+// LCG maps s -> A^(2^k) s + C_(2^k) (mod 2^64), k = 0..63: a thread's start state is the
+// composition over the set bits of its draw number (~log2(g)/2 compositions of 2 multiplies,
+// instead of squaring the map through every bit).
+__constant__ uint64_t c_lcg_pow[64][2];
+
+__device__ __forceinline__ uint64_t lcg_state_after(uint64_t seed, uint64_t draws) {
+  uint64_t am = 1, ap = 0;
+  while (draws) {
+    const int k = __ffsll(static_cast<long long>(draws)) - 1;
+    const uint64_t m = c_lcg_pow[k][0], p = c_lcg_pow[k][1];
+    ap = ap * m + p;
+    am *= m;
+    draws &= draws - 1;
+  }
+  return am * seed + ap;
+}
+
+// below(b) = floor(s b / 2^64) for b < 2^32 (Lcg::below, quasi_rng.hpp:20-23): the high word of
+// the 96-bit product from one wide and one high 32-bit multiply.
+__device__ __forceinline__ uint32_t lcg_below32(uint64_t s, uint32_t b) {
+  const uint64_t hi = static_cast<uint64_t>(static_cast<uint32_t>(s >> 32)) * b;
+  return static_cast<uint32_t>((hi + __umulhi(static_cast<uint32_t>(s), b)) >> 32);
+}
+
 __global__ void fy_draws_kernel(uint64_t seed, int64_t n, uint64_t stride_mult, uint64_t stride_plus,
                                 uint32_t* __restrict__ keys, uint32_t* __restrict__ vals) {
   const int64_t G = static_cast<int64_t>(gridDim.x) * blockDim.x;
@@ -1381,12 +1405,10 @@ __global__ void fy_draws_kernel(uint64_t seed, int64_t n, uint64_t stride_mult, 
   }
   const int64_t draws = n - 1;
   if (g >= draws) return;
-  uint64_t jm, jp;
-  lcg_jump(static_cast<uint64_t>(g) + 1, jm, jp);
-  uint64_t s = jm * seed + jp;  // state after draw g
+  uint64_t s = lcg_state_after(seed, static_cast<uint64_t>(g) + 1);  // state after draw g
   for (int64_t t = g; t < draws; t += G) {
-    const int64_t i = n - 1 - t;
-    keys[i] = static_cast<uint32_t>(__umul64hi(s, static_cast<uint64_t>(i) + 1));
+    const int64_t i = n - 1 - t;  // i + 1 <= n - 1 < 2^32
+    keys[i] = lcg_below32(s, static_cast<uint32_t>(i + 1));
     vals[i] = static_cast<uint32_t>(i);
     s = stride_mult * s + stride_plus;
   }
@@ -1408,26 +1430,65 @@ __global__ void fy_first_kernel(const uint32_t* __restrict__ sk, const uint32_t*
 // sorted order as (i, perm[i]) for the binned scatter below (large n, where a
 // direct perm[i] store is a random 4-byte write: a read-modify-write of a
 // whole DRAM burst); otherwise it is stored directly.
-__global__ void fy_assign_kernel(const uint32_t* __restrict__ sk, const uint32_t* __restrict__ sv, int64_t n,
-                                 const uint32_t* __restrict__ F, uint32_t* __restrict__ perm,
-                                 uint2* __restrict__ pairs, uint32_t add) {
-  const int64_t q = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (q >= n) return;
+// Each thread follows kChase chains at once (entries q, q + B, ..., B = the block's span), so a
+// warp keeps kChase independent random F reads in flight instead of one dependent chain: the
+// pass is bound by the latency of that chase (~1 random F read per entry on average).
+constexpr int kChase = 4;
+__global__ void __launch_bounds__(256) fy_assign_kernel(const uint32_t* __restrict__ sk,
+                                                        const uint32_t* __restrict__ sv, int64_t n,
+                                                        const uint32_t* __restrict__ F, uint32_t* __restrict__ perm,
+                                                        uint2* __restrict__ pairs, uint32_t add) {
+  const int64_t q0 = static_cast<int64_t>(blockIdx.x) * (blockDim.x * kChase) + threadIdx.x;
+  uint32_t y[kChase], out[kChase], idx[kChase];
+  bool live[kChase], chase[kChase];
   // the sorted pairs stream through once (evict-first) so that F, read at random,
   // keeps its place in L2
-  const uint32_t x = __ldcs(sk + q), i = __ldcs(sv + q);
-  uint32_t out = x;
-  if (q + 1 < n && __ldcs(sk + q + 1) == x) {
-    uint32_t y = __ldcs(sv + q + 1);
-    for (uint32_t f = __ldg(F + y); f != kNone; f = __ldg(F + y)) y = f;
-    out = y;
+#pragma unroll
+  for (int k = 0; k < kChase; ++k) {
+    const int64_t q = q0 + k * blockDim.x;
+    live[k] = q < n;
+    chase[k] = false;
+    if (live[k]) {
+      const uint32_t x = __ldcs(sk + q);
+      idx[k] = __ldcs(sv + q);
+      out[k] = x;
+      if (q + 1 < n && __ldcs(sk + q + 1) == x) {
+        y[k] = __ldcs(sv + q + 1);
+        chase[k] = true;
+      }
+    }
   }
+  bool any = false;
+#pragma unroll
+  for (int k = 0; k < kChase; ++k) any |= chase[k];
+  while (any) {
+    uint32_t f[kChase];
+#pragma unroll
+    for (int k = 0; k < kChase; ++k) f[k] = chase[k] ? __ldg(F + y[k]) : kNone;
+    any = false;
+#pragma unroll
+    for (int k = 0; k < kChase; ++k) {
+      if (chase[k]) {
+        if (f[k] != kNone) y[k] = f[k];
+        else {
+          out[k] = y[k];
+          chase[k] = false;
+        }
+      }
+      any |= chase[k];
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < kChase; ++k) {
+    if (!live[k]) continue;
+    const int64_t q = q0 + k * blockDim.x;
 #ifdef QMCG_K1_COALESCED_PROBE
-  perm[q] = out + i;  // timing probe only: coalesced store (wrong result)
+    perm[q] = out[k] + idx[k];  // timing probe only: coalesced store (wrong result)
 #else
-  if (pairs) __stcs(pairs + q, make_uint2(i, out + add));
-  else __stcs(perm + i, out + add);
+    if (pairs) __stcs(pairs + q, make_uint2(idx[k], out[k] + add));
+    else __stcs(perm + idx[k], out[k] + add);
 #endif
+  }
 }
 
 // Binned scatter, pass 1: partition the (i, perm[i]) pairs by i >> bin_shift
@@ -1773,6 +1834,7 @@ constexpr int kGThreads = 128;
 #define QMCG_G_MINB 6
 #endif
 constexpr int kGCap = 12;  // candidates per path kept in shared memory before a flush
+constexpr int kGLeafQ = 4;  // strikes staged per fused-leaf round (a 4 KB row of values)
 
 template <int KIND>
 __device__ __noinline__ void group_flush(const ContractParams* __restrict__ cp, const GroupParams* __restrict__ g,
@@ -1910,6 +1972,12 @@ __global__ void __launch_bounds__(kGThreads, QMCG_G_MINB) walk_group_kernel(cons
   const double sl = exp(X);
   const double dm = __ldg(g->dpow + m);
   const double inv_vst = 1.0 / g->bs_vsqrt;
+  // fused leaves (B.node_sums): this block's 128 paths are one node of the reference tree at its
+  // leaf depth (n a power of two), so the two ordered 64-value leaf sums of each strike are
+  // formed here from a shared-memory row and 16 bytes per (contract, node) leave the kernel
+  // instead of 8 bytes per (contract, path)
+  const uint32_t vrow = smem_u32(smg) + kGThreads * kGCap * 20;
+  const bool fused = B.node_sums != nullptr;
 #pragma unroll 1
   for (int s = 0; s < g->count; ++s) {
     const ContractParams& q = B.cp[g->first + s];
@@ -1950,14 +2018,41 @@ __global__ void __launch_bounds__(kGThreads, QMCG_G_MINB) walk_group_kernel(cons
     intr = intr > 0.0 ? intr : 0.0;
     const double cm = intr > cont ? intr : cont;
     const double term_m = cm * dm;
-    if (pw < B.n) B.values[static_cast<int64_t>(g->first + s) * B.n + pw] = best > term_m ? best : term_m;
+    const double v = best > term_m ? best : term_m;
+    if (B.store_values && pw < B.n) B.values[static_cast<int64_t>(g->first + s) * B.n + pw] = v;
+    if (fused) {
+      const int u = s % kGLeafQ;
+      sts_f64(vrow + (u * kGThreads + threadIdx.x) * 8, v);
+      if (u == kGLeafQ - 1 || s == g->count - 1) {  // a chunk of strikes is staged: their leaf sums
+        __syncthreads();
+        const int t = threadIdx.x;
+        double x = 0.0, x2 = 0.0;
+        if (t < 2 * (u + 1)) {  // (strike s - u + t / 2, half t % 2): 64 values in path order from 0.0
+          const uint32_t a = vrow + ((t >> 1) * kGThreads + (t & 1) * 64) * 8;
+#pragma unroll 8
+          for (int k = 0; k < 64; ++k) {
+            const double y = lds_f64(a + k * 8);
+            x = __dadd_rn(x, y);
+            x2 = __dadd_rn(x2, __dmul_rn(y, y));
+          }
+        }
+        const double y = __shfl_down_sync(kFull, x, 1), y2 = __shfl_down_sync(kFull, x2, 1);
+        if (t < 2 * (u + 1) && !(t & 1)) {  // the node splits at 64 (pairwise_sum): left + right
+          double* o = B.node_sums + (static_cast<int64_t>(g->first + s - u + (t >> 1)) * gridDim.y + blockIdx.y) * 2;
+          o[0] = __dadd_rn(x, y);
+          o[1] = __dadd_rn(x2, y2);
+        }
+        __syncthreads();  // the row is restaged by the next chunk
+      }
+    }
   }
 }
 
 cudaError_t launch_walk_group(const BatchParams& B, int kind, cudaStream_t s) {
   if (B.n_groups <= 0 || B.n <= 0) return cudaSuccess;
   const dim3 grid(static_cast<unsigned>(B.n_groups), static_cast<unsigned>((B.n + kGThreads - 1) / kGThreads));
-  const size_t smem = kGThreads * kGCap * 20;
+  if (B.node_sums && (B.n % kGThreads != 0)) return cudaErrorInvalidValue;  // nodes must be whole blocks
+  const size_t smem = kGThreads * kGCap * 20 + (B.node_sums ? kGLeafQ * kGThreads * 8 : 0);
   auto kern = kind == 0 ? walk_group_kernel<0> : walk_group_kernel<1>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   if (e != cudaSuccess) return e;
@@ -1967,11 +2062,16 @@ cudaError_t launch_walk_group(const BatchParams& B, int kind, cudaStream_t s) {
 
 cudaError_t ensure_log_table(cudaStream_t s) {
   static bool done[64] = {};
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lock(mu);
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return e;
   if (dev < 64 && done[dev]) return cudaSuccess;
   e = cudaMemcpyToSymbolAsync(c_log_table, kLogTable, sizeof(kLogTable), 0, cudaMemcpyHostToDevice, s);
+  uint64_t pw[64][2];
+  for (int k = 0; k < 64; ++k) lcg_jump(uint64_t{1} << k, pw[k][0], pw[k][1]);
+  if (e == cudaSuccess) e = cudaMemcpyToSymbolAsync(c_lcg_pow, pw, sizeof(pw), 0, cudaMemcpyHostToDevice, s);
   if (e == cudaSuccess) e = cudaStreamSynchronize(s);
   if (e == cudaSuccess && dev < 64) done[dev] = true;
   return e;
@@ -2148,6 +2248,8 @@ cudaError_t launch_perm_build(uint64_t seed64, int64_t n, uint32_t* out, void* s
                               cudaStream_t s, int* launches, uint32_t add) {
   const PermScratchLayout L = perm_layout(n);
   if (scratch_bytes < L.total) return cudaErrorInvalidValue;
+  cudaError_t e = ensure_log_table(s);  // also the LCG power table of fy_draws_kernel
+  if (e != cudaSuccess) return e;
   char* base = static_cast<char*>(scratch);
   auto* keys = reinterpret_cast<uint32_t*>(base + L.keys);
   auto* vals = reinterpret_cast<uint32_t*>(base + L.vals);
@@ -2167,7 +2269,7 @@ cudaError_t launch_perm_build(uint64_t seed64, int64_t n, uint32_t* out, void* s
   lcg_jump(static_cast<uint64_t>(blocks) * threads, sm, sp);
   fy_draws_kernel<<<static_cast<unsigned>(blocks), threads, 0, s>>>(seed64, n, sm, sp, keys, vals);
   size_t temp_bytes = L.temp_bytes;
-  cudaError_t e = cub::DeviceRadixSort::SortPairs(base + L.temp, temp_bytes, keys, skeys, vals, svals,
+  e = cub::DeviceRadixSort::SortPairs(base + L.temp, temp_bytes, keys, skeys, vals, svals,
                                                   static_cast<int64_t>(n), 0, bits, s);
   if (e != cudaSuccess) return e;
   e = cudaMemsetAsync(F, 0xff, static_cast<size_t>(n) * sizeof(uint32_t), s);
@@ -2182,8 +2284,9 @@ cudaError_t launch_perm_build(uint64_t seed64, int64_t n, uint32_t* out, void* s
   auto* binned_pairs = reinterpret_cast<uint2*>(base + L.skeys);
   fy_first_kernel<<<static_cast<unsigned>(eb), threads, 0, s>>>(skeys, svals, n, F, binned ? cursor : nullptr,
                                                                  shift);
-  fy_assign_kernel<<<static_cast<unsigned>(eb), threads, 0, s>>>(skeys, svals, n, F, out,
-                                                                  binned ? pairs : nullptr, add);
+  const int64_t ab = (n + threads * kChase - 1) / (threads * kChase);
+  fy_assign_kernel<<<static_cast<unsigned>(ab), threads, 0, s>>>(skeys, svals, n, F, out, binned ? pairs : nullptr,
+                                                                  add);
   if (binned) {
     const int64_t bb = (n + kBinThreads * kBinPer - 1) / (kBinThreads * kBinPer);
     fy_bin_kernel<<<static_cast<unsigned>(bb), kBinThreads, 0, s>>>(pairs, n, shift, cursor, binned_pairs);
@@ -2191,6 +2294,14 @@ cudaError_t launch_perm_build(uint64_t seed64, int64_t n, uint32_t* out, void* s
   }
   if (launches) *launches += 4 + 1 + (binned ? 2 : 0);  // draws, sort (>=1), first, assign (+ memset) [+ bin, scatter]
   return cudaGetLastError();
+}
+
+cudaError_t pairwise_upper(double* a, int64_t nodes, int count, int64_t sa, double* b, int64_t sb, double* out2,
+                           cudaStream_t s, int* launches);
+
+cudaError_t launch_pairwise_from_nodes(double* node_sums, int64_t nodes, int count, double* scratch, double* out2,
+                                       cudaStream_t s, int* launches) {
+  return pairwise_upper(node_sums, nodes, count, 2 * nodes, scratch, 2 * ((nodes + 1023) / 1024), out2, s, launches);
 }
 
 size_t reduce_scratch_doubles(int64_t len) {
@@ -2215,6 +2326,18 @@ cudaError_t launch_pairwise_batched(const double* v, int64_t len, int count, dou
                     static_cast<unsigned>(count));
     pairwise_leaves_kernel<<<grid, kLeafWarps * 32, 0, s>>>(v, len, D, nodes == 1 ? out2 : a, nodes == 1 ? 2 : sa);
     if (launches) ++*launches;
+  }
+  if (nodes == 1) return cudaGetLastError();  // the leaf pass wrote the result
+  return pairwise_upper(a, nodes, count, sa, b, sb, out2, s, launches);
+}
+
+// The perfect-binary levels above a level of `nodes` node sums per vector (level at a, stride sa
+// per vector), ping-ponging with b (stride sb), into out2[2c, 2c + 1].
+cudaError_t pairwise_upper(double* a, int64_t nodes, int count, int64_t sa, double* b, int64_t sb, double* out2,
+                           cudaStream_t s, int* launches) {
+  if (nodes == 1 && a != out2) {  // a single node: its sums are the result
+    return cudaMemcpy2DAsync(out2, 2 * sizeof(double), a, static_cast<size_t>(sa) * sizeof(double),
+                             2 * sizeof(double), static_cast<size_t>(count), cudaMemcpyDeviceToDevice, s);
   }
   while (nodes > 1) {
     const int group = static_cast<int>(std::min<int64_t>(nodes, 1024));

@@ -43,7 +43,7 @@ EXPORTS = (
     "qmcg_last_window_count", "qmcg_price_american_nodes", "qmcg_simulate_batch", "qmcg_sweep_batch",
     "qmcg_backward_sweep", "qmcg_build_tables", "qmcg_import_tables", "qmcg_uniform_rows",
     "qmcg_create_multi", "qmcg_device_count", "qmcg_time_device_nodes", "qmcg_get_member_stream",
-    "qmcg_member_device",
+    "qmcg_member_device", "qmcg_price_american_batch_values",
 )
 
 
@@ -134,6 +134,8 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
         L.qmcg_price_american.argtypes = [P, C.POINTER(_CSpec), I64, I64, U64, U32, C.POINTER(_CResult)]
         L.qmcg_mc_european_price.argtypes = [P, C.POINTER(_CSpec), I64, U64, U32, C.POINTER(_CResult)]
         L.qmcg_price_american_batch.argtypes = [P, C.POINTER(_CSpec), I64, I64, I64, U64, U32, C.POINTER(_CResult)]
+        L.qmcg_price_american_batch_values.argtypes = [P, C.POINTER(_CSpec), I64, I64, I64, U64, U32,
+                                                       C.POINTER(_CResult), P]
         L.qmcg_price_american_node.argtypes = [P, C.POINTER(_CSpec), I64, I64, U64, U32, C.c_int, I64, PD]
         L.qmcg_price_american_nodes.argtypes = [P, C.POINTER(_CSpec), I64, I64, U64, U32, C.c_int, I64, I64, PD]
         L.qmcg_tree_node_range.argtypes = [I64, C.c_int, I64, C.POINTER(I64), C.POINTER(I64)]
@@ -262,6 +264,16 @@ class Context:
         _check(self._lib.qmcg_price_american_batch(self._h, arr, len(specs), int(m), int(n_paths), int(seed),
                                                     flags, res))
         return [_result(r) for r in res]
+
+    def price_american_batch_values(self, specs: Sequence[OptionSpec], m: int, n_paths: int, seed: int,
+                                    allow_put: bool = False):
+        """(results, (len(specs), n_paths) per-path t0 values) from the same batch launches."""
+        arr = (_CSpec * len(specs))(*[_cspec(s) for s in specs])
+        res = (_CResult * len(specs))()
+        vals = np.zeros((len(specs), int(n_paths)), dtype=np.float64)
+        _check(self._lib.qmcg_price_american_batch_values(self._h, arr, len(specs), int(m), int(n_paths), int(seed),
+                                                           FLAG_ALLOW_PUT if allow_put else 0, res, vals.ctypes.data))
+        return [_result(r) for r in res], vals
 
     def price_american_batch_arrays(self, spot, strike, rate, volatility, maturity, kind, m: int, n_paths: int,
                                     seed: int, allow_put: bool = False) -> np.ndarray:

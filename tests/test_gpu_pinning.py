@@ -108,3 +108,19 @@ def test_put_headline_bounds(ctx, qmcg, golden):
         assert r.price >= c["bs_put"] - 3 * r.std_error, (c, r)
         assert r.price >= c["american_put"] - 3 * r.std_error, (c, r)
         assert 0 < r.std_error < 0.01 * r.price
+
+
+@pytest.mark.parametrize("n", [1 << 14, 1 << 18, 100003, 4097])
+def test_batch_tree_equals_reference_reduce_stats(ctx, qmcg, reducer, n):
+    """The batch's tree (fused leaf sums inside the walk for power-of-two n, the leaves kernel
+    otherwise) equals the reference's reduce_stats of the same launch's per-path values."""
+    specs = [qmcg.OptionSpec(100.0, 80 + 40 * i / 5, 0.05, 0.1 + 0.4 * j / 5, 1.0, qmcg.OptionKind((i + j) % 2))
+             for i in range(6) for j in range(6)]
+    specs.append(qmcg.OptionSpec(100.0, 95.0, -0.01, 0.3, 1.0))  # r < 0: the single-contract kernel
+    res, vals = ctx.price_american_batch_values(specs, 24, n, 42, allow_put=True)
+    plain = ctx.price_american_batch(specs, 24, n, 42, allow_put=True)
+    for i, r in enumerate(res):
+        assert (r.price, r.std_error) == reducer(vals[i]), (n, i)
+        assert (plain[i].price, plain[i].std_error) == (r.price, r.std_error), (n, i)
+        one = ctx.price_american(specs[i], 24, n, 42, allow_put=True)
+        assert abs(one.price - r.price) <= 1e-12 * one.price, (n, i)
