@@ -113,7 +113,13 @@ namespace b200 {
 PricingResult price_american_put_extension(const OptionSpec& spec, Index m, Index n_paths,
                                            std::uint64_t seed);
 // Select the CUDA device used by the process-wide context (default: 0).
+// The drop-in prices on every visible GPU (a device group; QMCG_DEVICES narrows it) unless told
+// otherwise here. Changing the devices or release() destroys the process-wide context, which
+// frees its cached permutation tables.
 void set_device(int device);
+void set_devices(const std::vector<int>& devices);
+void release();
+int device_count();
 }  // namespace b200
 
 }  // namespace qmc

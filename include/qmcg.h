@@ -85,6 +85,9 @@ qmcg_status qmcg_create(int device, qmcg_ctx** out);
  * date windows the same way. qmcg_price_american_batch shards contracts. Every other call runs on
  * the first member; the per-device node / table-exchange calls return QMCG_UNSUPPORTED. */
 qmcg_status qmcg_create_multi(const int* dev_ids, int n_dev, qmcg_ctx** out);
+/* The context the C++ drop-in uses: every visible CUDA device (a device group when there are
+ * several), or the comma-separated list in the environment variable QMCG_DEVICES. */
+qmcg_status qmcg_create_default(qmcg_ctx** out);
 /* Number of devices a context drives (1 for qmcg_create). */
 int qmcg_device_count(qmcg_ctx* ctx);
 void qmcg_destroy(qmcg_ctx* ctx);

@@ -30,9 +30,11 @@ CALL, PUT = 0, 1
 ALLOW_PUT = 1
 
 
-def build(quiet: bool = True) -> None:
-    """Compile the C restatement and, when the reference tree exists, oracle/_ref."""
-    out = subprocess.run(["make", "-C", HERE, "all"], capture_output=True, text=True)
+def build(quiet: bool = True, suites: bool = False) -> None:
+    """Compile the C restatement and, when the reference tree exists, oracle/_ref; with `suites`
+    also the reference's own test binaries linked against libqmcg.so (build that first)."""
+    out = subprocess.run(["make", "-C", HERE, "all"] + (["ref_suites"] if suites else []),
+                         capture_output=True, text=True)
     if out.returncode != 0:
         raise RuntimeError("oracle build failed:\n" + out.stdout + out.stderr)
     if not quiet:

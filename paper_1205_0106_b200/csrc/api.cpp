@@ -744,6 +744,29 @@ qmcg_status qmcg_create_multi(const int* dev_ids, int n_dev, qmcg_ctx** out) {
   return QMCG_OK;
 }
 
+qmcg_status qmcg_create_default(qmcg_ctx** out) {
+  if (!out) return fail(QMCG_INVALID_ARGUMENT, "qmcg_create_default: out must not be null");
+  std::vector<int> devs;
+  if (const char* env = std::getenv("QMCG_DEVICES"); env && *env) {
+    const char* p = env;
+    while (*p) {
+      char* end = nullptr;
+      const long d = std::strtol(p, &end, 10);
+      if (end == p) return fail(QMCG_INVALID_ARGUMENT, std::string("QMCG_DEVICES: not a device list: ") + env);
+      devs.push_back(static_cast<int>(d));
+      p = *end == ',' ? end + 1 : end;
+      if (*end && *end != ',') return fail(QMCG_INVALID_ARGUMENT, std::string("QMCG_DEVICES: not a device list: ") + env);
+    }
+  } else {
+    int count = 0;
+    QMCG_CUDA(cudaGetDeviceCount(&count));
+    for (int d = 0; d < count; ++d) devs.push_back(d);
+  }
+  if (devs.empty()) return fail(QMCG_CUDA_ERROR, "qmcg_create_default: no CUDA device");
+  if (devs.size() == 1) return qmcg_create(devs[0], out);
+  return qmcg_create_multi(devs.data(), static_cast<int>(devs.size()), out);
+}
+
 int qmcg_device_count(qmcg_ctx* c) { return !c ? 0 : c->members.empty() ? 1 : static_cast<int>(c->members.size()); }
 
 void qmcg_destroy(qmcg_ctx* c) {
@@ -1868,7 +1891,7 @@ static qmcg_status batch_impl(qmcg_ctx* c, const qmcg_option_spec* specs, int64_
       if (fused) QMCG_CUDA(c->d_bnodes[k].reserve(cnt * static_cast<size_t>(2 * nodes)));
       qmcg::BatchParams B{c->d_z.ptr, n, n, static_cast<int32_t>(m), static_cast<int32_t>(cnt), c->d_cparams[k].ptr,
                           c->d_bvalues[k].ptr, c->d_groups[k].ptr, static_cast<int32_t>(groups.size()),
-                          (values_host || !fused) ? 1 : 0, fused ? c->d_bnodes[k].ptr : nullptr};
+                          values_host ? 1 : 0, fused ? c->d_bnodes[k].ptr : nullptr};
       QMCG_CUDA(qmcg::launch_walk_group(B, k, c->stream));
       int launches = 1;
       if (fused)

@@ -8,6 +8,7 @@
 #include <chrono>
 #include <mutex>
 #include <stdexcept>
+#include <vector>
 
 namespace qmc {
 
@@ -15,12 +16,21 @@ namespace {
 
 std::mutex g_mu;
 qmcg_ctx* g_ctx = nullptr;
-int g_device = 0;
+std::vector<int> g_devices;  // empty: every visible device (or QMCG_DEVICES), qmcg_create_default
 
+// The process-wide context: a device group over all visible GPUs unless narrowed with
+// b200::set_devices / set_device (the reference's ExecPolicy lanes stay a hint, as there).
 qmcg_ctx* context() {
   std::lock_guard<std::mutex> lock(g_mu);
   if (!g_ctx) {
-    if (qmcg_create(g_device, &g_ctx) != QMCG_OK) throw std::runtime_error(qmcg_last_error());
+    qmcg_status st;
+    if (g_devices.empty()) st = qmcg_create_default(&g_ctx);
+    else if (g_devices.size() == 1) st = qmcg_create(g_devices[0], &g_ctx);
+    else st = qmcg_create_multi(g_devices.data(), static_cast<int>(g_devices.size()), &g_ctx);
+    if (st != QMCG_OK) {
+      g_ctx = nullptr;
+      throw std::runtime_error(qmcg_last_error());
+    }
   }
   return g_ctx;
 }
@@ -167,14 +177,26 @@ PricingResult price_american_put_extension(const OptionSpec& spec, Index m, Inde
   return price(spec, m, n_paths, seed, QMCG_FLAG_ALLOW_PUT);
 }
 
-void set_device(int device) {
+void set_devices(const std::vector<int>& devices) {
   std::lock_guard<std::mutex> lock(g_mu);
   if (g_ctx) {
     qmcg_destroy(g_ctx);
     g_ctx = nullptr;
   }
-  g_device = device;
+  g_devices = devices;
 }
+
+void set_device(int device) { set_devices({device}); }
+
+void release() {
+  std::lock_guard<std::mutex> lock(g_mu);
+  if (g_ctx) {
+    qmcg_destroy(g_ctx);  // frees the permutation-table cache (17 GB at config 3) and all scratch
+    g_ctx = nullptr;
+  }
+}
+
+int device_count() { return qmcg_device_count(context()); }
 
 }  // namespace b200
 

@@ -1834,7 +1834,6 @@ constexpr int kGThreads = 128;
 #define QMCG_G_MINB 6
 #endif
 constexpr int kGCap = 12;  // candidates per path kept in shared memory before a flush
-constexpr int kGLeafQ = 4;  // strikes staged per fused-leaf round (a 4 KB row of values)
 
 template <int KIND>
 __device__ __noinline__ void group_flush(const ContractParams* __restrict__ cp, const GroupParams* __restrict__ g,
@@ -1972,12 +1971,6 @@ __global__ void __launch_bounds__(kGThreads, QMCG_G_MINB) walk_group_kernel(cons
   const double sl = exp(X);
   const double dm = __ldg(g->dpow + m);
   const double inv_vst = 1.0 / g->bs_vsqrt;
-  // fused leaves (B.node_sums): this block's 128 paths are one node of the reference tree at its
-  // leaf depth (n a power of two), so the two ordered 64-value leaf sums of each strike are
-  // formed here from a shared-memory row and 16 bytes per (contract, node) leave the kernel
-  // instead of 8 bytes per (contract, path)
-  const uint32_t vrow = smem_u32(smg) + kGThreads * kGCap * 20;
-  const bool fused = B.node_sums != nullptr;
 #pragma unroll 1
   for (int s = 0; s < g->count; ++s) {
     const ContractParams& q = B.cp[g->first + s];
@@ -2018,31 +2011,42 @@ __global__ void __launch_bounds__(kGThreads, QMCG_G_MINB) walk_group_kernel(cons
     intr = intr > 0.0 ? intr : 0.0;
     const double cm = intr > cont ? intr : cont;
     const double term_m = cm * dm;
-    const double v = best > term_m ? best : term_m;
-    if (B.store_values && pw < B.n) B.values[static_cast<int64_t>(g->first + s) * B.n + pw] = v;
-    if (fused) {
-      const int u = s % kGLeafQ;
-      sts_f64(vrow + (u * kGThreads + threadIdx.x) * 8, v);
-      if (u == kGLeafQ - 1 || s == g->count - 1) {  // a chunk of strikes is staged: their leaf sums
-        __syncthreads();
-        const int t = threadIdx.x;
-        double x = 0.0, x2 = 0.0;
-        if (t < 2 * (u + 1)) {  // (strike s - u + t / 2, half t % 2): 64 values in path order from 0.0
-          const uint32_t a = vrow + ((t >> 1) * kGThreads + (t & 1) * 64) * 8;
+    if (pw < B.n) B.values[static_cast<int64_t>(g->first + s) * B.n + pw] = best > term_m ? best : term_m;
+  }
+  // Fused leaves (B.node_sums; n a power of two): this block's 128 paths are one node of the
+  // reference tree at its leaf depth, split at 64 (pairwise_sum, path_engine.cpp:39-47). The
+  // block's value rows were just written (L2-resident, 1 KB per strike): warp 0 forms the two
+  // ordered 64-value leaf sums of 16 strikes at a time, one chain per lane (the other warps are
+  // done), writes 16 bytes per (contract, node) and discards the rows from L2 without write-back,
+  // so the per-path values never travel to DRAM and no second pass reads them.
+  if (B.node_sums) {
+    __syncthreads();  // every warp's value rows are written
+    if (threadIdx.x >= 32) return;
+    const int lane = threadIdx.x;
+    for (int s0 = 0; s0 < g->count; s0 += 16) {
+      const int s = s0 + (lane >> 1);
+      double x = 0.0, x2 = 0.0;
+      const double* row = nullptr;
+      if (s < g->count) {
+        row = B.values + static_cast<int64_t>(g->first + s) * B.n + static_cast<int64_t>(blockIdx.y) * kGThreads +
+              (lane & 1) * 64;
 #pragma unroll 8
-          for (int k = 0; k < 64; ++k) {
-            const double y = lds_f64(a + k * 8);
-            x = __dadd_rn(x, y);
-            x2 = __dadd_rn(x2, __dmul_rn(y, y));
-          }
+        for (int k = 0; k < 64; ++k) {
+          const double y = __ldcg(row + k);
+          x = __dadd_rn(x, y);
+          x2 = __dadd_rn(x2, __dmul_rn(y, y));
         }
-        const double y = __shfl_down_sync(kFull, x, 1), y2 = __shfl_down_sync(kFull, x2, 1);
-        if (t < 2 * (u + 1) && !(t & 1)) {  // the node splits at 64 (pairwise_sum): left + right
-          double* o = B.node_sums + (static_cast<int64_t>(g->first + s - u + (t >> 1)) * gridDim.y + blockIdx.y) * 2;
+      }
+      const double y = __shfl_down_sync(kFull, x, 1), y2 = __shfl_down_sync(kFull, x2, 1);
+      if (s < g->count) {
+        if (!(lane & 1)) {
+          double* o = B.node_sums + (static_cast<int64_t>(g->first + s) * gridDim.y + blockIdx.y) * 2;
           o[0] = __dadd_rn(x, y);
           o[1] = __dadd_rn(x2, y2);
         }
-        __syncthreads();  // the row is restaged by the next chunk
+        if (!B.store_values)  // 512 B = 4 lines of this half row, 128-byte aligned (n % 128 == 0)
+#pragma unroll
+          for (int l = 0; l < 4; ++l) asm volatile("discard.global.L2 [%0], 128;" ::"l"(row + l * 16) : "memory");
       }
     }
   }
@@ -2052,7 +2056,7 @@ cudaError_t launch_walk_group(const BatchParams& B, int kind, cudaStream_t s) {
   if (B.n_groups <= 0 || B.n <= 0) return cudaSuccess;
   const dim3 grid(static_cast<unsigned>(B.n_groups), static_cast<unsigned>((B.n + kGThreads - 1) / kGThreads));
   if (B.node_sums && (B.n % kGThreads != 0)) return cudaErrorInvalidValue;  // nodes must be whole blocks
-  const size_t smem = kGThreads * kGCap * 20 + (B.node_sums ? kGLeafQ * kGThreads * 8 : 0);
+  const size_t smem = kGThreads * kGCap * 20;
   auto kern = kind == 0 ? walk_group_kernel<0> : walk_group_kernel<1>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   if (e != cudaSuccess) return e;

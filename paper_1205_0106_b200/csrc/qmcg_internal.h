@@ -118,7 +118,8 @@ struct BatchParams {
   double* values;             // [count][n]
   const GroupParams* groups;      // grouped walk: one walk per (group, path)
   int32_t n_groups;
-  int32_t store_values;           // write every per-path value to `values` (else only rare flushes use it)
+  int32_t store_values;           // keep the per-path values in `values` (parity export); else a fused walk
+                                  // discards them from L2 once its leaf sums are formed
   double* node_sums;              // fused leaves: [count][n / 128][2] leaf-depth node sums (n % 128 == 0), or null
 };
 

@@ -43,7 +43,7 @@ EXPORTS = (
     "qmcg_last_window_count", "qmcg_price_american_nodes", "qmcg_simulate_batch", "qmcg_sweep_batch",
     "qmcg_backward_sweep", "qmcg_build_tables", "qmcg_import_tables", "qmcg_uniform_rows",
     "qmcg_create_multi", "qmcg_device_count", "qmcg_time_device_nodes", "qmcg_get_member_stream",
-    "qmcg_member_device", "qmcg_price_american_batch_values",
+    "qmcg_member_device", "qmcg_price_american_batch_values", "qmcg_create_default",
 )
 
 
