@@ -8,6 +8,8 @@
 #include "qmcg.h"
 #include "qmcg_internal.h"
 
+#include <nvtx3/nvToolsExt.h>
+
 #include <algorithm>
 #include <array>
 #include <chrono>
@@ -114,6 +116,15 @@ struct Trace {
                  std::chrono::duration<double, std::micro>(now - t0).count());
     last = now;
   }
+};
+
+// NVTX phase ranges (header-only NVTX 3: no-ops unless a profiler injects itself), named after
+// the kernels of DESIGN.md 3: K1 table builds, K2 pricing, K3 tree, group exchange, batches.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
 };
 
 uint64_t bits_of(double x) {
@@ -457,6 +468,7 @@ qmcg_status ensure_perms(qmcg_ctx* c, uint64_t seed, int64_t n, int64_t b, int64
   qmcg_status rs = reserve_table(c, seed, n, b, e, m, rebuild);
   if (rs) return rs;
   if (c->cache_dims >= m) return QMCG_OK;
+  NvtxRange nv("qmcg.K1.perm_build");
   const int64_t ld = qmcg::table_ld(e - b);
   const size_t copy_bytes = static_cast<size_t>(e - b) * sizeof(uint32_t);
   const bool full = (b == 0 && e == n);
@@ -587,6 +599,7 @@ qmcg_status map_err(uint32_t err) {
 // into d_sums[slot*2 .. slot*2+1]. Tables must be resident.
 // Launch the pricing kernel over paths [b, e) (tables resident) into d_values.
 qmcg_status enqueue_values(qmcg_ctx* c, CallPlan& plan, int64_t b, int64_t e, cudaEvent_t after_kernel = nullptr) {
+  NvtxRange nv("qmcg.K2.price_kernel");
   const int64_t cnt = e - b;
   QMCG_CUDA(c->d_values.reserve(static_cast<size_t>(cnt)));
   QMCG_CUDA(c->d_red.reserve(qmcg::reduce_scratch_doubles(cnt)));
@@ -974,6 +987,7 @@ size_t table_bytes_allowed(qmcg_ctx* c, int64_t n, int64_t cols, bool full) {
 // The pairwise sums of the `count` consecutive tree nodes [node0, node0 + count) at `depth`
 // from the per-path values of paths [b, ...) in d_values, into d_sums[2k, 2k + 1].
 qmcg_status enqueue_node_sums(qmcg_ctx* c, int64_t n, int depth, int64_t node0, int64_t count, int64_t b) {
+  NvtxRange nv("qmcg.K3.pairwise_tree");
   for (int64_t k = 0; k < count; ++k) {
     int64_t off, size;
     tree_node(n, depth, node0 + k, off, size);
@@ -992,6 +1006,7 @@ qmcg_status enqueue_node_sums(qmcg_ctx* c, int64_t n, int depth, int64_t node0, 
 // best) in HBM to the next window. Results are identical to resident tables.
 qmcg_status enqueue_streamed(qmcg_ctx* c, CallPlan& plan, uint64_t seed, int64_t n, int64_t b, int64_t e,
                              size_t budget) {
+  NvtxRange nv("qmcg.streamed_windows");
   const int64_t cols = e - b, m = plan.P.m;
   const int64_t ld = qmcg::table_ld(cols);
   const size_t row_bytes = static_cast<size_t>(ld) * sizeof(uint32_t);
@@ -1241,6 +1256,7 @@ qmcg_status group_ensure_tables(qmcg_ctx* g, uint64_t seed, int64_t n, int64_t m
     d0 = std::min(d0, R[s].e > R[s].b ? (same ? c->cache_dims : 0) : m);
   }
   if (d0 >= m) return QMCG_OK;
+  NvtxRange nv("qmcg.group.sharded_table_build");
   for (size_t s = 0; s < M.size(); ++s) {
     if (R[s].e <= R[s].b) continue;
     DeviceGuard dg(M[s]->device);
@@ -1283,6 +1299,7 @@ qmcg_status group_ensure_tables(qmcg_ctx* g, uint64_t seed, int64_t n, int64_t m
 // walk state carried in HBM, as enqueue_streamed). Returns the node sums via enqueue_results.
 qmcg_status group_enqueue_streamed(qmcg_ctx* g, std::vector<CallPlan>& plans, uint64_t seed, int64_t n, int64_t m,
                                    int depth, const std::vector<MemberRange>& R) {
+  NvtxRange nv("qmcg.group.streamed_windows");
   const auto& M = g->members;
   const int G = static_cast<int>(M.size());
   int64_t W = (m + 7) / 8 * 8;
@@ -1614,6 +1631,7 @@ extern "C" {
 qmcg_status qmcg_price_american(qmcg_ctx* c, const qmcg_option_spec* spec, int64_t m, int64_t n, uint64_t seed,
                                 uint32_t flags, qmcg_pricing_result* out) {
   if (!c || !spec || !out) return fail(QMCG_INVALID_ARGUMENT, "qmcg_price_american: null argument");
+  NvtxRange nv("qmcg_price_american");
   const auto t0 = std::chrono::steady_clock::now();
   std::lock_guard<std::mutex> lock(c->mu);
   DeviceGuard g(c->device);
@@ -1758,6 +1776,7 @@ qmcg_status qmcg_price_american_batch_values(qmcg_ctx* c, const qmcg_option_spec
 static qmcg_status batch_impl(qmcg_ctx* c, const qmcg_option_spec* specs, int64_t n_specs, int64_t m, int64_t n,
                               uint64_t seed, uint32_t flags, qmcg_pricing_result* out, double* values_host) {
   if (!c || !specs || !out || n_specs < 0) return fail(QMCG_INVALID_ARGUMENT, "qmcg_price_american_batch: bad argument");
+  NvtxRange nv("qmcg_price_american_batch");
   if (flags & QMCG_FLAG_FP32)
     return fail(QMCG_UNSUPPORTED, "qmcg_price_american_batch: QMCG_FLAG_FP32 is not supported (the batch walk is FP64)");
   const auto t0 = std::chrono::steady_clock::now();
@@ -1886,7 +1905,11 @@ static qmcg_status batch_impl(qmcg_ctx* c, const qmcg_option_spec* specs, int64_
       QMCG_CUDA(c->d_bsums[k].reserve(2 * cnt));
       // n a power of two >= 128: every leaf-depth node of the reference tree is one 128-path block
       // of the walk, which then writes the node sums itself (no per-path values round trip)
-      const bool fused = n >= 128 && (n & (n - 1)) == 0;
+      static const bool no_fuse = [] {  // A/B knob (tools): QMCG_NO_FUSED_LEAVES=1 keeps the leaves kernel
+        const char* e = std::getenv("QMCG_NO_FUSED_LEAVES");
+        return e && *e && *e != '0';
+      }();
+      const bool fused = !no_fuse && n >= 128 && (n & (n - 1)) == 0;
       const int64_t nodes = n / 128;
       if (fused) QMCG_CUDA(c->d_bnodes[k].reserve(cnt * static_cast<size_t>(2 * nodes)));
       qmcg::BatchParams B{c->d_z.ptr, n, n, static_cast<int32_t>(m), static_cast<int32_t>(cnt), c->d_cparams[k].ptr,
