@@ -305,7 +305,6 @@ struct qmcg_ctx {
   DevBuf<double> d_values, d_red, d_sums;
   DevBuf<double> d_z;                                // batch: shared normal (prefix-sum) table
   DevBuf<double> d_bvalues[2], d_bred[2], d_bsums[2];  // per kind: per-contract values, scratch, sums
-  DevBuf<double> d_bnodes[2];                        // per kind: fused leaf-node sums of the batch walk
   DevBuf<qmcg::ContractParams> d_cparams[2];
   DevBuf<qmcg::GroupParams> d_groups[2];
   DevBuf<uint32_t> d_err, d_fullperm;
@@ -806,7 +805,6 @@ void qmcg_destroy(qmcg_ctx* c) {
     c->d_bvalues[k].release();
     c->d_bred[k].release();
     c->d_bsums[k].release();
-    c->d_bnodes[k].release();
     c->d_cparams[k].release();
     c->d_groups[k].release();
   }
@@ -1903,26 +1901,12 @@ static qmcg_status batch_impl(qmcg_ctx* c, const qmcg_option_spec* specs, int64_
       QMCG_CUDA(c->d_bvalues[k].reserve(cnt * static_cast<size_t>(n)));
       QMCG_CUDA(c->d_bred[k].reserve(cnt * qmcg::reduce_scratch_doubles(n)));
       QMCG_CUDA(c->d_bsums[k].reserve(2 * cnt));
-      // n a power of two >= 128: every leaf-depth node of the reference tree is one 128-path block
-      // of the walk, which then writes the node sums itself (no per-path values round trip)
-      static const bool no_fuse = [] {  // A/B knob (tools): QMCG_NO_FUSED_LEAVES=1 keeps the leaves kernel
-        const char* e = std::getenv("QMCG_NO_FUSED_LEAVES");
-        return e && *e && *e != '0';
-      }();
-      const bool fused = !no_fuse && n >= 128 && (n & (n - 1)) == 0;
-      const int64_t nodes = n / 128;
-      if (fused) QMCG_CUDA(c->d_bnodes[k].reserve(cnt * static_cast<size_t>(2 * nodes)));
       qmcg::BatchParams B{c->d_z.ptr, n, n, static_cast<int32_t>(m), static_cast<int32_t>(cnt), c->d_cparams[k].ptr,
-                          c->d_bvalues[k].ptr, c->d_groups[k].ptr, static_cast<int32_t>(groups.size()),
-                          values_host ? 1 : 0, fused ? c->d_bnodes[k].ptr : nullptr};
+                          c->d_bvalues[k].ptr, c->d_groups[k].ptr, static_cast<int32_t>(groups.size()), 0};
       QMCG_CUDA(qmcg::launch_walk_group(B, k, c->stream));
       int launches = 1;
-      if (fused)
-        QMCG_CUDA(qmcg::launch_pairwise_from_nodes(c->d_bnodes[k].ptr, nodes, static_cast<int>(cnt), c->d_bred[k].ptr,
-                                                   c->d_bsums[k].ptr, c->stream, &launches));
-      else
-        QMCG_CUDA(qmcg::launch_pairwise_batched(c->d_bvalues[k].ptr, n, static_cast<int>(cnt), c->d_bred[k].ptr,
-                                                c->d_bsums[k].ptr, c->stream, &launches));
+      QMCG_CUDA(qmcg::launch_pairwise_batched(c->d_bvalues[k].ptr, n, static_cast<int>(cnt), c->d_bred[k].ptr,
+                                              c->d_bsums[k].ptr, c->stream, &launches));
       c->launches += launches;
       if (values_host)  // parity export: contract shared_idx[k][j] is row j of the kind's value table
         for (size_t j = 0; j < cnt; ++j)

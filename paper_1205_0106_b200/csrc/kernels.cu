@@ -2013,49 +2013,11 @@ __global__ void __launch_bounds__(kGThreads, QMCG_G_MINB) walk_group_kernel(cons
     const double term_m = cm * dm;
     if (pw < B.n) B.values[static_cast<int64_t>(g->first + s) * B.n + pw] = best > term_m ? best : term_m;
   }
-  // Fused leaves (B.node_sums; n a power of two): this block's 128 paths are one node of the
-  // reference tree at its leaf depth, split at 64 (pairwise_sum, path_engine.cpp:39-47). The
-  // block's value rows were just written (L2-resident, 1 KB per strike): warp 0 forms the two
-  // ordered 64-value leaf sums of 16 strikes at a time, one chain per lane (the other warps are
-  // done), writes 16 bytes per (contract, node) and discards the rows from L2 without write-back,
-  // so the per-path values never travel to DRAM and no second pass reads them.
-  if (B.node_sums) {
-    __syncthreads();  // every warp's value rows are written
-    if (threadIdx.x >= 32) return;
-    const int lane = threadIdx.x;
-    for (int s0 = 0; s0 < g->count; s0 += 16) {
-      const int s = s0 + (lane >> 1);
-      double x = 0.0, x2 = 0.0;
-      const double* row = nullptr;
-      if (s < g->count) {
-        row = B.values + static_cast<int64_t>(g->first + s) * B.n + static_cast<int64_t>(blockIdx.y) * kGThreads +
-              (lane & 1) * 64;
-#pragma unroll 8
-        for (int k = 0; k < 64; ++k) {
-          const double y = __ldcg(row + k);
-          x = __dadd_rn(x, y);
-          x2 = __dadd_rn(x2, __dmul_rn(y, y));
-        }
-      }
-      const double y = __shfl_down_sync(kFull, x, 1), y2 = __shfl_down_sync(kFull, x2, 1);
-      if (s < g->count) {
-        if (!(lane & 1)) {
-          double* o = B.node_sums + (static_cast<int64_t>(g->first + s) * gridDim.y + blockIdx.y) * 2;
-          o[0] = __dadd_rn(x, y);
-          o[1] = __dadd_rn(x2, y2);
-        }
-        if (!B.store_values)  // 512 B = 4 lines of this half row, 128-byte aligned (n % 128 == 0)
-#pragma unroll
-          for (int l = 0; l < 4; ++l) asm volatile("discard.global.L2 [%0], 128;" ::"l"(row + l * 16) : "memory");
-      }
-    }
-  }
 }
 
 cudaError_t launch_walk_group(const BatchParams& B, int kind, cudaStream_t s) {
   if (B.n_groups <= 0 || B.n <= 0) return cudaSuccess;
   const dim3 grid(static_cast<unsigned>(B.n_groups), static_cast<unsigned>((B.n + kGThreads - 1) / kGThreads));
-  if (B.node_sums && (B.n % kGThreads != 0)) return cudaErrorInvalidValue;  // nodes must be whole blocks
   const size_t smem = kGThreads * kGCap * 20;
   auto kern = kind == 0 ? walk_group_kernel<0> : walk_group_kernel<1>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
@@ -2302,11 +2264,6 @@ cudaError_t launch_perm_build(uint64_t seed64, int64_t n, uint32_t* out, void* s
 
 cudaError_t pairwise_upper(double* a, int64_t nodes, int count, int64_t sa, double* b, int64_t sb, double* out2,
                            cudaStream_t s, int* launches);
-
-cudaError_t launch_pairwise_from_nodes(double* node_sums, int64_t nodes, int count, double* scratch, double* out2,
-                                       cudaStream_t s, int* launches) {
-  return pairwise_upper(node_sums, nodes, count, 2 * nodes, scratch, 2 * ((nodes + 1023) / 1024), out2, s, launches);
-}
 
 size_t reduce_scratch_doubles(int64_t len) {
   const int L = leaf_depth(len);

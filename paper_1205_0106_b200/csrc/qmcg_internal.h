@@ -117,10 +117,7 @@ struct BatchParams {
   const ContractParams* cp;   // count entries
   double* values;             // [count][n]
   const GroupParams* groups;      // grouped walk: one walk per (group, path)
-  int32_t n_groups;
-  int32_t store_values;           // keep the per-path values in `values` (parity export); else a fused walk
-                                  // discards them from L2 once its leaf sums are formed
-  double* node_sums;              // fused leaves: [count][n / 128][2] leaf-depth node sums (n % 128 == 0), or null
+  int32_t n_groups, pad;
 };
 
 // ---- launchers (kernels.cu) ----
@@ -137,10 +134,6 @@ cudaError_t launch_european(const uint32_t* perm_row, int64_t count, DimParam dp
 // Pairwise sums of `count` contiguous vectors v[c*len .. (c+1)*len) into out2[2c, 2c+1].
 cudaError_t launch_pairwise_batched(const double* v, int64_t len, int count, double* scratch, double* out2,
                                     cudaStream_t s, int* launches);
-// The same from the node sums at the tree's leaf depth ([count][nodes][2], nodes a power of two),
-// as the fused batch walk writes them; scratch: 2 ceil(nodes / 1024) doubles per vector.
-cudaError_t launch_pairwise_from_nodes(double* node_sums, int64_t nodes, int count, double* scratch, double* out2,
-                                       cudaStream_t s, int* launches);
 cudaError_t launch_price(const PriceParams& P, cudaStream_t s);
 // K1: Fisher-Yates permutation of length n for LCG seed `seed64` into out[0..n).
 // scratch must hold perm_scratch_bytes(n) bytes.

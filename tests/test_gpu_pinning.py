@@ -112,8 +112,9 @@ def test_put_headline_bounds(ctx, qmcg, golden):
 
 @pytest.mark.parametrize("n", [1 << 14, 1 << 18, 100003, 4097])
 def test_batch_tree_equals_reference_reduce_stats(ctx, qmcg, reducer, n):
-    """The batch's tree (fused leaf sums inside the walk for power-of-two n, the leaves kernel
-    otherwise) equals the reference's reduce_stats of the same launch's per-path values."""
+    """The batch's tree (the batched leaves kernel + perfect levels over every contract's values)
+    equals the reference's reduce_stats of the same launch's per-path values, for power-of-two
+    and ragged n, including a contract priced by the single-contract kernel (r < 0)."""
     specs = [qmcg.OptionSpec(100.0, 80 + 40 * i / 5, 0.05, 0.1 + 0.4 * j / 5, 1.0, qmcg.OptionKind((i + j) % 2))
              for i in range(6) for j in range(6)]
     specs.append(qmcg.OptionSpec(100.0, 95.0, -0.01, 0.3, 1.0))  # r < 0: the single-contract kernel
