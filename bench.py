@@ -316,6 +316,15 @@ def main():
         tm = DeviceTimer()
         t0 = time.perf_counter()
         tm.start()
+        sharded5 = False
+        if mode == "ranks":
+            # dims built once each (rank d mod N), column slices exchanged a chunk at a time, when the
+            # rank's slice of all 365 tables fits (N >= 4: <= 98 GB); else every rank streams windows
+            b5, e5 = distributed.rank_columns(n5, world, rank)
+            free_b, _ = torch.cuda.mem_get_info(device)
+            sharded5 = max_over_ranks(float((e5 - b5 + 64) * 4 * m5 > 0.85 * free_b))[0] == 0.0
+            if sharded5:
+                distributed.warm_tables_sharded(ctx, n5, SEED, m5)
         p5, se5 = price(call, m5, n5, fp32=True)
         ms5 = tm.stop()
         w5 = time.perf_counter() - t0
@@ -327,6 +336,8 @@ def main():
                           + (f", dims built sharded over {n_gpus} devices" if n_gpus > 1 else ""),
               "value": n5 * m5 / (ms5 * 1e-3), "unit": "path-steps/s", "ms_per_option": ms5,
               "e2e_ms_per_option": 1e3 * w5, "date_windows_member0": windows,
+              "k1": ("dimension-sharded over the devices" if (mode == "group" or sharded5) else
+                     "every table built on this device" if n_gpus == 1 else "replicated per rank (slice > HBM)"),
               "tables": "streamed date windows" if windows > 1 else "resident", "price": p5, "std_error": se5}
         ctx.clear_cache()
 

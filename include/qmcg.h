@@ -159,6 +159,14 @@ qmcg_status qmcg_build_tables(qmcg_ctx* ctx, int64_t n_paths, uint64_t seed, int
                               int64_t dim_stride, int64_t count, uint32_t* out_dev, int64_t ld);
 qmcg_status qmcg_import_tables(qmcg_ctx* ctx, int64_t n_paths, uint64_t seed, int64_t col_begin,
                                int64_t col_end, int64_t dims, const uint32_t* src_dev, int64_t src_ld);
+/* The same row block by row block: rows [row_begin, row_begin + row_count) of the slice of dims
+ * [0, dims) (src_dev holds row_count rows, stride src_ld). row_begin = 0 starts a fresh slice
+ * table sized for `dims` rows; each later call continues where the previous one stopped, so a
+ * rank can exchange and install the tables a chunk of dims at a time (config 5: 1 GiB per dim).
+ * Pricing of up to row_begin + row_count dates is warm after each call. */
+qmcg_status qmcg_import_rows(qmcg_ctx* ctx, int64_t n_paths, uint64_t seed, int64_t col_begin,
+                             int64_t col_end, int64_t dims, int64_t row_begin, int64_t row_count,
+                             const uint32_t* src_dev, int64_t src_ld);
 /* Cap the bytes the permutation tables may occupy (0 = whatever free device
  * memory allows). A pricing whose tables exceed it runs in date windows
  * ("streamed tables": each window's rows are built, walked, and replaced,
@@ -230,6 +238,10 @@ qmcg_status qmcg_time_device_nodes(qmcg_ctx* ctx, const qmcg_option_spec* spec, 
 /* Device time (ms) of rebuilding the permutation tables for dims [0, dims). */
 qmcg_status qmcg_time_perm_build(qmcg_ctx* ctx, int64_t n_paths, uint64_t seed, int64_t dims,
                                  double* ms);
+/* Out-of-bounds write check (the process must run with QMCG_CANARY=1 from its first allocation):
+ * every device buffer of every context is bracketed by 4 KB guard regions; this verifies them
+ * all and names the first clobbered one. QMCG_UNSUPPORTED without QMCG_CANARY=1. */
+qmcg_status qmcg_check_canaries(void);
 /* Number of kernels the last qmcg_price_american* call launched. */
 int64_t qmcg_last_launch_count(qmcg_ctx* ctx);
 /* The context's CUDA stream (a cudaStream_t) so a caller can record its own

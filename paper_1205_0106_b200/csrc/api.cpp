@@ -262,21 +262,81 @@ void build_dim_tables(int64_t n, int64_t m, DimTables& T) {
   T.m = m;
 }
 
+// Device allocations of the context. With QMCG_CANARY=1 in the environment (the out-of-bounds
+// write check; compute-sanitizer is closed on this pool) every allocation is bracketed by 4 KB
+// guard regions filled with 0xA5, registered, and qmcg_check_canaries() verifies them after the
+// kernels ran: any K1-K4 write past either end of a buffer (the permutation tables, values,
+// scratch, walk state) shows up as a clobbered guard.
+constexpr size_t kGuard = 4096;
+struct Guarded {
+  char* base;
+  size_t bytes;
+  int device;
+};
+std::mutex g_alloc_mu;
+std::vector<std::pair<void*, Guarded>>& guarded_allocs() {
+  static std::vector<std::pair<void*, Guarded>> v;
+  return v;
+}
+bool canary_mode() {
+  static const bool on = [] {
+    const char* e = std::getenv("QMCG_CANARY");
+    return e && *e && *e != '0';
+  }();
+  return on;
+}
+
+cudaError_t dev_alloc(void** p, size_t bytes) {
+  if (!canary_mode()) return cudaMalloc(p, bytes);
+  char* base = nullptr;
+  cudaError_t e = cudaMalloc(&base, bytes + 2 * kGuard);
+  if (e != cudaSuccess) return e;
+  e = cudaMemset(base, 0xA5, kGuard);
+  if (e == cudaSuccess) e = cudaMemset(base + kGuard + bytes, 0xA5, kGuard);
+  if (e != cudaSuccess) {
+    cudaFree(base);
+    return e;
+  }
+  int dev = 0;
+  cudaGetDevice(&dev);
+  *p = base + kGuard;
+  std::lock_guard<std::mutex> lock(g_alloc_mu);
+  guarded_allocs().push_back({*p, Guarded{base, bytes, dev}});
+  return cudaSuccess;
+}
+
+void dev_free(void* p) {
+  if (!p) return;
+  if (!canary_mode()) {
+    cudaFree(p);
+    return;
+  }
+  std::lock_guard<std::mutex> lock(g_alloc_mu);
+  auto& v = guarded_allocs();
+  for (size_t i = 0; i < v.size(); ++i)
+    if (v[i].first == p) {
+      cudaFree(v[i].second.base);
+      v.erase(v.begin() + static_cast<std::ptrdiff_t>(i));
+      return;
+    }
+  cudaFree(p);
+}
+
 template <class T>
 struct DevBuf {
   T* ptr = nullptr;
   size_t cap = 0;  // elements
   cudaError_t reserve(size_t count) {
     if (count <= cap) return cudaSuccess;
-    if (ptr) cudaFree(ptr);
+    dev_free(ptr);
     ptr = nullptr;
     cap = 0;
-    cudaError_t e = cudaMalloc(&ptr, std::max<size_t>(count, 1) * sizeof(T));
+    cudaError_t e = dev_alloc(reinterpret_cast<void**>(&ptr), std::max<size_t>(count, 1) * sizeof(T));
     if (e == cudaSuccess) cap = count;
     return e;
   }
   void release() {
-    if (ptr) cudaFree(ptr);
+    dev_free(ptr);
     ptr = nullptr;
     cap = 0;
   }
@@ -334,7 +394,7 @@ struct qmcg_ctx {
 namespace {
 
 void drop_cache(qmcg_ctx* c) {
-  if (c->table) cudaFree(c->table);
+  dev_free(c->table);
   c->table = nullptr;
   c->table_rows_cap = 0;
   c->cache_dims = 0;
@@ -436,7 +496,7 @@ qmcg_status reserve_table(qmcg_ctx* c, uint64_t seed, int64_t n, int64_t b, int6
   const size_t row_bytes = static_cast<size_t>(ld) * sizeof(uint32_t);
   if (static_cast<size_t>(m) > c->table_rows_cap) {
     uint32_t* nt = nullptr;
-    cudaError_t err = cudaMalloc(&nt, row_bytes * static_cast<size_t>(m) + qmcg::kTablePad * sizeof(uint32_t));
+    cudaError_t err = dev_alloc(reinterpret_cast<void**>(&nt), row_bytes * static_cast<size_t>(m) + qmcg::kTablePad * sizeof(uint32_t));
     if (err != cudaSuccess) {
       cudaGetLastError();
       char msg[256];
@@ -451,7 +511,7 @@ qmcg_status reserve_table(qmcg_ctx* c, uint64_t seed, int64_t n, int64_t b, int6
       QMCG_CUDA(cudaMemcpyAsync(nt, c->table, row_bytes * static_cast<size_t>(c->cache_dims),
                                 cudaMemcpyDeviceToDevice, c->stream));
     QMCG_CUDA(cudaStreamSynchronize(c->stream));
-    if (c->table) cudaFree(c->table);
+    dev_free(c->table);
     c->table = nt;
     c->table_rows_cap = static_cast<size_t>(m);
   }
@@ -779,6 +839,28 @@ qmcg_status qmcg_create_default(qmcg_ctx** out) {
   return qmcg_create_multi(devs.data(), static_cast<int>(devs.size()), out);
 }
 
+qmcg_status qmcg_check_canaries(void) {
+  if (!canary_mode()) return fail(QMCG_UNSUPPORTED, "qmcg_check_canaries: set QMCG_CANARY=1 before the first allocation");
+  std::lock_guard<std::mutex> lock(g_alloc_mu);
+  std::vector<unsigned char> h(kGuard);
+  for (const auto& a : guarded_allocs()) {
+    DeviceGuard g(a.second.device);
+    QMCG_CUDA(cudaDeviceSynchronize());
+    for (int side = 0; side < 2; ++side) {
+      const char* src = side == 0 ? a.second.base : a.second.base + kGuard + a.second.bytes;
+      QMCG_CUDA(cudaMemcpy(h.data(), src, kGuard, cudaMemcpyDeviceToHost));
+      for (size_t i = 0; i < kGuard; ++i)
+        if (h[i] != 0xA5) {
+          char msg[192];
+          std::snprintf(msg, sizeof msg, "qmcg_check_canaries: guard %s a %zu-byte buffer on device %d clobbered at +%zu",
+                        side == 0 ? "before" : "after", a.second.bytes, a.second.device, i);
+          return fail(QMCG_CUDA_ERROR, msg);
+        }
+    }
+  }
+  return QMCG_OK;
+}
+
 int qmcg_device_count(qmcg_ctx* c) { return !c ? 0 : c->members.empty() ? 1 : static_cast<int>(c->members.size()); }
 
 void qmcg_destroy(qmcg_ctx* c) {
@@ -921,7 +1003,7 @@ qmcg_status qmcg_import_tables(qmcg_ctx* c, int64_t n, uint64_t seed, int64_t co
   const int64_t ld = qmcg::table_ld(cols);
   const size_t row_bytes = static_cast<size_t>(ld) * sizeof(uint32_t);
   uint32_t* nt = nullptr;
-  if (cudaMalloc(&nt, row_bytes * static_cast<size_t>(dims) + qmcg::kTablePad * sizeof(uint32_t)) != cudaSuccess) {
+  if (dev_alloc(reinterpret_cast<void**>(&nt), row_bytes * static_cast<size_t>(dims) + qmcg::kTablePad * sizeof(uint32_t)) != cudaSuccess) {
     cudaGetLastError();
     return fail(QMCG_OUT_OF_MEMORY, "qmcg_import_tables: tables do not fit in device memory");
   }
@@ -936,6 +1018,34 @@ qmcg_status qmcg_import_tables(qmcg_ctx* c, int64_t n, uint64_t seed, int64_t co
   c->col_begin = col_begin;
   c->col_end = col_end;
   c->cache_dims = dims;
+  return QMCG_OK;
+}
+
+qmcg_status qmcg_import_rows(qmcg_ctx* c, int64_t n, uint64_t seed, int64_t col_begin, int64_t col_end, int64_t dims,
+                             int64_t row_begin, int64_t row_count, const uint32_t* src_dev, int64_t src_ld) {
+  if (!c || !src_dev) return fail(QMCG_INVALID_ARGUMENT, "qmcg_import_rows: null argument");
+  if (!c->members.empty())
+    return fail(QMCG_UNSUPPORTED, "qmcg_import_rows: a per-device call (use a single-device context per rank)");
+  const int64_t cols = col_end - col_begin;
+  if (n < 1 || static_cast<uint64_t>(n) > 0xffffffffULL || col_begin < 0 || cols < 1 || col_end > n || dims < 1 ||
+      row_begin < 0 || row_count < 1 || row_begin + row_count > dims || src_ld < cols)
+    return fail(QMCG_INVALID_ARGUMENT, "qmcg_import_rows: bad size");
+  std::lock_guard<std::mutex> lock(c->mu);
+  DeviceGuard g(c->device);
+  if (row_begin == 0) {
+    qmcg_status st = reserve_table(c, seed, n, col_begin, col_end, dims, true);  // a fresh slice table
+    if (st) return st;
+  } else if (c->cache_n != n || c->cache_seed != seed || c->col_begin != col_begin || c->col_end != col_end ||
+             c->cache_dims != row_begin || c->table_rows_cap < static_cast<size_t>(dims)) {
+    return fail(QMCG_INVALID_ARGUMENT, "qmcg_import_rows: rows must continue the slice imported so far");
+  }
+  const int64_t ld = qmcg::table_ld(cols);
+  QMCG_CUDA(cudaMemcpy2DAsync(c->table + static_cast<size_t>(row_begin) * static_cast<size_t>(ld),
+                              static_cast<size_t>(ld) * sizeof(uint32_t), src_dev,
+                              static_cast<size_t>(src_ld) * sizeof(uint32_t), static_cast<size_t>(cols) * sizeof(uint32_t),
+                              static_cast<size_t>(row_count), cudaMemcpyDeviceToDevice, c->stream));
+  QMCG_CUDA(cudaStreamSynchronize(c->stream));
+  c->cache_dims = row_begin + row_count;
   return QMCG_OK;
 }
 
@@ -1014,7 +1124,7 @@ qmcg_status enqueue_streamed(qmcg_ctx* c, CallPlan& plan, uint64_t seed, int64_t
   W = std::min<int64_t>(W, (m + 7) / 8 * 8);
   drop_cache(c);
   uint32_t* nt = nullptr;
-  if (cudaMalloc(&nt, row_bytes * static_cast<size_t>(W) + qmcg::kTablePad * sizeof(uint32_t)) != cudaSuccess) {
+  if (dev_alloc(reinterpret_cast<void**>(&nt), row_bytes * static_cast<size_t>(W) + qmcg::kTablePad * sizeof(uint32_t)) != cudaSuccess) {
     cudaGetLastError();
     return fail(QMCG_OUT_OF_MEMORY, "price_american: permutation window does not fit in device memory");
   }
@@ -1324,7 +1434,7 @@ qmcg_status group_enqueue_streamed(qmcg_ctx* g, std::vector<CallPlan>& plans, ui
     const int64_t cols = R[s].e - R[s].b;
     const int64_t ld = qmcg::table_ld(cols);
     uint32_t* nt = nullptr;
-    if (cudaMalloc(&nt, static_cast<size_t>(ld) * 4 * static_cast<size_t>(W) + qmcg::kTablePad * 4) != cudaSuccess) {
+    if (dev_alloc(reinterpret_cast<void**>(&nt), static_cast<size_t>(ld) * 4 * static_cast<size_t>(W) + qmcg::kTablePad * 4) != cudaSuccess) {
       cudaGetLastError();
       return fail(QMCG_OUT_OF_MEMORY, "price_american: permutation window does not fit in device memory");
     }

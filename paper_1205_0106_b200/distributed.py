@@ -147,12 +147,16 @@ def rank_columns(n_paths: int, world: int, rank: int) -> Tuple[int, int]:
 
 def warm_tables_sharded(ctx: Optional["qmcg.Context"], n_paths: int, seed: int, dims: int, *, group=None,
                         build_fn: Optional[Callable] = None, import_fn: Optional[Callable] = None,
-                        device=None) -> None:
+                        device=None, tables_per_chunk: Optional[int] = None) -> None:
     """Cold table build over the ranks of `group`: the permutation table of dim d
     is built (full n) by rank d mod G only, then an all-to-all sends each rank its column slice of
     every table, which it installs in its context -- G times less K1 work than every rank
-    building every table. Afterwards price_american_sharded on the same (n_paths, seed) is warm.
-    build_fn(k_dims, dim_begin, stride, buf) / import_fn(b, e, table) replace the GPU calls (tests)."""
+    building every table (the loop replaced is proj/src/quasi_rng.cpp:91-93). The dims go in
+    chunks of G * tables_per_chunk (each rank builds tables_per_chunk full tables per chunk, ~1 GiB
+    of scratch by default), so config 5 (2^28 paths x 365 dates, a 1 GiB table per dim) needs a
+    few GiB per rank besides its slice. Afterwards price_american_sharded on the same
+    (n_paths, seed) is warm. build_fn(k_dims, dim_begin, stride, buf) /
+    import_fn(b, e, row_begin, rows, dims) replace the GPU calls (tests)."""
     import torch
     import torch.distributed as dist
 
@@ -162,44 +166,50 @@ def warm_tables_sharded(ctx: Optional["qmcg.Context"], n_paths: int, seed: int, 
     comm = torch.device("cuda", torch.cuda.current_device()) if backend == "nccl" else torch.device("cpu")
     if device is None:  # where K1 writes: the GPU when the context builds, else the collective's device
         device = torch.device("cuda", torch.cuda.current_device()) if build_fn is None else comm
+    if tables_per_chunk is None:
+        tables_per_chunk = max(1, min(32, (1 << 28) // max(1, n_paths)))
     cols = [rank_columns(n_paths, world, r) for r in range(world)]
-    my_dims = list(range(rank, dims, world))
-    k = len(my_dims)
-    buf = torch.empty((max(k, 1), n_paths), dtype=torch.int32, device=device)  # uint32 bit patterns
-    if k:
-        if build_fn is not None:
-            build_fn(k, rank, world, buf)
-        else:
-            # the context writes `buf` on its own (non-blocking) stream: torch's stream must be idle
-            # first (the allocator may hand out memory still in use by queued torch work); the
-            # call returns after its stream has synchronised, so later torch work sees the rows
-            _sync_torch_stream(buf)
-            ctx.build_tables(n_paths, seed, rank, world, k, buf.data_ptr(), n_paths)
     b_me, e_me = cols[rank]
     w_me = e_me - b_me
-    if world == 1:
-        table = buf[:dims]
-    else:
-        send = (torch.cat([buf[:k, b:e].reshape(-1) for (b, e) in cols]) if k else
-                torch.empty(0, dtype=torch.int32, device=device)).to(comm)
-        k_of = [len(range(r, dims, world)) for r in range(world)]
-        recv = torch.empty(sum(k_of) * w_me, dtype=torch.int32, device=comm)
-        dist.all_to_all_single(recv, send, output_split_sizes=[kk * w_me for kk in k_of],
-                               input_split_sizes=[k * (e - b) for (b, e) in cols], group=group)
-        table = torch.empty((dims, w_me), dtype=torch.int32, device=comm)
-        for r, piece in enumerate(recv.split([kk * w_me for kk in k_of])):
-            if k_of[r]:
-                table[r::world] = piece.view(k_of[r], w_me)
-    if import_fn is not None:
-        import_fn(b_me, e_me, table)
-    else:
-        if table.device.type != "cuda":
-            table = table.cuda()
-        table = table.contiguous()
-        # the all-to-all and the slice copies above are queued on torch's stream; the context
-        # copies from `table` on its own non-blocking stream, so wait for them to finish
-        _sync_torch_stream(table)
-        ctx.import_tables(n_paths, seed, b_me, e_me, dims, table.data_ptr(), table.stride(0))
+    span = world * tables_per_chunk
+    buf = torch.empty((tables_per_chunk, n_paths), dtype=torch.int32, device=device)  # uint32 bit patterns
+    for c0 in range(0, dims, span):
+        c1 = min(dims, c0 + span)
+        # dims of this chunk built by rank r: c0 + ((r - c0) mod G) + t G, t = 0, 1, ...
+        first = [c0 + (r - c0) % world for r in range(world)]
+        k_of = [len(range(first[r], c1, world)) for r in range(world)]
+        k = k_of[rank]
+        if k:
+            if build_fn is not None:
+                build_fn(k, first[rank], world, buf)
+            else:
+                # the context writes `buf` on its own (non-blocking) stream: torch's stream must be
+                # idle first (the allocator may hand out memory still in use by queued torch work);
+                # the call returns after its stream has synchronised, so later torch work sees the rows
+                _sync_torch_stream(buf)
+                ctx.build_tables(n_paths, seed, first[rank], world, k, buf.data_ptr(), n_paths)
+        if world == 1:
+            rows = buf[:k]
+        else:
+            send = (torch.cat([buf[:k, b:e].reshape(-1) for (b, e) in cols]) if k else
+                    torch.empty(0, dtype=torch.int32, device=device)).to(comm)
+            recv = torch.empty(sum(k_of) * w_me, dtype=torch.int32, device=comm)
+            dist.all_to_all_single(recv, send, output_split_sizes=[kk * w_me for kk in k_of],
+                                   input_split_sizes=[k * (e - b) for (b, e) in cols], group=group)
+            rows = torch.empty((c1 - c0, w_me), dtype=torch.int32, device=comm)
+            for r, piece in enumerate(recv.split([kk * w_me for kk in k_of])):
+                if k_of[r]:
+                    rows[first[r] - c0::world] = piece.view(k_of[r], w_me)
+        if import_fn is not None:
+            import_fn(b_me, e_me, c0, rows, dims)
+        else:
+            if rows.device.type != "cuda":
+                rows = rows.cuda()
+            rows = rows.contiguous()
+            # the all-to-all and the slice copies above are queued on torch's stream; the context
+            # copies from `rows` on its own non-blocking stream, so wait for them to finish
+            _sync_torch_stream(rows)
+            ctx.import_rows(n_paths, seed, b_me, e_me, dims, c0, c1 - c0, rows.data_ptr(), rows.stride(0))
 
 
 def _sync_torch_stream(t) -> None:

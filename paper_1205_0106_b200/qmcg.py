@@ -43,7 +43,8 @@ EXPORTS = (
     "qmcg_last_window_count", "qmcg_price_american_nodes", "qmcg_simulate_batch", "qmcg_sweep_batch",
     "qmcg_backward_sweep", "qmcg_build_tables", "qmcg_import_tables", "qmcg_uniform_rows",
     "qmcg_create_multi", "qmcg_device_count", "qmcg_time_device_nodes", "qmcg_get_member_stream",
-    "qmcg_member_device", "qmcg_price_american_batch_values", "qmcg_create_default",
+    "qmcg_member_device", "qmcg_price_american_batch_values", "qmcg_create_default", "qmcg_import_rows",
+    "qmcg_check_canaries",
 )
 
 
@@ -145,6 +146,7 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
         L.qmcg_set_table_budget.argtypes = [P, U64]
         L.qmcg_build_tables.argtypes = [P, I64, U64, I64, I64, I64, P, I64]
         L.qmcg_import_tables.argtypes = [P, I64, U64, I64, I64, I64, P, I64]
+        L.qmcg_import_rows.argtypes = [P, I64, U64, I64, I64, I64, I64, I64, P, I64]
         L.qmcg_simulate_batch.argtypes = [P, C.POINTER(_CSpec), I64, I64, U64, U32, C.c_int, P]
         L.qmcg_sweep_batch.argtypes = [P, C.POINTER(_CSpec), I64, I64, U64, U32, P, P]
         L.qmcg_backward_sweep.argtypes = [P, I64, C.POINTER(_CSpec), I64, U32, P, C.POINTER(I64)]
@@ -164,6 +166,7 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
         L.qmcg_get_member_stream.restype = P
         L.qmcg_member_device.argtypes = [P, C.c_int]
         L.qmcg_member_device.restype = C.c_int
+        L.qmcg_check_canaries.argtypes = []
         L.qmcg_last_launch_count.argtypes = [P]
         L.qmcg_last_launch_count.restype = I64
         L.qmcg_get_stream.argtypes = [P]
@@ -353,6 +356,12 @@ class Context:
         _check(self._lib.qmcg_import_tables(self._h, int(n_paths), int(seed), int(col_begin), int(col_end), int(dims),
                                             C.c_void_p(src_ptr), int(src_ld)))
 
+    def import_rows(self, n_paths: int, seed: int, col_begin: int, col_end: int, dims: int, row_begin: int,
+                    row_count: int, src_ptr: int, src_ld: int) -> None:
+        """Install rows [row_begin, +row_count) of the slice [col_begin, col_end) of dims [0, dims)."""
+        _check(self._lib.qmcg_import_rows(self._h, int(n_paths), int(seed), int(col_begin), int(col_end), int(dims),
+                                          int(row_begin), int(row_count), C.c_void_p(src_ptr), int(src_ld)))
+
     def set_table_budget(self, nbytes: int) -> None:
         """Cap the permutation-table bytes (0 = free device memory); larger pricings stream date windows."""
         _check(self._lib.qmcg_set_table_budget(self._h, int(nbytes)))
@@ -441,6 +450,11 @@ class Context:
         out = C.c_double()
         _check(self._lib.qmcg_fp64_peak(self._h, float(ms), C.byref(out)))
         return out.value
+
+
+def check_canaries() -> None:
+    """Verify the guard regions of every device buffer (process started with QMCG_CANARY=1)."""
+    _check(load_library().qmcg_check_canaries())
 
 
 def tree_node_range(n_paths: int, depth: int, node: int):

@@ -125,14 +125,17 @@ def _tables_worker(rank, world, port, n, dims, out):
             perm = O.permutation_indices(n, O.dimension_seed(42, d))[:n].astype(np.int64) + 1
             buf[j] = torch.from_numpy(perm.astype(np.uint32).view(np.int32))
 
-    got = {}
+    got = {"rows": {}}
 
-    def imp(b, e, table):
+    def imp(b, e, row_begin, rows, total):
+        assert total == dims and row_begin == sum(len(v) for v in got["rows"].values())
         got["range"] = (b, e)
-        got["table"] = table.numpy().view(np.uint32).copy()
+        got["rows"][row_begin] = rows.numpy().view(np.uint32).copy()
 
-    distributed.warm_tables_sharded(None, n, 42, dims, build_fn=build, import_fn=imp)
-    out[rank] = (built, got["range"], got["table"])
+    # one table per rank per chunk: several chunks, the last one ragged
+    distributed.warm_tables_sharded(None, n, 42, dims, build_fn=build, import_fn=imp, tables_per_chunk=1)
+    table = np.concatenate([got["rows"][k] for k in sorted(got["rows"])])
+    out[rank] = (built, got["range"], table)
     dist.barrier()
     dist.destroy_process_group()
 
