@@ -461,10 +461,8 @@ qmcg_status build_rows_overlapped(qmcg_ctx* c, uint64_t seed, int64_t n, uint32_
   if (!c->ev_fork) QMCG_CUDA(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
   QMCG_CUDA(cudaEventRecord(c->ev_fork, c->stream));
   for (int l = 0; l + 1 < kK1Lanes; ++l) {
-    if (!c->side[l]) {
-      QMCG_CUDA(cudaStreamCreateWithFlags(&c->side[l], cudaStreamNonBlocking));
-      QMCG_CUDA(cudaEventCreateWithFlags(&c->ev_join[l], cudaEventDisableTiming));
-    }
+    if (!c->side[l]) QMCG_CUDA(cudaStreamCreateWithFlags(&c->side[l], cudaStreamNonBlocking));
+    if (!c->ev_join[l]) QMCG_CUDA(cudaEventCreateWithFlags(&c->ev_join[l], cudaEventDisableTiming));
     QMCG_CUDA(c->d_permscratch_side[l].reserve(need));
     QMCG_CUDA(cudaStreamWaitEvent(c->side[l], c->ev_fork, 0));
   }
@@ -1944,6 +1942,7 @@ static qmcg_status batch_impl(qmcg_ctx* c, const qmcg_option_spec* specs, int64_
                                 static_cast<size_t>(n) * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
   }
   std::vector<double> shared_sums[2];
+  bool tree_on_side = false;
   if (use_shared) {
     QMCG_CUDA(c->d_z.reserve(static_cast<size_t>(m + 8) * static_cast<size_t>(n)));  // + 8 prefetch rows
     PriceParams G = plans[static_cast<size_t>(shared_idx[0].empty() ? shared_idx[1][0] : shared_idx[0][0])].P;
@@ -2015,8 +2014,20 @@ static qmcg_status batch_impl(qmcg_ctx* c, const qmcg_option_spec* specs, int64_
                           c->d_bvalues[k].ptr, c->d_groups[k].ptr, static_cast<int32_t>(groups.size()), 0};
       QMCG_CUDA(qmcg::launch_walk_group(B, k, c->stream));
       int launches = 1;
+      // the calls' tree (HBM-bound leaves) runs on a side stream under the puts' walk (issue-bound)
+      cudaStream_t ts = c->stream;
+      if (k == 0 && !shared_idx[1].empty()) {
+        if (!c->side[0]) QMCG_CUDA(cudaStreamCreateWithFlags(&c->side[0], cudaStreamNonBlocking));
+        st = ensure_events(c);
+        if (st) return st;
+        QMCG_CUDA(cudaEventRecord(c->ev_built, c->stream));
+        QMCG_CUDA(cudaStreamWaitEvent(c->side[0], c->ev_built, 0));
+        ts = c->side[0];
+        tree_on_side = true;
+      }
       QMCG_CUDA(qmcg::launch_pairwise_batched(c->d_bvalues[k].ptr, n, static_cast<int>(cnt), c->d_bred[k].ptr,
-                                              c->d_bsums[k].ptr, c->stream, &launches));
+                                              c->d_bsums[k].ptr, ts, &launches));
+      if (ts != c->stream) QMCG_CUDA(cudaEventRecord(c->ev_priced, ts));
       c->launches += launches;
       if (values_host)  // parity export: contract shared_idx[k][j] is row j of the kind's value table
         for (size_t j = 0; j < cnt; ++j)
@@ -2026,6 +2037,7 @@ static qmcg_status batch_impl(qmcg_ctx* c, const qmcg_option_spec* specs, int64_
       shared_sums[k].resize(2 * cnt);  // read back with the other results (no sync between the kinds)
       tr.mark(k == 0 ? "calls enqueued" : "puts enqueued");
     }
+    if (tree_on_side) QMCG_CUDA(cudaStreamWaitEvent(c->stream, c->ev_priced, 0));
     for (int k = 0; k < 2; ++k)
       if (!shared_sums[k].empty())
         QMCG_CUDA(cudaMemcpyAsync(shared_sums[k].data(), c->d_bsums[k].ptr, shared_sums[k].size() * sizeof(double),
