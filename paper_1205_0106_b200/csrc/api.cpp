@@ -167,6 +167,11 @@ struct DimTables {
 
 void build_dim_tables(int64_t n, int64_t m, DimTables& T) {
   const auto& primes = primes_upto_count(m);
+  // test knob: QMCG_FORCE_WIDE=1 takes the 64-bit-magic digit division and the endpoint clamp on
+  // every dimension (the SLOW kernel instantiations, otherwise reached only near n = 2^32), so
+  // tests can check them bit for bit against the fast path at small n
+  const char* fw = std::getenv("QMCG_FORCE_WIDE");
+  const bool force_wide = fw && *fw && *fw != '0';
   T.dims.resize(static_cast<size_t>(m));
   T.sc.clear();
   T.nc.clear();
@@ -193,14 +198,14 @@ void build_dim_tables(int64_t n, int64_t m, DimTables& T) {
       scale *= inv_base;
     }
     // clamp can only trigger when p^-D approaches kEndpointEps
-    if (T.sc.back() < 2e-12) dp.flags |= qmcg::DIM_CLAMP;
+    if (T.sc.back() < 2e-12 || force_wide) dp.flags |= qmcg::DIM_CLAMP;
     // magic division, exact for x <= max_index (< 2^32)
     uint32_t sh = 0;
     while ((uint64_t{1} << (sh + 1)) < p) ++sh;  // sh = ceil(log2 p) - 1
     const unsigned __int128 two = static_cast<unsigned __int128>(1) << (32 + sh);
     const unsigned __int128 M = (two + p - 1) / p;
     const unsigned __int128 e = M * p - two;
-    if (M < (static_cast<unsigned __int128>(1) << 32) &&
+    if (!force_wide && M < (static_cast<unsigned __int128>(1) << 32) &&
         static_cast<unsigned __int128>(max_index) * e < two) {
       dp.magic = static_cast<uint32_t>(M);
       dp.shift = sh;
