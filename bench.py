@@ -495,13 +495,27 @@ def main():
     cpu = None
     if rank == 0 and n_gpus == 1 and not args.no_cpu_baseline:
         try:
-            cpu_full = cpu_reference(steps=1, warmup=1)
+            cpu_full = cpu_reference(steps=3, warmup=1)  # the reference's method: warm-up + median of 3
             cpu = {k: cpu_full[k] for k in ("value", "unit", "cores", "kind", "sample")}
             cpu["cpu_model"] = cpu_model()
-            one = cpu_reference(steps=1, warmup=0, n_paths=1 << 18, lanes=1)
+            one = cpu_reference(steps=3, warmup=0, n_paths=1 << 17, lanes=1)
             cpu["lanes1"] = {"value": one["value"], "unit": "path-steps/s", "cores": 1,
-                             "sample": f"{1 << 18} paths x {M_DATES} dates, one call, ExecPolicy lanes = 1",
+                             "sample": f"{1 << 17} paths x {M_DATES} dates, median of 3 calls, ExecPolicy lanes = 1",
                              "seconds_per_call": one["seconds_per_call"]}
+            if batch is not None:  # config 4 on the CPU = sampled contracts, per contract-path-step
+                import oracle
+                ref = oracle.Reference()
+                t0 = time.perf_counter()
+                for (i, j) in ((0, 0), (31, 31)):  # calls of the grid (the reference rejects puts)
+                    ref.price_american(100.0, 80 + 40 * i / 31, 0.05, 0.10 + 0.40 * j / 31, 1.0, 128, 1 << 18, SEED,
+                                       lanes=os.cpu_count() or 1)
+                per = (time.perf_counter() - t0) / 2
+                batch["cpu_baseline"] = {"value": (1 << 18) * 128 / per, "unit": "contract-path-steps/s",
+                                         "cores": os.cpu_count() or 1, "kind": "reference",
+                                         "sample": "2 calls of the grid (K=80, sigma=0.10; K=120, sigma=0.50) at "
+                                                   "2^18 x 128, one reference price_american each (tables built per "
+                                                   "call, as the reference does)",
+                                         "seconds_per_contract": per}
             if args.records:  # the reference's CSV schema: GPU row (lanes = -1) next to its CPU row
                 from paper_1205_0106_b200 import records as R
                 gpu_row = R.BenchmarkRecord(q.Method.AmericanUpperBound, n_paths, M_DATES, R.GPU_LANES, 4096,

@@ -20,6 +20,9 @@
 #include <limits>
 #include <mutex>
 #include <string>
+#include <condition_variable>
+#include <functional>
+#include <memory>
 #include <thread>
 #include <vector>
 
@@ -347,6 +350,54 @@ struct DevBuf {
   }
 };
 
+// One persistent host thread per device-group member: the warm group pricing enqueues and waits on
+// every member concurrently (a member's host work -- plan upload, tensor-map encode, launches -- is
+// ~50-80 us; done one member after another it would stagger the devices' start by that much each).
+class MemberWorker {
+ public:
+  MemberWorker() : th_([this] { loop(); }) {}
+  ~MemberWorker() {
+    {
+      std::lock_guard<std::mutex> lock(mu_);
+      stop_ = true;
+    }
+    cv_.notify_all();
+    th_.join();
+  }
+  void submit(std::function<void()> job) {
+    {
+      std::lock_guard<std::mutex> lock(mu_);
+      job_ = std::move(job);
+      busy_ = true;
+    }
+    cv_.notify_all();
+  }
+  void wait() {
+    std::unique_lock<std::mutex> lock(mu_);
+    cv_.wait(lock, [this] { return !busy_; });
+  }
+
+ private:
+  void loop() {
+    std::unique_lock<std::mutex> lock(mu_);
+    for (;;) {
+      cv_.wait(lock, [this] { return stop_ || busy_; });
+      if (stop_) return;
+      auto job = std::move(job_);
+      lock.unlock();
+      job();
+      lock.lock();
+      busy_ = false;
+      cv_.notify_all();
+    }
+  }
+  std::mutex mu_;
+  std::condition_variable cv_;
+  std::function<void()> job_;
+  bool busy_ = false, stop_ = false;
+  std::thread th_;
+};
+
 }  // namespace
 
 struct qmcg_ctx {
@@ -367,6 +418,7 @@ struct qmcg_ctx {
   DevBuf<uint64_t> d_m64;
   DevBuf<uint32_t> d_pairs;
   DevBuf<double> d_sc, d_nc, d_scnc, d_dpow;
+  std::vector<double> dpow_host;  // what d_dpow holds for single-contract calls (skips the re-upload)
   DevBuf<double> d_values, d_red, d_sums;
   DevBuf<double> d_z;                                // batch: shared normal (prefix-sum) table
   DevBuf<double> d_bvalues[2], d_bred[2], d_bsums[2];  // per kind: per-contract values, scratch, sums
@@ -386,6 +438,7 @@ struct qmcg_ctx {
   // device group (qmcg_create_multi): members[r] is the context of the r-th listed device; the
   // group handle owns them and dispatches (its own stream, cache and scratch stay unused)
   std::vector<qmcg_ctx*> members;
+  std::vector<std::unique_ptr<MemberWorker>> workers;       // one host thread per member (warm pricing)
   DevBuf<uint32_t> d_gtmp;                                  // builder rows of a group table build
   cudaEvent_t ev_built = nullptr, ev_priced = nullptr;      // cross-member ordering of group builds
   int64_t last_windows = 0;  // date windows of the last pricing (1 = resident tables)
@@ -643,9 +696,12 @@ qmcg_status upload_plan(qmcg_ctx* c, CallPlan& plan, int64_t n) {
   const int64_t m = plan.P.m;
   qmcg_status st = ensure_dim_tables(c, n, m);
   if (st) return st;
-  QMCG_CUDA(c->d_dpow.reserve(plan.dpow.size()));
-  QMCG_CUDA(cudaMemcpyAsync(c->d_dpow.ptr, plan.dpow.data(), plan.dpow.size() * sizeof(double),
-                            cudaMemcpyHostToDevice, c->stream));
+  if (c->dpow_host != plan.dpow) {  // the discount chain of the last single-contract call is still there
+    QMCG_CUDA(c->d_dpow.reserve(plan.dpow.size()));
+    QMCG_CUDA(cudaMemcpyAsync(c->d_dpow.ptr, plan.dpow.data(), plan.dpow.size() * sizeof(double),
+                              cudaMemcpyHostToDevice, c->stream));
+    c->dpow_host = plan.dpow;
+  }
   attach_dims(c, plan.P);
   plan.P.dpow = c->d_dpow.ptr;
   return QMCG_OK;
@@ -803,6 +859,7 @@ qmcg_status qmcg_create_multi(const int* dev_ids, int n_dev, qmcg_ctx** out) {
       return st;
     }
     g->members.push_back(c);
+    g->workers.push_back(std::make_unique<MemberWorker>());
   }
   // peer access between distinct listed devices (NVLink / NVSwitch); the slice copies also work
   // without it (staged by the driver), so failures here are not errors
@@ -1560,14 +1617,25 @@ qmcg_status group_price_nodes(qmcg_ctx* g, const qmcg_option_spec& spec, int64_t
       st = group_ensure_tables(g, seed, n, m, R, rebuild);
       if (st) return st;
     }
+    // every member prices its nodes on its own host thread (flags without NO_CACHE: the slices are in
+    // place, a cold call rebuilt them above); the node sums land in disjoint parts of `sums`
+    std::vector<qmcg_status> res(M.size(), QMCG_OK);
+    std::vector<std::string> msg(M.size());
+    const uint32_t mflags = flags & ~static_cast<uint32_t>(QMCG_FLAG_NO_CACHE);
     for (size_t s = 0; s < M.size(); ++s) {
       if (!R[s].count) continue;
-      DeviceGuard dg(M[s]->device);
-      // flags without NO_CACHE: the slices are in place (a cold call rebuilt them above)
-      st = price_nodes_enqueue(M[s], &spec, m, n, seed, flags & ~static_cast<uint32_t>(QMCG_FLAG_NO_CACHE), depth,
-                               R[s].node0, R[s].count);
-      if (st) return st;
+      g->workers[s]->submit([&, s] {
+        DeviceGuard dg(M[s]->device);
+        res[s] = price_nodes(M[s], &spec, m, n, seed, mflags, depth, R[s].node0, R[s].count,
+                             sums.data() + 2 * R[s].node0);
+        if (res[s]) msg[s] = g_last_error;  // thread-local: carried to the caller's thread
+      });
     }
+    for (size_t s = 0; s < M.size(); ++s)
+      if (R[s].count) g->workers[s]->wait();
+    for (size_t s = 0; s < M.size(); ++s)
+      if (res[s]) return fail(res[s], msg[s]);
+    return QMCG_OK;
   }
   for (size_t s = 0; s < M.size(); ++s) {
     if (!R[s].count) continue;
@@ -1614,16 +1682,16 @@ qmcg_status group_batch(qmcg_ctx* g, const qmcg_option_spec* specs, int64_t n_sp
   const uint32_t mflags = flags & ~static_cast<uint32_t>(QMCG_FLAG_NO_CACHE);
   std::vector<qmcg_status> res(M.size(), QMCG_OK);
   std::vector<std::string> msg(M.size());
-  std::vector<std::thread> th;
   for (int r = 0; r < G; ++r) {
     const int64_t b = n_specs * r / G, e = n_specs * (r + 1) / G;
     if (e <= b) continue;
-    th.emplace_back([&, r, b, e] {
+    g->workers[static_cast<size_t>(r)]->submit([&, r, b, e] {
       res[r] = qmcg_price_american_batch(M[r], specs + b, e - b, m, n, seed, mflags, out + b);
       if (res[r]) msg[r] = g_last_error;  // thread-local: carry the text to the caller's thread
     });
   }
-  for (auto& t : th) t.join();
+  for (int r = 0; r < G; ++r)
+    if (n_specs * (r + 1) / G > n_specs * r / G) g->workers[static_cast<size_t>(r)]->wait();
   for (int r = 0; r < G; ++r)
     if (res[r]) return fail(res[r], msg[r]);
   return QMCG_OK;
@@ -1915,6 +1983,7 @@ static qmcg_status batch_impl(qmcg_ctx* c, const qmcg_option_spec* specs, int64_
   st = prepare_scratch(c, static_cast<size_t>(n_specs));
   if (st) return st;
   // discount chains of every contract in one upload
+  c->dpow_host.clear();
   QMCG_CUDA(c->d_dpow.reserve(static_cast<size_t>(m + 1) * static_cast<size_t>(n_specs)));
   {
     std::vector<double> all(static_cast<size_t>(m + 1) * static_cast<size_t>(n_specs));
