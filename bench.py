@@ -540,8 +540,11 @@ def main():
                            "parallelism": f"paths sharded over {n_gpus} GPU(s) (pairwise-tree nodes); {layout}",
                            "tables": "warm: permutation tables resident in HBM (cold call measured separately)",
                            "l2": "inputs larger than L2 (4 B x 2^24 x 256 = 17.2 GB of tables per step)"},
-                "e2e": {"value": e2e_value, "unit": "path-steps/s", "h2d_bytes_per_step": 8 * (M_DATES + 1),
+                "e2e": {"value": e2e_value, "unit": "path-steps/s", "h2d_bytes_per_step": 48,
                         "d2h_bytes_per_step": 20, "ms_per_option": 1e3 * wall_call,
+                        "bytes_note": "in: the 48-byte qmcg_option_spec, which reaches the device inside the "
+                                      "kernel parameters (the discount chain, 8 (m + 1) B, is uploaded only when "
+                                      "it changes); out: (sum v, sum v^2) + the error word, pinned D2H",
                         "api": "qmcg_price_american (C ABI) per step" + (
                             " per rank + all-gather" if mode == "ranks" else "")},
                 "roofline": roofline, "cpu_baseline": cpu, "gpu_launches": launches, "clocks": clocks,
