@@ -161,18 +161,13 @@ struct DimTables {
   int64_t n = -1, m = -1;
   std::vector<DimParam> dims;
   std::vector<double> sc, nc;
-  std::vector<qmcg::DimPack> pack;
-  std::vector<double> scnc;  // interleaved {sc, nc}
-  std::vector<uint64_t> magic64;
-  std::vector<uint32_t> pairs;  // 4 per dimension (DIM_PAIR)
-  bool any_wide = false, any_clamp = false;
 };
 
 void build_dim_tables(int64_t n, int64_t m, DimTables& T) {
   const auto& primes = primes_upto_count(m);
   // test knob: QMCG_FORCE_WIDE=1 takes the 64-bit-magic digit division and the endpoint clamp on
-  // every dimension (the SLOW kernel instantiations, otherwise reached only near n = 2^32), so
-  // tests can check them bit for bit against the fast path at small n
+  // every dimension (otherwise reached only near n = 2^32), so tests can check them bit for bit
+  // against the 32-bit magic at small n
   const char* fw = std::getenv("QMCG_FORCE_WIDE");
   const bool force_wide = fw && *fw && *fw != '0';
   T.dims.resize(static_cast<size_t>(m));
@@ -218,53 +213,6 @@ void build_dim_tables(int64_t n, int64_t m, DimTables& T) {
       dp.magic64 = static_cast<uint64_t>((two64 + p - 1) / p);
     }
     T.dims[static_cast<size_t>(d)] = dp;
-  }
-  // two-digit extraction for bases with >= 5 digits (p > 2: base 2 is a bit reversal)
-  T.pairs.assign(4 * T.dims.size(), 0u);
-  for (size_t d = 0; d < T.dims.size(); ++d) {
-    DimParam& dp = T.dims[d];
-    if (dp.ndig < 5 || dp.p == 2 || (dp.flags & qmcg::DIM_WIDE)) continue;
-    const uint64_t p2 = static_cast<uint64_t>(dp.p) * dp.p;
-    if (p2 >= (uint64_t{1} << 31)) continue;
-    uint32_t sh = 0;
-    while ((uint64_t{1} << (sh + 1)) < p2) ++sh;
-    const unsigned __int128 two = static_cast<unsigned __int128>(1) << (32 + sh);
-    const unsigned __int128 M = (two + p2 - 1) / p2;
-    const unsigned __int128 e = M * p2 - two;
-    if (!(M < (static_cast<unsigned __int128>(1) << 32) && static_cast<unsigned __int128>(max_index) * e < two))
-      continue;
-    // split r < p^2 by p: (r * sm) >> ss, verified for every r
-    uint32_t ss = 0, sm = 0;
-    for (uint32_t s2 = 1; s2 < 32 && !sm; ++s2) {
-      const uint64_t cand = ((uint64_t{1} << s2) + dp.p - 1) / dp.p;
-      bool ok = cand * (p2 - 1) < (uint64_t{1} << 32);
-      for (uint64_t r = 0; ok && r < p2; ++r) ok = ((r * cand) >> s2) == r / dp.p;
-      if (ok) {
-        ss = s2;
-        sm = static_cast<uint32_t>(cand);
-      }
-    }
-    if (!sm) continue;
-    dp.flags |= qmcg::DIM_PAIR;
-    T.pairs[4 * d] = static_cast<uint32_t>(p2);
-    T.pairs[4 * d + 1] = static_cast<uint32_t>(M);
-    T.pairs[4 * d + 2] = sh | (ss << 8);
-    T.pairs[4 * d + 3] = sm;
-  }
-  T.pack.resize(T.dims.size());
-  T.magic64.resize(T.dims.size());
-  T.scnc.resize(2 * T.sc.size());
-  T.any_wide = T.any_clamp = false;
-  for (size_t i = 0; i < T.dims.size(); ++i) {
-    const DimParam& dp = T.dims[i];
-    T.pack[i] = qmcg::DimPack{dp.p, dp.magic, dp.shift | (dp.ndig << 8) | (dp.flags << 16), dp.doff};
-    T.magic64[i] = dp.magic64;
-    T.any_wide = T.any_wide || (dp.flags & qmcg::DIM_WIDE);
-    T.any_clamp = T.any_clamp || (dp.flags & qmcg::DIM_CLAMP);
-  }
-  for (size_t j = 0; j < T.sc.size(); ++j) {
-    T.scnc[2 * j] = T.sc[j];
-    T.scnc[2 * j + 1] = T.nc[j];
   }
   T.n = n;
   T.m = m;
@@ -407,17 +355,13 @@ struct qmcg_ctx {
   // permutation-table cache: rows [0, dims) of columns [col_begin, col_end)
   uint64_t cache_seed = 0;
   int64_t cache_n = -1, col_begin = 0, col_end = 0, cache_dims = 0;
-  uint32_t* table = nullptr;
+  double* table = nullptr;  // the uniform table: uniform_at(path, dim) of rows [0, cache_dims), f64
   size_t table_rows_cap = 0;
   // host-side dimension constants mirrored on the device
   DimTables dt;
-  DevBuf<qmcg::DimPack> d_pack;
-  DevBuf<DimParam> d_dimp;           // per-dimension digit parameters (path-matrix export)
   DevBuf<double> d_path, d_path_t;   // path matrix [point][path] (+ path-major transpose)
   DevBuf<int32_t> d_ex;              // per-path exercise points
-  DevBuf<uint64_t> d_m64;
-  DevBuf<uint32_t> d_pairs;
-  DevBuf<double> d_sc, d_nc, d_scnc, d_dpow;
+  DevBuf<double> d_sc, d_nc, d_dpow;
   std::vector<double> dpow_host;  // what d_dpow holds for single-contract calls (skips the re-upload)
   DevBuf<double> d_values, d_red, d_sums;
   DevBuf<double> d_z;                                // batch: shared normal (prefix-sum) table
@@ -430,6 +374,7 @@ struct qmcg_ctx {
   // assign pass overlaps the next table's sort (n <= kOverlapMaxN)
   cudaStream_t side[2] = {nullptr, nullptr};
   DevBuf<char> d_permscratch_side[2];
+  DevBuf<uint32_t> d_xrow_side[2];  // the side lanes' rows of perm + 1 on their way into the uniform table
   cudaEvent_t ev_fork = nullptr, ev_join[2] = {nullptr, nullptr};
   // streamed tables (date windows): per-path walk state carried between windows
   DevBuf<double> d_stV, d_stc, d_stcd, d_stbest;
@@ -439,7 +384,7 @@ struct qmcg_ctx {
   // group handle owns them and dispatches (its own stream, cache and scratch stay unused)
   std::vector<qmcg_ctx*> members;
   std::vector<std::unique_ptr<MemberWorker>> workers;       // one host thread per member (warm pricing)
-  DevBuf<uint32_t> d_gtmp;                                  // builder rows of a group table build
+  DevBuf<double> d_gtmp;                                    // builder rows of a group table build
   cudaEvent_t ev_built = nullptr, ev_priced = nullptr;      // cross-member ordering of group builds
   int64_t last_windows = 0;  // date windows of the last pricing (1 = resident tables)
   double* h_pinned = nullptr;  // [0..1] sums, [2] err as double bits
@@ -462,23 +407,9 @@ void drop_cache(qmcg_ctx* c) {
 qmcg_status ensure_dim_tables(qmcg_ctx* c, int64_t n, int64_t m) {
   if (c->dt.n == n && c->dt.m >= m) return QMCG_OK;
   build_dim_tables(n, std::max<int64_t>(m, c->dt.n == n ? c->dt.m : 0), c->dt);
-  QMCG_CUDA(c->d_pack.reserve(c->dt.pack.size()));
-  QMCG_CUDA(c->d_dimp.reserve(c->dt.dims.size()));
-  QMCG_CUDA(cudaMemcpyAsync(c->d_dimp.ptr, c->dt.dims.data(), c->dt.dims.size() * sizeof(DimParam),
-                            cudaMemcpyHostToDevice, c->stream));
-  QMCG_CUDA(c->d_m64.reserve(c->dt.magic64.size()));
-  QMCG_CUDA(c->d_pairs.reserve(c->dt.pairs.size()));
-  QMCG_CUDA(cudaMemcpyAsync(c->d_pairs.ptr, c->dt.pairs.data(), c->dt.pairs.size() * sizeof(uint32_t),
-                            cudaMemcpyHostToDevice, c->stream));
+  QMCG_CUDA(cudaStreamSynchronize(c->stream));  // nothing queued still reads the arrays about to change
   QMCG_CUDA(c->d_sc.reserve(c->dt.sc.size()));
   QMCG_CUDA(c->d_nc.reserve(c->dt.nc.size()));
-  QMCG_CUDA(c->d_scnc.reserve(c->dt.scnc.size()));
-  QMCG_CUDA(cudaMemcpyAsync(c->d_pack.ptr, c->dt.pack.data(), c->dt.pack.size() * sizeof(qmcg::DimPack),
-                            cudaMemcpyHostToDevice, c->stream));
-  QMCG_CUDA(cudaMemcpyAsync(c->d_m64.ptr, c->dt.magic64.data(), c->dt.magic64.size() * sizeof(uint64_t),
-                            cudaMemcpyHostToDevice, c->stream));
-  QMCG_CUDA(cudaMemcpyAsync(c->d_scnc.ptr, c->dt.scnc.data(), c->dt.scnc.size() * sizeof(double),
-                            cudaMemcpyHostToDevice, c->stream));
   QMCG_CUDA(cudaMemcpyAsync(c->d_sc.ptr, c->dt.sc.data(), c->dt.sc.size() * sizeof(double),
                             cudaMemcpyHostToDevice, c->stream));
   QMCG_CUDA(cudaMemcpyAsync(c->d_nc.ptr, c->dt.nc.data(), c->dt.nc.size() * sizeof(double),
@@ -507,34 +438,49 @@ constexpr int kK1Lanes = QMCG_K1_LANES;             // K1 builds in flight (main
 static_assert(kK1Lanes >= 2 && kK1Lanes <= 3, "one or two side lanes");
 constexpr int64_t kOverlapMaxN = int64_t{1} << 25;  // the extra K1 scratch stays below ~0.6 GB per lane
 
-// Rows [d0, d1) of full tables (n columns, leading dimension ld) with kK1Lanes K1 builds in
-// flight: row d on lane (d - d0) mod kK1Lanes (lane 0 = `stream`), each lane with its own
-// scratch, so one table's latency-bound assign pass overlaps the next table's sort; `stream`
-// then waits for the side lanes, so everything after sees all rows.
-// Row k holds dimension dim_begin + k * dim_stride.
-qmcg_status build_rows_overlapped(qmcg_ctx* c, uint64_t seed, int64_t n, uint32_t* table, int64_t ld,
-                                  int64_t d0, int64_t d1, int64_t dim_begin = 0, int64_t dim_stride = 1) {
+// Rows [d0, d1) of a table, row k holding dimension dim_begin + k * dim_stride, with `lanes` K1
+// builds in flight: row k on lane (k - d0) mod lanes (lane 0 = `stream`, the others side streams
+// with their own scratch), so one table's latency-bound assign pass overlaps the next table's
+// sort; `stream` then waits for the side lanes, so everything after sees all rows.
+//   xdst: the rows are perm + 1 (u32, leading dimension ld, all n columns) -- the exchange format
+//         of qmcg_build_tables;
+//   udst: the rows are the uniforms uniform_at(p, dim) of columns [cb, ce) (f64, leading dimension
+//         ld) -- the uniform table K2 reads: K1 writes the lane's row of perm + 1, then
+//         uniforms_kernel turns the column slice into bit-exact radical inverses.
+// The caller has made the dimension constants of every built dim resident (ensure_dim_tables).
+qmcg_status build_rows(qmcg_ctx* c, uint64_t seed, int64_t n, uint32_t* xdst, double* udst, int64_t ld, int64_t cb,
+                       int64_t ce, int64_t d0, int64_t d1, int64_t dim_begin, int64_t dim_stride) {
+  if (d1 <= d0) return QMCG_OK;
+  const int lanes = (n <= kOverlapMaxN && d1 - d0 >= 2) ? kK1Lanes : 1;
   const size_t need = qmcg::perm_scratch_bytes(n);
   QMCG_CUDA(c->d_permscratch.reserve(need));
+  if (udst) QMCG_CUDA(c->d_fullperm.reserve(static_cast<size_t>(n)));
   if (!c->ev_fork) QMCG_CUDA(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
   QMCG_CUDA(cudaEventRecord(c->ev_fork, c->stream));
-  for (int l = 0; l + 1 < kK1Lanes; ++l) {
+  for (int l = 0; l + 1 < lanes; ++l) {
     if (!c->side[l]) QMCG_CUDA(cudaStreamCreateWithFlags(&c->side[l], cudaStreamNonBlocking));
     if (!c->ev_join[l]) QMCG_CUDA(cudaEventCreateWithFlags(&c->ev_join[l], cudaEventDisableTiming));
     QMCG_CUDA(c->d_permscratch_side[l].reserve(need));
+    if (udst) QMCG_CUDA(c->d_xrow_side[l].reserve(static_cast<size_t>(n)));
     QMCG_CUDA(cudaStreamWaitEvent(c->side[l], c->ev_fork, 0));
   }
-  for (int64_t d = d0; d < d1; ++d) {
-    const int lane = static_cast<int>((d - d0) % kK1Lanes);
+  for (int64_t k = d0; k < d1; ++k) {
+    const int lane = static_cast<int>((k - d0) % lanes);
     DevBuf<char>& scratch = lane == 0 ? c->d_permscratch : c->d_permscratch_side[lane - 1];
     cudaStream_t s = lane == 0 ? c->stream : c->side[lane - 1];
-    uint32_t* row = table + static_cast<size_t>(d) * static_cast<size_t>(ld);
+    const int64_t dim = dim_begin + k * dim_stride;
+    uint32_t* xrow = xdst ? xdst + static_cast<size_t>(k) * static_cast<size_t>(ld)
+                          : (lane == 0 ? c->d_fullperm.ptr : c->d_xrow_side[lane - 1].ptr);
     int launches = 0;
-    QMCG_CUDA(qmcg::launch_perm_build(dimension_seed(seed, dim_begin + d * dim_stride), n, row, scratch.ptr,
-                                      scratch.cap, s, &launches, 1));
+    QMCG_CUDA(qmcg::launch_perm_build(dimension_seed(seed, dim), n, xrow, scratch.ptr, scratch.cap, s, &launches, 1));
+    if (udst) {
+      QMCG_CUDA(qmcg::launch_uniforms(xrow + cb, ce - cb, c->dt.dims[static_cast<size_t>(dim)], c->d_sc.ptr,
+                                      c->d_nc.ptr, 0, udst + static_cast<size_t>(k) * static_cast<size_t>(ld), s));
+      ++launches;
+    }
     c->launches += launches;
   }
-  for (int l = 0; l + 1 < kK1Lanes; ++l) {
+  for (int l = 0; l + 1 < lanes; ++l) {
     QMCG_CUDA(cudaEventRecord(c->ev_join[l], c->side[l]));
     QMCG_CUDA(cudaStreamWaitEvent(c->stream, c->ev_join[l], 0));
   }
@@ -549,15 +495,15 @@ qmcg_status reserve_table(qmcg_ctx* c, uint64_t seed, int64_t n, int64_t b, int6
   if (c->cache_n == n && c->cache_dims >= m) return QMCG_OK;
   const int64_t cols = e - b;
   const int64_t ld = qmcg::table_ld(cols);
-  const size_t row_bytes = static_cast<size_t>(ld) * sizeof(uint32_t);
+  const size_t row_bytes = static_cast<size_t>(ld) * sizeof(double);
   if (static_cast<size_t>(m) > c->table_rows_cap) {
-    uint32_t* nt = nullptr;
-    cudaError_t err = dev_alloc(reinterpret_cast<void**>(&nt), row_bytes * static_cast<size_t>(m) + qmcg::kTablePad * sizeof(uint32_t));
+    double* nt = nullptr;
+    cudaError_t err = dev_alloc(reinterpret_cast<void**>(&nt), row_bytes * static_cast<size_t>(m) + qmcg::kTablePad * sizeof(double));
     if (err != cudaSuccess) {
       cudaGetLastError();
       char msg[256];
       std::snprintf(msg, sizeof msg,
-                    "price_american: permutation tables of %lld dates x %lld paths (%.3g bytes) do not fit "
+                    "price_american: uniform tables of %lld dates x %lld paths (%.3g bytes) do not fit "
                     "in device memory",
                     static_cast<long long>(m), static_cast<long long>(cols),
                     static_cast<double>(row_bytes) * static_cast<double>(m));
@@ -578,32 +524,17 @@ qmcg_status reserve_table(qmcg_ctx* c, uint64_t seed, int64_t n, int64_t b, int6
   return QMCG_OK;
 }
 
-// Make rows [0, m) of the table for (seed, n) over columns [b, e) resident.
+// Make rows [0, m) of the uniform table for (seed, n) over columns [b, e) resident.
 qmcg_status ensure_perms(qmcg_ctx* c, uint64_t seed, int64_t n, int64_t b, int64_t e, int64_t m, bool rebuild) {
-  qmcg_status rs = reserve_table(c, seed, n, b, e, m, rebuild);
-  if (rs) return rs;
+  qmcg_status st = ensure_dim_tables(c, n, m);
+  if (st) return st;
+  st = reserve_table(c, seed, n, b, e, m, rebuild);
+  if (st) return st;
   if (c->cache_dims >= m) return QMCG_OK;
-  NvtxRange nv("qmcg.K1.perm_build");
-  const int64_t ld = qmcg::table_ld(e - b);
-  const size_t copy_bytes = static_cast<size_t>(e - b) * sizeof(uint32_t);
-  const bool full = (b == 0 && e == n);
-  if (!full) QMCG_CUDA(c->d_fullperm.reserve(static_cast<size_t>(n)));
-#ifndef QMCG_NO_K1_OVERLAP
-  if (full && n <= kOverlapMaxN && m - c->cache_dims >= 2) {
-    qmcg_status st = build_rows_overlapped(c, seed, n, c->table, ld, c->cache_dims, m);
-    if (st) return st;
-    c->cache_dims = m;
-    return QMCG_OK;
-  }
-#endif
-  for (int64_t d = c->cache_dims; d < m; ++d) {
-    uint32_t* row = c->table + static_cast<size_t>(d) * static_cast<size_t>(ld);
-    qmcg_status st = build_perm(c, dimension_seed(seed, d), n, full ? row : c->d_fullperm.ptr);
-    if (st) return st;
-    if (!full)
-      QMCG_CUDA(cudaMemcpyAsync(row, c->d_fullperm.ptr + b, copy_bytes, cudaMemcpyDeviceToDevice, c->stream));
-    c->cache_dims = d + 1;
-  }
+  NvtxRange nv("qmcg.K1.table_build");
+  st = build_rows(c, seed, n, nullptr, c->table, qmcg::table_ld(e - b), b, e, c->cache_dims, m, 0, 1);
+  if (st) return st;
+  c->cache_dims = m;
   return QMCG_OK;
 }
 
@@ -683,14 +614,6 @@ qmcg_status plan_call(const qmcg_option_spec& s, int64_t m, int64_t n, uint32_t 
   return QMCG_OK;
 }
 
-void attach_dims(qmcg_ctx* c, PriceParams& P) {
-  P.dims = c->d_pack.ptr;
-  P.scnc = reinterpret_cast<const double2*>(c->d_scnc.ptr);
-  P.magic64 = c->d_m64.ptr;
-  P.pairs = reinterpret_cast<const uint4*>(c->d_pairs.ptr);
-  P.any_wide = c->dt.any_wide;
-  P.any_clamp = c->dt.any_clamp;
-}
 
 qmcg_status upload_plan(qmcg_ctx* c, CallPlan& plan, int64_t n) {
   const int64_t m = plan.P.m;
@@ -702,7 +625,6 @@ qmcg_status upload_plan(qmcg_ctx* c, CallPlan& plan, int64_t n) {
                               cudaMemcpyHostToDevice, c->stream));
     c->dpow_host = plan.dpow;
   }
-  attach_dims(c, plan.P);
   plan.P.dpow = c->d_dpow.ptr;
   return QMCG_OK;
 }
@@ -722,7 +644,7 @@ qmcg_status enqueue_values(qmcg_ctx* c, CallPlan& plan, int64_t b, int64_t e, cu
   QMCG_CUDA(c->d_values.reserve(static_cast<size_t>(cnt)));
   QMCG_CUDA(c->d_red.reserve(qmcg::reduce_scratch_doubles(cnt)));
   PriceParams P = plan.P;
-  P.perm = c->table;
+  P.table = c->table;
   P.ld = qmcg::table_ld(c->col_end - c->col_begin);
   if ((b - c->col_begin) % 4 != 0) return fail(QMCG_INVALID_ARGUMENT, "internal: unaligned path range");
   P.col_begin = c->col_begin;
@@ -933,10 +855,7 @@ void qmcg_destroy(qmcg_ctx* c) {
   DeviceGuard g(c->device);
   cudaStreamSynchronize(c->stream);
   drop_cache(c);
-  c->d_pack.release();
-  c->d_m64.release();
-  c->d_pairs.release();
-  c->d_scnc.release();
+
   c->d_sc.release();
   c->d_nc.release();
   c->d_dpow.release();
@@ -957,6 +876,7 @@ void qmcg_destroy(qmcg_ctx* c) {
   for (int l = 0; l < 2; ++l) {
     if (c->side[l]) cudaStreamSynchronize(c->side[l]);
     c->d_permscratch_side[l].release();
+    c->d_xrow_side[l].release();
     if (c->side[l]) cudaStreamDestroy(c->side[l]);
     if (c->ev_join[l]) cudaEventDestroy(c->ev_join[l]);
   }
@@ -964,7 +884,7 @@ void qmcg_destroy(qmcg_ctx* c) {
   if (c->ev_built) cudaEventDestroy(c->ev_built);
   if (c->ev_priced) cudaEventDestroy(c->ev_priced);
   c->d_gtmp.release();
-  c->d_dimp.release();
+
   c->d_path.release();
   c->d_path_t.release();
   c->d_ex.release();
@@ -1034,19 +954,42 @@ qmcg_status qmcg_build_tables(qmcg_ctx* c, int64_t n, uint64_t seed, int64_t dim
   std::lock_guard<std::mutex> lock(c->mu);
   DeviceGuard g(c->device);
   c->launches = 0;
-  if (n <= kOverlapMaxN && count >= 2) {
-    qmcg_status st = build_rows_overlapped(c, seed, n, out_dev, ld, 0, count, dim_begin, dim_stride);
-    if (st) return st;
-  } else {
-    for (int64_t k = 0; k < count; ++k) {
-      qmcg_status st = build_perm(c, dimension_seed(seed, dim_begin + k * dim_stride), n,
-                                  out_dev + static_cast<size_t>(k) * static_cast<size_t>(ld));
-      if (st) return st;
-    }
-  }
+  qmcg_status st = build_rows(c, seed, n, out_dev, nullptr, ld, 0, n, 0, count, dim_begin, dim_stride);
+  if (st) return st;
   QMCG_CUDA(cudaStreamSynchronize(c->stream));
   return QMCG_OK;
 }
+
+}  // extern "C"
+
+namespace {
+// Rows [row_begin, row_begin + row_count) of the slice [col_begin, col_end) of the uniform table
+// for dims [0, dims), from rows of perm + 1 (src_dev, stride src_ld): each row is turned into its
+// dimension's uniforms by uniforms_kernel. row_begin = 0 starts a fresh slice table.
+qmcg_status import_x_rows(qmcg_ctx* c, int64_t n, uint64_t seed, int64_t col_begin, int64_t col_end, int64_t dims,
+                          int64_t row_begin, int64_t row_count, const uint32_t* src_dev, int64_t src_ld) {
+  const int64_t cols = col_end - col_begin;
+  qmcg_status st = ensure_dim_tables(c, n, dims);
+  if (st) return st;
+  if (row_begin == 0) {
+    st = reserve_table(c, seed, n, col_begin, col_end, dims, true);  // a fresh slice table
+    if (st) return st;
+  } else if (c->cache_n != n || c->cache_seed != seed || c->col_begin != col_begin || c->col_end != col_end ||
+             c->cache_dims != row_begin || c->table_rows_cap < static_cast<size_t>(dims)) {
+    return fail(QMCG_INVALID_ARGUMENT, "qmcg_import_rows: rows must continue the slice imported so far");
+  }
+  const int64_t ld = qmcg::table_ld(cols);
+  for (int64_t k = 0; k < row_count; ++k)
+    QMCG_CUDA(qmcg::launch_uniforms(src_dev + static_cast<size_t>(k) * static_cast<size_t>(src_ld), cols,
+                                    c->dt.dims[static_cast<size_t>(row_begin + k)], c->d_sc.ptr, c->d_nc.ptr, 0,
+                                    c->table + static_cast<size_t>(row_begin + k) * static_cast<size_t>(ld), c->stream));
+  QMCG_CUDA(cudaStreamSynchronize(c->stream));
+  c->cache_dims = row_begin + row_count;
+  return QMCG_OK;
+}
+}  // namespace
+
+extern "C" {
 
 qmcg_status qmcg_import_tables(qmcg_ctx* c, int64_t n, uint64_t seed, int64_t col_begin, int64_t col_end,
                                int64_t dims, const uint32_t* src_dev, int64_t src_ld) {
@@ -1059,26 +1002,7 @@ qmcg_status qmcg_import_tables(qmcg_ctx* c, int64_t n, uint64_t seed, int64_t co
     return fail(QMCG_INVALID_ARGUMENT, "qmcg_import_tables: bad size");
   std::lock_guard<std::mutex> lock(c->mu);
   DeviceGuard g(c->device);
-  drop_cache(c);
-  const int64_t ld = qmcg::table_ld(cols);
-  const size_t row_bytes = static_cast<size_t>(ld) * sizeof(uint32_t);
-  uint32_t* nt = nullptr;
-  if (dev_alloc(reinterpret_cast<void**>(&nt), row_bytes * static_cast<size_t>(dims) + qmcg::kTablePad * sizeof(uint32_t)) != cudaSuccess) {
-    cudaGetLastError();
-    return fail(QMCG_OUT_OF_MEMORY, "qmcg_import_tables: tables do not fit in device memory");
-  }
-  c->table = nt;
-  c->table_rows_cap = static_cast<size_t>(dims);
-  QMCG_CUDA(cudaMemcpy2DAsync(nt, row_bytes, src_dev, static_cast<size_t>(src_ld) * sizeof(uint32_t),
-                              static_cast<size_t>(cols) * sizeof(uint32_t), static_cast<size_t>(dims),
-                              cudaMemcpyDeviceToDevice, c->stream));
-  QMCG_CUDA(cudaStreamSynchronize(c->stream));
-  c->cache_n = n;
-  c->cache_seed = seed;
-  c->col_begin = col_begin;
-  c->col_end = col_end;
-  c->cache_dims = dims;
-  return QMCG_OK;
+  return import_x_rows(c, n, seed, col_begin, col_end, dims, 0, dims, src_dev, src_ld);
 }
 
 qmcg_status qmcg_import_rows(qmcg_ctx* c, int64_t n, uint64_t seed, int64_t col_begin, int64_t col_end, int64_t dims,
@@ -1092,21 +1016,7 @@ qmcg_status qmcg_import_rows(qmcg_ctx* c, int64_t n, uint64_t seed, int64_t col_
     return fail(QMCG_INVALID_ARGUMENT, "qmcg_import_rows: bad size");
   std::lock_guard<std::mutex> lock(c->mu);
   DeviceGuard g(c->device);
-  if (row_begin == 0) {
-    qmcg_status st = reserve_table(c, seed, n, col_begin, col_end, dims, true);  // a fresh slice table
-    if (st) return st;
-  } else if (c->cache_n != n || c->cache_seed != seed || c->col_begin != col_begin || c->col_end != col_end ||
-             c->cache_dims != row_begin || c->table_rows_cap < static_cast<size_t>(dims)) {
-    return fail(QMCG_INVALID_ARGUMENT, "qmcg_import_rows: rows must continue the slice imported so far");
-  }
-  const int64_t ld = qmcg::table_ld(cols);
-  QMCG_CUDA(cudaMemcpy2DAsync(c->table + static_cast<size_t>(row_begin) * static_cast<size_t>(ld),
-                              static_cast<size_t>(ld) * sizeof(uint32_t), src_dev,
-                              static_cast<size_t>(src_ld) * sizeof(uint32_t), static_cast<size_t>(cols) * sizeof(uint32_t),
-                              static_cast<size_t>(row_count), cudaMemcpyDeviceToDevice, c->stream));
-  QMCG_CUDA(cudaStreamSynchronize(c->stream));
-  c->cache_dims = row_begin + row_count;
-  return QMCG_OK;
+  return import_x_rows(c, n, seed, col_begin, col_end, dims, row_begin, row_count, src_dev, src_ld);
 }
 
 qmcg_status qmcg_set_table_budget(qmcg_ctx* c, uint64_t bytes) {
@@ -1145,8 +1055,11 @@ size_t table_bytes_allowed(qmcg_ctx* c, int64_t n, int64_t cols, bool full) {
   size_t free_b = 0, total_b = 0;
   cudaMemGetInfo(&free_b, &total_b);
   const int64_t held_ld = qmcg::table_ld(c->col_end - c->col_begin);
-  const size_t held = c->table ? c->table_rows_cap * static_cast<size_t>(held_ld) * sizeof(uint32_t) : 0;
-  const size_t reserve = qmcg::perm_scratch_bytes(n) + (full ? 0 : static_cast<size_t>(n) * 4) +
+  const size_t held = c->table ? c->table_rows_cap * static_cast<size_t>(held_ld) * sizeof(double) : 0;
+  // K1 scratch and a row of perm + 1 per build lane, the carried walk state, values, a margin
+  const size_t lanes = n <= kOverlapMaxN ? kK1Lanes : 1;
+  (void)full;
+  const size_t reserve = lanes * (qmcg::perm_scratch_bytes(n) + static_cast<size_t>(n) * 4) +
                          static_cast<size_t>(cols) * (4 * 8 + 4 + 8 + 8) + (size_t{1} << 30);
   const size_t avail = free_b + held > reserve ? free_b + held - reserve : 0;
   return c->table_budget ? std::min(c->table_budget, avail) : avail;
@@ -1177,30 +1090,30 @@ qmcg_status enqueue_streamed(qmcg_ctx* c, CallPlan& plan, uint64_t seed, int64_t
   NvtxRange nv("qmcg.streamed_windows");
   const int64_t cols = e - b, m = plan.P.m;
   const int64_t ld = qmcg::table_ld(cols);
-  const size_t row_bytes = static_cast<size_t>(ld) * sizeof(uint32_t);
+  const size_t row_bytes = static_cast<size_t>(ld) * sizeof(double);
   int64_t W = static_cast<int64_t>(budget / row_bytes) / 8 * 8;
   if (W < 8)
-    return fail(QMCG_OUT_OF_MEMORY, "price_american: not enough device memory for 8 permutation rows");
+    return fail(QMCG_OUT_OF_MEMORY, "price_american: not enough device memory for 8 uniform-table rows");
   W = std::min<int64_t>(W, (m + 7) / 8 * 8);
+  qmcg_status st = ensure_dim_tables(c, n, m);
+  if (st) return st;
   drop_cache(c);
-  uint32_t* nt = nullptr;
-  if (dev_alloc(reinterpret_cast<void**>(&nt), row_bytes * static_cast<size_t>(W) + qmcg::kTablePad * sizeof(uint32_t)) != cudaSuccess) {
+  double* nt = nullptr;
+  if (dev_alloc(reinterpret_cast<void**>(&nt), row_bytes * static_cast<size_t>(W) + qmcg::kTablePad * sizeof(double)) != cudaSuccess) {
     cudaGetLastError();
-    return fail(QMCG_OUT_OF_MEMORY, "price_american: permutation window does not fit in device memory");
+    return fail(QMCG_OUT_OF_MEMORY, "price_american: uniform-table window does not fit in device memory");
   }
   c->table = nt;
   c->table_rows_cap = static_cast<size_t>(W);
   c->col_begin = b;  // the buffer holds a window, never a cache (cache_n stays -1)
   c->col_end = e;
-  const bool full = (b == 0 && e == n);
-  if (!full) QMCG_CUDA(c->d_fullperm.reserve(static_cast<size_t>(n)));
   QMCG_CUDA(c->d_values.reserve(static_cast<size_t>(cols)));
   QMCG_CUDA(c->d_red.reserve(qmcg::reduce_scratch_doubles(cols)));
   for (auto* buf : {&c->d_stV, &c->d_stc, &c->d_stcd, &c->d_stbest})
     QMCG_CUDA(buf->reserve(static_cast<size_t>(cols)));
   QMCG_CUDA(c->d_stpend.reserve(static_cast<size_t>(cols)));
   PriceParams P = plan.P;
-  P.perm = c->table;
+  P.table = c->table;
   P.ld = ld;
   P.col_begin = b;
   P.path_begin = b;
@@ -1215,14 +1128,8 @@ qmcg_status enqueue_streamed(qmcg_ctx* c, CallPlan& plan, uint64_t seed, int64_t
   c->last_windows = 0;
   for (int64_t d0 = 0; d0 < m; d0 += W) {
     const int64_t d1 = std::min(m, d0 + W);
-    for (int64_t d = d0; d < d1; ++d) {
-      uint32_t* row = c->table + static_cast<size_t>(d - d0) * static_cast<size_t>(ld);
-      qmcg_status st = build_perm(c, dimension_seed(seed, d), n, full ? row : c->d_fullperm.ptr);
-      if (st) return st;
-      if (!full)
-        QMCG_CUDA(cudaMemcpyAsync(row, c->d_fullperm.ptr + b, static_cast<size_t>(cols) * sizeof(uint32_t),
-                                  cudaMemcpyDeviceToDevice, c->stream));
-    }
+    st = build_rows(c, seed, n, nullptr, c->table, ld, b, e, 0, d1 - d0, d0, 1);  // window row k = dim d0 + k
+    if (st) return st;
     P.d_begin = static_cast<int32_t>(d0);
     P.d_end = static_cast<int32_t>(d1);
     P.perm_row0 = static_cast<int32_t>(d0);
@@ -1260,7 +1167,7 @@ static qmcg_status price_nodes_enqueue(qmcg_ctx* c, const qmcg_option_spec* spec
   size_t budget = 0;
   if (!cached && !plan.P.deterministic) {
     budget = table_bytes_allowed(c, n, e - b, b == 0 && e == n);
-    const size_t need = static_cast<size_t>(qmcg::table_ld(e - b)) * sizeof(uint32_t) * static_cast<size_t>(m);
+    const size_t need = static_cast<size_t>(qmcg::table_ld(e - b)) * sizeof(double) * static_cast<size_t>(m);
     streamed = need > budget;
   }
   st = prepare_scratch(c, static_cast<size_t>(count));
@@ -1374,25 +1281,21 @@ qmcg_status cross_wait(const std::vector<qmcg_ctx*>& from, const std::vector<qmc
   return QMCG_OK;
 }
 
-// Rows of dims `dims` (full n) built by member `bc` into its scratch `tmp` (rows of n entries),
-// then row k's slice [R[s].b, R[s].e) copied into row dst_row[k] of member s's table.
+// Uniform-table rows of dims `dims` (all n columns) built by member `bc` into its scratch `tmp`
+// (rows of n entries), then row k's slice [R[s].b, R[s].e) copied into row dst_row[k] of member s's
+// table. The builder needs the dimension constants of every dim it builds (ensure_dim_tables).
 qmcg_status build_and_scatter(qmcg_ctx* bc, uint64_t seed, int64_t n, const std::vector<int64_t>& dims,
                               const std::vector<int64_t>& dst_row, const std::vector<qmcg_ctx*>& M,
-                              const std::vector<MemberRange>& R, uint32_t* tmp, int64_t tmp_rows) {
+                              const std::vector<MemberRange>& R, double* tmp, int64_t tmp_rows) {
   DeviceGuard g(bc->device);
+  qmcg_status st = ensure_dim_tables(bc, n, dims.back() + 1);
+  if (st) return st;
   for (size_t k0 = 0; k0 < dims.size(); k0 += static_cast<size_t>(tmp_rows)) {
     const size_t cnt = std::min(dims.size() - k0, static_cast<size_t>(tmp_rows));
     // dims of a member are an arithmetic progression with stride G
     const int64_t stride = cnt > 1 ? dims[k0 + 1] - dims[k0] : 1;
-    if (n <= kOverlapMaxN && cnt >= 2) {
-      qmcg_status st = build_rows_overlapped(bc, seed, n, tmp, n, 0, static_cast<int64_t>(cnt), dims[k0], stride);
-      if (st) return st;
-    } else {
-      for (size_t k = 0; k < cnt; ++k) {
-        qmcg_status st = build_perm(bc, dimension_seed(seed, dims[k0 + k]), n, tmp + k * static_cast<size_t>(n));
-        if (st) return st;
-      }
-    }
+    st = build_rows(bc, seed, n, nullptr, tmp, n, 0, n, 0, static_cast<int64_t>(cnt), dims[k0], stride);
+    if (st) return st;
     for (size_t s = 0; s < M.size(); ++s) {
       const MemberRange& r = R[s];
       if (r.e <= r.b) continue;
@@ -1400,7 +1303,7 @@ qmcg_status build_and_scatter(qmcg_ctx* bc, uint64_t seed, int64_t n, const std:
       for (size_t k = 0; k < cnt; ++k)
         QMCG_CUDA(cudaMemcpyPeerAsync(M[s]->table + static_cast<size_t>(dst_row[k0 + k]) * ld, M[s]->device,
                                       tmp + k * static_cast<size_t>(n) + r.b, bc->device,
-                                      static_cast<size_t>(r.e - r.b) * sizeof(uint32_t), bc->stream));
+                                      static_cast<size_t>(r.e - r.b) * sizeof(double), bc->stream));
     }
   }
   return QMCG_OK;
@@ -1408,7 +1311,7 @@ qmcg_status build_and_scatter(qmcg_ctx* bc, uint64_t seed, int64_t n, const std:
 
 // Scratch rows a builder holds for the sharded build (~512 MB, at least one row).
 int64_t group_tmp_rows(int64_t n) {
-  return std::max<int64_t>(1, std::min<int64_t>(8, (int64_t{1} << 29) / (4 * n)));
+  return std::max<int64_t>(1, std::min<int64_t>(8, (int64_t{1} << 29) / (8 * n)));
 }
 
 // Resident tables for (seed, n) rows [0, m) on every member, each over its range R[s]:
@@ -1476,13 +1379,13 @@ qmcg_status group_enqueue_streamed(qmcg_ctx* g, std::vector<CallPlan>& plans, ui
     DeviceGuard dg(M[s]->device);
     drop_cache(M[s]);
     const int64_t cols = R[s].e - R[s].b;
-    const size_t row_bytes = static_cast<size_t>(qmcg::table_ld(cols)) * sizeof(uint32_t);
+    const size_t row_bytes = static_cast<size_t>(qmcg::table_ld(cols)) * sizeof(double);
     // the builder scratch (one full row) lives on every member as well
     size_t budget = table_bytes_allowed(M[s], n, cols, false);
-    budget = budget > static_cast<size_t>(n) * 4 ? budget - static_cast<size_t>(n) * 4 : 0;
+    budget = budget > static_cast<size_t>(n) * 8 ? budget - static_cast<size_t>(n) * 8 : 0;
     W = std::min<int64_t>(W, static_cast<int64_t>(budget / row_bytes) / 8 * 8);
   }
-  if (W < 8) return fail(QMCG_OUT_OF_MEMORY, "price_american: not enough device memory for 8 permutation rows");
+  if (W < 8) return fail(QMCG_OUT_OF_MEMORY, "price_american: not enough device memory for 8 uniform-table rows");
   std::vector<PriceParams> P(M.size());
   for (size_t s = 0; s < M.size(); ++s) {
     qmcg_ctx* c = M[s];
@@ -1493,10 +1396,10 @@ qmcg_status group_enqueue_streamed(qmcg_ctx* g, std::vector<CallPlan>& plans, ui
     if (R[s].e <= R[s].b) continue;
     const int64_t cols = R[s].e - R[s].b;
     const int64_t ld = qmcg::table_ld(cols);
-    uint32_t* nt = nullptr;
-    if (dev_alloc(reinterpret_cast<void**>(&nt), static_cast<size_t>(ld) * 4 * static_cast<size_t>(W) + qmcg::kTablePad * 4) != cudaSuccess) {
+    double* nt = nullptr;
+    if (dev_alloc(reinterpret_cast<void**>(&nt), static_cast<size_t>(ld) * 8 * static_cast<size_t>(W) + qmcg::kTablePad * 8) != cudaSuccess) {
       cudaGetLastError();
-      return fail(QMCG_OUT_OF_MEMORY, "price_american: permutation window does not fit in device memory");
+      return fail(QMCG_OUT_OF_MEMORY, "price_american: uniform-table window does not fit in device memory");
     }
     c->table = nt;
     c->table_rows_cap = static_cast<size_t>(W);
@@ -1508,7 +1411,7 @@ qmcg_status group_enqueue_streamed(qmcg_ctx* g, std::vector<CallPlan>& plans, ui
     QMCG_CUDA(c->d_stpend.reserve(static_cast<size_t>(cols)));
     PriceParams& p = P[s];
     p = plans[s].P;
-    p.perm = c->table;
+    p.table = c->table;
     p.ld = ld;
     p.col_begin = R[s].b;
     p.path_begin = R[s].b;
@@ -1595,8 +1498,8 @@ qmcg_status group_price_nodes(qmcg_ctx* g, const qmcg_option_spec& spec, int64_t
                           c->col_end == r.e && c->cache_dims >= m;
       if (cached) continue;
       DeviceGuard dg(c->device);
-      const size_t need = static_cast<size_t>(qmcg::table_ld(r.e - r.b)) * 4 * static_cast<size_t>(m) +
-                          static_cast<size_t>(group_tmp_rows(n)) * static_cast<size_t>(n) * 4;
+      const size_t need = static_cast<size_t>(qmcg::table_ld(r.e - r.b)) * 8 * static_cast<size_t>(m) +
+                          static_cast<size_t>(group_tmp_rows(n)) * static_cast<size_t>(n) * 8;
       if (need > table_bytes_allowed(c, n, r.e - r.b, false)) streamed = true;
     }
   }
@@ -1877,8 +1780,8 @@ qmcg_status qmcg_mc_european_price(qmcg_ctx* c, const qmcg_option_spec* spec, in
   const double a = (r - 0.5 * v * v) * T;  // gbm_step with dt = T
   const double bsd = v * std::sqrt(T);
   const double disc = std::exp(-r * T);
-  QMCG_CUDA(qmcg::launch_european(c->table, n, c->dt.dims[0], c->d_sc.ptr, c->d_nc.ptr, spec->spot, a, bsd,
-                                  spec->strike, disc, spec->kind, c->d_values.ptr, c->stream));
+  QMCG_CUDA(qmcg::launch_european(c->table, n, spec->spot, a, bsd, spec->strike, disc, spec->kind, c->d_values.ptr,
+                                  c->stream));
   int launches = 1;
   QMCG_CUDA(qmcg::launch_pairwise(c->d_values.ptr, n, c->d_red.ptr, c->d_sums.ptr, c->stream, &launches));
   c->launches += launches;
@@ -2000,7 +1903,6 @@ static qmcg_status batch_impl(qmcg_ctx* c, const qmcg_option_spec* specs, int64_
   std::vector<int64_t> shared_idx[2], single_idx;
   for (int64_t i = 0; i < n_specs; ++i) {
     const PriceParams& P = plans[static_cast<size_t>(i)].P;
-    attach_dims(c, plans[static_cast<size_t>(i)].P);
     plans[static_cast<size_t>(i)].P.dpow = c->d_dpow.ptr + static_cast<size_t>(i) * static_cast<size_t>(m + 1);
     if (!P.deterministic && !P.check_range && !P.rate_negative) shared_idx[P.kind].push_back(i);
     else single_idx.push_back(i);
@@ -2020,7 +1922,7 @@ static qmcg_status batch_impl(qmcg_ctx* c, const qmcg_option_spec* specs, int64_
   if (use_shared) {
     QMCG_CUDA(c->d_z.reserve(static_cast<size_t>(m + 8) * static_cast<size_t>(n)));  // + 8 prefetch rows
     PriceParams G = plans[static_cast<size_t>(shared_idx[0].empty() ? shared_idx[1][0] : shared_idx[0][0])].P;
-    G.perm = c->table;
+    G.table = c->table;
     G.ld = qmcg::table_ld(c->col_end - c->col_begin);
     G.col_begin = c->col_begin;
     G.path_begin = 0;
@@ -2203,7 +2105,7 @@ qmcg_status qmcg_normal_table(qmcg_ctx* c, int64_t n, uint64_t seed, int64_t dim
   if (st) return st;
   QMCG_CUDA(c->d_z.reserve(static_cast<size_t>(dims) * static_cast<size_t>(n)));
   PriceParams G = plan.P;
-  G.perm = c->table;
+  G.table = c->table;
   G.ld = qmcg::table_ld(c->col_end - c->col_begin);
   G.col_begin = c->col_begin;
   G.path_begin = 0;
@@ -2226,27 +2128,14 @@ qmcg_status qmcg_uniform_rows(qmcg_ctx* c, int64_t n, uint64_t seed, int64_t dim
   std::lock_guard<std::mutex> lock(c->mu);
   DeviceGuard g(c->device);
   const int64_t dims = dim_begin + dim_count;
-  qmcg_option_spec s{100.0, 100.0, 0.05, 0.2, 1.0, QMCG_CALL};
-  CallPlan plan;
-  qmcg_status st = plan_call(s, dims, n, 0, plan);
+  qmcg_status st = ensure_perms(c, seed, n, 0, n, dims, false);
   if (st) return st;
-  st = upload_plan(c, plan, n);
-  if (st) return st;
-  st = ensure_perms(c, seed, n, 0, n, dims, false);
-  if (st) return st;
-  QMCG_CUDA(c->d_z.reserve(static_cast<size_t>(dim_count) * static_cast<size_t>(n)));
-  PriceParams G = plan.P;
-  G.perm = c->table;
-  G.ld = qmcg::table_ld(c->col_end - c->col_begin);
-  G.col_begin = c->col_begin;
-  G.path_begin = 0;
-  G.path_count = n;
-  G.d_begin = static_cast<int32_t>(dim_begin);
-  G.d_end = static_cast<int32_t>(dims);
-  QMCG_CUDA(qmcg::launch_gen_z(G, c->d_z.ptr, n, c->stream, qmcg::kGenUniform));
-  QMCG_CUDA(cudaMemcpyAsync(out_host, c->d_z.ptr,
-                            static_cast<size_t>(dim_count) * static_cast<size_t>(n) * sizeof(double),
-                            cudaMemcpyDeviceToHost, c->stream));
+  // the uniform table the pricing kernels read (built by uniforms_kernel from K1's permutations)
+  const size_t ld = static_cast<size_t>(qmcg::table_ld(n));
+  QMCG_CUDA(cudaMemcpy2DAsync(out_host, static_cast<size_t>(n) * sizeof(double),
+                              c->table + static_cast<size_t>(dim_begin) * ld, ld * sizeof(double),
+                              static_cast<size_t>(n) * sizeof(double), static_cast<size_t>(dim_count),
+                              cudaMemcpyDeviceToHost, c->stream));
   QMCG_CUDA(cudaStreamSynchronize(c->stream));
   return QMCG_OK;
 }
@@ -2479,9 +2368,8 @@ qmcg_status simulate_device(qmcg_ctx* c, const qmcg_option_spec& s, int64_t m, i
   const double dt = s.maturity / static_cast<double>(points);  // make_schedule
   const double a = (s.rate - 0.5 * s.volatility * s.volatility) * dt;
   const double bsd = s.volatility * std::sqrt(dt);
-  QMCG_CUDA(qmcg::launch_path_matrix(c->table, qmcg::table_ld(n), c->d_dimp.ptr, c->d_sc.ptr, c->d_nc.ptr, n,
-                                     static_cast<int>(points), s.spot, a, bsd, c->d_path.ptr, c->d_err.ptr,
-                                     c->stream));
+  QMCG_CUDA(qmcg::launch_path_matrix(c->table, qmcg::table_ld(n), n, static_cast<int>(points), s.spot, a, bsd,
+                                     c->d_path.ptr, c->d_err.ptr, c->stream));
   c->launches += 1;
   return QMCG_OK;
 }

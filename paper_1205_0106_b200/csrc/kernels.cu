@@ -169,6 +169,9 @@ __device__ __forceinline__ void sts_f64(uint32_t a, double v) {
 __device__ __forceinline__ void sts_u32(uint32_t a, uint32_t v) {
   asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
 }
+__device__ __forceinline__ void sts_u8(uint32_t a, uint32_t v) {
+  asm volatile("st.shared.u8 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
 __device__ __forceinline__ void sts_v2f64(uint32_t a, double2 v) {
   asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(a), "d"(v.x), "d"(v.y) : "memory");
 }
@@ -334,62 +337,6 @@ __device__ __forceinline__ unsigned lanemask_lt() {
   return m;
 }
 
-// ---- radical inverse with the digit count fixed per date (warp-uniform) ----
-template <bool WIDE>
-__device__ __forceinline__ uint32_t divp(uint32_t x, uint32_t magic, uint32_t shift, uint64_t m64) {
-  if (WIDE) return static_cast<uint32_t>(__umul64hi(x, m64));
-  return __umulhi(x, magic) >> shift;
-}
-
-template <bool WIDE>
-__device__ __forceinline__ double halton_digits(uint32_t x, uint32_t p, uint32_t magic, uint32_t shift, uint64_t m64,
-                                                int D, const double2* __restrict__ sn) {
-  // D digits, least significant first; the last digit is the remaining quotient.
-  if (D == 3) {
-    const double2 s0 = sn[0], s1 = sn[1], s2 = sn[2];
-    const uint32_t q1 = divp<WIDE>(x, magic, shift, m64);
-    const uint32_t q2 = divp<WIDE>(q1, magic, shift, m64);
-    double v = digit_term(x - q1 * p, s0.x, s0.y);
-    v = __dadd_rn(v, digit_term(q1 - q2 * p, s1.x, s1.y));
-    return __dadd_rn(v, digit_term(q2, s2.x, s2.y));
-  }
-  if (D == 2) {
-    const double2 s0 = sn[0], s1 = sn[1];
-    const uint32_t q1 = divp<WIDE>(x, magic, shift, m64);
-    const double v = digit_term(x - q1 * p, s0.x, s0.y);
-    return __dadd_rn(v, digit_term(q1, s1.x, s1.y));
-  }
-  if (D == 4) {
-    const double2 s0 = sn[0], s1 = sn[1], s2 = sn[2], s3 = sn[3];
-    const uint32_t q1 = divp<WIDE>(x, magic, shift, m64);
-    const uint32_t q2 = divp<WIDE>(q1, magic, shift, m64);
-    const uint32_t q3 = divp<WIDE>(q2, magic, shift, m64);
-    double v = digit_term(x - q1 * p, s0.x, s0.y);
-    v = __dadd_rn(v, digit_term(q1 - q2 * p, s1.x, s1.y));
-    v = __dadd_rn(v, digit_term(q2 - q3 * p, s2.x, s2.y));
-    return __dadd_rn(v, digit_term(q3, s3.x, s3.y));
-  }
-  if (D == 1) {
-    const double2 s0 = sn[0];
-    return digit_term(x, s0.x, s0.y);
-  }
-  // base 2: the digit products d_j 2^-(j+1) and their running sums are exact, so
-  // radical_inverse(x, 2) is the bit reversal of x times 2^-32, exactly
-  if (p == 2u) return static_cast<double>(__brev(x)) * 0x1p-32;
-  uint32_t q = divp<WIDE>(x, magic, shift, m64);
-  double2 s = sn[0];
-  double v = digit_term(x - q * p, s.x, s.y);
-  x = q;
-  for (int j = 1; j < D - 1; ++j) {
-    q = divp<WIDE>(x, magic, shift, m64);
-    s = sn[j];
-    v = __dadd_rn(v, digit_term(x - q * p, s.x, s.y));
-    x = q;
-  }
-  s = sn[D - 1];
-  return __dadd_rn(v, digit_term(x, s.x, s.y));
-}
-
 __device__ __forceinline__ double clamp_endpoints(double v) {  // quasi_rng.cpp:80-81
   if (v < 1e-12) v = 1e-12;
   if (v > 1.0 - 1e-12) v = 1.0 - 1e-12;
@@ -401,36 +348,17 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 // Shared memory of one 256-path block (byte offsets from the dynamic base):
-//   perm[2][kTile][256] u32   permutation entries, bulk-copied, double-buffered
-//   zt[2][kTile][256]   f64   z_k + alpha per (date, path); reused for V_k in the walk
+//   zt[2][kTile][256]   f64   the tile's uniforms u (2-D TMA copy of the uniform table), turned
+//                             in place into z_k + alpha per (date, path) and walked; double-buffered
 //   logtab[128]         f64x2 log reduction table
-//   bar[2]              mbarriers of the two perm buffers
-//   per warp: rq_v[64] f64 | best[32] u64 | rq_code[64] u32 | tail_idx[256 + 32] u8
-// A Moro-tail point keeps its uniform u in its z slot until the row's tail queue
-// (indices only) is evaluated and overwrites it with z.
+//   bar[2]              mbarriers of the two tile buffers
+//   per warp: rq_v[128] f64 | best[32] u64 | rq_code[128] u32 | tail_idx[256 + 32] u8
+// A Moro-tail point keeps its uniform u in its slot until the row's tail queue (indices
+// only) is evaluated and overwrites it with z. FP32 variant: z is an f32 in the slot's low half.
 constexpr uint32_t kTailCap = kThreads;  // a whole date row can be queued: no mid-row flush
-constexpr uint32_t kPermOff = 0;
-constexpr uint32_t kPermBuf = kTile * kThreads * 4;
-#ifndef QMCG_PERM_BUFFERS
-#define QMCG_PERM_BUFFERS 1
-#endif
-// 2: permutation rows double-buffered (row of tile k + 2 staged after tile k);
-// 1: one buffer, the row of tile k + 1 staged as soon as the warp has read row k
-// (measured 1.2% faster at config 3: the copy is in flight during the walk).
-#ifndef QMCG_TMA
-#define QMCG_TMA 1
-#endif
-// QMCG_TMA: price_kernel stages each tile with one 2-D TMA copy (double-buffered)
-constexpr bool kTma = QMCG_TMA != 0;
-constexpr int kPermBuffers = kTma ? 2 : QMCG_PERM_BUFFERS;
-constexpr uint32_t kZtOff = kPermOff + kPermBuffers * kPermBuf;
+constexpr uint32_t kZtOff = 0;
 constexpr uint32_t kZtBuf = kTile * kThreads * 8;
-#ifndef QMCG_ZT_BUFFERS
-#define QMCG_ZT_BUFFERS 1
-#endif
-// 2: double-buffered z tiles (one block barrier per tile); 1: single buffer and a
-// second barrier after the walk (smaller shared footprint).
-constexpr int kZtBuffers = QMCG_ZT_BUFFERS;
+constexpr int kZtBuffers = 2;
 constexpr uint32_t kLogOff = kZtOff + kZtBuffers * kZtBuf;
 constexpr uint32_t kBarOff = kLogOff + 128 * 16;
 constexpr uint32_t kWarpOff = kBarOff + 128;
@@ -494,40 +422,13 @@ __device__ __forceinline__ double rneg_threshold(const PriceParams& P, double be
   return room > 0.0 ? (log(room) - P.X0) / P.b : -INFINITY;
 }
 
-// Issue the bulk copy of one permutation row (date d) into row w of buffer b,
-// completing on that row's own mbarrier (bar[b][w]). Each warp stages the row
-// it generates, right after it has consumed the previous contents, so no warp
-// waits for a block-wide copy and no single thread issues a whole tile.
-__device__ __forceinline__ void issue_row(const PriceParams& P, uint32_t sbase, int d, int b, int w, int64_t col0,
-                                          uint32_t bytes) {
-  const uint32_t bar = sbase + kBarOff + (b * kTile + w) * 8;
-  const uint32_t dst = sbase + kPermOff + b * kPermBuf + w * kThreads * 4;
-  const uint32_t* src = P.perm + static_cast<int64_t>(d - P.perm_row0) * P.ld + col0;
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
-      "l"(src), "r"(bytes), "r"(bar)
-      : "memory");
-}
-
-// The same with the source row given as a pointer (advanced per tile by the caller).
-__device__ __forceinline__ void issue_row_src(const uint32_t* src, uint32_t sbase, int b, int w, uint32_t bytes) {
-  const uint32_t bar = sbase + kBarOff + (b * kTile + w) * 8;
-  const uint32_t dst = sbase + kPermOff + b * kPermBuf + w * kThreads * 4;
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
-      "l"(src), "r"(bytes), "r"(bar)
-      : "memory");
-}
-
 // One 2-D TMA copy of a whole tile (kTile dates x 256 paths of the [date][path]
-// table) into perm buffer b, completing on the buffer's mbarrier bar[b][0].
+// uniform table, f64) into tile buffer b, completing on the buffer's mbarrier bar[b][0].
 // Out-of-range rows/columns (last tile, last block) arrive zero-filled.
 __device__ __forceinline__ void issue_tile_tma(const CUtensorMap* tmap, uint32_t sbase, int b, int col, int row) {
   const uint32_t bar = sbase + kBarOff + b * kTile * 8;
-  const uint32_t dst = sbase + kPermOff + b * kPermBuf;
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(kPermBuf) : "memory");
+  const uint32_t dst = sbase + kZtOff + b * kZtBuf;
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(kZtBuf) : "memory");
   asm volatile(
       "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::
           "r"(dst),
@@ -558,7 +459,8 @@ __device__ __forceinline__ void mbar_wait_u32(uint32_t bar, uint32_t parity) {
 __device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(a, b); }
 __device__ __forceinline__ float add_rn(float a, float b) { return __fadd_rn(a, b); }
 
-// z-tile slot access: FP64 (8 B) or, for the FP32 variant, FP32 (4 B).
+// z-tile slot access (8-byte slots that first hold the uniform): FP64, or for the FP32 variant an
+// f32 in the slot's low half.
 template <bool F32> struct ZSlot;
 template <> struct ZSlot<false> {
   using T = double;
@@ -568,7 +470,7 @@ template <> struct ZSlot<false> {
 };
 template <> struct ZSlot<true> {
   using T = float;
-  static constexpr uint32_t kSize = 4;
+  static constexpr uint32_t kSize = 8;
   static __device__ __forceinline__ T load(uint32_t a) {
     float v;
     asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a) : "memory");
@@ -579,93 +481,73 @@ template <> struct ZSlot<true> {
   }
 };
 
-// The value a tail point parks in its slot until flush_tail: FP64 mode the
-// uniform u itself; FP32 mode the exact FP64 w = u or 1 - u rounded to FP32,
-// negative when y > 0 (w = 1 - u).
-template <bool F32>
-__device__ __forceinline__ typename ZSlot<F32>::T tail_park(double u, double y) {
-  if (F32) return static_cast<float>(y > 0.0 ? -__dadd_rn(1.0, -u) : u);
-  return u;
-}
-
 template <bool F32>
 __device__ __forceinline__ typename ZSlot<F32>::T central_z(double y, double alpha) {
   if (F32) return moro_central_f32(static_cast<float>(y), static_cast<float>(alpha));
   return moro_central_plus(y, alpha);
 }
 
-// UEXP: the generator's uniform u goes to the slot instead of the normal (parity
-// export of exactly the digits the pricing kernel computes; FP64 slots only).
-template <bool F32, bool UEXP>
-__device__ __forceinline__ typename ZSlot<F32>::T central_or_u(double u, double y, double alpha) {
-  static_assert(!(F32 && UEXP), "uniform export uses FP64 slots");
-  if constexpr (UEXP) return u;
-  else return central_z<F32>(y, alpha);
-}
-
-// Store one generated point: z in its slot; a tail point (|u - 1/2| > 0.42, the
-// reference's branch on the bit-exact uniform) then overwrites the slot with its
-// parked value and queues its index at ntail + rank. One predicate feeds the
-// ballot and both predicated stores (no selects, no dummy queue slots).
+// One point pair of a date row, in place: the slots hold u; a central point's slot gets
+// z + alpha, a tail point (|u - 1/2| > 0.42, the reference's branch on the bit-exact uniform)
+// keeps u and queues its index in the warp's tail queue at ntail + rank. The second chunk's
+// rank adds the first chunk's count in one 3-input add, and ntail advances by both counts.
 template <bool F32>
-__device__ __forceinline__ void park_point(uint32_t zslot, uint32_t qbase, uint32_t idx,
-                                           typename ZSlot<F32>::T z, typename ZSlot<F32>::T park, double y,
-                                           unsigned lt, uint32_t& ntail) {
-  unsigned b;
+__device__ __forceinline__ void park_pair(uint32_t sa, uint32_t sb, uint32_t qbase, uint32_t idx_a,
+                                          typename ZSlot<F32>::T za, double ya, typename ZSlot<F32>::T zb, double yb,
+                                          unsigned lt, uint32_t& ntail) {
   if constexpr (F32) {
     asm volatile(
-        "{\n .reg .pred p;\n .reg .f64 ay;\n .reg .b32 m, a;\n"
-        " abs.f64 ay, %4;\n setp.gt.f64 p, ay, %8;\n"
-        " vote.sync.ballot.b32 %0, p, 0xffffffff;\n"
-        " st.shared.f32 [%1], %2;\n @p st.shared.f32 [%1], %3;\n"
-        " and.b32 m, %0, %5;\n popc.b32 m, m;\n add.u32 a, %6, m;\n @p st.shared.u8 [a], %7;\n}"
-        : "=r"(b)
-        : "r"(zslot), "f"(z), "f"(park), "d"(y), "r"(lt), "r"(qbase + ntail), "r"(idx), "d"(c_tail_y)
+        "{\n .reg .pred pa, pb;\n .reg .f64 ay;\n .reg .b32 ba, bb, ca, ra, rb, q, a;\n"
+        " abs.f64 ay, %3;\n setp.gt.f64 pa, ay, %9;\n"
+        " abs.f64 ay, %6;\n setp.gt.f64 pb, ay, %9;\n"
+        " vote.sync.ballot.b32 ba, pa, 0xffffffff;\n"
+        " vote.sync.ballot.b32 bb, pb, 0xffffffff;\n"
+        " @!pa st.shared.f32 [%1], %2;\n @!pb st.shared.f32 [%4], %5;\n"
+        " add.u32 q, %7, %0;\n"
+        " and.b32 ra, ba, %8;\n popc.b32 ra, ra;\n popc.b32 ca, ba;\n"
+        " and.b32 rb, bb, %8;\n popc.b32 rb, rb;\n"
+        " add.u32 a, q, ra;\n @pa st.shared.u8 [a], %10;\n"
+        " add.u32 a, q, ca;\n add.u32 a, a, rb;\n @pb st.shared.u8 [a], %11;\n"
+        " popc.b32 bb, bb;\n add.u32 %0, %0, ca;\n add.u32 %0, %0, bb;\n}"
+        : "+r"(ntail)
+        : "r"(sa), "f"(za), "d"(ya), "r"(sb), "f"(zb), "d"(yb), "r"(qbase), "r"(lt), "d"(c_tail_y), "r"(idx_a),
+          "r"(idx_a + 32)
         : "memory");
   } else {
     asm volatile(
-        "{\n .reg .pred p;\n .reg .f64 ay;\n .reg .b32 m, a;\n"
-        " abs.f64 ay, %4;\n setp.gt.f64 p, ay, %8;\n"
-        " vote.sync.ballot.b32 %0, p, 0xffffffff;\n"
-        " st.shared.f64 [%1], %2;\n @p st.shared.f64 [%1], %3;\n"
-        " and.b32 m, %0, %5;\n popc.b32 m, m;\n add.u32 a, %6, m;\n @p st.shared.u8 [a], %7;\n}"
-        : "=r"(b)
-        : "r"(zslot), "d"(z), "d"(park), "d"(y), "r"(lt), "r"(qbase + ntail), "r"(idx), "d"(c_tail_y)
+        "{\n .reg .pred pa, pb;\n .reg .f64 ay;\n .reg .b32 ba, bb, ca, ra, rb, q, a;\n"
+        " abs.f64 ay, %3;\n setp.gt.f64 pa, ay, %9;\n"
+        " abs.f64 ay, %6;\n setp.gt.f64 pb, ay, %9;\n"
+        " vote.sync.ballot.b32 ba, pa, 0xffffffff;\n"
+        " vote.sync.ballot.b32 bb, pb, 0xffffffff;\n"
+        " @!pa st.shared.f64 [%1], %2;\n @!pb st.shared.f64 [%4], %5;\n"
+        " add.u32 q, %7, %0;\n"
+        " and.b32 ra, ba, %8;\n popc.b32 ra, ra;\n popc.b32 ca, ba;\n"
+        " and.b32 rb, bb, %8;\n popc.b32 rb, rb;\n"
+        " add.u32 a, q, ra;\n @pa st.shared.u8 [a], %10;\n"
+        " add.u32 a, q, ca;\n add.u32 a, a, rb;\n @pb st.shared.u8 [a], %11;\n"
+        " popc.b32 bb, bb;\n add.u32 %0, %0, ca;\n add.u32 %0, %0, bb;\n}"
+        : "+r"(ntail)
+        : "r"(sa), "d"(za), "d"(ya), "r"(sb), "d"(zb), "d"(yb), "r"(qbase), "r"(lt), "d"(c_tail_y), "r"(idx_a),
+          "r"(idx_a + 32)
         : "memory");
   }
+}
+
+// The same for one point (a row's odd last chunk).
+template <bool F32>
+__device__ __forceinline__ void park_one(uint32_t sa, uint32_t qbase, uint32_t idx, typename ZSlot<F32>::T za,
+                                         double ya, unsigned lt, uint32_t& ntail) {
+  const bool tail = moro_is_tail(ya);
+  const unsigned b = __ballot_sync(kFull, tail);
+  if (tail) sts_u8(qbase + ntail + __popc(b & lt), idx);
+  else ZSlot<F32>::store(sa, za);
   ntail += __popc(b);
 }
 
-// Two chunks' points at once (FP64): the queue base is formed once, the second
-// chunk's rank adds the first chunk's count in one 3-input add, and ntail
-// advances by both counts in another.
-__device__ __forceinline__ void park_pair(uint32_t zslot_a, uint32_t zslot_b, uint32_t qbase, uint32_t idx_a,
-                                          double za, double ua, double ya, double zb, double ub, double yb,
-                                          unsigned lt, uint32_t& ntail) {
-  asm volatile(
-      "{\n .reg .pred pa, pb;\n .reg .f64 ay;\n .reg .b32 ba, bb, ca, ra, rb, q, a;\n"
-      " abs.f64 ay, %4;\n setp.gt.f64 pa, ay, %11;\n"
-      " abs.f64 ay, %7;\n setp.gt.f64 pb, ay, %11;\n"
-      " vote.sync.ballot.b32 ba, pa, 0xffffffff;\n"
-      " vote.sync.ballot.b32 bb, pb, 0xffffffff;\n"
-      " st.shared.f64 [%1], %2;\n @pa st.shared.f64 [%1], %3;\n"
-      " st.shared.f64 [%5], %6;\n @pb st.shared.f64 [%5], %8;\n"
-      " add.u32 q, %9, %0;\n"
-      " and.b32 ra, ba, %10;\n popc.b32 ra, ra;\n popc.b32 ca, ba;\n"
-      " and.b32 rb, bb, %10;\n popc.b32 rb, rb;\n"
-      " add.u32 a, q, ra;\n @pa st.shared.u8 [a], %12;\n"
-      " add.u32 a, q, ca;\n add.u32 a, a, rb;\n @pb st.shared.u8 [a], %13;\n"
-      " popc.b32 bb, bb;\n add.u32 %0, %0, ca;\n add.u32 %0, %0, bb;\n}"
-      : "+r"(ntail)
-      : "r"(zslot_a), "d"(za), "d"(ua), "d"(ya), "r"(zslot_b), "d"(zb), "d"(yb), "d"(ub), "r"(qbase), "r"(lt),
-        "d"(c_tail_y), "r"(idx_a), "r"(idx_a + 32)
-      : "memory");
-}
-
-// One queued Moro-tail point: u (parked in its z slot) -> w = u or 1 - u,
-// z = +-P8(log(-log w)) + alpha. A queued point has u < 0.08 or u > 0.92, so
-// y = u - 1/2 > 0 iff the high word of u is at least that of 0.5 (integer
-// test, no FP64 compare); -x for y < 0 by flipping the sign bit.
+// One queued Moro-tail point: u (in its slot) -> w = u or 1 - u, z = +-P8(log(-log w)) + alpha.
+// A queued point has u < 0.08 or u > 0.92, so y = u - 1/2 > 0 iff the high word of u is at
+// least that of 0.5 (integer test, no FP64 compare); -x for y < 0 by flipping the sign bit.
 __device__ __forceinline__ double tail_z(double u, uint32_t logtab, double alpha) {
   const bool up = __double2hiint(u) >= 0x3fe00000;
   const double x = moro_tail_poly(up ? __dadd_rn(1.0, -u) : u, logtab);
@@ -692,9 +574,10 @@ __device__ __forceinline__ void flush_tail(uint32_t ws, uint32_t zrow, uint32_t 
       const uint32_t q = r + lane;
       if (q < ntail) {
         const uint32_t slot = zrow + lds_u8(qbase + q) * Z::kSize;
-        const float wsg = Z::load(slot);
-        const float x = moro_tail_poly_f32(fabsf(wsg));
-        Z::store(slot, (wsg < 0.0f ? x : -x) + static_cast<float>(alpha));
+        const double u = lds_f64(slot);
+        const bool up = __double2hiint(u) >= 0x3fe00000;
+        const float x = moro_tail_poly_f32(static_cast<float>(up ? __dadd_rn(1.0, -u) : u));
+        Z::store(slot, (up ? x : -x) + static_cast<float>(alpha));
       }
     }
   } else {
@@ -719,189 +602,31 @@ __device__ __forceinline__ void flush_tail(uint32_t ws, uint32_t zrow, uint32_t 
   __syncwarp();
 }
 
-// One point of a date row: tail test; a tail point parks u in its z slot and
-// queues its index (branch-free: other lanes write a dummy slot); otherwise
-// the central normal + alpha goes to the slot.
-template <bool CLAMP, bool F32, bool UEXP>
-__device__ __forceinline__ void finish_point(uint32_t ws, uint32_t zslot, uint32_t idx, double u, bool clamp,
-                                             double alpha, int lane, unsigned lt, uint32_t& ntail) {
-  if (CLAMP && clamp) u = clamp_endpoints(u);
-  const double y = __dadd_rn(u, -0.5);
-  park_point<F32>(zslot, ws + kWTailIdx, idx, central_or_u<F32, UEXP>(u, y, alpha), tail_park<F32>(u, y), y, lt,
-                  ntail);
-}
-
-// radical_inverse with the digits taken two at a time (DIM_PAIR): q = x / p^2,
-// r = x - q p^2, high digit (r * sm) >> ss, low digit r - high * p. The products
-// and the running sum are formed digit by digit in the reference's order.
-__device__ __forceinline__ double halton_pairs(uint32_t x, uint32_t p, const uint4& pp, int D,
-                                               const double2* __restrict__ sn) {
-  const uint32_t p2 = pp.x, m2 = pp.y, sh2 = pp.z & 0xffu, ss = pp.z >> 8, sm = pp.w;
-  double v = 0.0;
-  int j = 0;
-#pragma unroll 1
-  for (; j + 2 < D; j += 2) {  // digits j, j+1, neither the last
-    const uint32_t q = __umulhi(x, m2) >> sh2;
-    const uint32_t r = x - q * p2;
-    const uint32_t hi = (r * sm) >> ss;
-    const uint32_t lo = r - hi * p;
-    const double2 s0 = sn[j], s1 = sn[j + 1];
-    v = __dadd_rn(v, digit_term(lo, s0.x, s0.y));
-    v = __dadd_rn(v, digit_term(hi, s1.x, s1.y));
-    x = q;
-  }
-  if (j == D - 2) {  // two digits left: x < p^2
-    const uint32_t hi = (x * sm) >> ss;
-    const double2 s0 = sn[j], s1 = sn[j + 1];
-    v = __dadd_rn(v, digit_term(x - hi * p, s0.x, s0.y));
-    return __dadd_rn(v, digit_term(hi, s1.x, s1.y));
-  }
-  const double2 s0 = sn[j];
-  return __dadd_rn(v, digit_term(x, s0.x, s0.y));
-}
-
-// The same with the digit count fixed at compile time (fully unrolled; the
-// scale loads are independent of the division chain and issue early).
-template <int D>
-__device__ __forceinline__ double halton_pairs_fixed(uint32_t x, uint32_t p, const uint4& pp,
-                                                     const double2* __restrict__ sn) {
-  const uint32_t p2 = pp.x, m2 = pp.y, sh2 = pp.z & 0xffu, ss = pp.z >> 8, sm = pp.w;
-  double2 s[D];
-#pragma unroll
-  for (int j = 0; j < D; ++j) s[j] = __ldg(sn + j);
-  double v = 0.0;
-#pragma unroll
-  for (int j = 0; j + 2 < D; j += 2) {
-    const uint32_t q = __umulhi(x, m2) >> sh2;
-    const uint32_t r = x - q * p2;
-    const uint32_t hi = (r * sm) >> ss;
-    v = __dadd_rn(v, digit_term(r - hi * p, s[j].x, s[j].y));
-    v = __dadd_rn(v, digit_term(hi, s[j + 1].x, s[j + 1].y));
-    x = q;
-  }
-  if (D % 2 == 0) {
-    const uint32_t hi = (x * sm) >> ss;
-    v = __dadd_rn(v, digit_term(x - hi * p, s[D - 2].x, s[D - 2].y));
-    return __dadd_rn(v, digit_term(hi, s[D - 1].x, s[D - 1].y));
-  }
-  return __dadd_rn(v, digit_term(x, s[D - 1].x, s[D - 1].y));
-}
-
-template <bool WIDE>
-__device__ __forceinline__ double halton_any(uint32_t x, const uint4& dp, uint64_t m64, const double2* sn) {
-  return halton_digits<WIDE>(x, dp.x, dp.y, dp.z & 0xffu, m64, static_cast<int>((dp.z >> 8) & 0xffu), sn);
-}
-
-template <int D>
-__device__ __forceinline__ double halton_fixed(uint32_t x, uint32_t magic, uint32_t shift, uint32_t negp,
-                                               const double2 (&sc)[4]) {
-  // D digits, least significant first; the last digit is the remaining quotient.
-  double u;
-  uint32_t r = x;
-#pragma unroll
-  for (int j = 0; j < D; ++j) {
-    double term;
-    uint32_t q = 0;
-    if (j < D - 1) {
-      q = __umulhi(r, magic) >> shift;
-      term = digit_term(q * negp + r, sc[j].x, sc[j].y);
-    } else {
-      term = digit_term(r, sc[j].x, sc[j].y);
-    }
-    u = j == 0 ? term : __dadd_rn(u, term);
-    r = q;
-  }
-  return u;
-}
-
-// Two independent 32-path chunks (ch, ch + 1) of one fixed-digit row.
-template <int D, bool F32, bool UEXP>
-__device__ __forceinline__ void generate_chunk_pair(const double2 (&sc)[4], uint32_t magic, uint32_t shift,
-                                                    uint32_t negp, uint32_t ws, uint32_t prow, uint32_t zrow, int ch,
-                                                    int lane, unsigned lt, double alpha, uint32_t& ntail) {
-  using Z = ZSlot<F32>;
-  constexpr uint32_t kCh = 32 * Z::kSize;  // bytes per 32-path chunk of a row
-  const uint32_t xa = lds_u32(prow + ch * 128);  // tables hold perm + 1 (the Halton index)
-  const uint32_t xb = lds_u32(prow + ch * 128 + 128);
-  const double ua = halton_fixed<D>(xa, magic, shift, negp, sc);
-  const double ub = halton_fixed<D>(xb, magic, shift, negp, sc);
-  const double ya = __dadd_rn(ua, -0.5);
-  const double yb = __dadd_rn(ub, -0.5);
-  // UEXP (parity export): the slot receives the uniform itself, through the same digit code
-  const auto za = central_or_u<F32, UEXP>(ua, ya, alpha);
-  const auto zb = central_or_u<F32, UEXP>(ub, yb, alpha);
-  if constexpr (!F32) {
-    park_pair(zrow + ch * kCh, zrow + ch * kCh + kCh, ws + kWTailIdx, ch * 32 + lane, za, ua, ya, zb, ub, yb, lt,
-              ntail);
-  } else {
-    park_point<F32>(zrow + ch * kCh, ws + kWTailIdx, ch * 32 + lane, za, tail_park<F32>(ua, ya), ya, lt, ntail);
-    park_point<F32>(zrow + ch * kCh + kCh, ws + kWTailIdx, ch * 32 + 32 + lane, zb, tail_park<F32>(ub, yb), yb, lt,
-                    ntail);
-  }
-}
-
-template <int D, bool F32, bool UEXP>
-__device__ __forceinline__ uint32_t generate_row_fixed(const double2* sn, uint32_t magic, uint32_t shift,
-                                                       uint32_t negp, uint32_t ws, uint32_t prow, uint32_t zrow,
-                                                       int nchunks, int lane, unsigned lt, double alpha) {
-  using Z = ZSlot<F32>;
-  constexpr uint32_t kCh = 32 * Z::kSize;
-  double2 sc[4];
-#pragma unroll
-  for (int j = 0; j < 4; ++j) sc[j] = j < D ? __ldg(sn + j) : make_double2(0.0, 0.0);
+// One date row of the tile, in place: warp w turns row w of uniforms (already in shared
+// memory: the TMA'd uniform table, built bit-exactly by uniforms_kernel from the K1 tables) into
+// z + alpha. Two independent 32-path chunks in flight per iteration.
+template <bool F32>
+__device__ __forceinline__ void generate_row(uint32_t ws, uint32_t zrow, uint32_t logtab, int nchunks, int lane,
+                                             unsigned lt, double alpha) {
+  const uint32_t zl = zrow + lane * 8;
+  const uint32_t qbase = ws + kWTailIdx;
   uint32_t ntail = 0;
   int ch = 0;
 #pragma unroll 1
-  for (; ch + 1 < nchunks; ch += 2)  // two independent chunks in flight
-    generate_chunk_pair<D, F32, UEXP>(sc, magic, shift, negp, ws, prow, zrow, ch, lane, lt, alpha, ntail);
-  if (ch < nchunks) {
-    const uint32_t x = lds_u32(prow + ch * 128);
-    const double u = halton_fixed<D>(x, magic, shift, negp, sc);
-    finish_point<false, F32, UEXP>(ws, zrow + ch * kCh, ch * 32 + lane, u, false, alpha, lane, lt, ntail);
+  for (; ch + 1 < nchunks; ch += 2) {
+    const uint32_t sa = zl + ch * 256, sb = sa + 256;
+    const double ua = lds_f64(sa), ub = lds_f64(sb);
+    const double ya = __dadd_rn(ua, -0.5), yb = __dadd_rn(ub, -0.5);
+    park_pair<F32>(sa, sb, qbase, ch * 32 + lane, central_z<F32>(ya, alpha), ya, central_z<F32>(yb, alpha), yb, lt,
+                   ntail);
   }
-  return ntail;
-}
-
-template <bool SLOW, bool F32, bool UEXP = false>
-__device__ __forceinline__ void generate_row(const PriceParams& P, uint32_t ws, int d, uint32_t prow, uint32_t zrow,
-                                             uint32_t logtab, int nchunks, int lane, unsigned lt) {
-  using Z = ZSlot<F32>;
-  const uint4 dp = __ldg(reinterpret_cast<const uint4*>(P.dims) + d);
-  const uint32_t magic = dp.y, shift = dp.z & 0xffu, negp = 0u - dp.x;
-  const int D = static_cast<int>((dp.z >> 8) & 0xffu);
-  const double2* sn = P.scnc + dp.w;
-  const double alpha = P.alpha;
-  const uint32_t pl = prow + lane * 4;
-  const uint32_t zl = zrow + lane * Z::kSize;
-  uint32_t ntail = 0;
-  if (!SLOW && D == 3) {
-    ntail = generate_row_fixed<3, F32, UEXP>(sn, magic, shift, negp, ws, pl, zl, nchunks, lane, lt, alpha);
-  } else if (!SLOW && D == 4) {
-    ntail = generate_row_fixed<4, F32, UEXP>(sn, magic, shift, negp, ws, pl, zl, nchunks, lane, lt, alpha);
-  } else if (!SLOW && D == 2) {
-    ntail = generate_row_fixed<2, F32, UEXP>(sn, magic, shift, negp, ws, pl, zl, nchunks, lane, lt, alpha);
-  } else if (!SLOW && ((dp.z >> 16) & DIM_PAIR)) {
-    const uint4 pp = __ldg(P.pairs + d);
-    for (int ch = 0; ch < nchunks; ++ch) {
-      const uint32_t x = lds_u32(pl + ch * 128);
-      const double u = D == 5   ? halton_pairs_fixed<5>(x, dp.x, pp, sn)
-                       : D == 6 ? halton_pairs_fixed<6>(x, dp.x, pp, sn)
-                       : D == 7 ? halton_pairs_fixed<7>(x, dp.x, pp, sn)
-                                : halton_pairs(x, dp.x, pp, D, sn);
-      finish_point<false, F32, UEXP>(ws, zl + ch * 32 * Z::kSize, ch * 32 + lane, u, false, alpha, lane, lt, ntail);
-    }
-  } else {
-    const bool clamp = SLOW && ((dp.z >> 16) & DIM_CLAMP);
-    const bool wide = SLOW && ((dp.z >> 16) & DIM_WIDE);
-    const uint64_t m64 = wide ? __ldg(P.magic64 + d) : 0ull;
-    for (int ch = 0; ch < nchunks; ++ch) {
-      const uint32_t x = lds_u32(pl + ch * 128);
-      const double u = wide ? halton_any<true>(x, dp, m64, sn) : halton_any<false>(x, dp, m64, sn);
-      finish_point<SLOW, F32, UEXP>(ws, zl + ch * 32 * Z::kSize, ch * 32 + lane, u, clamp, alpha, lane, lt, ntail);
-    }
+  if (ch < nchunks) {
+    const uint32_t sa = zl + ch * 256;
+    const double ya = __dadd_rn(lds_f64(sa), -0.5);
+    park_one<F32>(sa, qbase, ch * 32 + lane, central_z<F32>(ya, alpha), ya, lt, ntail);
   }
 #ifndef QMCG_PROBE_NOTAIL  // timing probe only (wrong results): skip the Moro tail
-  if (!UEXP && ntail) flush_tail<F32>(ws, zrow, ntail, logtab, alpha, lane);
+  if (ntail) flush_tail<F32>(ws, zrow, ntail, logtab, alpha, lane);
 #endif
 }
 
@@ -991,8 +716,9 @@ constexpr int kPushGroup = QMCG_PUSH_GROUP;
 static_assert(kTile % kPushGroup == 0, "push groups tile the dates");
 
 // One block = 256 consecutive paths; thread i walks path i. Per tile of
-// kTile dates: (1) the permutation rows arrive by cp.async.bulk; (2) warp w
-// generates date row w of the tile (uniform -> normal, bit-exact uniforms);
+// kTile dates: (1) the tile's uniforms (the [date][path] uniform table: bit-exact
+// scrambled-Halton values built once per table by uniforms_kernel) arrive by one 2-D TMA
+// copy, double-buffered; (2) warp w turns date row w of the tile into normals in place;
 // (3) every thread walks its path through the tile: V_k = sum (z_j + alpha)
 // is the log-price in units of b, X_k = X0 + b V_k. A date k can only set the
 // foresight maximum max_k disc^k I_k if I_k exceeds every earlier intrinsic
@@ -1001,7 +727,8 @@ static_assert(kTile % kPushGroup == 0, "push groups tile the dates");
 // the new record k dominates it (S_k disc^(k-j) >= S_j, i.e. key_k >= key_j
 // with key = V - slope*date, slope = r*dt/b, calls), otherwise j is queued
 // for exact evaluation (exp + discount) in warp-wide batches of 32.
-// SLOW = any of: volatility 0, range checks, 64-bit magic, endpoint clamp.
+// SLOW = volatility 0 or range checks. One block barrier per tile: after it every warp has
+// generated tile k and walked tile k - 1, so the buffer of tile k - 1 takes tile k + 1.
 template <int KIND, bool RNEG, bool SLOW, bool F32>
 __global__ void __launch_bounds__(kThreads, QMCG_MINB)
     price_kernel(const PriceParams P, const __grid_constant__ CUtensorMap tmap) {
@@ -1027,9 +754,8 @@ __global__ void __launch_bounds__(kThreads, QMCG_MINB)
   const int ntiles = (dend - dbeg + kTile - 1) / kTile;
   const int64_t block_paths = min(static_cast<int64_t>(kThreads), P.path_count - block_first);
   const int nchunks = static_cast<int>((block_paths + 31) / 32);
-  // columns of this block in the table (16-byte aligned: path_begin - col_begin and ld are multiples of 4)
+  // columns of this block in the table
   const int64_t col0 = P.path_begin - P.col_begin + block_first;
-  const uint32_t bytes = static_cast<uint32_t>(((block_paths + 3) / 4) * 16);
   using Z = ZSlot<F32>;
   using T = typename Z::T;
   T slope = static_cast<T>(P.dom_slope);
@@ -1056,49 +782,27 @@ __global__ void __launch_bounds__(kThreads, QMCG_MINB)
   }
   if (threadIdx.x < 128) sts_v2f64(logtab + threadIdx.x * 16, c_log_table[threadIdx.x]);
   __syncthreads();
-  if (kTma) {
-    if (threadIdx.x == 0 && !det) {
-      issue_tile_tma(&tmap, sbase, 0, static_cast<int>(col0), dbeg - P.perm_row0);
-      if (ntiles > 1) issue_tile_tma(&tmap, sbase, 1, static_cast<int>(col0), dbeg + kTile - P.perm_row0);
-    }
-  } else if (lane == 0 && !det) {
-    if (dbeg + warp < dend) issue_row(P, sbase, dbeg + warp, 0, warp, col0, bytes);
-    if (kPermBuffers == 2 && dbeg + kTile + warp < dend) issue_row(P, sbase, dbeg + kTile + warp, 1, warp, col0, bytes);
+  if (threadIdx.x == 0 && !det) {
+    issue_tile_tma(&tmap, sbase, 0, static_cast<int>(col0), dbeg - P.perm_row0);
+    if (ntiles > 1) issue_tile_tma(&tmap, sbase, 1, static_cast<int>(col0), dbeg + kTile - P.perm_row0);
   }
 
   uint32_t rq_head = 0, rq_tail = 0;
   uint32_t err = 0;
-  // this warp's last staged row (date dbeg + warp + (kPermBuffers - 1) kTile), advanced one tile
-  // per pass: a pointer add instead of the row address arithmetic per copy
-  const uint32_t* nsrc = P.perm + static_cast<int64_t>(dbeg + warp + (kPermBuffers - 1) * kTile - P.perm_row0) * P.ld + col0;
 
   for (int k = 0; k < ntiles; ++k) {
     const int k0 = dbeg + k * kTile;
     const int b = k & 1;
-    const uint32_t zb = kZtBuffers == 2 ? b : 0;
-    const uint32_t zcol = sbase + kZtOff + zb * kZtBuf + threadIdx.x * Z::kSize;
-    if (kTma && !det) {
+    const uint32_t ztile = sbase + kZtOff + b * kZtBuf;
+    const uint32_t zcol = ztile + threadIdx.x * Z::kSize;
+    if (!det) {
       if (k0 + warp < dend) {
         mbar_wait_u32(sbase + kBarOff + b * kTile * 8, static_cast<uint32_t>((k >> 1) & 1));
-        generate_row<SLOW, F32>(P, ws, k0 + warp, sbase + kPermOff + b * kPermBuf + warp * kThreads * 4,
-                                sbase + kZtOff + zb * kZtBuf + warp * kThreads * Z::kSize, logtab, nchunks, lane, lt);
+        generate_row<F32>(ws, ztile + warp * kThreads * Z::kSize, logtab, nchunks, lane, lt, P.alpha);
       }
-      __syncthreads();  // z tile complete; perm buffer b consumed by every warp
-      if (threadIdx.x == 0 && k + 2 < ntiles)
-        issue_tile_tma(&tmap, sbase, b, static_cast<int>(col0), k0 + 2 * kTile - P.perm_row0);
-    } else if (!det) {
-      if (k0 + warp < dend) {
-        const int pb = kPermBuffers == 2 ? b : 0;
-        mbar_wait_u32(sbase + kBarOff + (pb * kTile + warp) * 8,
-                      static_cast<uint32_t>(kPermBuffers == 2 ? (k >> 1) & 1 : k & 1));
-        generate_row<SLOW, F32>(P, ws, k0 + warp, sbase + kPermOff + pb * kPermBuf + warp * kThreads * 4,
-                                sbase + kZtOff + zb * kZtBuf + warp * kThreads * Z::kSize, logtab, nchunks, lane, lt);
-        __syncwarp();  // this warp's perm row is consumed: stage its row of the tile kPermBuffers ahead
-        const int dn = k0 + kPermBuffers * kTile + warp;
-        nsrc += kTile * P.ld;  // row dn of this warp's column slice
-        if (lane == 0 && dn < dend) issue_row_src(nsrc, sbase, pb, warp, bytes);
-      }
-      __syncthreads();  // z tile complete
+      __syncthreads();  // tile k generated; every warp has walked tile k - 1: its buffer takes tile k + 1
+      if (threadIdx.x == 0 && k >= 1 && k + 1 < ntiles)
+        issue_tile_tma(&tmap, sbase, b ^ 1, static_cast<int>(col0), k0 + kTile - P.perm_row0);
     }
     // ---- walk ----
     // c = V of the last record (= the pending record when pend_d >= 0);
@@ -1183,7 +887,6 @@ __global__ void __launch_bounds__(kThreads, QMCG_MINB)
         }
       }
     }
-    if (kZtBuffers == 1) __syncthreads();  // the z tile is rewritten by the next generation
     if (RNEG && rq_tail - rq_head >= 32) {  // r < 0: the threshold follows the evaluated best
       __syncwarp();
       process_records_inline<KIND, RNEG>(P, ws, rq_head, 32, lane);
@@ -1252,14 +955,13 @@ __global__ void __launch_bounds__(kThreads, QMCG_MINB)
 }
 
 // Generation only (batches): the QMC normal table z[d][p] = moro_inv_cnd of the
-// bit-exact scrambled-Halton uniform, for all dates of this block's 256 paths.
-// Same tile staging and generation as price_kernel; rows are then streamed to
-// HBM (coalesced, 2 KB per warp-row).
+// bit-exact scrambled-Halton uniform, for all dates of this block's 256 paths: each warp
+// loads its row of the uniform table (coalesced) into its shared-memory row and turns it into
+// normals in place with the pricing kernel's generate_row; rows are then streamed to HBM
+// (coalesced, 2 KB per warp-row).
 // MODE kGenPrefix: instead of z, each path's running sum S_k = z_0 + ... + z_k (the
 // contract-independent part of the batch walk, V_k = S_k + (k+1) alpha_c).
-// MODE kGenUniform: the scrambled-Halton uniforms the generator computes (parity
-// export of the pricing kernel's own digit code, generate_row<..., UEXP>).
-template <bool SLOW, int MODE>
+template <int MODE>
 __global__ void __launch_bounds__(kThreads, QMCG_MINB) gen_z_kernel(const PriceParams P, double* __restrict__ z,
                                                                     int64_t ldz) {
   constexpr bool PREFIX = MODE == kGenPrefix;
@@ -1278,30 +980,22 @@ __global__ void __launch_bounds__(kThreads, QMCG_MINB) gen_z_kernel(const PriceP
   const int64_t block_paths = min(static_cast<int64_t>(kThreads), P.path_count - block_first);
   const int nchunks = static_cast<int>((block_paths + 31) / 32);
   const int64_t col0 = P.path_begin - P.col_begin + block_first;
-  const uint32_t bytes = static_cast<uint32_t>(((block_paths + 3) / 4) * 16);
-  init_row_barriers(sbase);
   if (threadIdx.x < 128) sts_v2f64(logtab + threadIdx.x * 16, c_log_table[threadIdx.x]);
   __syncthreads();
-  if (lane == 0) {
-    if (dbeg + warp < dend) issue_row(P, sbase, dbeg + warp, 0, warp, col0, bytes);
-    if (kPermBuffers == 2 && dbeg + kTile + warp < dend) issue_row(P, sbase, dbeg + kTile + warp, 1, warp, col0, bytes);
-  }
   double run = 0.0;  // PREFIX: S of this thread's path
   const int64_t my = P.path_begin + block_first + threadIdx.x;
+  const uint32_t ztile = sbase + kZtOff;
+  const uint32_t zrow = ztile + warp * kThreads * 8;
   for (int k = 0; k < ntiles; ++k) {
     const int k0 = dbeg + k * kTile;
-    const int b = k & 1;
-    const uint32_t ztile = sbase + kZtOff + (kZtBuffers == 2 ? b : 0) * kZtBuf;
-    const uint32_t zrow = ztile + warp * kThreads * 8;
     if (k0 + warp < dend) {
-      const int pb = kPermBuffers == 2 ? b : 0;
-      mbar_wait_u32(sbase + kBarOff + (pb * kTile + warp) * 8,
-                    static_cast<uint32_t>(kPermBuffers == 2 ? (k >> 1) & 1 : k & 1));
-      generate_row<SLOW, false, MODE == kGenUniform>(P, ws, k0 + warp, sbase + kPermOff + pb * kPermBuf + warp * kThreads * 4,
-                                                     zrow, logtab, nchunks, lane, lt);
-      __syncwarp();  // perm row consumed: stage this warp's row of the tile kPermBuffers ahead
-      const int dn = k0 + kPermBuffers * kTile + warp;
-      if (lane == 0 && dn < dend) issue_row(P, sbase, dn, pb, warp, col0, bytes);
+      const double* src = P.table + static_cast<int64_t>(k0 + warp - P.perm_row0) * P.ld + col0;
+      for (int ch = 0; ch < nchunks; ++ch) {  // padding lanes of the last chunk get a central u
+        const int idx = ch * 32 + lane;
+        sts_f64(zrow + idx * 8, idx < block_paths ? __ldg(src + idx) : 0.5);
+      }
+      __syncwarp();
+      generate_row<false>(ws, zrow, logtab, nchunks, lane, lt, P.alpha);
       if (!PREFIX) {
         __syncwarp();
         double* dst = z + static_cast<int64_t>(k0 + warp - dbeg) * ldz + P.path_begin + block_first;
@@ -1320,19 +1014,18 @@ __global__ void __launch_bounds__(kThreads, QMCG_MINB) gen_z_kernel(const PriceP
         }
       }
     }
-    __syncthreads();  // z tile b stored
+    __syncthreads();  // the tile's rows are stored before they are reloaded
   }
 }
 
 // European pricing (reference mc_european_price, mc_european.cpp:11-46, with
 // simulate_terminal, path_engine.cpp:154-172): one GBM step of width T from the
-// dimension-0 scrambled-Halton normal, discounted intrinsic per path.
-__global__ void european_kernel(const uint32_t* __restrict__ perm_row, int64_t count, DimParam dp,
-                                const double* __restrict__ sc, const double* __restrict__ nc, double s0, double a,
-                                double bsd, double strike, double disc, int kind, double* __restrict__ out) {
+// dimension-0 scrambled-Halton normal (row 0 of the uniform table), discounted intrinsic per path.
+__global__ void european_kernel(const double* __restrict__ urow, int64_t count, double s0, double a, double bsd,
+                                double strike, double disc, int kind, double* __restrict__ out) {
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= count) return;
-  const double z = moro_full(halton(perm_row[i], dp, sc, nc));  // table entry = perm + 1
+  const double z = moro_full(urow[i]);
   const double st = s0 * exp(fma(bsd, z, a));
   const double diff = kind == 0 ? st - strike : strike - st;
   out[i] = disc * (diff > 0.0 ? diff : 0.0);
@@ -1726,7 +1419,7 @@ int leaf_depth(int64_t len) {
 
 }  // namespace
 
-// Tensor map of the permutation table slice for the pricing kernel's tile copies:
+// Tensor map of the uniform-table slice (f64) for the pricing kernel's tile copies:
 // dim 0 = columns (ld entries per row), dim 1 = the rows [0, d_end - perm_row0),
 // box = kTile rows x kThreads columns (one tile of one block).
 cudaError_t encode_perm_tmap(const PriceParams& P, CUtensorMap* map) {
@@ -1742,10 +1435,10 @@ cudaError_t encode_perm_tmap(const PriceParams& P, CUtensorMap* map) {
   });
   if (init_err != cudaSuccess) return init_err;
   const cuuint64_t dims[2] = {static_cast<cuuint64_t>(P.ld), static_cast<cuuint64_t>(P.d_end - P.perm_row0)};
-  const cuuint64_t strides[1] = {static_cast<cuuint64_t>(P.ld) * sizeof(uint32_t)};
+  const cuuint64_t strides[1] = {static_cast<cuuint64_t>(P.ld) * sizeof(double)};
   const cuuint32_t box[2] = {static_cast<cuuint32_t>(kThreads), static_cast<cuuint32_t>(kTile)};
   const cuuint32_t estr[2] = {1, 1};
-  const CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, const_cast<uint32_t*>(P.perm), dims, strides, box,
+  const CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(P.table), dims, strides, box,
                             estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
@@ -1759,7 +1452,7 @@ cudaError_t launch_price_t(const PriceParams& P, cudaStream_t s) {
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   if (e != cudaSuccess) return e;
   alignas(64) CUtensorMap tmap{};
-  if (kTma && !(SLOW && P.deterministic)) {
+  if (!(SLOW && P.deterministic)) {
     e = encode_perm_tmap(P, &tmap);
     if (e != cudaSuccess) return e;
   }
@@ -1769,7 +1462,7 @@ cudaError_t launch_price_t(const PriceParams& P, cudaStream_t s) {
 
 template <int KIND, bool RNEG>
 cudaError_t launch_price_k(const PriceParams& P, cudaStream_t s) {
-  const bool slow = P.any_wide || P.any_clamp || P.deterministic || P.check_range;
+  const bool slow = P.deterministic || P.check_range;  // digit division / clamp live in the table build
   if (P.fp32)
     return slow ? launch_price_t<KIND, RNEG, true, true>(P, s) : launch_price_t<KIND, RNEG, false, true>(P, s);
   return slow ? launch_price_t<KIND, RNEG, true, false>(P, s) : launch_price_t<KIND, RNEG, false, false>(P, s);
@@ -1806,10 +1499,7 @@ cudaError_t launch_gen_z(const PriceParams& P, double* z, int64_t ldz, cudaStrea
   cudaError_t e = ensure_log_table(s);
   if (e != cudaSuccess) return e;
   const int64_t blocks = (P.path_count + kThreads - 1) / kThreads;
-  const bool slow = P.any_wide || P.any_clamp;
-  auto kern = mode == kGenPrefix    ? (slow ? gen_z_kernel<true, kGenPrefix> : gen_z_kernel<false, kGenPrefix>)
-              : mode == kGenUniform ? (slow ? gen_z_kernel<true, kGenUniform> : gen_z_kernel<false, kGenUniform>)
-                                    : (slow ? gen_z_kernel<true, kGenZ> : gen_z_kernel<false, kGenZ>);
+  auto kern = mode == kGenPrefix ? gen_z_kernel<kGenPrefix> : gen_z_kernel<kGenZ>;
   e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmemBytes));
   if (e != cudaSuccess) return e;
   kern<<<static_cast<unsigned>(blocks), kThreads, kSmemBytes, s>>>(P, z, ldz);
@@ -2051,12 +1741,10 @@ cudaError_t launch_price(const PriceParams& P, cudaStream_t s) {
   return P.rate_negative ? launch_price_k<1, true>(P, s) : launch_price_k<1, false>(P, s);
 }
 
-cudaError_t launch_european(const uint32_t* perm_row, int64_t count, DimParam dp, const double* sc, const double* nc,
-                            double s0, double a, double bsd, double strike, double disc, int kind, double* out,
-                            cudaStream_t s) {
+cudaError_t launch_european(const double* urow, int64_t count, double s0, double a, double bsd, double strike,
+                            double disc, int kind, double* out, cudaStream_t s) {
   const int64_t blocks = (count + 255) / 256;
-  european_kernel<<<static_cast<unsigned>(blocks), 256, 0, s>>>(perm_row, count, dp, sc, nc, s0, a, bsd, strike, disc,
-                                                                kind, out);
+  european_kernel<<<static_cast<unsigned>(blocks), 256, 0, s>>>(urow, count, s0, a, bsd, strike, disc, kind, out);
   return cudaGetLastError();
 }
 
@@ -2076,17 +1764,14 @@ namespace {
 // prices[k][p] (point-major, coalesced stores): S at t_1..t_m, T from
 // s = s * exp(a + bsd * z) with the reference's operation order (gbm_step,
 // path_engine.hpp:51-56: drift and diffusion rounded separately, no FMA).
-__global__ void path_matrix_kernel(const uint32_t* __restrict__ table, int64_t ld, const DimParam* __restrict__ dims,
-                                   const double* __restrict__ sc, const double* __restrict__ nc, int64_t n,
-                                   int points, double s0, double a, double bsd, double* __restrict__ out,
-                                   uint32_t* err) {
+__global__ void path_matrix_kernel(const double* __restrict__ table, int64_t ld, int64_t n, int points, double s0,
+                                   double a, double bsd, double* __restrict__ out, uint32_t* err) {
   const int64_t p = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (p >= n) return;
   double s = s0;
   uint32_t e = 0;
   for (int k = 0; k < points; ++k) {
-    const DimParam dp = dims[k];
-    const double z = moro_full(halton(table[k * ld + p], dp, sc, nc));  // table entry = perm + 1
+    const double z = moro_full(table[k * ld + p]);  // the uniform table: uniform_at(p, k)
     if (!(s > 0.0)) e |= ERR_SPOT_NONPOSITIVE;  // gbm_step's s_prev check
     s = __dmul_rn(s, exp(__dadd_rn(a, __dmul_rn(bsd, z))));
     __stcs(out + k * n + p, s);
@@ -2162,11 +1847,10 @@ __global__ void sweep_kernel(const double* __restrict__ prices, int64_t n, int m
 }
 }  // namespace
 
-cudaError_t launch_path_matrix(const uint32_t* table, int64_t ld, const DimParam* dims, const double* sc,
-                               const double* nc, int64_t n, int points, double s0, double a, double bsd, double* out,
-                               uint32_t* err, cudaStream_t s) {
-  path_matrix_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(table, ld, dims, sc, nc, n, points, s0,
-                                                                             a, bsd, out, err);
+cudaError_t launch_path_matrix(const double* table, int64_t ld, int64_t n, int points, double s0, double a,
+                               double bsd, double* out, uint32_t* err, cudaStream_t s) {
+  path_matrix_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(table, ld, n, points, s0, a, bsd, out,
+                                                                             err);
   return cudaGetLastError();
 }
 

@@ -21,34 +21,20 @@ struct DimParam {
   uint32_t flags;    // DIM_CLAMP: endpoint clamp can trigger; DIM_WIDE: 64-bit magic
   uint64_t magic64;  // ceil(2^64 / p) for DIM_WIDE
 };
-// Kernel-side packed form: {p, magic, shift | ndig << 8 | flags << 16, doff}
-// (one 16-byte uniform load per date) and interleaved {sc[j], nc[j]} pairs.
-struct DimPack {
-  uint32_t p, magic, meta, doff;
-};
-// DIM_PAIR: digits extracted two at a time (divide by p^2, then split the
-// remainder by p), which halves the dependent division chain of bases with
-// many digits; pairs[d] = {p^2, magic(p^2), shift(p^2) | split_shift << 8, split_magic}.
-enum : uint32_t { DIM_CLAMP = 1u, DIM_WIDE = 2u, DIM_PAIR = 4u };
+enum : uint32_t { DIM_CLAMP = 1u, DIM_WIDE = 2u };
 
 // Error bits raised by the pricing kernel (mapped to the reference's
 // exception text on the host).
 enum : uint32_t { ERR_SPOT_NONPOSITIVE = 1u, ERR_SPOT_NONFINITE = 2u };
 
 struct PriceParams {
-  const uint32_t* perm;  // [m][ld] permutation table slice (column = path - col_begin)
+  const double* table;   // [m][ld] uniform-table slice: uniform_at(path, date), column = path - col_begin
   int64_t ld;            // row stride of the table
   int64_t col_begin;     // first path held by the table
   int64_t path_begin;    // first path of this launch
   int64_t path_count;    // paths in this launch
   int32_t m;             // exercise dates (dims used: 0..m-1)
   int32_t kind;          // 0 call, 1 put
-  const DimPack* dims;
-  const double2* scnc;     // {sc[j], nc[j]} per digit, indexed by DimPack::doff
-  const uint64_t* magic64; // per dimension, used when any dimension needs it
-  const uint4* pairs;      // per dimension, DIM_PAIR parameters
-  int32_t any_wide;        // some dimension needs the 64-bit magic division
-  int32_t any_clamp;       // some dimension can hit the endpoint clamp
   const double* dpow;    // dpow[k] = disc^k as the host's rounded chain, k = 0..m
   double X0;             // log(spot)
   double b;              // log-price scale: X_k = X0 + b * V_k
@@ -121,16 +107,14 @@ struct BatchParams {
 };
 
 // ---- launchers (kernels.cu) ----
-// Generation only: the QMC normal table z[d][p] (d < m, p in [path_begin, +path_count)) of the
-// context's permutation table (PriceParams fields perm/ld/col_begin/dims/... ; alpha ignored).
+// Generation only: the QMC normal table z[d][p] (d < m, p in [path_begin, +path_count)) from the
+// context's uniform table (PriceParams fields table/ld/col_begin/perm_row0/d_begin/d_end; + alpha).
 cudaError_t launch_walk_group(const BatchParams& B, int kind, cudaStream_t s);  // the batch walk reads prefix sums S (gen_z prefix mode)
 // mode: kGenZ (normals), kGenPrefix (per-path running sums of the normals, the batch walk's input),
-// kGenUniform (the uniforms themselves: parity export of the pricing kernel's generator).
-enum : int { kGenZ = 0, kGenPrefix = 1, kGenUniform = 2 };
+enum : int { kGenZ = 0, kGenPrefix = 1 };
 cudaError_t launch_gen_z(const PriceParams& P, double* z, int64_t ldz, cudaStream_t s, int mode = kGenZ);
-cudaError_t launch_european(const uint32_t* perm_row, int64_t count, DimParam dp, const double* sc, const double* nc,
-                            double s0, double a, double bsd, double strike, double disc, int kind, double* out,
-                            cudaStream_t s);
+cudaError_t launch_european(const double* urow, int64_t count, double s0, double a, double bsd, double strike,
+                            double disc, int kind, double* out, cudaStream_t s);
 // Pairwise sums of `count` contiguous vectors v[c*len .. (c+1)*len) into out2[2c, 2c+1].
 cudaError_t launch_pairwise_batched(const double* v, int64_t len, int count, double* scratch, double* out2,
                                     cudaStream_t s, int* launches);
@@ -138,19 +122,20 @@ cudaError_t launch_price(const PriceParams& P, cudaStream_t s);
 // K1: Fisher-Yates permutation of length n for LCG seed `seed64` into out[0..n).
 // scratch must hold perm_scratch_bytes(n) bytes.
 size_t perm_scratch_bytes(int64_t n);
-cudaError_t launch_path_matrix(const uint32_t* table, int64_t ld, const DimParam* dims, const double* sc,
-                               const double* nc, int64_t n, int points, double s0, double a, double bsd, double* out,
-                               uint32_t* err, cudaStream_t s);
+cudaError_t launch_path_matrix(const double* table, int64_t ld, int64_t n, int points, double s0, double a,
+                               double bsd, double* out, uint32_t* err, cudaStream_t s);
 cudaError_t launch_transpose(const double* in, int64_t rows, int64_t cols, double* out, cudaStream_t s);
 cudaError_t launch_sweep(const double* prices, int64_t n, int m, double spot, double strike, double rate, double vol,
                          double dt, double disc, int kind, double* values, int32_t* exercise, cudaStream_t s);
 cudaError_t launch_perm_build(uint64_t seed64, int64_t n, uint32_t* out, void* scratch,
                               size_t scratch_bytes, cudaStream_t s, int* launches, uint32_t add);
-// Copy columns [c0, c1) of a freshly built permutation into a table row.
+// uniform_at (or, with `normals`, normal_at) of `count` table entries perm + 1 of one dimension:
+// radical_inverse with the reference's rounding (bit-exact). Builds the rows of the uniform table
+// from K1's permutations (normals = 0) and serves the D1 exports.
 cudaError_t launch_uniforms(const uint32_t* perm_row, int64_t count, DimParam dp, const double* sc,
                             const double* nc, int normals, double* out, cudaStream_t s);
-// Row stride (in paths) of the permutation table: padded so every row starts
-// 16-byte aligned for the bulk-copy staging of K2.
+// Row stride (in paths) of the uniform table: padded to 64 entries so every row starts 512-byte
+// aligned (the TMA tile copies of K2 need 16).
 inline int64_t table_ld(int64_t cols) { return (cols + 63) / 64 * 64; }
 // Extra elements allocated after the last row (bulk copies of a partial block
 // may read up to one block past the end of a row).

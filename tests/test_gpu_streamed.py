@@ -14,7 +14,7 @@ REF = (100.0, 100.0, 0.05, 0.2, 1.0)
 
 
 def row_bytes(cols):
-    return (cols + 63) // 64 * 64 * 4
+    return (cols + 63) // 64 * 64 * 8  # the uniform table: f64 entries
 
 
 CASES = [  # (spec, kind, m, n, fp32)

@@ -24,7 +24,7 @@ out.append(ctx.price_american(q.OptionSpec(100.0, 95.0, -0.02, 0.3, 1.0), 12, 20
 check()
 out.append(ctx.price_american(q.OptionSpec(100.0, 100.0, 0.05, 0.0, 1.0), 6, 100, 7).price)   # sigma = 0
 check()
-ctx.set_table_budget(8 * 4 * 4224)                                              # streamed date windows
+ctx.set_table_budget(8 * 8 * 4224)                                              # streamed date windows
 out.append(ctx.price_american(spec, 40, 4097, 42).price)
 check()
 ctx.set_table_budget(0)
