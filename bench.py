@@ -70,12 +70,20 @@ class ClockSampler:
         self.proc = None
 
     def __enter__(self):
+        self.first = []
         try:
             self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}",
                                           "--format=csv,noheader,nounits", "-lms", "100"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except OSError:
             self.proc = None
+            return self
+        # nvidia-smi needs a few hundred ms to start: wait for its first sample so that the samples
+        # cover the timed region that follows (a K = 20 step region lasts only ~0.25 s)
+        import select
+        ready, _, _ = select.select([self.proc.stdout], [], [], 5.0)
+        if ready:
+            self.first.append(self.proc.stdout.readline())
         return self
 
     def __exit__(self, *exc):
@@ -87,7 +95,7 @@ class ClockSampler:
             except subprocess.TimeoutExpired:
                 self.proc.kill()
                 out, _ = self.proc.communicate()
-            self.lines = [ln for ln in out.splitlines() if ln.strip()]
+            self.lines = [ln for ln in out.splitlines() if ln.strip()]  # samples during the timed regions
 
     def summary(self):
         sm, smax, reasons = [], None, set()
@@ -371,15 +379,12 @@ def main():
         if rep:
             cold_e2e.append(w)
 
-    def timed(spec, allow_put=False, sample_clocks=False):
+    def timed(spec, allow_put=False):
         for _ in range(warmup):
             price(spec, M_DATES, n_paths, allow_put=allow_put)
         if dist:
             dist.barrier()
         sync_all()
-        sampler = ClockSampler(sorted({dv for dv, _ in members})[0]) if sample_clocks else None
-        if sampler:
-            sampler.__enter__()
         launches = 0
         tm = DeviceTimer()
         t0 = time.perf_counter()
@@ -389,15 +394,20 @@ def main():
             launches += ctx.last_launch_count()
         dev_ms = tm.stop()
         wall = time.perf_counter() - t0
-        if sampler:
-            sampler.__exit__(None, None, None)
         if dist:
             dist.barrier()
             dev_ms, wall = max_over_ranks(dev_ms, wall)
-        return dev_ms / steps, wall / steps, res, launches, (sampler.summary() if sampler else None)
+        return dev_ms / steps, wall / steps, res, launches
 
-    ms_call, wall_call, (price_c, se), launches, clocks = timed(call, sample_clocks=True)
-    ms_put, wall_put, (price_put, se_put), _, _ = timed(put, allow_put=True)
+    # clocks sampled across both timed regions (call, then put)
+    for _ in range(warmup):
+        price(call, M_DATES, n_paths)
+    sampler = ClockSampler(sorted({dv for dv, _ in members})[0])
+    sampler.__enter__()
+    ms_call, wall_call, (price_c, se), launches = timed(call)
+    ms_put, wall_put, (price_put, se_put), _ = timed(put, allow_put=True)
+    sampler.__exit__(None, None, None)
+    clocks = sampler.summary()
 
     # ---- dominant kernel alone (CUDA events around price_kernel on each pricing stream), every N:
     # one GPU / a group: qmcg_time_device (max over members); ranks: this rank's nodes, max over ranks ----
@@ -462,6 +472,7 @@ def main():
     except OSError:
         pass
     fp64_per_step = prof.get("fp64_inst_per_path_step")
+    bytes_per_step = prof.get("algorithmic_bytes_per_path_step", 8)  # one f64 uniform-table entry
     roofline = None
     # per-device work: each device prices n_paths / n_gpus paths in kernel_ms
     dev_path_steps = path_steps / n_gpus
@@ -473,10 +484,10 @@ def main():
                     "algorithmic_per_path_step": fp64_per_step,
                     "peak_source": "measured live: DFMA issue-rate probe (qmcg_fp64_peak) on this GPU",
                     "kernel_ms": kernel_ms, "per_device": n_gpus > 1,
-                    "hbm": {"achieved": 4.0 * dev_path_steps / (kernel_ms * 1e-3) / 1e9,
+                    "hbm": {"achieved": bytes_per_step * dev_path_steps / (kernel_ms * 1e-3) / 1e9,
                             "peak": peaks.get("hbm_gbs", 6650.0), "unit": "GB/s",
-                            "frac": 4.0 * dev_path_steps / (kernel_ms * 1e-3) / 1e9 / peaks.get("hbm_gbs", 6650.0),
-                            "algorithmic_bytes_per_path_step": 4,
+                            "frac": bytes_per_step * dev_path_steps / (kernel_ms * 1e-3) / 1e9 / peaks.get("hbm_gbs", 6650.0),
+                            "algorithmic_bytes_per_path_step": bytes_per_step,
                             "peak_source": "MEASURED_PEAKS.json" if "hbm_gbs" in peaks else "fallback"}}
         if n_gpus > 1:
             roofline["note"] = ("per device: the slowest device's pricing kernel over its n/N paths; traffic is the "
@@ -489,7 +500,7 @@ def main():
             issue_ach = wi * (dev_path_steps / 32) / (kernel_ms * 1e-3)
             roofline["issue"] = {"achieved": issue_ach / 1e12, "peak": issue_peak / 1e12, "unit": "T warp-inst/s",
                                  "frac": issue_ach / issue_peak, "warp_inst_per_warp_date": wi,
-                                 "note": "FP64 instructions are 30% of the kernel's issue slots; the schedulers' "
+                                 "note": "FP64 instructions are a third of the kernel's issue slots; the schedulers' "
                                          "issue rate, not the FP64 pipe, bounds the kernel"}
 
     cpu = None
@@ -538,8 +549,9 @@ def main():
                 "data": "synthetic (QMC paths from the reference's scrambled Halton stream, seed 42)",
                 "config": {"workload": WORKLOAD, "n_paths": n_paths, "m_dates": M_DATES, "seed": SEED,
                            "parallelism": f"paths sharded over {n_gpus} GPU(s) (pairwise-tree nodes); {layout}",
-                           "tables": "warm: permutation tables resident in HBM (cold call measured separately)",
-                           "l2": "inputs larger than L2 (4 B x 2^24 x 256 = 17.2 GB of tables per step)"},
+                           "tables": "warm: the uniform table (uniform_at of every date and path, built from the K1 "
+                                     "permutations) resident in HBM; the cold call is measured separately",
+                           "l2": "inputs larger than L2 (8 B x 2^24 x 256 = 34.4 GB of uniform table per step)"},
                 "e2e": {"value": e2e_value, "unit": "path-steps/s", "h2d_bytes_per_step": 48,
                         "d2h_bytes_per_step": 20, "ms_per_option": 1e3 * wall_call,
                         "bytes_note": "in: the 48-byte qmcg_option_spec, which reaches the device inside the "
