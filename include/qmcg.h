@@ -45,7 +45,7 @@ enum { QMCG_METHOD_CLOSED_FORM = 0, QMCG_METHOD_EUROPEAN_MC = 1, QMCG_METHOD_AME
 /* flags */
 enum {
   QMCG_FLAG_ALLOW_PUT = 1u << 0, /* opt-in put extension (reference rejects puts: american.cpp:106-109) */
-  QMCG_FLAG_NO_CACHE = 1u << 1,  /* rebuild the permutation tables for this call (cold timing) */
+  QMCG_FLAG_NO_CACHE = 1u << 1,  /* rebuild the uniform tables for this call (cold timing) */
   QMCG_FLAG_FP32 = 1u << 2,      /* FP32 normals + walk (uniforms stay bit-exact FP64); price within QMC error */
 };
 
@@ -71,14 +71,14 @@ typedef struct {
 
 typedef struct qmcg_ctx qmcg_ctx;
 
-/* Context on one CUDA device: owns the stream, scratch and the permutation-table
+/* Context on one CUDA device: owns the stream, scratch and the uniform-table
  * cache keyed by (seed, n_paths). */
 qmcg_status qmcg_create(int device, qmcg_ctx** out);
 /* Context over a device group (one process, n_dev listed CUDA devices; a device may be listed
  * more than once). It replaces the reference's host thread pool (ExecPolicy lanes,
  * proj/src/path_engine.cpp:83-122, and the fork-join reduction :51-59) at the GPU level:
  * qmcg_price_american shards the paths as whole pairwise-tree nodes over the members (member r
- * owns a contiguous column slice of the permutation tables), each member reduces its nodes and
+ * owns a contiguous column slice of the uniform tables), each member reduces its nodes and
  * the host folds the 16-byte node sums with the reference's tree, so results are bit-identical
  * to one device for any member count. Cold tables are built dimension-sharded (dim d on member
  * d mod n_dev) and column slices copied peer to peer; tables larger than memory are streamed in
@@ -145,7 +145,7 @@ qmcg_status qmcg_tree_node_range(int64_t n_paths, int depth, int64_t node, int64
 qmcg_status qmcg_combine_nodes(int64_t n_paths, int depth, const double* node_sums,
                                double* price, double* std_error);
 
-/* Build (or extend) the cached permutation tables for dims [0, dims). */
+/* Build (or extend) the cached uniform tables (K1 permutations -> uniform_at, f64) for dims [0, dims). */
 qmcg_status qmcg_warm(qmcg_ctx* ctx, int64_t n_paths, uint64_t seed, int64_t dims);
 /* Drop every cached table. */
 qmcg_status qmcg_clear_cache(qmcg_ctx* ctx);
@@ -167,7 +167,7 @@ qmcg_status qmcg_import_tables(qmcg_ctx* ctx, int64_t n_paths, uint64_t seed, in
 qmcg_status qmcg_import_rows(qmcg_ctx* ctx, int64_t n_paths, uint64_t seed, int64_t col_begin,
                              int64_t col_end, int64_t dims, int64_t row_begin, int64_t row_count,
                              const uint32_t* src_dev, int64_t src_ld);
-/* Cap the bytes the permutation tables may occupy (0 = whatever free device
+/* Cap the bytes the uniform tables may occupy (0 = whatever free device
  * memory allows). A pricing whose tables exceed it runs in date windows
  * ("streamed tables": each window's rows are built, walked, and replaced,
  * with the per-path walk state carried in HBM) with identical results; this
@@ -235,7 +235,7 @@ qmcg_status qmcg_time_device_nodes(qmcg_ctx* ctx, const qmcg_option_spec* spec, 
                                    uint64_t seed, uint32_t flags, int depth, int64_t node_begin,
                                    int64_t node_count, int reps, double* kernel_ms, double* step_ms,
                                    double* out_sums);
-/* Device time (ms) of rebuilding the permutation tables for dims [0, dims). */
+/* Device time (ms) of rebuilding the uniform tables (K1 + conversion) for dims [0, dims). */
 qmcg_status qmcg_time_perm_build(qmcg_ctx* ctx, int64_t n_paths, uint64_t seed, int64_t dims,
                                  double* ms);
 /* Out-of-bounds write check (the process must run with QMCG_CANARY=1 from its first allocation):

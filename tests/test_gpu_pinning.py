@@ -1,10 +1,10 @@
 """Reference-pinned bit-level parity of the pricing path itself (not only the D1 exports).
 
-* The uniforms that the pricing kernels' generator computes (generate_row: fixed digit
-  counts, digit pairs, the base-2 bit reversal; exported with qmcg_uniform_rows) are
-  bit-identical to the reference's uniform_at (proj/src/quasi_rng.cpp:71-83,96-101) for
-  every column the config-2 and config-3 pricings read: FNV-1a-64 of each column against
-  hashes produced by the reference itself (oracle/gen_golden.py --only-columns).
+* The uniforms the pricing kernels read -- the resident uniform table, built by K1 +
+  uniforms_kernel and exported with qmcg_uniform_rows -- are bit-identical to the reference's
+  uniform_at (proj/src/quasi_rng.cpp:71-83,96-101) for every column the config-2 and config-3
+  pricings read: FNV-1a-64 of each column against hashes produced by the reference itself
+  (oracle/gen_golden.py --only-columns).
 * The GPU pairwise tree (K3) returns exactly the reference's reduce_stats
   (proj/src/path_engine.cpp:39-47,191-205) of the GPU's own per-path values, with `==`,
   for ragged and power-of-two n.

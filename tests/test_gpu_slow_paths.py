@@ -1,6 +1,6 @@
-"""The SLOW instantiations of the pricing kernel and of the generator (64-bit-magic digit division,
-endpoint clamp: otherwise reached only near n = 2^32) and the range-checked walk
-(large m * sigma): bit-identical to the fast path / within the parity bar of the oracle."""
+"""The table build's 64-bit-magic digit division and endpoint clamp (otherwise reached only near
+n = 2^32) bit-identical to the 32-bit path, and the range-checked walk (large m * sigma, the SLOW
+pricing-kernel instantiation) within the parity bar of the oracle."""
 import os
 import subprocess
 import sys
