@@ -374,6 +374,7 @@ struct qmcg_ctx {
   // assign pass overlaps the next table's sort (n <= kOverlapMaxN)
   cudaStream_t side[2] = {nullptr, nullptr};
   DevBuf<char> d_permscratch_side[2];
+  DevBuf<uint32_t> d_xrow_side[2];  // the side lanes' rows of perm + 1 on their way into the uniform table
   cudaEvent_t ev_fork = nullptr, ev_join[2] = {nullptr, nullptr};
   // streamed tables (date windows): per-path walk state carried between windows
   DevBuf<double> d_stV, d_stc, d_stcd, d_stbest;
@@ -444,9 +445,10 @@ constexpr int64_t kOverlapMaxN = int64_t{1} << 25;  // the extra K1 scratch stay
 //   xdst: the rows are perm + 1 (u32, leading dimension ld, all n columns) -- the exchange format
 //         of qmcg_build_tables;
 //   udst: the rows are the uniforms uniform_at(p, dim) of columns [cb, ce) (f64, leading dimension
-//         ld) -- the uniform table K2 reads: K1's last pass (assign, or the binned scatter) writes
-//         the bit-exact radical inverse of perm + 1 instead of perm + 1 (halton(), the same code
-//         uniforms_kernel runs for the D1 exports).
+//         ld) -- the uniform table K2 reads: K1 writes the lane's row of perm + 1, then
+//         uniforms_kernel turns the column slice into bit-exact radical inverses (writing the
+//         uniforms from K1's assign pass instead measured slower: its latency-bound chase grew by
+//         the digit division, 2^24 table 0.87 -> 1.07 ms).
 // The caller has made the dimension constants of every built dim resident (ensure_dim_tables).
 qmcg_status build_rows(qmcg_ctx* c, uint64_t seed, int64_t n, uint32_t* xdst, double* udst, int64_t ld, int64_t cb,
                        int64_t ce, int64_t d0, int64_t d1, int64_t dim_begin, int64_t dim_stride) {
@@ -454,12 +456,14 @@ qmcg_status build_rows(qmcg_ctx* c, uint64_t seed, int64_t n, uint32_t* xdst, do
   const int lanes = (n <= kOverlapMaxN && d1 - d0 >= 2) ? kK1Lanes : 1;
   const size_t need = qmcg::perm_scratch_bytes(n);
   QMCG_CUDA(c->d_permscratch.reserve(need));
+  if (udst) QMCG_CUDA(c->d_fullperm.reserve(static_cast<size_t>(n)));
   if (!c->ev_fork) QMCG_CUDA(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
   QMCG_CUDA(cudaEventRecord(c->ev_fork, c->stream));
   for (int l = 0; l + 1 < lanes; ++l) {
     if (!c->side[l]) QMCG_CUDA(cudaStreamCreateWithFlags(&c->side[l], cudaStreamNonBlocking));
     if (!c->ev_join[l]) QMCG_CUDA(cudaEventCreateWithFlags(&c->ev_join[l], cudaEventDisableTiming));
     QMCG_CUDA(c->d_permscratch_side[l].reserve(need));
+    if (udst) QMCG_CUDA(c->d_xrow_side[l].reserve(static_cast<size_t>(n)));
     QMCG_CUDA(cudaStreamWaitEvent(c->side[l], c->ev_fork, 0));
   }
   for (int64_t k = d0; k < d1; ++k) {
@@ -467,14 +471,15 @@ qmcg_status build_rows(qmcg_ctx* c, uint64_t seed, int64_t n, uint32_t* xdst, do
     DevBuf<char>& scratch = lane == 0 ? c->d_permscratch : c->d_permscratch_side[lane - 1];
     cudaStream_t s = lane == 0 ? c->stream : c->side[lane - 1];
     const int64_t dim = dim_begin + k * dim_stride;
-    uint32_t* xrow = xdst ? xdst + static_cast<size_t>(k) * static_cast<size_t>(ld) : nullptr;
+    uint32_t* xrow = xdst ? xdst + static_cast<size_t>(k) * static_cast<size_t>(ld)
+                          : (lane == 0 ? c->d_fullperm.ptr : c->d_xrow_side[lane - 1].ptr);
     int launches = 0;
-    qmcg::UniformSink sink{};
-    if (udst)
-      sink = qmcg::UniformSink{udst + static_cast<size_t>(k) * static_cast<size_t>(ld), cb, ce,
-                               c->dt.dims[static_cast<size_t>(dim)], c->d_sc.ptr, c->d_nc.ptr};
-    QMCG_CUDA(qmcg::launch_perm_build(dimension_seed(seed, dim), n, xrow, scratch.ptr, scratch.cap, s, &launches, 1,
-                                      udst ? &sink : nullptr));
+    QMCG_CUDA(qmcg::launch_perm_build(dimension_seed(seed, dim), n, xrow, scratch.ptr, scratch.cap, s, &launches, 1));
+    if (udst) {
+      QMCG_CUDA(qmcg::launch_uniforms(xrow + cb, ce - cb, c->dt.dims[static_cast<size_t>(dim)], c->d_sc.ptr,
+                                      c->d_nc.ptr, 0, udst + static_cast<size_t>(k) * static_cast<size_t>(ld), s));
+      ++launches;
+    }
     c->launches += launches;
   }
   for (int l = 0; l + 1 < lanes; ++l) {
@@ -883,6 +888,7 @@ void qmcg_destroy(qmcg_ctx* c) {
   for (int l = 0; l < 2; ++l) {
     if (c->side[l]) cudaStreamSynchronize(c->side[l]);
     c->d_permscratch_side[l].release();
+    c->d_xrow_side[l].release();
     if (c->side[l]) cudaStreamDestroy(c->side[l]);
     if (c->ev_join[l]) cudaEventDestroy(c->ev_join[l]);
   }
@@ -1062,10 +1068,10 @@ size_t table_bytes_allowed(qmcg_ctx* c, int64_t n, int64_t cols, bool full) {
   cudaMemGetInfo(&free_b, &total_b);
   const int64_t held_ld = qmcg::table_ld(c->col_end - c->col_begin);
   const size_t held = c->table ? c->table_rows_cap * static_cast<size_t>(held_ld) * sizeof(double) : 0;
-  // K1 scratch per build lane, the carried walk state, values, a margin
+  // K1 scratch and a row of perm + 1 per build lane, the carried walk state, values, a margin
   const size_t lanes = n <= kOverlapMaxN ? kK1Lanes : 1;
   (void)full;
-  const size_t reserve = lanes * qmcg::perm_scratch_bytes(n) +
+  const size_t reserve = lanes * (qmcg::perm_scratch_bytes(n) + static_cast<size_t>(n) * 4) +
                          static_cast<size_t>(cols) * (4 * 8 + 4 + 8 + 8) + (size_t{1} << 30);
   const size_t avail = free_b + held > reserve ? free_b + held - reserve : 0;
   return c->table_budget ? std::min(c->table_budget, avail) : avail;

@@ -1127,21 +1127,10 @@ __global__ void fy_first_kernel(const uint32_t* __restrict__ sk, const uint32_t*
 // warp keeps kChase independent random F reads in flight instead of one dependent chain: the
 // pass is bound by the latency of that chase (~1 random F read per entry on average).
 constexpr int kChase = 4;
-// us.u set: instead of perm[i] = x (x = perm + 1), the uniform-table entry radical_inverse(x) of
-// columns [us.cb, us.ce) is written (the table build without a separate conversion pass).
-__device__ __forceinline__ void store_entry(uint32_t* __restrict__ perm, const UniformSink& us, uint32_t i,
-                                            uint32_t x) {
-  if (us.u) {
-    if (i >= us.cb && i < us.ce) __stcs(us.u + (i - us.cb), halton(x, us.dp, us.sc, us.nc));
-  } else {
-    __stcs(perm + i, x);
-  }
-}
-
 __global__ void __launch_bounds__(256) fy_assign_kernel(const uint32_t* __restrict__ sk,
                                                         const uint32_t* __restrict__ sv, int64_t n,
                                                         const uint32_t* __restrict__ F, uint32_t* __restrict__ perm,
-                                                        uint2* __restrict__ pairs, uint32_t add, const UniformSink us) {
+                                                        uint2* __restrict__ pairs, uint32_t add) {
   const int64_t q0 = static_cast<int64_t>(blockIdx.x) * (blockDim.x * kChase) + threadIdx.x;
   uint32_t y[kChase], out[kChase], idx[kChase];
   bool live[kChase], chase[kChase];
@@ -1190,7 +1179,7 @@ __global__ void __launch_bounds__(256) fy_assign_kernel(const uint32_t* __restri
     perm[q] = out[k] + idx[k];  // timing probe only: coalesced store (wrong result)
 #else
     if (pairs) __stcs(pairs + q, make_uint2(idx[k], out[k] + add));
-    else store_entry(perm, us, idx[k], out[k] + add);
+    else __stcs(perm + idx[k], out[k] + add);
 #endif
   }
 }
@@ -1256,17 +1245,15 @@ __global__ void __launch_bounds__(kBinThreads) fy_bin_kernel(const uint2* __rest
 }
 
 __global__ void fill_u32_kernel(uint32_t* out, uint32_t v) { *out = v; }
-__global__ void fill_uniform_kernel(const UniformSink us, uint32_t x) { store_entry(nullptr, us, 0, x); }
 
 // Pass 2: perm[i] = p for the binned pairs. Consecutive blocks cover
 // consecutive bins, so the destination window in flight is a few bins
 // (<< L2) and every 32-byte sector is completed in L2 before write-back.
-__global__ void fy_scatter_kernel(const uint2* __restrict__ in, int64_t n, uint32_t* __restrict__ perm,
-                                  const UniformSink us) {
+__global__ void fy_scatter_kernel(const uint2* __restrict__ in, int64_t n, uint32_t* __restrict__ perm) {
   const int64_t q = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (q >= n) return;
   const uint2 v = in[q];
-  store_entry(perm, us, v.x, v.y);
+  perm[v.x] = v.y;
 }
 
 // ---------------------------------------------------------------------------
@@ -1908,8 +1895,7 @@ PermScratchLayout perm_layout(int64_t n) {
 size_t perm_scratch_bytes(int64_t n) { return perm_layout(n).total; }
 
 cudaError_t launch_perm_build(uint64_t seed64, int64_t n, uint32_t* out, void* scratch, size_t scratch_bytes,
-                              cudaStream_t s, int* launches, uint32_t add, const UniformSink* sink) {
-  const UniformSink us = sink ? *sink : UniformSink{};
+                              cudaStream_t s, int* launches, uint32_t add) {
   const PermScratchLayout L = perm_layout(n);
   if (scratch_bytes < L.total) return cudaErrorInvalidValue;
   cudaError_t e = ensure_log_table(s);  // also the LCG power table of fy_draws_kernel
@@ -1920,9 +1906,8 @@ cudaError_t launch_perm_build(uint64_t seed64, int64_t n, uint32_t* out, void* s
   auto* skeys = reinterpret_cast<uint32_t*>(base + L.skeys);
   auto* svals = reinterpret_cast<uint32_t*>(base + L.svals);
   auto* F = reinterpret_cast<uint32_t*>(base + L.F);
-  if (n == 1) {  // the one-element permutation is [0]
-    if (us.u) fill_uniform_kernel<<<1, 1, 0, s>>>(us, add);
-    else fill_u32_kernel<<<1, 1, 0, s>>>(out, add);
+  if (n == 1) {
+    fill_u32_kernel<<<1, 1, 0, s>>>(out, add);
     return cudaGetLastError();
   }
   int bits = 1;
@@ -1951,11 +1936,11 @@ cudaError_t launch_perm_build(uint64_t seed64, int64_t n, uint32_t* out, void* s
                                                                  shift);
   const int64_t ab = (n + threads * kChase - 1) / (threads * kChase);
   fy_assign_kernel<<<static_cast<unsigned>(ab), threads, 0, s>>>(skeys, svals, n, F, out, binned ? pairs : nullptr,
-                                                                  add, us);
+                                                                  add);
   if (binned) {
     const int64_t bb = (n + kBinThreads * kBinPer - 1) / (kBinThreads * kBinPer);
     fy_bin_kernel<<<static_cast<unsigned>(bb), kBinThreads, 0, s>>>(pairs, n, shift, cursor, binned_pairs);
-    fy_scatter_kernel<<<static_cast<unsigned>(eb), threads, 0, s>>>(binned_pairs, n, out, us);
+    fy_scatter_kernel<<<static_cast<unsigned>(eb), threads, 0, s>>>(binned_pairs, n, out);
   }
   if (launches) *launches += 4 + 1 + (binned ? 2 : 0);  // draws, sort (>=1), first, assign (+ memset) [+ bin, scatter]
   return cudaGetLastError();

@@ -127,19 +127,8 @@ cudaError_t launch_path_matrix(const double* table, int64_t ld, int64_t n, int p
 cudaError_t launch_transpose(const double* in, int64_t rows, int64_t cols, double* out, cudaStream_t s);
 cudaError_t launch_sweep(const double* prices, int64_t n, int m, double spot, double strike, double rate, double vol,
                          double dt, double disc, int kind, double* values, int32_t* exercise, cudaStream_t s);
-// With `sink`, the result is not perm + add in out[] but the uniform-table entries
-// radical_inverse(perm + add) of columns [sink->cb, sink->ce) in sink->u (out is then unused
-// scratch-free: pass any buffer of n entries).
-struct UniformSink {
-  double* u;
-  int64_t cb, ce;
-  DimParam dp;
-  const double* sc;
-  const double* nc;
-};
 cudaError_t launch_perm_build(uint64_t seed64, int64_t n, uint32_t* out, void* scratch,
-                              size_t scratch_bytes, cudaStream_t s, int* launches, uint32_t add,
-                              const UniformSink* sink = nullptr);
+                              size_t scratch_bytes, cudaStream_t s, int* launches, uint32_t add);
 // uniform_at (or, with `normals`, normal_at) of `count` table entries perm + 1 of one dimension:
 // radical_inverse with the reference's rounding (bit-exact). Builds the rows of the uniform table
 // from K1's permutations (normals = 0) and serves the D1 exports.
