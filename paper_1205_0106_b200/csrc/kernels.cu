@@ -798,7 +798,9 @@ __global__ void __launch_bounds__(kThreads, QMCG_MINB)
     if (!det) {
       if (k0 + warp < dend) {
         mbar_wait_u32(sbase + kBarOff + b * kTile * 8, static_cast<uint32_t>((k >> 1) & 1));
+#ifndef QMCG_PROBE_NOGEN  // timing probe only (wrong results): walk the tile as loaded
         generate_row<F32>(ws, ztile + warp * kThreads * Z::kSize, logtab, nchunks, lane, lt, P.alpha);
+#endif
       }
       __syncthreads();  // tile k generated; every warp has walked tile k - 1: its buffer takes tile k + 1
       if (threadIdx.x == 0 && k >= 1 && k + 1 < ntiles)
