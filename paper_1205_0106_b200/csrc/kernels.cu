@@ -1090,9 +1090,11 @@ __device__ __forceinline__ uint32_t lcg_below32(uint64_t s, uint32_t b) {
   return static_cast<uint32_t>((hi + __umulhi(static_cast<uint32_t>(s), b)) >> 32);
 }
 
+// keys[i] = j_i >> G, vals[i] = (j_i mod 2^G) << IB | i (IB = bits of n - 1, G + IB <= 32): the
+// radix sort only orders the high bits of j; fy_span_kernel finishes each 256-value span of j.
 __global__ void fy_draws_kernel(uint64_t seed, int64_t n, uint64_t stride_mult, uint64_t stride_plus,
-                                uint32_t* __restrict__ keys, uint32_t* __restrict__ vals) {
-  const int64_t G = static_cast<int64_t>(gridDim.x) * blockDim.x;
+                                uint32_t* __restrict__ keys, uint32_t* __restrict__ vals, int G, int IB) {
+  const int64_t G_ = static_cast<int64_t>(gridDim.x) * blockDim.x;
   const int64_t g = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (g == 0) {
     keys[0] = 0;
@@ -1100,57 +1102,136 @@ __global__ void fy_draws_kernel(uint64_t seed, int64_t n, uint64_t stride_mult, 
   }
   const int64_t draws = n - 1;
   if (g >= draws) return;
+  const uint32_t lowmask = (1u << G) - 1u;  // G <= 8
   uint64_t s = lcg_state_after(seed, static_cast<uint64_t>(g) + 1);  // state after draw g
-  for (int64_t t = g; t < draws; t += G) {
+  for (int64_t t = g; t < draws; t += G_) {
     const int64_t i = n - 1 - t;  // i + 1 <= n - 1 < 2^32
-    keys[i] = lcg_below32(s, static_cast<uint32_t>(i + 1));
-    vals[i] = static_cast<uint32_t>(i);
+    const uint32_t j = lcg_below32(s, static_cast<uint32_t>(i + 1));
+    keys[i] = j >> G;
+    vals[i] = (G ? (j & lowmask) << IB : 0u) | static_cast<uint32_t>(i);
     s = stride_mult * s + stride_plus;
   }
 }
 
-__global__ void fy_first_kernel(const uint32_t* __restrict__ sk, const uint32_t* __restrict__ sv, int64_t n,
-                                uint32_t* __restrict__ F, uint32_t* __restrict__ cursor, int bin_shift) {
-  const int64_t q = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (cursor && q < kBins) cursor[q * kCursorStride] = static_cast<uint32_t>(q) << bin_shift;
-  if (q >= n) return;
-  const uint32_t x = sk[q], i = sv[q];
-  if (i > x) {
-    const bool prev_above = q > 0 && sk[q - 1] == x && sv[q - 1] > x;
-    if (!prev_above) F[x] = i;
+// sstart[w] = first sorted entry whose j lies in span w (j >> 8 >= w), w = 0..nspans; also the
+// bin cursors of the binned scatter. Four sorted keys per thread (one 16-byte load).
+__global__ void fy_span_start_kernel(const uint32_t* __restrict__ sk, int64_t n, int sh, uint32_t nspans,
+                                     uint32_t* __restrict__ sstart, uint32_t* __restrict__ cursor, int bin_shift) {
+  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (cursor && t < kBins) cursor[t * kCursorStride] = static_cast<uint32_t>(t) << bin_shift;
+  const int64_t q0 = 4 * t;
+  if (q0 > n) return;
+  uint32_t key[4];
+  if (q0 + 3 < n) {
+    const uint4 k4 = __ldg(reinterpret_cast<const uint4*>(sk + q0));
+    key[0] = k4.x >> sh, key[1] = k4.y >> sh, key[2] = k4.z >> sh, key[3] = k4.w >> sh;
+  } else {
+#pragma unroll
+    for (int u = 0; u < 4; ++u) key[u] = q0 + u < n ? __ldg(sk + q0 + u) >> sh : nspans;
+  }
+  uint32_t next = q0 > 0 ? (__ldg(sk + q0 - 1) >> sh) + 1 : 0;  // first span not started before q0
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    if (q0 + u > n) break;
+    for (uint32_t w = next; w <= key[u]; ++w) sstart[w] = static_cast<uint32_t>(q0 + u);
+    next = key[u] + 1;
   }
 }
 
-// perm[i] for the sorted entry q. With `pairs`, the result is written in
-// sorted order as (i, perm[i]) for the binned scatter below (large n, where a
-// direct perm[i] store is a random 4-byte write: a read-modify-write of a
-// whole DRAM burst); otherwise it is stored directly.
-// Each thread follows kChase chains at once (entries q, q + B, ..., B = the block's span), so a
-// warp keeps kChase independent random F reads in flight instead of one dependent chain: the
-// pass is bound by the latency of that chase (~1 random F read per entry on average).
+// One warp per span of 256 consecutive j. A span's entries are contiguous after the sort, and
+// each bucket's entries (one j) lie in ascending i (the sort is stable and they share a key), so a
+// right-to-left sweep in 32-entry chunks finds, per entry, the next larger i of its bucket: the
+// next lane of the chunk with the same bucket (8 ballots), else last[b], the smallest i seen so
+// far to the right. Likewise fa[b] = the smallest i > x of bucket x seen so far. Outputs:
+//   F[x] = min{i in bucket(x) : i > x} (or none) for every x of the span (coalesced, no memset),
+//   pairs[q] = (i, S(i)) when a successor S exists, else (i, j_i).
+// S > i and j_i <= i, so the chase pass tells the two apart without a flag. Two 1 KB arrays per
+// warp, any span size, loads issued 8 chunks at a time.
+constexpr int kSpan = 256, kSpanWarps = 8, kSpanLook = 8;
+__device__ __forceinline__ uint32_t span_bucket(uint32_t key, uint32_t val, int G, int IB) {
+  const uint32_t j = (key << G) | (G ? val >> IB : 0u);
+  return j & (kSpan - 1);
+}
+__global__ void __launch_bounds__(kSpanWarps * 32) fy_span_kernel(const uint32_t* __restrict__ sk,
+                                                                  const uint32_t* __restrict__ sv, int64_t n, int G,
+                                                                  int IB, const uint32_t* __restrict__ sstart,
+                                                                  int64_t nspans, uint32_t* __restrict__ F,
+                                                                  uint2* __restrict__ pairs) {
+  __shared__ uint32_t s_last[kSpanWarps][kSpan], s_fa[kSpanWarps][kSpan];
+  const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t w = static_cast<int64_t>(blockIdx.x) * kSpanWarps + wib;
+  if (w >= nspans) return;  // no block-wide barrier below
+  uint32_t* last = s_last[wib];
+  uint32_t* fa = s_fa[wib];
+  const uint32_t imask = IB >= 32 ? 0xffffffffu : (1u << IB) - 1u;
+  const int64_t s = sstart[w], e = sstart[w + 1];
+  const uint32_t jlo = static_cast<uint32_t>(w * kSpan);
+  const unsigned lt = lanemask_lt(), gt = ~lt & ~(1u << lane);
+  for (int b = lane; b < kSpan; b += 32) {
+    last[b] = kNone;
+    fa[b] = kNone;
+  }
+  __syncwarp();
+  for (int64_t hi = e; hi > s; hi -= 32 * kSpanLook) {
+    uint32_t kk[kSpanLook], vv[kSpanLook];
+#pragma unroll
+    for (int u = 0; u < kSpanLook; ++u) {
+      const int64_t p = hi - 32 * (u + 1) + lane;
+      if (p >= s) {
+        kk[u] = __ldg(sk + p);
+        vv[u] = __ldg(sv + p);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kSpanLook; ++u) {
+      const int64_t p = hi - 32 * (u + 1) + lane;
+      if (hi - 32 * u <= s) break;  // warp-uniform: no entry left
+      const bool valid = p >= s;
+      const uint32_t b = valid ? span_bucket(kk[u], vv[u], G, IB) : 0u;
+      const uint32_t i = vv[u] & imask;
+      const uint32_t x = jlo + b;
+      unsigned eq = __ballot_sync(kFull, valid);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const bool bit = (b >> k) & 1u;
+        const unsigned bb = __ballot_sync(kFull, bit);
+        eq &= bit ? bb : ~bb;
+      }
+      const unsigned up = eq & gt;
+      const uint32_t inext = __shfl_sync(kFull, i, up ? __ffs(up) - 1 : lane);
+      const uint32_t S = up ? inext : (valid ? last[b] : kNone);
+      const bool above = valid && i > x;
+      const unsigned ab = __ballot_sync(kFull, above);
+      __syncwarp();
+      if (valid && (eq & lt) == 0) last[b] = i;    // the bucket's smallest i in this chunk
+      if (above && (eq & lt & ab) == 0) fa[b] = i;  // its smallest i > x in this chunk
+      __syncwarp();
+      if (valid) __stcs(pairs + p, make_uint2(i, S != kNone ? S : x));
+    }
+  }
+  for (int b = lane; b < kSpan; b += 32)
+    if (static_cast<int64_t>(jlo) + b < n) F[jlo + b] = fa[b];
+}
+
+// perm[i] = v when v <= i (no successor: v = j_i), else R(v): follow F from v to the chain's end.
+// Each thread follows kChase chains at once.
 constexpr int kChase = 4;
-__global__ void __launch_bounds__(256) fy_assign_kernel(const uint32_t* __restrict__ sk,
-                                                        const uint32_t* __restrict__ sv, int64_t n,
-                                                        const uint32_t* __restrict__ F, uint32_t* __restrict__ perm,
-                                                        uint2* __restrict__ pairs, uint32_t add) {
+__global__ void __launch_bounds__(256) fy_chase_kernel(const uint2* __restrict__ in, int64_t n,
+                                                       const uint32_t* __restrict__ F, uint32_t* __restrict__ perm,
+                                                       uint2* __restrict__ pairs, uint32_t add) {
   const int64_t q0 = static_cast<int64_t>(blockIdx.x) * (blockDim.x * kChase) + threadIdx.x;
-  uint32_t y[kChase], out[kChase], idx[kChase];
+  uint32_t y[kChase], idx[kChase];
   bool live[kChase], chase[kChase];
-  // the sorted pairs stream through once (evict-first) so that F, read at random,
-  // keeps its place in L2
 #pragma unroll
   for (int k = 0; k < kChase; ++k) {
     const int64_t q = q0 + k * blockDim.x;
     live[k] = q < n;
     chase[k] = false;
     if (live[k]) {
-      const uint32_t x = __ldcs(sk + q);
-      idx[k] = __ldcs(sv + q);
-      out[k] = x;
-      if (q + 1 < n && __ldcs(sk + q + 1) == x) {
-        y[k] = __ldcs(sv + q + 1);
-        chase[k] = true;
-      }
+      const uint2 pv = __ldcs(in + q);
+      idx[k] = pv.x;
+      y[k] = pv.y;
+      chase[k] = pv.y > pv.x;
     }
   }
   bool any = false;
@@ -1165,10 +1246,7 @@ __global__ void __launch_bounds__(256) fy_assign_kernel(const uint32_t* __restri
     for (int k = 0; k < kChase; ++k) {
       if (chase[k]) {
         if (f[k] != kNone) y[k] = f[k];
-        else {
-          out[k] = y[k];
-          chase[k] = false;
-        }
+        else chase[k] = false;
       }
       any |= chase[k];
     }
@@ -1177,12 +1255,8 @@ __global__ void __launch_bounds__(256) fy_assign_kernel(const uint32_t* __restri
   for (int k = 0; k < kChase; ++k) {
     if (!live[k]) continue;
     const int64_t q = q0 + k * blockDim.x;
-#ifdef QMCG_K1_COALESCED_PROBE
-    perm[q] = out[k] + idx[k];  // timing probe only: coalesced store (wrong result)
-#else
-    if (pairs) __stcs(pairs + q, make_uint2(idx[k], out[k] + add));
-    else __stcs(perm + idx[k], out[k] + add);
-#endif
+    if (pairs) __stcs(pairs + q, make_uint2(idx[k], y[k] + add));
+    else __stcs(perm + idx[k], y[k] + add);
   }
 }
 
@@ -1871,8 +1945,18 @@ cudaError_t launch_sweep(const double* prices, int64_t n, int m, double spot, do
 
 namespace {
 struct PermScratchLayout {
-  size_t keys, vals, skeys, svals, F, cursor, temp, temp_bytes, total;
+  size_t keys, vals, skeys, svals, F, cursor, sstart, temp, temp_bytes, total;
 };
+// bits of n - 1 (the index width IB), the j bits carried in the value (G) and the sorted key bits
+struct PermBits {
+  int IB, G, sort_bits;
+};
+PermBits perm_bits(int64_t n) {
+  int IB = 1;
+  while (IB < 32 && (static_cast<uint64_t>(n - 1) >> IB) != 0) ++IB;
+  const int G = std::min(8, 32 - IB);
+  return PermBits{IB, G, std::max(0, IB - G)};
+}
 PermScratchLayout perm_layout(int64_t n) {
   auto align = [](size_t x) { return (x + 255) & ~size_t{255}; };
   PermScratchLayout L{};
@@ -1887,7 +1971,8 @@ PermScratchLayout perm_layout(int64_t n) {
   L.svals = L.skeys + arr;
   L.F = L.svals + arr;
   L.cursor = L.F + arr;
-  L.temp = L.cursor + align(kBins * kCursorStride * sizeof(uint32_t));
+  L.sstart = L.cursor + align(kBins * kCursorStride * sizeof(uint32_t));
+  L.temp = L.sstart + align(static_cast<size_t>((n + kSpan - 1) / kSpan + 1) * sizeof(uint32_t));
   L.temp_bytes = align(temp_bytes);
   L.total = L.temp + L.temp_bytes;
   return L;
@@ -1896,6 +1981,8 @@ PermScratchLayout perm_layout(int64_t n) {
 
 size_t perm_scratch_bytes(int64_t n) { return perm_layout(n).total; }
 
+// K1 launch sequence: draws -> radix sort of j's high bits (CUB onesweep) -> span starts -> spans
+// (F, chase starts) -> chase (-> binned scatter for n >= QMCG_K1_BIN_MIN).
 cudaError_t launch_perm_build(uint64_t seed64, int64_t n, uint32_t* out, void* scratch, size_t scratch_bytes,
                               cudaStream_t s, int* launches, uint32_t add) {
   const PermScratchLayout L = perm_layout(n);
@@ -1905,46 +1992,56 @@ cudaError_t launch_perm_build(uint64_t seed64, int64_t n, uint32_t* out, void* s
   char* base = static_cast<char*>(scratch);
   auto* keys = reinterpret_cast<uint32_t*>(base + L.keys);
   auto* vals = reinterpret_cast<uint32_t*>(base + L.vals);
-  auto* skeys = reinterpret_cast<uint32_t*>(base + L.skeys);
-  auto* svals = reinterpret_cast<uint32_t*>(base + L.svals);
   auto* F = reinterpret_cast<uint32_t*>(base + L.F);
+  auto* sstart = reinterpret_cast<uint32_t*>(base + L.sstart);
+  auto* cursor = reinterpret_cast<uint32_t*>(base + L.cursor);
   if (n == 1) {
     fill_u32_kernel<<<1, 1, 0, s>>>(out, add);
     return cudaGetLastError();
   }
-  int bits = 1;
-  while (bits < 32 && (static_cast<uint64_t>(n - 1) >> bits) != 0) ++bits;
+  const PermBits pb = perm_bits(n);
   const int threads = 256;
   const int64_t want = (n - 1 + 15) / 16;  // ~16 draws per thread
   const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((want + threads - 1) / threads, 148 * 64));
   uint64_t sm, sp;
   lcg_jump(static_cast<uint64_t>(blocks) * threads, sm, sp);
-  fy_draws_kernel<<<static_cast<unsigned>(blocks), threads, 0, s>>>(seed64, n, sm, sp, keys, vals);
-  size_t temp_bytes = L.temp_bytes;
-  e = cub::DeviceRadixSort::SortPairs(base + L.temp, temp_bytes, keys, skeys, vals, svals,
-                                                  static_cast<int64_t>(n), 0, bits, s);
-  if (e != cudaSuccess) return e;
-  e = cudaMemsetAsync(F, 0xff, static_cast<size_t>(n) * sizeof(uint32_t), s);
-  if (e != cudaSuccess) return e;
-  const int64_t eb = (n + threads - 1) / threads;
+  fy_draws_kernel<<<static_cast<unsigned>(blocks), threads, 0, s>>>(seed64, n, sm, sp, keys, vals, pb.G, pb.IB);
+  // sorted entries in region A (keys+vals, or skeys+svals after a sort); the chase starts go to
+  // the other region B, the binned pairs back to A
+  char* regA = base + L.keys;
+  char* regB = base + L.skeys;
+  int nl = 3;
+  if (pb.sort_bits > 0) {
+    size_t temp_bytes = L.temp_bytes;
+    e = cub::DeviceRadixSort::SortPairs(base + L.temp, temp_bytes, keys, reinterpret_cast<uint32_t*>(base + L.skeys),
+                                        vals, reinterpret_cast<uint32_t*>(base + L.svals), static_cast<int64_t>(n), 0,
+                                        pb.sort_bits, s);
+    if (e != cudaSuccess) return e;
+    std::swap(regA, regB);
+    nl += 2;
+  }
+  const auto* sk = reinterpret_cast<const uint32_t*>(regA);
+  const auto* sv = reinterpret_cast<const uint32_t*>(regA + (L.vals - L.keys));
+  auto* starts = reinterpret_cast<uint2*>(regB);
   const bool binned = n >= QMCG_K1_BIN_MIN;
   int shift = 0;
   while (shift < 32 && (static_cast<uint64_t>(n - 1) >> shift) >= static_cast<uint64_t>(kBins)) ++shift;
-  auto* cursor = reinterpret_cast<uint32_t*>(base + L.cursor);
-  // keys+vals (free after the sort) hold the pairs; skeys+svals (free after assign) the bins
-  auto* pairs = reinterpret_cast<uint2*>(base + L.keys);
-  auto* binned_pairs = reinterpret_cast<uint2*>(base + L.skeys);
-  fy_first_kernel<<<static_cast<unsigned>(eb), threads, 0, s>>>(skeys, svals, n, F, binned ? cursor : nullptr,
-                                                                 shift);
+  const int64_t nspans = (n + kSpan - 1) / kSpan;
+  fy_span_start_kernel<<<static_cast<unsigned>((n / 4 + 1 + threads - 1) / threads), threads, 0, s>>>(
+      sk, n, 8 - pb.G, static_cast<uint32_t>(nspans), sstart, binned ? cursor : nullptr, shift);
+  fy_span_kernel<<<static_cast<unsigned>((nspans + kSpanWarps - 1) / kSpanWarps), kSpanWarps * 32, 0, s>>>(
+      sk, sv, n, pb.G, pb.IB, sstart, nspans, F, starts);
   const int64_t ab = (n + threads * kChase - 1) / (threads * kChase);
-  fy_assign_kernel<<<static_cast<unsigned>(ab), threads, 0, s>>>(skeys, svals, n, F, out, binned ? pairs : nullptr,
-                                                                  add);
+  auto* pairs = reinterpret_cast<uint2*>(regA);  // the sorted entries are consumed by now
+  fy_chase_kernel<<<static_cast<unsigned>(ab), threads, 0, s>>>(starts, n, F, out, binned ? pairs : nullptr, add);
   if (binned) {
+    auto* binned_pairs = reinterpret_cast<uint2*>(regB);
     const int64_t bb = (n + kBinThreads * kBinPer - 1) / (kBinThreads * kBinPer);
     fy_bin_kernel<<<static_cast<unsigned>(bb), kBinThreads, 0, s>>>(pairs, n, shift, cursor, binned_pairs);
-    fy_scatter_kernel<<<static_cast<unsigned>(eb), threads, 0, s>>>(binned_pairs, n, out);
+    fy_scatter_kernel<<<static_cast<unsigned>((n + threads - 1) / threads), threads, 0, s>>>(binned_pairs, n, out);
+    nl += 2;
   }
-  if (launches) *launches += 4 + 1 + (binned ? 2 : 0);  // draws, sort (>=1), first, assign (+ memset) [+ bin, scatter]
+  if (launches) *launches += nl;  // draws, [sort: histogram + >=1 pass], span starts, spans, chase [+ bin, scatter]
   return cudaGetLastError();
 }
 
