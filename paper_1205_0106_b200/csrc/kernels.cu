@@ -1146,8 +1146,14 @@ __global__ void fy_span_start_kernel(const uint32_t* __restrict__ sk, int64_t n,
 //   F[x] = min{i in bucket(x) : i > x} (or none) for every x of the span (coalesced, no memset),
 //   pairs[q] = (i, S(i)) when a successor S exists, else (i, j_i).
 // S > i and j_i <= i, so the chase pass tells the two apart without a flag. Two 1 KB arrays per
-// warp, any span size, loads issued 8 chunks at a time.
-constexpr int kSpan = 256, kSpanWarps = 8, kSpanLook = 8;
+// warp, any span size, loads issued 4 chunks at a time (8 or 16: no faster).
+#ifndef QMCG_SPAN_WARPS
+#define QMCG_SPAN_WARPS 8
+#endif
+#ifndef QMCG_SPAN_LOOK
+#define QMCG_SPAN_LOOK 4
+#endif
+constexpr int kSpan = 256, kSpanWarps = QMCG_SPAN_WARPS, kSpanLook = QMCG_SPAN_LOOK;
 __device__ __forceinline__ uint32_t span_bucket(uint32_t key, uint32_t val, int G, int IB) {
   const uint32_t j = (key << G) | (G ? val >> IB : 0u);
   return j & (kSpan - 1);
