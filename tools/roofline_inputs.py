@@ -51,7 +51,7 @@ doc = {"kernel": "price_kernel (K2)", "report": rep.split("/")[-1], "n_paths": n
        "fp64_inst_per_path_step": fp64_warp * 32 / path_steps,
        "fp64_thread_inst_per_path_step": fp64_thread / path_steps,
        "warp_inst_per_warp_date": total_warp / (path_steps / 32),
-       "dram_bytes_per_launch": dram, "algorithmic_bytes_per_launch": 4 * path_steps,
+       "dram_bytes_per_launch": dram, "algorithmic_bytes_per_launch": 8 * path_steps, "algorithmic_bytes_per_path_step": 8,
        "duration_ms_under_ncu": dur * 1e3,
        "note": "fp64_inst_per_path_step counts FP64-pipe warp instructions x 32 lanes (issue slots the "
                "roofline charges); the thread-level count excludes predicated-off lanes"}
