@@ -679,8 +679,10 @@ __device__ __forceinline__ void push_record(uint32_t ws, const PriceParams& P, b
 //          (pl + k0 >= 0) and the accumulator bound of record_dominates<1> fails
 //          (V and cd already advanced by the caller).
 template <int KIND>
-__device__ __forceinline__ uint32_t walk_date(double V, double& c, double& cd, int& pl, int t, int k0, double& pv,
-                                              int& pdl, double b, double x0mk) {
+//   (puts: negk0 = -k0; bs = b / M and x0mks = x0mk / M with M = 1 + 4504 * 2^-52, so u1 / M comes
+//   out of one FMA and the margin of record_dominates<1> needs no multiply by cd)
+__device__ __forceinline__ uint32_t walk_date(double V, double& c, double& cd, int& pl, int t, int negk0, double& pv,
+                                              int& pdl, double b, double bs, double x0mks) {
   uint32_t pu32;
   if constexpr (KIND == 0) {
     asm("{\n .reg .pred r, pu;\n"
@@ -691,18 +693,18 @@ __device__ __forceinline__ uint32_t walk_date(double V, double& c, double& cd, i
         : "+d"(c), "+d"(cd), "+r"(pl), "=d"(pv), "=r"(pdl), "=r"(pu32)
         : "r"(t), "d"(V));
   } else {
-    asm("{\n .reg .pred r, pe, a, b, e, dm, pu;\n .reg .f64 u1, dv, s, t, pr, th;\n .reg .s32 pk;\n"
-        " setp.lt.f64 r, %7, %0;\n add.s32 pk, %2, %8;\n setp.ge.s32 pe, pk, 0;\n"
-        " fma.rn.f64 u1, %9, %0, %10;\n sub.rn.f64 dv, %0, %7;\n fma.rn.f64 s, %9, dv, %1;\n"
+    asm("{\n .reg .pred r, pe, a, b, e, dm, pu;\n .reg .f64 u1, dv, s, t, pr;\n"
+        " setp.lt.f64 r, %7, %0;\n setp.ge.s32 pe, %2, %8;\n"
+        " fma.rn.f64 u1, %10, %0, %11;\n sub.rn.f64 dv, %0, %7;\n fma.rn.f64 s, %9, dv, %1;\n"
         " fma.rn.f64 t, 0dBFE0000000000000, s, 0d3FF0000000000000;\n mul.rn.f64 pr, u1, s;\n"
-        " mul.rn.f64 pr, pr, t;\n mul.rn.f64 th, %1, 0d3FF0000000001198;\n"
+        " mul.rn.f64 pr, pr, t;\n"
         " setp.gt.f64 a, u1, 0d0000000000000000;\n setp.lt.and.f64 b, s, 0d4000000000000000, a;\n"
-        " setp.ge.and.f64 dm, pr, th, b;\n and.pred pu, r, pe;\n not.pred e, dm;\n and.pred pu, pu, e;\n"
+        " setp.ge.and.f64 dm, pr, %1, b;\n and.pred pu, r, pe;\n not.pred e, dm;\n and.pred pu, pu, e;\n"
         " mov.b64 %3, %0;\n mov.b32 %4, %2;\n"
         " selp.f64 %0, %7, %0, r;\n selp.f64 %1, 0d0000000000000000, %1, r;\n selp.b32 %2, %6, %2, r;\n"
         " selp.u32 %5, 1, 0, pu;\n}"
         : "+d"(c), "+d"(cd), "+r"(pl), "=d"(pv), "=r"(pdl), "=r"(pu32)
-        : "r"(t), "d"(V), "r"(k0), "d"(b), "d"(x0mk));
+        : "r"(t), "d"(V), "r"(negk0), "d"(b), "d"(bs), "d"(x0mks));
   }
   return pu32;
 }
@@ -820,7 +822,8 @@ __global__ void __launch_bounds__(kThreads, QMCG_MINB)
       // calls need no "pending exists" test: cd = -inf until the first record
       int pl = pend_d - k0;
       if constexpr (!F32) {  // FP64: grouped predicated walk; FP32 takes the generic loop below
-        const double bd = P.b, x0mkd = P.x0mk;
+        constexpr double kMargin = 1.0 + 0x1198p-52;  // record_dominates<1>'s 1e-12 margin, folded into u1
+        const double bd = P.b, bsd = P.b / kMargin, x0mks = P.x0mk / kMargin;
 #pragma unroll
         for (int g = 0; g < kTile; g += kPushGroup) {
           double pv[kPushGroup];
@@ -831,7 +834,7 @@ __global__ void __launch_bounds__(kThreads, QMCG_MINB)
           for (int u = 0; u < kPushGroup; ++u) {
             V = add_rn(V, Z::load(zcol + (g + u) * kThreads * Z::kSize));
             cd = add_rn(cd, slope);
-            pu[u] = walk_date<KIND>(V, c, cd, pl, g + u, k0, pv[u], pdl[u], bd, x0mkd);
+            pu[u] = walk_date<KIND>(V, c, cd, pl, g + u, -k0, pv[u], pdl[u], bd, bsd, x0mks);
             anyp |= pu[u];
           }
 #ifndef QMCG_PROBE_NOPUSH
@@ -1642,6 +1645,9 @@ __global__ void __launch_bounds__(kGThreads, QMCG_G_MINB) walk_group_kernel(cons
   const uint32_t cs = smem_u32(smg) + threadIdx.x * (kGCap * 20);
   const uint32_t cj = cs + kGCap * 8;
   const double alpha = g->alpha, beta = g->beta, gb = g->b, gx = g->x0mk;
+  // puts: record_dominates<1>'s 1e-12 margin folded into u1 (u1 / M from one FMA, M = 1 + 4504 * 2^-52)
+  constexpr double kMargin = 1.0 + 0x1198p-52;
+  const double gbs = gb / kMargin, gxs = gx / kMargin;
   double c = g->c0;
   double cd = KIND == 0 ? -INFINITY : 0.0;
   int pend = -1;
@@ -1676,20 +1682,19 @@ __global__ void __launch_bounds__(kGThreads, QMCG_G_MINB) walk_group_kernel(cons
       // puts, predicated: rec = V < c; acc += slope; dominated iff u1 > 0 && s < 2 &&
       // u1 s (1 - s/2) >= acc (1 + 1e-12) (record_dominates<1>); push = rec && pending && !dominated
       asm volatile(
-          "{\n .reg .pred r, pe, a, b, e, dm, pu;\n .reg .f64 v, u1, dv, s, t, pr, th;\n .reg .b32 ad;\n"
+          "{\n .reg .pred r, pe, a, b, e, dm, pu;\n .reg .f64 v, u1, dv, s, t, pr;\n .reg .b32 ad;\n"
           " fma.rn.f64 v, %4, %5, %6;\n add.rn.f64 %1, %1, %7;\n"
           " setp.lt.f64 r, v, %0;\n setp.ge.s32 pe, %2, 0;\n"
-          " fma.rn.f64 u1, %8, %0, %9;\n sub.rn.f64 dv, %0, v;\n fma.rn.f64 s, %8, dv, %1;\n"
+          " fma.rn.f64 u1, %13, %0, %14;\n sub.rn.f64 dv, %0, v;\n fma.rn.f64 s, %8, dv, %1;\n"
           " fma.rn.f64 t, 0dBFE0000000000000, s, 0d3FF0000000000000;\n mul.rn.f64 pr, u1, s;\n mul.rn.f64 pr, pr, t;\n"
-          " mul.rn.f64 th, %1, 0d3FF0000000001198;\n"
           " setp.gt.f64 a, u1, 0d0000000000000000;\n setp.lt.and.f64 b, s, 0d4000000000000000, a;\n"
-          " setp.ge.and.f64 dm, pr, th, b;\n"
+          " setp.ge.and.f64 dm, pr, %1, b;\n"
           " and.pred pu, r, pe;\n not.pred e, dm;\n and.pred pu, pu, e;\n"
           " mad.lo.u32 ad, %3, 8, %10;\n @pu st.shared.f64 [ad], %0;\n"
           " mad.lo.u32 ad, %3, 4, %11;\n @pu st.shared.u32 [ad], %2;\n @pu add.u32 %3, %3, 1;\n"
           " selp.f64 %0, v, %0, r;\n selp.f64 %1, 0d0000000000000000, %1, r;\n selp.b32 %2, %12, %2, r;\n}"
           : "+d"(c), "+d"(cd), "+r"(pend), "+r"(cnt)
-          : "d"(alpha), "d"(kd), "d"(S), "d"(beta), "d"(gb), "d"(gx), "r"(cs), "r"(cj), "r"(d)
+          : "d"(alpha), "d"(kd), "d"(S), "d"(beta), "d"(gb), "d"(gx), "r"(cs), "r"(cj), "r"(d), "d"(gbs), "d"(gxs)
           : "memory");
     }
   };
