@@ -1095,8 +1095,10 @@ __device__ __forceinline__ uint32_t lcg_below32(uint64_t s, uint32_t b) {
 
 // keys[i] = j_i >> G, vals[i] = (j_i mod 2^G) << IB | i (IB = bits of n - 1, G + IB <= 32): the
 // radix sort only orders the high bits of j; fy_span_kernel finishes each 256-value span of j.
+// KeyT = uint16_t when the key has at most 16 bits (n <= 2^24): a quarter less sort traffic.
+template <typename KeyT>
 __global__ void fy_draws_kernel(uint64_t seed, int64_t n, uint64_t stride_mult, uint64_t stride_plus,
-                                uint32_t* __restrict__ keys, uint32_t* __restrict__ vals, int G, int IB) {
+                                KeyT* __restrict__ keys, uint32_t* __restrict__ vals, int G, int IB) {
   const int64_t G_ = static_cast<int64_t>(gridDim.x) * blockDim.x;
   const int64_t g = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (g == 0) {
@@ -1110,15 +1112,16 @@ __global__ void fy_draws_kernel(uint64_t seed, int64_t n, uint64_t stride_mult, 
   for (int64_t t = g; t < draws; t += G_) {
     const int64_t i = n - 1 - t;  // i + 1 <= n - 1 < 2^32
     const uint32_t j = lcg_below32(s, static_cast<uint32_t>(i + 1));
-    keys[i] = j >> G;
+    keys[i] = static_cast<KeyT>(j >> G);
     vals[i] = (G ? (j & lowmask) << IB : 0u) | static_cast<uint32_t>(i);
     s = stride_mult * s + stride_plus;
   }
 }
 
 // sstart[w] = first sorted entry whose j lies in span w (j >> 8 >= w), w = 0..nspans; also the
-// bin cursors of the binned scatter. Four sorted keys per thread (one 16-byte load).
-__global__ void fy_span_start_kernel(const uint32_t* __restrict__ sk, int64_t n, int sh, uint32_t nspans,
+// bin cursors of the binned scatter. Four sorted keys per thread (one vector load).
+template <typename KeyT>
+__global__ void fy_span_start_kernel(const KeyT* __restrict__ sk, int64_t n, int sh, uint32_t nspans,
                                      uint32_t* __restrict__ sstart, uint32_t* __restrict__ cursor, int bin_shift) {
   const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (cursor && t < kBins) cursor[t * kCursorStride] = static_cast<uint32_t>(t) << bin_shift;
@@ -1126,13 +1129,19 @@ __global__ void fy_span_start_kernel(const uint32_t* __restrict__ sk, int64_t n,
   if (q0 > n) return;
   uint32_t key[4];
   if (q0 + 3 < n) {
-    const uint4 k4 = __ldg(reinterpret_cast<const uint4*>(sk + q0));
-    key[0] = k4.x >> sh, key[1] = k4.y >> sh, key[2] = k4.z >> sh, key[3] = k4.w >> sh;
+    if constexpr (sizeof(KeyT) == 4) {
+      const uint4 k4 = __ldg(reinterpret_cast<const uint4*>(sk + q0));
+      key[0] = k4.x >> sh, key[1] = k4.y >> sh, key[2] = k4.z >> sh, key[3] = k4.w >> sh;
+    } else {
+      const uint2 k2 = __ldg(reinterpret_cast<const uint2*>(sk + q0));
+      key[0] = (k2.x & 0xffffu) >> sh, key[1] = (k2.x >> 16) >> sh;
+      key[2] = (k2.y & 0xffffu) >> sh, key[3] = (k2.y >> 16) >> sh;
+    }
   } else {
 #pragma unroll
-    for (int u = 0; u < 4; ++u) key[u] = q0 + u < n ? __ldg(sk + q0 + u) >> sh : nspans;
+    for (int u = 0; u < 4; ++u) key[u] = q0 + u < n ? static_cast<uint32_t>(__ldg(sk + q0 + u)) >> sh : nspans;
   }
-  uint32_t next = q0 > 0 ? (__ldg(sk + q0 - 1) >> sh) + 1 : 0;  // first span not started before q0
+  uint32_t next = q0 > 0 ? (static_cast<uint32_t>(__ldg(sk + q0 - 1)) >> sh) + 1 : 0;  // first span not started before q0
 #pragma unroll
   for (int u = 0; u < 4; ++u) {
     if (q0 + u > n) break;
@@ -1161,7 +1170,8 @@ __device__ __forceinline__ uint32_t span_bucket(uint32_t key, uint32_t val, int 
   const uint32_t j = (key << G) | (G ? val >> IB : 0u);
   return j & (kSpan - 1);
 }
-__global__ void __launch_bounds__(kSpanWarps * 32) fy_span_kernel(const uint32_t* __restrict__ sk,
+template <typename KeyT>
+__global__ void __launch_bounds__(kSpanWarps * 32) fy_span_kernel(const KeyT* __restrict__ sk,
                                                                   const uint32_t* __restrict__ sv, int64_t n, int G,
                                                                   int IB, const uint32_t* __restrict__ sstart,
                                                                   int64_t nspans, uint32_t* __restrict__ F,
@@ -1972,10 +1982,14 @@ PermScratchLayout perm_layout(int64_t n) {
   auto align = [](size_t x) { return (x + 255) & ~size_t{255}; };
   PermScratchLayout L{};
   const size_t arr = align(static_cast<size_t>(n) * sizeof(uint32_t));
-  size_t temp_bytes = 0;
+  size_t temp_bytes = 0, temp16 = 0;
   cub::DeviceRadixSort::SortPairs(nullptr, temp_bytes, static_cast<const uint32_t*>(nullptr),
                                   static_cast<uint32_t*>(nullptr), static_cast<const uint32_t*>(nullptr),
                                   static_cast<uint32_t*>(nullptr), static_cast<int64_t>(n), 0, 32);
+  cub::DeviceRadixSort::SortPairs(nullptr, temp16, static_cast<const uint16_t*>(nullptr),
+                                  static_cast<uint16_t*>(nullptr), static_cast<const uint32_t*>(nullptr),
+                                  static_cast<uint32_t*>(nullptr), static_cast<int64_t>(n), 0, 16);
+  temp_bytes = std::max(temp_bytes, temp16);
   L.keys = 0;
   L.vals = L.keys + arr;
   L.skeys = L.vals + arr;
@@ -1992,6 +2006,43 @@ PermScratchLayout perm_layout(int64_t n) {
 
 size_t perm_scratch_bytes(int64_t n) { return perm_layout(n).total; }
 
+namespace {
+// draws -> CUB sort of the KeyT keys (j's high bits) -> span starts -> span sweep (F and the chase
+// starts in region B); regA/regB are swapped when a sort ran
+template <typename KeyT>
+cudaError_t k1_grouped(uint64_t seed64, int64_t n, const PermBits& pb, char* base, const PermScratchLayout& L,
+                       cudaStream_t s, bool binned, int shift, char*& regA, char*& regB, int& nl) {
+  const int threads = 256;
+  auto* keys = reinterpret_cast<KeyT*>(base + L.keys);
+  auto* vals = reinterpret_cast<uint32_t*>(base + L.vals);
+  auto* F = reinterpret_cast<uint32_t*>(base + L.F);
+  auto* sstart = reinterpret_cast<uint32_t*>(base + L.sstart);
+  auto* cursor = reinterpret_cast<uint32_t*>(base + L.cursor);
+  const int64_t want = (n - 1 + 15) / 16;  // ~16 draws per thread
+  const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((want + threads - 1) / threads, 148 * 64));
+  uint64_t sm, sp;
+  lcg_jump(static_cast<uint64_t>(blocks) * threads, sm, sp);
+  fy_draws_kernel<KeyT><<<static_cast<unsigned>(blocks), threads, 0, s>>>(seed64, n, sm, sp, keys, vals, pb.G, pb.IB);
+  if (pb.sort_bits > 0) {
+    size_t temp_bytes = L.temp_bytes;
+    const cudaError_t e = cub::DeviceRadixSort::SortPairs(
+        base + L.temp, temp_bytes, keys, reinterpret_cast<KeyT*>(base + L.skeys), vals,
+        reinterpret_cast<uint32_t*>(base + L.svals), static_cast<int64_t>(n), 0, pb.sort_bits, s);
+    if (e != cudaSuccess) return e;
+    std::swap(regA, regB);
+    nl += 2 + (pb.sort_bits + 7) / 8;  // histogram, scan, one onesweep pass per 8 key bits
+  }
+  const auto* sk = reinterpret_cast<const KeyT*>(regA);
+  const auto* sv = reinterpret_cast<const uint32_t*>(regA + (L.vals - L.keys));
+  const int64_t nspans = (n + kSpan - 1) / kSpan;
+  fy_span_start_kernel<KeyT><<<static_cast<unsigned>((n / 4 + 1 + threads - 1) / threads), threads, 0, s>>>(
+      sk, n, 8 - pb.G, static_cast<uint32_t>(nspans), sstart, binned ? cursor : nullptr, shift);
+  fy_span_kernel<KeyT><<<static_cast<unsigned>((nspans + kSpanWarps - 1) / kSpanWarps), kSpanWarps * 32, 0, s>>>(
+      sk, sv, n, pb.G, pb.IB, sstart, nspans, F, reinterpret_cast<uint2*>(regB));
+  return cudaGetLastError();
+}
+}  // namespace
+
 // K1 launch sequence: draws -> radix sort of j's high bits (CUB onesweep) -> span starts -> spans
 // (F, chase starts) -> chase (-> binned scatter for n >= QMCG_K1_BIN_MIN).
 cudaError_t launch_perm_build(uint64_t seed64, int64_t n, uint32_t* out, void* scratch, size_t scratch_bytes,
@@ -2001,10 +2052,7 @@ cudaError_t launch_perm_build(uint64_t seed64, int64_t n, uint32_t* out, void* s
   cudaError_t e = ensure_log_table(s);  // also the LCG power table of fy_draws_kernel
   if (e != cudaSuccess) return e;
   char* base = static_cast<char*>(scratch);
-  auto* keys = reinterpret_cast<uint32_t*>(base + L.keys);
-  auto* vals = reinterpret_cast<uint32_t*>(base + L.vals);
   auto* F = reinterpret_cast<uint32_t*>(base + L.F);
-  auto* sstart = reinterpret_cast<uint32_t*>(base + L.sstart);
   auto* cursor = reinterpret_cast<uint32_t*>(base + L.cursor);
   if (n == 1) {
     fill_u32_kernel<<<1, 1, 0, s>>>(out, add);
@@ -2012,36 +2060,18 @@ cudaError_t launch_perm_build(uint64_t seed64, int64_t n, uint32_t* out, void* s
   }
   const PermBits pb = perm_bits(n);
   const int threads = 256;
-  const int64_t want = (n - 1 + 15) / 16;  // ~16 draws per thread
-  const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((want + threads - 1) / threads, 148 * 64));
-  uint64_t sm, sp;
-  lcg_jump(static_cast<uint64_t>(blocks) * threads, sm, sp);
-  fy_draws_kernel<<<static_cast<unsigned>(blocks), threads, 0, s>>>(seed64, n, sm, sp, keys, vals, pb.G, pb.IB);
+  const bool binned = n >= QMCG_K1_BIN_MIN;
+  int shift = 0;
+  while (shift < 32 && (static_cast<uint64_t>(n - 1) >> shift) >= static_cast<uint64_t>(kBins)) ++shift;
   // sorted entries in region A (keys+vals, or skeys+svals after a sort); the chase starts go to
   // the other region B, the binned pairs back to A
   char* regA = base + L.keys;
   char* regB = base + L.skeys;
-  int nl = 3;
-  if (pb.sort_bits > 0) {
-    size_t temp_bytes = L.temp_bytes;
-    e = cub::DeviceRadixSort::SortPairs(base + L.temp, temp_bytes, keys, reinterpret_cast<uint32_t*>(base + L.skeys),
-                                        vals, reinterpret_cast<uint32_t*>(base + L.svals), static_cast<int64_t>(n), 0,
-                                        pb.sort_bits, s);
-    if (e != cudaSuccess) return e;
-    std::swap(regA, regB);
-    nl += 2;
-  }
-  const auto* sk = reinterpret_cast<const uint32_t*>(regA);
-  const auto* sv = reinterpret_cast<const uint32_t*>(regA + (L.vals - L.keys));
+  int nl = 4;  // draws, span starts, spans, chase
+  e = pb.sort_bits <= 16 ? k1_grouped<uint16_t>(seed64, n, pb, base, L, s, binned, shift, regA, regB, nl)
+                         : k1_grouped<uint32_t>(seed64, n, pb, base, L, s, binned, shift, regA, regB, nl);
+  if (e != cudaSuccess) return e;
   auto* starts = reinterpret_cast<uint2*>(regB);
-  const bool binned = n >= QMCG_K1_BIN_MIN;
-  int shift = 0;
-  while (shift < 32 && (static_cast<uint64_t>(n - 1) >> shift) >= static_cast<uint64_t>(kBins)) ++shift;
-  const int64_t nspans = (n + kSpan - 1) / kSpan;
-  fy_span_start_kernel<<<static_cast<unsigned>((n / 4 + 1 + threads - 1) / threads), threads, 0, s>>>(
-      sk, n, 8 - pb.G, static_cast<uint32_t>(nspans), sstart, binned ? cursor : nullptr, shift);
-  fy_span_kernel<<<static_cast<unsigned>((nspans + kSpanWarps - 1) / kSpanWarps), kSpanWarps * 32, 0, s>>>(
-      sk, sv, n, pb.G, pb.IB, sstart, nspans, F, starts);
   const int64_t ab = (n + threads * kChase - 1) / (threads * kChase);
   auto* pairs = reinterpret_cast<uint2*>(regA);  // the sorted entries are consumed by now
   fy_chase_kernel<<<static_cast<unsigned>(ab), threads, 0, s>>>(starts, n, F, out, binned ? pairs : nullptr, add);
@@ -2052,7 +2082,7 @@ cudaError_t launch_perm_build(uint64_t seed64, int64_t n, uint32_t* out, void* s
     fy_scatter_kernel<<<static_cast<unsigned>((n + threads - 1) / threads), threads, 0, s>>>(binned_pairs, n, out);
     nl += 2;
   }
-  if (launches) *launches += nl;  // draws, [sort: histogram + >=1 pass], span starts, spans, chase [+ bin, scatter]
+  if (launches) *launches += nl;
   return cudaGetLastError();
 }
 
