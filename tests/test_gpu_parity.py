@@ -250,6 +250,14 @@ def test_fp32_variant_within_qmc_error(ctx, qmcg, s, kind, m, n):
     assert err <= 5e-5 * s[0], err
 
 
+@pytest.mark.parametrize("n", [(1 << 23) + 5, (1 << 24) - 1, (1 << 24) + 1])
+def test_permutations_key_width_boundary(ctx, oracle_lib, n):
+    """K1 sorts 16-bit keys up to n = 2^24 (8 low bits of j ride in the value) and 32-bit keys
+    above (2^24 + 1: 25 index bits, 7 carried bits, 18 sorted): both sides of the switch."""
+    s = 0x243F6A8885A308D3 ^ n
+    assert np.array_equal(ctx.permutation(n, s)[:n], oracle_lib.permutation_indices(n, s)[:n])
+
+
 @pytest.mark.parametrize("n", [(1 << 25) + 3, 1 << 26])
 def test_permutations_binned_scatter_bit_exact(ctx, oracle_lib, n):
     """K1 from 2^25 entries scatters through 256 i-bins (QMCG_K1_BIN_MIN); same table as the
