@@ -19,7 +19,8 @@ for lg in 24 28; do
   echo k1_${lg}_rc=$?
 done
 python tools/c4_batch.py > gpurun_out/r2f_c4.log 2>&1 && \
-  ncu --metrics $M,smsp__issue_active.avg.pct_of_peak_sustained_active --clock-control none -c 12 --csv \
+  ncu --metrics $M,smsp__issue_active.avg.pct_of_peak_sustained_active --clock-control none \
+      -k regex:"walk_group|pairwise|gen_z" -c 9 --csv \
       --log-file gpurun_out/r2f_c4.csv python tools/c4_batch.py > /dev/null 2>&1
 echo c4_rc=$?
 for kind in 0 1; do
