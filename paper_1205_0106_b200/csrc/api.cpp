@@ -1990,7 +1990,7 @@ static qmcg_status batch_impl(qmcg_ctx* c, const qmcg_option_spec* specs, int64_
         const PriceParams& P = plans[static_cast<size_t>(shared_idx[k][j])].P;
         cps[j] = qmcg::ContractParams{P.dpow, P.X0, P.b, P.alpha, P.c0, P.strike, P.best0, P.log_strike,
                                       P.dom_slope, P.bs_vsqrt, P.bs_mu_t, P.bs_kdisc, P.bs_fwd_growth, P.bs_disc,
-                                      P.x0mk, P.bs_v_zero, 0};
+                                      P.x0mk, 1.0 / P.bs_kdisc, P.bs_v_zero, 0};
       }
       QMCG_CUDA(c->d_cparams[k].reserve(cnt));
       QMCG_CUDA(cudaMemcpyAsync(c->d_cparams[k].ptr, cps.data(), cnt * sizeof(qmcg::ContractParams),

@@ -140,6 +140,9 @@ __device__ __forceinline__ double moro_central_plus(double y, double alpha) {
 __constant__ double2 c_log_table[128];
 __constant__ double c_tail_y = 0.42;  // Moro branch point |u - 1/2| > 0.42 (analytic.cpp:87)
 __constant__ double c_log_consts[2] = {0.0 /* unused */, 0x1.62e42fefa39efp-1 /* ln 2 */};
+// dev_log's polynomial in the constant bank: the DFMAs take them as c[][] operands (as 64-bit
+// immediates each cost a UMOV pair per use, ~1 warp instruction per warp-date in the tail)
+__constant__ double c_log_poly[4] = {0x1.999999999999ap-3, -0x1.0001p-2, 0x1.5555555555555p-2, -0x1.ffffffffap-2};
 
 // Shared-memory accessors on 32-bit shared-window addresses (keeps the
 // compiler from rebuilding generic->shared windows inside the hot loops).
@@ -191,9 +194,9 @@ __device__ __forceinline__ double dev_log(double x, uint32_t tab) {
   const double2 t = lds_v2f64(tab + (static_cast<uint32_t>(hi >> 9) & 0x7f0u));
   const double m = __hiloint2double((hi & 0x000fffff) | 0x3ff00000, lo);
   const double f = fma(m, t.x, -1.0);
-  double q = fma(f, 0x1.999999999999ap-3, -0x1.0001p-2);
-  q = fma(f, q, 0x1.5555555555555p-2);
-  q = fma(f, q, -0x1.ffffffffap-2);
+  double q = fma(f, c_log_poly[0], c_log_poly[1]);
+  q = fma(f, q, c_log_poly[2]);
+  q = fma(f, q, c_log_poly[3]);
   const double p = fma(f * f, q, f);
   const double de = static_cast<double>(e);  // exact: one I2F.F64 (the 2^52 magic took 3 issue slots)
   return fma(de, c_log_consts[1], t.y + p);
@@ -207,9 +210,9 @@ __device__ __forceinline__ double dev_neglog(double x, uint32_t tab) {
   const double2 t = lds_v2f64(tab + (static_cast<uint32_t>(hi >> 9) & 0x7f0u));
   const double m = __hiloint2double((hi & 0x000fffff) | 0x3ff00000, lo);
   const double f = fma(m, t.x, -1.0);
-  double q = fma(f, 0x1.999999999999ap-3, -0x1.0001p-2);
-  q = fma(f, q, 0x1.5555555555555p-2);
-  q = fma(f, q, -0x1.ffffffffap-2);
+  double q = fma(f, c_log_poly[0], c_log_poly[1]);
+  q = fma(f, q, c_log_poly[2]);
+  q = fma(f, q, c_log_poly[3]);
   const double p = fma(f * f, q, f);
   const double de = static_cast<double>(e);  // exact: one I2F.F64 (the 2^52 magic took 3 issue slots)
   return fma(de, -c_log_consts[1], -(t.y + p));
@@ -261,6 +264,30 @@ __device__ __forceinline__ double moro_full(double u) {
   if (!moro_is_tail(y)) return moro_central_plus<true>(y, 0.0);
   const double x = moro_tail_poly(y > 0.0 ? __dadd_rn(1.0, -u) : u);
   return y > 0.0 ? x : -x;
+}
+
+// exp for the batch walk (candidates, final interval): k = rint(x / ln 2) by the 1.5 * 2^52 trick,
+// r = x - k ln 2 (two-part ln 2), e^r by Horner on the Taylor series to r^13 (truncation < 4e-18 for
+// |r| <= ln2 / 2), scaled by 2^k in the exponent field; ~1 ulp like CUDA's exp, with the
+// coefficients in the constant bank instead of per-call immediates (CUDA's exp rebuilds ~24 of
+// them with UMOVs each call inside the per-strike loop). |x| beyond the normal range: CUDA's exp.
+__constant__ double c_exp_poly[12] = {1.6059043836821613e-10, 2.08767569878681e-09, 2.505210838544172e-08,
+                                      2.755731922398589e-07,  2.7557319223985893e-06, 2.48015873015873e-05,
+                                      1.984126984126984e-04,  1.388888888888889e-03,  8.333333333333333e-03,
+                                      4.1666666666666664e-02, 1.6666666666666666e-01, 0.5};
+__device__ __forceinline__ double dev_exp(double x) {
+  const double t = fma(x, 0x1.71547652b82fep0, 0x1.8p52);
+  const double kd = t - 0x1.8p52;
+  const int k = __double2loint(t);
+  double r = fma(kd, -0x1.62e42fefa39efp-1, x);
+  r = fma(kd, -0x1.abc9e3b39803fp-56, r);
+  double p = c_exp_poly[0];
+#pragma unroll
+  for (int i = 1; i < 12; ++i) p = fma(p, r, c_exp_poly[i]);
+  p = fma(p, r, 1.0);
+  p = fma(p, r, 1.0);
+  if (k < -1020 || k > 1020) return exp(x);
+  return __hiloint2double(__double2hiint(p) + (k << 20), __double2loint(p));
 }
 
 // Hart CND (analytic.cpp:33-72) for the batch's per-strike final interval,
@@ -1628,7 +1655,7 @@ __device__ __noinline__ void group_flush(const ContractParams* __restrict__ cp, 
   for (int i = 0; i < cnt; ++i) {
     const double v = lds_f64(cs + i * 8);
     const uint32_t j = lds_u32(cj + i * 4);
-    sts_f64(cs + i * 8, exp(fma(g->b, v, g->X0)));
+    sts_f64(cs + i * 8, dev_exp(fma(g->b, v, g->X0)));
     sts_f64(cj + kGCap * 4 + i * 8, __ldg(g->dpow + j + 1));
   }
   for (int s = 0; s < g->count; ++s) {
@@ -1750,12 +1777,12 @@ __global__ void __launch_bounds__(kGThreads, QMCG_G_MINB) walk_group_kernel(cons
   for (int i = 0; i < cnt; ++i) {
     const double v = lds_f64(cs + i * 8);
     const uint32_t j = lds_u32(cj + i * 4);
-    sts_f64(cs + i * 8, exp(fma(gb, v, g->X0)));
+    sts_f64(cs + i * 8, dev_exp(fma(gb, v, g->X0)));
     sts_f64(cj + kGCap * 4 + i * 8, __ldg(g->dpow + j + 1));
   }
   kd += 1.0;
   const double X = fma(gb, fma(alpha, kd, __ldg(zc + static_cast<int64_t>(mrec) * B.ldz)), g->X0);
-  const double sl = exp(X);
+  const double sl = dev_exp(X);
   const double dm = __ldg(g->dpow + m);
   const double inv_vst = 1.0 / g->bs_vsqrt;
 #pragma unroll 1
@@ -1788,8 +1815,8 @@ __global__ void __launch_bounds__(kGThreads, QMCG_G_MINB) walk_group_kernel(cons
     } else {
       const double d1 = (X - q.log_strike + g->bs_mu_t) * inv_vst;
       const double d2 = d1 - g->bs_vsqrt;
-      const double e1 = exp(-0.5 * d1 * d1);
-      const double e2 = e1 * (sl * rcp_nr(q.bs_kdisc));
+      const double e1 = dev_exp(-0.5 * d1 * d1);
+      const double e2 = e1 * (sl * q.bs_inv_kdisc);
       const double price = KIND == 0 ? sl * cnd_tail_form(d1, e1) - q.bs_kdisc * cnd_tail_form(d2, e2)
                                      : q.bs_kdisc * cnd_tail_form(-d2, e2) - sl * cnd_tail_form(-d1, e1);
       cont = price > 0.0 ? price : 0.0;

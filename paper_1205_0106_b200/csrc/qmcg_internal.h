@@ -78,6 +78,7 @@ struct ContractParams {
   double X0, b, alpha, c0, strike, best0, log_strike, dom_slope;
   double bs_vsqrt, bs_mu_t, bs_kdisc, bs_fwd_growth, bs_disc;
   double x0mk;
+  double bs_inv_kdisc;  // 1 / bs_kdisc (the batch's one-exp final interval)
   int32_t bs_v_zero, pad;
 };
 

@@ -18,8 +18,12 @@ for ln in dis.splitlines():
     m = re.match(r"\s*/\*([0-9a-f]{4,})\*/\s+(.*)", ln)
     if m and cur_fn and re.search(kre, cur_fn):
         line_of[int(m.group(1), 16)] = cur_line
+which = int(sys.argv[5]) if len(sys.argv) > 5 else 0  # which captured kernel of the report (0 = first)
 src = list(csv.reader(io.StringIO(subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"], capture_output=True, text=True).stdout)))
-h = src[1]; ix = {k: i for i, k in enumerate(h)}
+# a report with several kernels repeats the (kernel line, header) pair per kernel
+starts = [k for k, r in enumerate(src) if r and r[0] == "Address"]
+h = src[starts[which]]; ix = {k: i for i, k in enumerate(h)}
+src = [None] + src[starts[which]:(starts[which + 1] - 1 if which + 1 < len(starts) else len(src))]
 stalls = [k for k in h if k.startswith("stall_") and "Not Issued" not in k]
 rows = src[2:]
 base = int(rows[0][ix["Address"]], 16)
