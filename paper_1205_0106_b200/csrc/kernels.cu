@@ -1064,13 +1064,63 @@ __global__ void european_kernel(const double* __restrict__ urow, int64_t count, 
 }
 
 // D1: uniforms (or Moro normals) of one dimension for `count` paths.
-__global__ void uniforms_kernel(const uint32_t* __restrict__ perm_row, int64_t count, DimParam dp,
-                                const double* __restrict__ sc, const double* __restrict__ nc,
-                                int normals, double* __restrict__ out) {
-  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i >= count) return;
-  const double u = halton(perm_row[i], dp, sc, nc);  // table entry = perm + 1
-  out[i] = normals ? moro_full(u) : u;
+// Four entries per thread (block tile of 4 x 256, each load/store instruction coalesced), digit by
+// digit: the dimension's scale constants are loaded once per digit for the four, and the four
+// division chains are independent. Same arithmetic per entry as halton().
+constexpr int kUniPer = 4;
+__global__ void __launch_bounds__(256) uniforms_kernel(const uint32_t* __restrict__ perm_row, int64_t count,
+                                                       DimParam dp, const double* __restrict__ sc,
+                                                       const double* __restrict__ nc, int normals,
+                                                       double* __restrict__ out) {
+  const int64_t base = static_cast<int64_t>(blockIdx.x) * (blockDim.x * kUniPer) + threadIdx.x;
+  uint32_t x[kUniPer];
+  double v[kUniPer];
+#pragma unroll
+  for (int e = 0; e < kUniPer; ++e) {
+    const int64_t i = base + e * blockDim.x;
+    x[e] = i < count ? __ldg(perm_row + i) : 1u;  // table entry = perm + 1
+  }
+  const double* sp = sc + dp.doff;
+  const double* cp = nc + dp.doff;
+  const int D = static_cast<int>(dp.ndig);
+  if (D == 1) {
+    const double s0 = __ldg(sp), c0 = __ldg(cp);
+#pragma unroll
+    for (int e = 0; e < kUniPer; ++e) v[e] = digit_term(x[e], s0, c0);
+  } else {
+    double sj = __ldg(sp), cj = __ldg(cp);
+#pragma unroll
+    for (int e = 0; e < kUniPer; ++e) {
+      const uint32_t q = div_p(x[e], dp);
+      v[e] = digit_term(x[e] - q * dp.p, sj, cj);
+      x[e] = q;
+    }
+    for (int j = 1; j < D - 1; ++j) {
+      sj = __ldg(sp + j);
+      cj = __ldg(cp + j);
+#pragma unroll
+      for (int e = 0; e < kUniPer; ++e) {
+        const uint32_t q = div_p(x[e], dp);
+        v[e] = __dadd_rn(v[e], digit_term(x[e] - q * dp.p, sj, cj));
+        x[e] = q;
+      }
+    }
+    sj = __ldg(sp + D - 1);
+    cj = __ldg(cp + D - 1);
+#pragma unroll
+    for (int e = 0; e < kUniPer; ++e) v[e] = __dadd_rn(v[e], digit_term(x[e], sj, cj));
+  }
+#pragma unroll
+  for (int e = 0; e < kUniPer; ++e) {
+    const int64_t i = base + e * blockDim.x;
+    if (i >= count) continue;
+    double u = v[e];
+    if (dp.flags & DIM_CLAMP) {  // kEndpointEps clamp, quasi_rng.cpp:80-81 (as in halton())
+      if (u < 1e-12) u = 1e-12;
+      if (u > 1.0 - 1e-12) u = 1.0 - 1e-12;
+    }
+    out[i] = normals ? moro_full(u) : u;
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -1874,7 +1924,7 @@ cudaError_t launch_european(const double* urow, int64_t count, double s0, double
 
 cudaError_t launch_uniforms(const uint32_t* perm_row, int64_t count, DimParam dp, const double* sc,
                             const double* nc, int normals, double* out, cudaStream_t s) {
-  const int64_t blocks = (count + 255) / 256;
+  const int64_t blocks = (count + 256 * kUniPer - 1) / (256 * kUniPer);
   uniforms_kernel<<<static_cast<unsigned>(blocks), 256, 0, s>>>(perm_row, count, dp, sc, nc, normals, out);
   return cudaGetLastError();
 }
