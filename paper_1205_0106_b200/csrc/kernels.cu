@@ -1067,7 +1067,10 @@ __global__ void european_kernel(const double* __restrict__ urow, int64_t count, 
 // Four entries per thread (block tile of 4 x 256, each load/store instruction coalesced), digit by
 // digit: the dimension's scale constants are loaded once per digit for the four, and the four
 // division chains are independent. Same arithmetic per entry as halton().
-constexpr int kUniPer = 4;
+#ifndef QMCG_UNI_PER
+#define QMCG_UNI_PER 4
+#endif
+constexpr int kUniPer = QMCG_UNI_PER;
 __global__ void __launch_bounds__(256) uniforms_kernel(const uint32_t* __restrict__ perm_row, int64_t count,
                                                        DimParam dp, const double* __restrict__ sc,
                                                        const double* __restrict__ nc, int normals,
