@@ -558,7 +558,10 @@ struct CallPlan {
 // Validation + host constants, in the order of reference price_american
 // (american.cpp:103-116) -> make_schedule (path_engine.cpp:63-76) ->
 // simulate_batch (path_engine.cpp:124-136) -> QuasiStream (quasi_rng.cpp:85-94).
-qmcg_status plan_call(const qmcg_option_spec& s, int64_t m, int64_t n, uint32_t flags, CallPlan& plan) {
+// `chain`: a discount chain already computed for this m (a batch's previous contract); reused when
+// its discount factor is this contract's (the 128-step dependent multiply chain dominates a plan).
+qmcg_status plan_call(const qmcg_option_spec& s, int64_t m, int64_t n, uint32_t flags, CallPlan& plan,
+                      const std::vector<double>* chain = nullptr) {
   qmcg_status st = validate(s);
   if (st) return st;
   if (s.kind != QMCG_CALL && !(flags & QMCG_FLAG_ALLOW_PUT))
@@ -591,9 +594,13 @@ qmcg_status plan_call(const qmcg_option_spec& s, int64_t m, int64_t n, uint32_t 
     P.b = bdiff;
     P.alpha = a / bdiff;
   }
-  plan.dpow.resize(static_cast<size_t>(m) + 1);
-  plan.dpow[0] = 1.0;
-  for (int64_t k = 1; k <= m; ++k) plan.dpow[static_cast<size_t>(k)] = plan.dpow[static_cast<size_t>(k - 1)] * disc;
+  if (chain && chain->size() == static_cast<size_t>(m) + 1 && m >= 1 && bits_of((*chain)[1]) == bits_of(disc)) {
+    plan.dpow = *chain;
+  } else {
+    plan.dpow.resize(static_cast<size_t>(m) + 1);
+    plan.dpow[0] = 1.0;
+    for (int64_t k = 1; k <= m; ++k) plan.dpow[static_cast<size_t>(k)] = plan.dpow[static_cast<size_t>(k - 1)] * disc;
+  }
   P.rate_negative = disc > 1.0;
   P.dom_slope = s.kind == QMCG_CALL ? (r * dt) / P.b : r * dt;
   P.x0mk = 1.0 + P.X0 - P.log_strike;
@@ -1886,37 +1893,74 @@ static qmcg_status batch_impl(qmcg_ctx* c, const qmcg_option_spec* specs, int64_
   if (n_specs == 0) return QMCG_OK;
   Trace tr("batch");
   std::vector<CallPlan> plans(static_cast<size_t>(n_specs));
-  for (int64_t i = 0; i < n_specs; ++i) {
-    qmcg_status st = plan_call(specs[i], m, n, flags, plans[static_cast<size_t>(i)]);
-    if (st) return st;
-  }
-  tr.mark("plans");
-  qmcg_status st = ensure_dim_tables(c, n, m);
+  qmcg_status st = plan_call(specs[0], m, n, flags, plans[0]);
+  if (st) return st;
+  st = ensure_dim_tables(c, n, m);
   if (st) return st;
   st = ensure_perms(c, seed, n, 0, n, m, (flags & QMCG_FLAG_NO_CACHE) != 0);
   if (st) return st;
   st = prepare_scratch(c, static_cast<size_t>(n_specs));
   if (st) return st;
-  // discount chains of every contract in one upload
+  // The prefix sums S_k of the shared normals depend only on the table: enqueue them before the
+  // other contracts are planned, so the device works while the host plans (speculative when the
+  // first contract is plain; unused if fewer than two contracts turn out to be)
+  const auto plain = [](const PriceParams& P) { return !P.deterministic && !P.check_range && !P.rate_negative; };
+  bool z_ready = false;
+  if (n_specs >= 2 && plain(plans[0].P)) {
+    QMCG_CUDA(c->d_z.reserve(static_cast<size_t>(m + 8) * static_cast<size_t>(n)));  // + 8 prefetch rows
+    PriceParams G = plans[0].P;
+    G.table = c->table;
+    G.ld = qmcg::table_ld(c->col_end - c->col_begin);
+    G.col_begin = c->col_begin;
+    G.path_begin = 0;
+    G.path_count = n;
+    G.alpha = 0.0;
+    QMCG_CUDA(qmcg::launch_gen_z(G, c->d_z.ptr, n, c->stream, qmcg::kGenPrefix));
+    c->launches += 1;
+    z_ready = true;
+    tr.mark("gen_z enqueued");
+  }
+  for (int64_t i = 1; i < n_specs; ++i) {
+    st = plan_call(specs[i], m, n, flags, plans[static_cast<size_t>(i)], &plans[static_cast<size_t>(i - 1)].dpow);
+    if (st) return st;
+  }
+  tr.mark("plans");
+  // discount chains: one per distinct discount factor (a strike/volatility grid shares one), one
+  // upload from pageable memory (staged before the call returns: no synchronisation needed)
   c->dpow_host.clear();
-  QMCG_CUDA(c->d_dpow.reserve(static_cast<size_t>(m + 1) * static_cast<size_t>(n_specs)));
   {
-    std::vector<double> all(static_cast<size_t>(m + 1) * static_cast<size_t>(n_specs));
-    for (int64_t i = 0; i < n_specs; ++i)
-      std::copy(plans[static_cast<size_t>(i)].dpow.begin(), plans[static_cast<size_t>(i)].dpow.end(),
-                all.begin() + i * (m + 1));
+    std::vector<double> all;
+    std::vector<std::pair<uint64_t, size_t>> seen;  // (bits of disc, chain index)
+    std::vector<size_t> chain_of(static_cast<size_t>(n_specs));
+    for (int64_t i = 0; i < n_specs; ++i) {
+      const std::vector<double>& dp = plans[static_cast<size_t>(i)].dpow;
+      const uint64_t key = bits_of(dp.size() > 1 ? dp[1] : 1.0);
+      size_t idx = seen.size();
+      for (const auto& kv : seen)
+        if (kv.first == key) {
+          idx = kv.second;
+          break;
+        }
+      if (idx == seen.size()) {
+        seen.emplace_back(key, idx);
+        all.insert(all.end(), dp.begin(), dp.end());
+      }
+      chain_of[static_cast<size_t>(i)] = idx;
+    }
+    QMCG_CUDA(c->d_dpow.reserve(all.size()));
     QMCG_CUDA(cudaMemcpyAsync(c->d_dpow.ptr, all.data(), all.size() * sizeof(double), cudaMemcpyHostToDevice,
                               c->stream));
-    QMCG_CUDA(cudaStreamSynchronize(c->stream));
+    for (int64_t i = 0; i < n_specs; ++i)
+      plans[static_cast<size_t>(i)].P.dpow =
+          c->d_dpow.ptr + chain_of[static_cast<size_t>(i)] * static_cast<size_t>(m + 1);
   }
-  tr.mark("tables+dpow");
+  tr.mark("dpow");
   // Contracts on the plain path share one normal table (generated once, inside
   // this call) and are walked kCpt per thread; the rest use the fused kernel.
   std::vector<int64_t> shared_idx[2], single_idx;
   for (int64_t i = 0; i < n_specs; ++i) {
     const PriceParams& P = plans[static_cast<size_t>(i)].P;
-    plans[static_cast<size_t>(i)].P.dpow = c->d_dpow.ptr + static_cast<size_t>(i) * static_cast<size_t>(m + 1);
-    if (!P.deterministic && !P.check_range && !P.rate_negative) shared_idx[P.kind].push_back(i);
+    if (plain(P)) shared_idx[P.kind].push_back(i);
     else single_idx.push_back(i);
   }
   const bool use_shared = shared_idx[0].size() + shared_idx[1].size() >= 2;
@@ -1932,17 +1976,19 @@ static qmcg_status batch_impl(qmcg_ctx* c, const qmcg_option_spec* specs, int64_
   std::vector<double> shared_sums[2];
   bool tree_on_side = false;
   if (use_shared) {
-    QMCG_CUDA(c->d_z.reserve(static_cast<size_t>(m + 8) * static_cast<size_t>(n)));  // + 8 prefetch rows
-    PriceParams G = plans[static_cast<size_t>(shared_idx[0].empty() ? shared_idx[1][0] : shared_idx[0][0])].P;
-    G.table = c->table;
-    G.ld = qmcg::table_ld(c->col_end - c->col_begin);
-    G.col_begin = c->col_begin;
-    G.path_begin = 0;
-    G.path_count = n;
-    G.alpha = 0.0;
-    QMCG_CUDA(qmcg::launch_gen_z(G, c->d_z.ptr, n, c->stream, qmcg::kGenPrefix));
-    c->launches += 1;
-    tr.mark("gen_z enqueued");
+    if (!z_ready) {
+      QMCG_CUDA(c->d_z.reserve(static_cast<size_t>(m + 8) * static_cast<size_t>(n)));  // + 8 prefetch rows
+      PriceParams G = plans[static_cast<size_t>(shared_idx[0].empty() ? shared_idx[1][0] : shared_idx[0][0])].P;
+      G.table = c->table;
+      G.ld = qmcg::table_ld(c->col_end - c->col_begin);
+      G.col_begin = c->col_begin;
+      G.path_begin = 0;
+      G.path_count = n;
+      G.alpha = 0.0;
+      QMCG_CUDA(qmcg::launch_gen_z(G, c->d_z.ptr, n, c->stream, qmcg::kGenPrefix));
+      c->launches += 1;
+      tr.mark("gen_z enqueued");
+    }
     for (int k = 0; k < 2; ++k) {
       const size_t cnt = shared_idx[k].size();
       if (!cnt) continue;
