@@ -153,6 +153,26 @@ def test_batch_matches_single(ctx, qmcg):
         assert abs(one.std_error - r.std_error) <= 1e-9 * one.std_error + 1e-12
 
 
+@pytest.mark.parametrize("layout", ["one_plain_first", "plain_after_fused", "rates_interleaved"])
+def test_batch_host_ordering(ctx, qmcg, layout):
+    """The batch enqueues the shared prefix sums before planning the other contracts (speculatively
+    when the first is plain) and uploads one discount chain per distinct discount factor: results
+    must not depend on which contract comes first or how the rates interleave."""
+    plain = spec_of(qmcg, (100.0, 95.0, 0.05, 0.25, 1.0))
+    flat = spec_of(qmcg, (100.0, 100.0, 0.05, 0.0, 1.0))        # sigma = 0: fused path
+    if layout == "one_plain_first":  # speculative prefix sums, then no shared walk at all
+        specs = [plain, flat]
+    elif layout == "plain_after_fused":
+        specs = [flat, plain, spec_of(qmcg, (100.0, 110.0, 0.05, 0.25, 1.0), kind=1)]
+    else:
+        specs = [spec_of(qmcg, (100.0, 90 + 5 * i, (0.01, 0.07, 0.03)[i % 3], 0.2, 1.0), kind=i % 2) for i in range(9)]
+    n, m = (1 << 13) + 5, 20
+    batch = ctx.price_american_batch(specs, m, n, 42, allow_put=True)
+    for s, r in zip(specs, batch):
+        one = ctx.price_american(s, m, n, 42, allow_put=True)
+        assert abs(one.price - r.price) <= 1e-12 * max(one.price, 1e-300), (layout, s, one.price, r.price)
+
+
 @pytest.mark.parametrize("rate,vol", [(0.05, 0.2), (0.15, 0.05), (0.0, 0.3)])
 def test_batch_grouped_strikes(ctx, qmcg, rate, vol):
     """The grouped batch walk: many strikes of both kinds sharing (spot, rate, vol, maturity), plus a
