@@ -24,6 +24,7 @@
 #include <functional>
 #include <memory>
 #include <thread>
+#include <unordered_map>
 #include <vector>
 
 using qmcg::DimParam;
@@ -1930,22 +1931,13 @@ static qmcg_status batch_impl(qmcg_ctx* c, const qmcg_option_spec* specs, int64_
   c->dpow_host.clear();
   {
     std::vector<double> all;
-    std::vector<std::pair<uint64_t, size_t>> seen;  // (bits of disc, chain index)
+    std::unordered_map<uint64_t, size_t> seen;  // bits of the discount factor -> chain index
     std::vector<size_t> chain_of(static_cast<size_t>(n_specs));
     for (int64_t i = 0; i < n_specs; ++i) {
       const std::vector<double>& dp = plans[static_cast<size_t>(i)].dpow;
-      const uint64_t key = bits_of(dp.size() > 1 ? dp[1] : 1.0);
-      size_t idx = seen.size();
-      for (const auto& kv : seen)
-        if (kv.first == key) {
-          idx = kv.second;
-          break;
-        }
-      if (idx == seen.size()) {
-        seen.emplace_back(key, idx);
-        all.insert(all.end(), dp.begin(), dp.end());
-      }
-      chain_of[static_cast<size_t>(i)] = idx;
+      const auto ins = seen.emplace(bits_of(dp.size() > 1 ? dp[1] : 1.0), seen.size());
+      if (ins.second) all.insert(all.end(), dp.begin(), dp.end());
+      chain_of[static_cast<size_t>(i)] = ins.first->second;
     }
     QMCG_CUDA(c->d_dpow.reserve(all.size()));
     QMCG_CUDA(cudaMemcpyAsync(c->d_dpow.ptr, all.data(), all.size() * sizeof(double), cudaMemcpyHostToDevice,
