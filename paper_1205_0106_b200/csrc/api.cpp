@@ -372,7 +372,7 @@ struct qmcg_ctx {
   DevBuf<uint32_t> d_err, d_fullperm;
   DevBuf<char> d_permscratch;
   // second K1 lane: tables built alternately on `stream` and `side` so one table's latency-bound
-  // assign pass overlaps the next table's sort (n <= kOverlapMaxN)
+  // chase pass overlaps the next table's sort (n <= kOverlapMaxN)
   cudaStream_t side[2] = {nullptr, nullptr};
   DevBuf<char> d_permscratch_side[2];
   DevBuf<uint32_t> d_xrow_side[2];  // the side lanes' rows of perm + 1 on their way into the uniform table
@@ -441,14 +441,14 @@ constexpr int64_t kOverlapMaxN = int64_t{1} << 25;  // the extra K1 scratch stay
 
 // Rows [d0, d1) of a table, row k holding dimension dim_begin + k * dim_stride, with `lanes` K1
 // builds in flight: row k on lane (k - d0) mod lanes (lane 0 = `stream`, the others side streams
-// with their own scratch), so one table's latency-bound assign pass overlaps the next table's
+// with their own scratch), so one table's latency-bound chase pass overlaps the next table's
 // sort; `stream` then waits for the side lanes, so everything after sees all rows.
 //   xdst: the rows are perm + 1 (u32, leading dimension ld, all n columns) -- the exchange format
 //         of qmcg_build_tables;
 //   udst: the rows are the uniforms uniform_at(p, dim) of columns [cb, ce) (f64, leading dimension
 //         ld) -- the uniform table K2 reads: K1 writes the lane's row of perm + 1, then
 //         uniforms_kernel turns the column slice into bit-exact radical inverses (writing the
-//         uniforms from K1's assign pass instead measured slower: its latency-bound chase grew by
+//         uniforms from K1's chase pass instead measured slower: its latency-bound chase grew by
 //         the digit division, 2^24 table 0.87 -> 1.07 ms).
 // The caller has made the dimension constants of every built dim resident (ensure_dim_tables).
 qmcg_status build_rows(qmcg_ctx* c, uint64_t seed, int64_t n, uint32_t* xdst, double* udst, int64_t ld, int64_t cb,
