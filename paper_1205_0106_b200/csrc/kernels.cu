@@ -1246,6 +1246,22 @@ __global__ void fy_span_start_kernel(const KeyT* __restrict__ sk, int64_t n, int
 #define QMCG_SPAN_LOOK 4
 #endif
 constexpr int kSpan = 256, kSpanWarps = QMCG_SPAN_WARPS, kSpanLook = QMCG_SPAN_LOOK;
+// Lanes of `eq` whose byte b equals this lane's: one ballot per bit, each combined as
+// eq &= ~(ballot ^ m) with m = all ones when the bit is set (one LOP3): 3 ALU instructions per bit
+// (the C++ form compiled to 5: shift, test, compare, select, combine).
+__device__ __forceinline__ unsigned lanes_with_same_byte(uint32_t b, unsigned eq) {
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    asm("{\n .reg .pred p;\n .reg .b32 t, bb, m;\n"
+        " and.b32 t, %1, %2;\n setp.ne.u32 p, t, 0;\n"
+        " vote.sync.ballot.b32 bb, p, 0xffffffff;\n"
+        " selp.b32 m, -1, 0, p;\n"
+        " lop3.b32 %0, %0, bb, m, 0x90;\n}"
+        : "+r"(eq)
+        : "r"(b), "r"(1u << k));
+  }
+  return eq;
+}
 __device__ __forceinline__ uint32_t span_bucket(uint32_t key, uint32_t val, int G, int IB) {
   const uint32_t j = (key << G) | (G ? val >> IB : 0u);
   return j & (kSpan - 1);
@@ -1290,12 +1306,7 @@ __global__ void __launch_bounds__(kSpanWarps * 32) fy_span_kernel(const KeyT* __
       const uint32_t i = vv[u] & imask;
       const uint32_t x = jlo + b;
       unsigned eq = __ballot_sync(kFull, valid);
-#pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        const bool bit = (b >> k) & 1u;
-        const unsigned bb = __ballot_sync(kFull, bit);
-        eq &= bit ? bb : ~bb;
-      }
+      eq = lanes_with_same_byte(b, eq);
       const unsigned up = eq & gt;
       const uint32_t inext = __shfl_sync(kFull, i, up ? __ffs(up) - 1 : lane);
       const uint32_t S = up ? inext : (valid ? last[b] : kNone);
