@@ -1302,7 +1302,8 @@ __global__ void __launch_bounds__(kSpanWarps * 32) fy_span_kernel(const KeyT* __
       const int64_t p = hi - 32 * (u + 1) + lane;
       if (hi - 32 * u <= s) break;  // warp-uniform: no entry left
       const bool valid = p >= s;
-      const uint32_t b = valid ? span_bucket(kk[u], vv[u], G, IB) : 0u;
+      // 16-bit keys imply G = 8 (n <= 2^24): the span bucket is exactly j's low byte, vals >> IB
+      const uint32_t b = !valid ? 0u : sizeof(KeyT) == 2 ? vv[u] >> IB : span_bucket(kk[u], vv[u], G, IB);
       const uint32_t i = vv[u] & imask;
       const uint32_t x = jlo + b;
       unsigned eq = __ballot_sync(kFull, valid);
