@@ -874,19 +874,33 @@ __global__ void __launch_bounds__(kThreads, QMCG_MINB)
           (void)anyp;
 #endif
         }
-      } else
+      } else {  // FP32: the same grouping (one vote per kPushGroup dates), selects in single precision
 #pragma unroll
-      for (int t = 0; t < kTile; ++t) {
-        V = add_rn(V, Z::load(zcol + t * kThreads * Z::kSize));
-        cd = add_rn(cd, slope);
-        const bool rec = KIND == 0 ? V > c : V < c;
-        const bool push = rec && (KIND == 0 || pl + k0 >= 0) && !record_dominates<KIND>(V, c, cd, bT, x0mkT);
-        const double pv = c;
-        const int pdl = pl;
-        c = rec ? V : c;
-        cd = rec ? (KIND == 0 ? V : T(0)) : cd;
-        pl = rec ? t : pl;
-        push_record<KIND, RNEG>(ws, P, push, pv, k0 + pdl, lane, lt, rq_head, rq_tail);
+        for (int g = 0; g < kTile; g += kPushGroup) {
+          T pv[kPushGroup];
+          int pdl[kPushGroup];
+          bool pu[kPushGroup];
+          bool anyp = false;
+#pragma unroll
+          for (int u = 0; u < kPushGroup; ++u) {
+            V = add_rn(V, Z::load(zcol + (g + u) * kThreads * Z::kSize));
+            cd = add_rn(cd, slope);
+            const bool rec = KIND == 0 ? V > c : V < c;
+            pu[u] = rec && (KIND == 0 || pl + k0 >= 0) && !record_dominates<KIND>(V, c, cd, bT, x0mkT);
+            pv[u] = c;
+            pdl[u] = pl;
+            c = rec ? V : c;
+            cd = rec ? (KIND == 0 ? V : T(0)) : cd;
+            pl = rec ? g + u : pl;
+            anyp |= pu[u];
+          }
+          if (__any_sync(kFull, anyp)) {
+#pragma unroll
+            for (int u = 0; u < kPushGroup; ++u)
+              push_record<KIND, RNEG>(ws, P, pu[u], static_cast<double>(pv[u]), k0 + pdl[u], lane, lt, rq_head,
+                                      rq_tail);
+          }
+        }
       }
       pend_d = k0 + pl;
     } else {
