@@ -848,7 +848,7 @@ __global__ void __launch_bounds__(kThreads, QMCG_MINB)
       // pending date kept tile-relative (the select takes t as an immediate);
       // calls need no "pending exists" test: cd = -inf until the first record
       int pl = pend_d - k0;
-      if constexpr (!F32) {  // FP64: grouped predicated walk; FP32 takes the generic loop below
+      if constexpr (!F32) {  // FP64: grouped predicated walk (walk_date asm); FP32: the same grouping below
         constexpr double kMargin = 1.0 + 0x1198p-52;  // record_dominates<1>'s 1e-12 margin, folded into u1
         const double bd = P.b, bsd = P.b / kMargin, x0mks = P.x0mk / kMargin;
 #pragma unroll
