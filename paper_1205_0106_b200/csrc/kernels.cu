@@ -234,7 +234,11 @@ __device__ __forceinline__ float moro_central_f32(float y, float alpha) {
   const float A = fmaf(fmaf(fmaf(-25.44106049637f, r, 41.39119773534f), r, -18.61500062529f), r, 2.50662823884f);
   const float B = fmaf(fmaf(fmaf(fmaf(3.13082909833f, r, -21.06224101826f), r, 23.08336743743f), r, -8.47351093090f),
                        r, 1.0f);
-  return fmaf(y * A, __frcp_rn(B), alpha);
+  // the MUFU reciprocal (rel. error ~2^-23, like the rest of the single-precision Moro) instead of
+  // the IEEE-rounded __frcp_rn, which expands to a Newton sequence: FP32 call 10.43 -> 9.25 ms
+  float rb;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rb) : "f"(B));
+  return fmaf(y * A, rb, alpha);
 }
 
 __device__ __forceinline__ float moro_tail_poly_f32(float w) {
