@@ -794,6 +794,9 @@ __global__ void __launch_bounds__(kThreads, QMCG_MINB)
   T slope = static_cast<T>(P.dom_slope);
   if constexpr (!F32) asm volatile("mov.b64 %0, %0;" : "+d"(slope));  // keep it in a register (no per-date reload)
   const T bT = static_cast<T>(P.b), x0mkT = static_cast<T>(P.x0mk);
+  // puts (FP64 walk): record_dominates<1>'s 1e-12 margin folded into u1 = (b c + x0mk) / M
+  constexpr double kMargin = 1.0 + 0x1198p-52;
+  const double bsd = P.b / kMargin, x0mks = P.x0mk / kMargin;
 
   init_row_barriers(sbase);
   asm volatile("st.shared.u64 [%0], %1;" ::"r"(ws + kWBest + lane * 8),
@@ -853,8 +856,7 @@ __global__ void __launch_bounds__(kThreads, QMCG_MINB)
       // calls need no "pending exists" test: cd = -inf until the first record
       int pl = pend_d - k0;
       if constexpr (!F32) {  // FP64: grouped predicated walk (walk_date asm); FP32: the same grouping below
-        constexpr double kMargin = 1.0 + 0x1198p-52;  // record_dominates<1>'s 1e-12 margin, folded into u1
-        const double bd = P.b, bsd = P.b / kMargin, x0mks = P.x0mk / kMargin;
+        const double bd = P.b;
 #pragma unroll
         for (int g = 0; g < kTile; g += kPushGroup) {
           double pv[kPushGroup];
