@@ -1208,12 +1208,19 @@ __global__ void fy_draws_kernel(uint64_t seed, int64_t n, uint64_t stride_mult, 
   const int64_t draws = n - 1;
   if (g >= draws) return;
   const uint32_t lowmask = (1u << G) - 1u;  // G <= 8
-  uint64_t s = lcg_state_after(seed, static_cast<uint64_t>(g) + 1);  // state after draw g
-  for (int64_t t = g; t < draws; t += G_) {
-    const int64_t i = n - 1 - t;  // i + 1 <= n - 1 < 2^32
-    const uint32_t j = lcg_below32(s, static_cast<uint32_t>(i + 1));
+  // state after draw g: the warp's base state (the same jump for every lane: uniform constant
+  // reads) advanced by the lane's offset (a few more steps), instead of one jump per lane whose
+  // lane-dependent table indices serialise the constant cache
+  const uint64_t wbase = static_cast<uint64_t>(g) & ~uint64_t{31};
+  uint64_t s = lcg_state_after(lcg_state_after(seed, wbase + 1), static_cast<uint64_t>(g) - wbase);
+  // draw t = g + k G_ is step i = n - 1 - t (i + 1 <= n - 1 < 2^32): 32-bit index arithmetic
+  const uint32_t Gu = static_cast<uint32_t>(G_);
+  const uint32_t iters = static_cast<uint32_t>((draws - g + G_ - 1) / G_);
+  uint32_t i = static_cast<uint32_t>(draws - g);
+  for (uint32_t k = 0; k < iters; ++k, i -= Gu) {
+    const uint32_t j = lcg_below32(s, i + 1u);
     keys[i] = static_cast<KeyT>(j >> G);
-    vals[i] = (G ? (j & lowmask) << IB : 0u) | static_cast<uint32_t>(i);
+    vals[i] = (G ? (j & lowmask) << IB : 0u) | i;
     s = stride_mult * s + stride_plus;
   }
 }
@@ -2130,7 +2137,10 @@ cudaError_t k1_grouped(uint64_t seed64, int64_t n, const PermBits& pb, char* bas
   auto* F = reinterpret_cast<uint32_t*>(base + L.F);
   auto* sstart = reinterpret_cast<uint32_t*>(base + L.sstart);
   auto* cursor = reinterpret_cast<uint32_t*>(base + L.cursor);
-  const int64_t want = (n - 1 + 15) / 16;  // ~16 draws per thread
+#ifndef QMCG_DRAWS_PER_THREAD
+#define QMCG_DRAWS_PER_THREAD 64
+#endif
+  const int64_t want = (n - 1 + QMCG_DRAWS_PER_THREAD - 1) / QMCG_DRAWS_PER_THREAD;  // draws per thread
   const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((want + threads - 1) / threads, 148 * 64));
   uint64_t sm, sp;
   lcg_jump(static_cast<uint64_t>(blocks) * threads, sm, sp);
