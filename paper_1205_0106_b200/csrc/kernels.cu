@@ -1230,27 +1230,31 @@ __global__ void fy_draws_kernel(uint64_t seed, int64_t n, uint64_t stride_mult, 
 template <typename KeyT>
 __global__ void fy_span_start_kernel(const KeyT* __restrict__ sk, int64_t n, int sh, uint32_t nspans,
                                      uint32_t* __restrict__ sstart, uint32_t* __restrict__ cursor, int bin_shift) {
-  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (cursor && t < kBins) cursor[t * kCursorStride] = static_cast<uint32_t>(t) << bin_shift;
-  const int64_t q0 = 4 * t;
-  if (q0 > n) return;
-  uint32_t key[4];
-  if (q0 + 3 < n) {
-    if constexpr (sizeof(KeyT) == 4) {
-      const uint4 k4 = __ldg(reinterpret_cast<const uint4*>(sk + q0));
-      key[0] = k4.x >> sh, key[1] = k4.y >> sh, key[2] = k4.z >> sh, key[3] = k4.w >> sh;
-    } else {
-      const uint2 k2 = __ldg(reinterpret_cast<const uint2*>(sk + q0));
-      key[0] = (k2.x & 0xffffu) >> sh, key[1] = (k2.x >> 16) >> sh;
-      key[2] = (k2.y & 0xffffu) >> sh, key[3] = (k2.y >> 16) >> sh;
-    }
+  // 16 bytes of sorted keys per thread (8 16-bit or 4 32-bit keys); the key before a thread's
+  // first comes from the previous lane (lane 0 loads it)
+  constexpr int KPT = 16 / sizeof(KeyT);
+  const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  if (cursor && t < kBins) cursor[t * kCursorStride] = t << bin_shift;
+  const int64_t q0 = static_cast<int64_t>(t) * KPT;
+  uint32_t key[KPT];
+  if (q0 + KPT - 1 < n) {
+    const uint4 k4 = __ldg(reinterpret_cast<const uint4*>(sk + q0));
+    const uint32_t w[4] = {k4.x, k4.y, k4.z, k4.w};
+#pragma unroll
+    for (int u = 0; u < KPT; ++u)
+      key[u] = (sizeof(KeyT) == 4 ? w[u] : (w[u / 2] >> (16 * (u & 1))) & 0xffffu) >> sh;
   } else {
 #pragma unroll
-    for (int u = 0; u < 4; ++u) key[u] = q0 + u < n ? static_cast<uint32_t>(__ldg(sk + q0 + u)) >> sh : nspans;
+    for (int u = 0; u < KPT; ++u) key[u] = q0 + u < n ? static_cast<uint32_t>(__ldg(sk + q0 + u)) >> sh : nspans;
   }
-  uint32_t next = q0 > 0 ? (static_cast<uint32_t>(__ldg(sk + q0 - 1)) >> sh) + 1 : 0;  // first span not started before q0
+  const uint32_t from_left = __shfl_up_sync(kFull, key[KPT - 1], 1);
+  if (q0 > n) return;
+  uint32_t next = q0 == 0 ? 0u
+                  : lane > 0 ? from_left + 1
+                             : (static_cast<uint32_t>(__ldg(sk + q0 - 1)) >> sh) + 1;  // first span not started before q0
 #pragma unroll
-  for (int u = 0; u < 4; ++u) {
+  for (int u = 0; u < KPT; ++u) {
     if (q0 + u > n) break;
     for (uint32_t w = next; w <= key[u]; ++w) sstart[w] = static_cast<uint32_t>(q0 + u);
     next = key[u] + 1;
@@ -2157,7 +2161,7 @@ cudaError_t k1_grouped(uint64_t seed64, int64_t n, const PermBits& pb, char* bas
   const auto* sk = reinterpret_cast<const KeyT*>(regA);
   const auto* sv = reinterpret_cast<const uint32_t*>(regA + (L.vals - L.keys));
   const int64_t nspans = (n + kSpan - 1) / kSpan;
-  fy_span_start_kernel<KeyT><<<static_cast<unsigned>((n / 4 + 1 + threads - 1) / threads), threads, 0, s>>>(
+  fy_span_start_kernel<KeyT><<<static_cast<unsigned>((n / (16 / sizeof(KeyT)) + 1 + threads - 1) / threads), threads, 0, s>>>(
       sk, n, 8 - pb.G, static_cast<uint32_t>(nspans), sstart, binned ? cursor : nullptr, shift);
   fy_span_kernel<KeyT><<<static_cast<unsigned>((nspans + kSpanWarps - 1) / kSpanWarps), kSpanWarps * 32, 0, s>>>(
       sk, sv, n, pb.G, pb.IB, sstart, nspans, F, reinterpret_cast<uint2*>(regB));
